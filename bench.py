@@ -1,0 +1,548 @@
+#!/usr/bin/env python
+"""PuzzleMoE packed-expert MoE layer benchmark (B200, sm_100a).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config mixtral] [--batch 64] [--no-extra]
+
+One step = one puzzle_moe_forward over one batch: route + top-k gates (a3), gate/up
+projections over the on-the-fly decoded packed experts with SwiGLU (a4), down projection
+(a5), combine (a6) -- the whole hot path of SURVEY.md §8(a) (pack (a1) is offline; its
+GB/s is reported under "aux"). Default workload = BASELINE.json configs[1]: one
+Mixtral-8x7B MoE layer (4096 x 14336, 8 experts merged into 4 pairs, top-2) at decode
+batch 64 on one B200. Weights are synthetic (seeded N(0, 1/in) experts merged + packed on
+the GPU by puzzle_merge_experts_pack); the packed layer (1.41 GB) is >10x the 126 MB L2,
+so no L2 flush is needed for the headline (smaller secondary configs flush L2 per step).
+
+Rank 0 prints ONE JSON line. Under torchrun (N > 1) every rank runs an independent
+replica on its own batch (weak scaling; expert parallelism is tracked in DESIGN.md) and
+the time is the max over ranks.
+
+--impl reference times the CPU oracle (oracle/, plain C) on the host cores on a bounded
+sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "MoE-layer tokens/s at 1/2/4/8 B200 (decode & prefill); % HBM / tensor roofline"
+FALLBACK_HBM_GBS = 6650.0     # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+FALLBACK_BF16_TFLOPS = 1590.0
+
+
+def peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "bf16_tflops": float(p["bf16_tflops"]),
+                "bf16_tflops_sustained": float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": FALLBACK_HBM_GBS, "bf16_tflops": FALLBACK_BF16_TFLOPS,
+            "bf16_tflops_sustained": 1400.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# --------------------------------------------------------------------------- clocks (NVML)
+class ClockSampler:
+    """Samples SM clock + clock-event reasons every 20 ms on a thread (NVML)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device_index: int):
+        self.samples = []
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            bus = torch.cuda.get_device_properties(device_index).pci_bus_id if hasattr(
+                torch.cuda.get_device_properties(device_index), "pci_bus_id") else None
+            if bus:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode() if isinstance(bus, str) else bus)
+            else:
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                idx = int(vis.split(",")[device_index]) if vis and vis.split(",")[0].isdigit() else device_index
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nvml = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - reported in the JSON line
+            self.err = repr(e)
+        self._stop = threading.Event()
+        self.mark = None
+
+    def _run(self):
+        n = self.nvml
+        while not self._stop.is_set():
+            try:
+                mhz = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
+                try:
+                    reasons = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    reasons = n.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.samples.append((time.perf_counter(), mhz, reasons))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self, t0: float, t1: float) -> dict:
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "nvml")}
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        use = inside if inside else self.samples
+        mhz = [s[1] for s in use]
+        mask = 0
+        for s in use:
+            mask |= s[2]
+        reasons = [k for k, v in self.REASONS.items() if mask & v]
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(use), "samples_in_timed_region": len(inside)}
+
+
+# --------------------------------------------------------------------------- workload
+def build_layer_gpu(pz, cfg, seed: int, device):
+    """Synthetic experts drawn on the GPU (generator G1 statistics) and merged + packed by
+    puzzle_merge_experts_pack (Eq. 1-7 + pack, tau = 0.4)."""
+    import torch
+    _, slot = synth.pairing(cfg, seed)
+    w = synth.packed_statistical_torch(cfg, device, seed)
+    stats = pz.new_stats(device)
+    packed = {}
+    for name, (w_i, w_j, n_i, n_j) in w.items():
+        packed[name] = pz.merge_experts_pack(w_i, w_j, n_i, n_j, 0.4, stats=stats)
+    del w
+    w13 = torch.stack([packed["w1"], packed["w3"]], dim=1).contiguous()
+    layer = pz.PackedMoELayer(w13, packed["w2"].contiguous(), torch.from_numpy(slot).to(device))
+    torch.cuda.synchronize(device)
+    return layer, stats.cpu().tolist()
+
+
+def make_inputs(cfg, T: int, seed: int, device):
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    hidden = torch.randn((T, cfg.d_model), generator=g, device=device).to(torch.bfloat16)
+    logits = torch.randn((T, cfg.n_experts), generator=g, device=device)
+    return hidden, logits
+
+
+def touched_pairs(layer, logits, cfg) -> int:
+    _, _, off, _, _ = layer.route(logits, cfg.top_k, cfg.renormalize)
+    off = off.cpu().numpy()
+    cnt = np.diff(off).reshape(-1, 2).sum(1)
+    return int((cnt > 0).sum())
+
+
+def algorithmic_bytes(cfg, n_touched: int, T: int) -> dict:
+    """per touched pair the packed words are read once: w13 = 2*f*d*2 B,
+    w2 = d*f*2 B; activations are <1% and counted separately."""
+    w13 = n_touched * 2 * cfg.d_ff * cfg.d_model * 2
+    w2 = n_touched * cfg.d_model * cfg.d_ff * 2
+    acts = T * cfg.d_model * 2 + T * cfg.n_experts * 4 + T * cfg.d_model * 2
+    return {"w13": w13, "w2": w2, "acts": acts, "total": w13 + w2 + acts}
+
+
+def l2_bytes(device) -> int:
+    import torch
+    try:
+        return int(torch.cuda.get_device_properties(device).L2_cache_size)
+    except Exception:
+        return 126 * 1024 * 1024
+
+
+def timed_steps(step, K: int, flush=None, stream=None):
+    """Device time of K steps with CUDA events on the launching stream. Without flush:
+    one event pair around the K back-to-back steps. With flush: an event pair per step,
+    the L2 flush runs between timed steps outside the events."""
+    import torch
+    s = stream or torch.cuda.current_stream()
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(K):
+            step()
+        e1.record(s)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+    pairs = []
+    for _ in range(K):
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        step()
+        e1.record(s)
+        pairs.append((e0, e1))
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in pairs)
+
+
+def unpacked_baseline(pz, layer, cfg, hidden, logits, K: int, W: int):
+    """Unpacked bf16 expert-FFN baseline on the same box: experts decoded ONCE to dense bf16
+    (puzzle_unpack), then eager torch (cuBLAS) per-expert matmuls with the same routing."""
+    import torch
+    _, slot = synth.pairing(cfg, None)
+    dev = hidden.device
+    E, d, f = cfg.n_experts, cfg.d_model, cfg.d_ff
+    w13 = torch.empty((E, 2 * f, d), dtype=torch.bfloat16, device=dev)
+    w2 = torch.empty((E, d, f), dtype=torch.bfloat16, device=dev)
+    slot_dev = layer.expert_slot.cpu().numpy()
+    for e in range(E):
+        p, pos = divmod(int(slot_dev[e]), 2)
+        pz.unpack(layer.w13[p].reshape(-1), pos, out=w13[e].reshape(-1))
+        pz.unpack(layer.w2[p].reshape(-1), pos, out=w2[e].reshape(-1))
+    k, renorm = cfg.top_k, cfg.renormalize
+
+    def step():
+        if renorm:
+            tv, ti = torch.topk(logits, k, dim=-1)
+            gates = torch.softmax(tv, dim=-1)
+        else:
+            probs = torch.softmax(logits, dim=-1)
+            gates, ti = torch.topk(probs, k, dim=-1)
+        out = torch.zeros_like(hidden, dtype=torch.float32)
+        flat = ti.reshape(-1)
+        order = torch.argsort(flat)
+        counts = torch.bincount(flat, minlength=E).cpu().tolist()
+        tok = order // k
+        g = gates.reshape(-1)[order]
+        start = 0
+        for e, c in enumerate(counts):
+            if c == 0:
+                continue
+            idx = tok[start:start + c]
+            x = hidden[idx]
+            gu = x @ w13[e].T
+            h = torch.nn.functional.silu(gu[:, :f]) * gu[:, f:]
+            y = h @ w2[e].T
+            out.index_add_(0, idx, y.float() * g[start:start + c, None])
+            start += c
+        return out.to(torch.bfloat16)
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    ms = timed_steps(step, K) / K
+    n_exp = int((torch.bincount(torch.topk(logits, k, dim=-1)[1].reshape(-1), minlength=E) > 0).sum())
+    bytes_ = n_exp * 3 * d * f * 2
+    del w13, w2
+    return {"ms_per_step": ms, "tokens_per_s": hidden.shape[0] / (ms / 1e3), "weight_bytes": bytes_,
+            "achieved_gbs": bytes_ / (ms / 1e3) / 1e9,
+            "how": "puzzle_unpack once -> dense bf16 experts; per step torch topk/softmax + per-expert cuBLAS bf16 matmuls"}
+
+
+def cpu_oracle_timing(cfg, T_batch: int, budget_s: float = 12.0, max_calls: int | None = None):
+    """Time the oracle (as it stands) on host cores on a bounded sample of the workload:
+    `n` tokens of the same config with random packed words (timing is data-independent)."""
+    import oracle
+    threads = oracle.num_threads()
+    rng = np.random.default_rng(0)
+    P, d, f = cfg.n_pairs, cfg.d_model, cfg.d_ff
+    w13 = rng.integers(0, 1 << 16, (P, 2, f, d), dtype=np.uint16)
+    w2 = rng.integers(0, 1 << 16, (P, d, f), dtype=np.uint16)
+    _, slot = synth.pairing(cfg)
+    n = max(1, min(threads, T_batch))
+    hb = synth.hidden_bits(cfg, n)
+    lg = synth.router_logits(cfg, n)
+    calls, t_total = 0, 0.0
+    while True:
+        t0 = time.perf_counter()
+        oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize)
+        t_total += time.perf_counter() - t0
+        calls += 1
+        if t_total >= budget_s or (max_calls and calls >= max_calls):
+            break
+    return {"value": calls * n / t_total, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+            "sample": f"{calls} oracle calls x {n} tokens of {cfg.name} (d={d}, d_ff={f}, E={cfg.n_experts}, "
+                      f"top-{cfg.top_k}) on random packed words; f64 accumulation, OpenMP over tokens",
+            "seconds": t_total}
+
+
+# --------------------------------------------------------------------------- arms
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = synth.CONFIGS[args.config]
+    import oracle
+    oracle.build()
+    threads = oracle.num_threads()
+    rng = np.random.default_rng(0)
+    P, d, f = cfg.n_pairs, cfg.d_model, cfg.d_ff
+    w13 = rng.integers(0, 1 << 16, (P, 2, f, d), dtype=np.uint16)
+    w2 = rng.integers(0, 1 << 16, (P, d, f), dtype=np.uint16)
+    _, slot = synth.pairing(cfg)
+    # size each step so that (warmup + steps) x step time stays within ~150 s: one token per
+    # thread when that fits, else a single token per step
+    hb1, lg1 = synth.hidden_bits(cfg, 1), synth.router_logits(cfg, 1)
+    t_one = time.perf_counter()
+    oracle.moe_forward(w13, w2, slot, hb1, lg1, cfg.top_k, cfg.renormalize)
+    t_one = time.perf_counter() - t_one
+    per_step = 150.0 / max(args.steps + args.warmup, 1)
+    n = max(1, min(threads, args.batch)) if t_one <= per_step else 1
+    hb = synth.hidden_bits(cfg, n)
+    lg = synth.router_logits(cfg, n)
+    step = lambda: oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    ms = dt / args.steps * 1e3
+    value = n / (ms / 1e3)
+    sample = (f"each step = {n} of the {args.batch} tokens of the {cfg.name} decode batch through the oracle "
+              f"(plain C, f64, OpenMP over tokens), random packed words")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} single MoE layer decode, batch {args.batch} (sampled {n} tokens/step)",
+                       "d_model": d, "d_ff": f, "n_experts": cfg.n_experts, "top_k": cfg.top_k},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2511_04805_b200 as pz
+    from paper_2511_04805_b200 import build as pzbuild
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    if rank == 0 and not os.path.exists(pz.LIB_PATH):
+        pzbuild.build()
+    if world > 1:
+        dist.barrier()
+    pz.load_library()
+    pk = peaks()
+    cfg = synth.CONFIGS[args.config]
+    T, K, W = args.batch, args.steps, args.warmup
+    seed = synth.seeds(cfg)["weights"]
+    layer, pack_stats = build_layer_gpu(pz, cfg, seed, device)
+    hidden, logits = make_inputs(cfg, T, seed + 100 * rank + 2, device)
+    out = torch.empty_like(hidden)
+    ws = layer.workspace(T, cfg.top_k)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+
+    n_touched = touched_pairs(layer, logits, cfg)
+    ab = algorithmic_bytes(cfg, n_touched, T)
+    big = ab["w13"] + ab["w2"] > 4 * l2_bytes(device)
+    flush_buf = None if big else torch.empty(2 * l2_bytes(device), dtype=torch.uint8, device=device)
+    flush = None if big else (lambda: flush_buf.zero_())
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with pz.profile_window() as prof:
+        total_ms = timed_steps(step, K, flush)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t1 = time.perf_counter()
+    time.sleep(0.05)
+    clocks.stop()
+    ms = total_ms / K
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = T * world / (ms / 1e3)
+
+    # roofline of the dominant kernel (largest share of the profiled step)
+    kern = {k: {"launches": n, "total_ms": t, "avg_ms": t / max(n, 1)} for k, (n, t) in prof.kernels.items()}
+    gpu_launches = sum(v["launches"] for v in kern.values())
+    dom = max(kern, key=lambda k: kern[k]["total_ms"]) if kern else None
+    per_launch_bytes = {"w13_gemv": ab["w13"], "w2_gemv": ab["w2"]}
+    roof = None
+    if dom in per_launch_bytes:
+        achieved = per_launch_bytes[dom] / (kern[dom]["avg_ms"] / 1e3) / 1e9
+        traffic = ncu_traffic(cfg.name, T, dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "frac_of_nominal_8tbs": achieved / 8000.0,
+                "traffic": traffic, "algorithmic_bytes_per_launch": per_launch_bytes[dom],
+                "units_per_launch": n_touched, "unit_bytes": per_launch_bytes[dom] // max(n_touched, 1),
+                "peak_source": pk["source"],
+                "step_share": kern[dom]["total_ms"] / max(sum(v["total_ms"] for v in kern.values()), 1e-9)}
+    step_gbs = (ab["w13"] + ab["w2"]) / (ms / 1e3) / 1e9
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    h_host = hidden.cpu().pin_memory()
+    l_host = logits.cpu().pin_memory()
+    o_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    h_dev = torch.empty_like(hidden)
+    l_dev = torch.empty_like(logits)
+
+    def e2e_step():
+        h_dev.copy_(h_host, non_blocking=True)
+        l_dev.copy_(l_host, non_blocking=True)
+        layer.forward(h_dev, l_dev, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+        o_host.copy_(out, non_blocking=True)
+
+    for _ in range(W):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = timed_steps(e2e_step, K, flush) / K
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": T * world / (e2e_ms / 1e3), "unit": "tokens/s",
+           "h2d_bytes_per_step": h_host.numel() * 2 + l_host.numel() * 4, "d2h_bytes_per_step": o_host.numel() * 2,
+           "ms_per_step": e2e_ms, "api": "PackedMoELayer.forward -> puzzle_moe_forward_ex (host pinned buffers)"}
+
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded N(0,1/in) experts merged+packed on GPU, tau=0.4; N(0,1) hidden and logits)",
+            "config": {"workload": f"{cfg.name} single MoE layer decode, batch {T} per GPU"
+                                   + (" (BASELINE.json configs[1])" if cfg.name == "mixtral" else ""),
+                       "d_model": cfg.d_model, "d_ff": cfg.d_ff, "n_experts": cfg.n_experts,
+                       "n_pairs": cfg.n_pairs, "top_k": cfg.top_k, "batch_per_gpu": T,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (packed layer %.2f GB)" % (layer.packed_bytes / 1e9) if big
+                       else "L2 flushed between timed steps"},
+            "roofline": roof, "step_weight_gbs": step_gbs, "gpu_launches": gpu_launches,
+            "kernels": kern, "e2e": e2e}
+    if rank == 0:
+        line["clocks"] = clocks.summary(t0, t1)
+        line["aux"] = {"pack_stats": dict(zip(["rounded_up", "saturated", "nonfinite", "negative"], pack_stats)),
+                       "touched_pairs": n_touched}
+        if not args.no_extra:
+            try:
+                line["aux"]["unpacked_bf16_baseline"] = unpacked_baseline(pz, layer, cfg, hidden, logits, min(K, 50), W)
+            except Exception as e:  # pragma: no cover
+                line["aux"]["unpacked_bf16_baseline"] = {"error": repr(e)}
+            line["aux"]["packer"] = packer_rates(pz, layer, device)
+            line["aux"]["sweep"] = sweep(pz, args, device, pk)
+        if world == 1 and not args.no_cpu:
+            try:
+                line["cpu_baseline"] = cpu_oracle_timing(cfg, T)
+            except Exception as e:  # pragma: no cover
+                line["cpu_baseline"] = {"error": repr(e)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def ncu_traffic(cfg_name: str, T: int, kernel: str):
+    """dram bytes per launch from the committed ncu --set full capture, if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        tab = json.load(fh)
+    return tab.get(f"{cfg_name}/T{T}/{kernel}")
+
+
+def packer_rates(pz, layer, device):
+    import torch
+    n = layer.w13.numel()
+    src = layer.w13.reshape(-1)
+    out = torch.empty(n, dtype=torch.bfloat16, device=device)
+    for _ in range(2):
+        pz.unpack(src, 0, out=out)
+    torch.cuda.synchronize()
+    ms = timed_steps(lambda: pz.unpack(src, 0, out=out), 5) / 5
+    unpack_gbs = n * 4 / (ms / 1e3) / 1e9
+    m = 1 << 28
+    w = torch.rand(m, device=device)
+    planes = [torch.randint(0, 2, (m,), dtype=torch.uint8, device=device) for _ in range(4)]
+    po = torch.empty(m, dtype=torch.int16, device=device)
+    pz.merge_pack(w, *planes, out=po)
+    torch.cuda.synchronize()
+    ms2 = timed_steps(lambda: pz.merge_pack(w, *planes, out=po), 5) / 5
+    return {"unpack_gbs": unpack_gbs, "unpack_elems": n, "pack_gbs": m * 10 / (ms2 / 1e3) / 1e9, "pack_elems": m,
+            "note": "algorithmic bytes: unpack 4 B/elem, pack 10 B/elem"}
+
+
+def sweep(pz, args, device, pk):
+    """Secondary decode configs (BASELINE.json configs[1] batches and configs[3] shapes)."""
+    import torch
+    res = []
+    for name, T in (("mixtral", 1), ("mixtral", 16), ("qwen15", 1), ("qwen15", 16), ("qwen15", 64),
+                    ("deepseek", 1), ("deepseek", 16), ("deepseek", 64)):
+        cfg = synth.CONFIGS[name]
+        try:
+            layer, _ = build_layer_gpu(pz, cfg, synth.seeds(cfg)["weights"], device)
+            hidden, logits = make_inputs(cfg, T, synth.seeds(cfg)["activations"], device)
+            out = torch.empty_like(hidden)
+            ws = layer.workspace(T, cfg.top_k)
+            step = lambda: layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+            nt = touched_pairs(layer, logits, cfg)
+            ab = algorithmic_bytes(cfg, nt, T)
+            flush_buf = torch.empty(2 * l2_bytes(device), dtype=torch.uint8, device=device)
+            for _ in range(5):
+                step()
+            torch.cuda.synchronize()
+            K = 50
+            ms = timed_steps(step, K, lambda: flush_buf.zero_()) / K
+            gbs = (ab["w13"] + ab["w2"]) / (ms / 1e3) / 1e9
+            res.append({"config": name, "batch": T, "tokens_per_s": T / (ms / 1e3), "ms_per_step": ms,
+                        "touched_pairs": nt, "weight_gbs": gbs, "frac_hbm": gbs / pk["hbm_gbs"]})
+            del layer, flush_buf
+            torch.cuda.empty_cache()
+        except Exception as e:  # pragma: no cover
+            res.append({"config": name, "batch": T, "error": repr(e)})
+    return res
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(synth.CONFIGS), default="mixtral")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--no-extra", action="store_true", help="skip the unpacked baseline / sweep / packer lines")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

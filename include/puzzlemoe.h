@@ -1,0 +1,230 @@
+/*
+ * puzzlemoe.h -- C ABI of the B200-native PuzzleMoE packed-expert MoE FFN library
+ * (libpuzzlemoe.so, sm_100a).
+ *
+ * What it computes (arXiv 2511.04805, "PuzzleMoE"; P:n = PAPER.md line n, S:n = SPEC.md):
+ *   Pairs of experts are merged offline (Eq. 1-7) into one magnitude tensor
+ *   W_merged plus per-expert masks M_i, M_j and signs S_i, S_j. Those four bits are
+ *   embedded into the exponent field of a bf16 word ("packed bf16"):
+ *
+ *       bit 15 S_i | bit 14 S_j | bit 13 M_i | bit 12 M_j | bits 11..7 e' | bits 6..0 mantissa
+ *       e' = clamp(e, 112, 143) - 112,   e = bf16 exponent of W_merged
+ *
+ *   and decoded on the fly by Algorithm 1 to reconstruct expert `pos`
+ *   (0 = expert i, 1 = expert j) as  W^ = (-1)^S (.) M (.) W_merged  (Eq. 8).
+ *
+ * Conventions for every call:
+ *   - All tensor pointers are DEVICE pointers owned by the caller (the library never
+ *     allocates, frees or retains caller memory). bf16 tensors are passed as uint16_t
+ *     bit patterns. All layouts are dense row-major, little-endian.
+ *   - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t; NULL is
+ *     the legacy default stream). No call synchronises the host with the device.
+ *   - Argument errors are detected on the host BEFORE any launch and returned
+ *     synchronously; nothing is launched then. Launch failures return
+ *     PUZZLE_ERR_CUDA. `puzzle_last_error()` gives a thread-local detail string.
+ *   - Data-dependent conditions (exponent clamping, non-finite or negative magnitudes)
+ *     are not errors: they are COUNTED into a caller-provided device
+ *     `puzzle_pack_stats`, which may be NULL.
+ *   - Thread safety: calls are stateless; distinct host threads may call concurrently
+ *     on distinct streams. A workspace may be used by one in-flight call at a time.
+ *   - There is no CPU fallback: without a CUDA device every compute call returns
+ *     PUZZLE_ERR_CUDA.
+ */
+#ifndef PUZZLEMOE_H_
+#define PUZZLEMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library builds with -fvisibility=hidden */
+#endif
+
+/* cudaStream_t without including cuda_runtime.h */
+typedef struct CUstream_st* puzzle_stream_t;
+
+typedef enum {
+  PUZZLE_OK = 0,
+  PUZZLE_ERR_INVALID_ARGUMENT = 1, /* null pointer, pos not in {0,1}, k > E, E != 2P, tau outside [0,1] */
+  PUZZLE_ERR_SHAPE_MISMATCH = 2,   /* SPEC ShapeMismatch / DimensionMismatch */
+  PUZZLE_ERR_UNSUPPORTED = 3,      /* shape outside the kernels' tiling: d_model or d_ff not a multiple of 64,
+                                      E > 512, misaligned pointer (16 B required for weights / activations) */
+  PUZZLE_ERR_WORKSPACE = 4,        /* workspace NULL or smaller than puzzle_moe_workspace_size() */
+  PUZZLE_ERR_CUDA = 5              /* CUDA launch / device error (including: no device) */
+} puzzle_status;
+
+/* Human-readable name of a status code (static storage). */
+const char* puzzle_status_string(int status);
+/* Thread-local detail of the last non-OK return on this thread ("" if none). */
+const char* puzzle_last_error(void);
+/* ABI version: (major << 16) | minor. */
+int puzzle_abi_version(void);
+
+/* Device-side counters, accumulated (never reset) by the pack calls. */
+typedef struct {
+  unsigned long long rounded_up; /* bf16 exponent e < 112, raised to 112 ("rounded up") */
+  unsigned long long saturated;  /* e > 143, saturated to 143 (reading R1; never hit by trained weights) */
+  unsigned long long nonfinite;  /* NaN / Inf magnitude (encoded per the same formula, but counted) */
+  unsigned long long negative;   /* magnitude < 0 (its |.| bits are encoded; counted) */
+} puzzle_pack_stats;
+
+/* ---------------------------------------------------------------------------------------
+ * puzzle_merge_pack -- (a1) merged magnitude + masks + signs -> packed bf16 words.
+ *   P:186-190 (exponent shift), P:196-209 (bit layout read back by Algorithm 1).
+ *   w_merged    f32 [n]  W_merged of Eq. 7 (>= 0, finite)
+ *   m0, m1      u8  [n]  M_i, M_j of Eq. 6 (nonzero = 1)
+ *   s0, s1      u8  [n]  S_i, S_j of Eq. 3 (nonzero = 1)
+ *   packed_out  u16 [n]  output words
+ *   stats       device puzzle_pack_stats*, accumulated; may be NULL
+ *   Rounding: f32 -> bf16 round-to-nearest-even BEFORE the exponent clamp (R3).
+ *   n == 0 is a no-op. Errors: INVALID_ARGUMENT (null pointer with n > 0, n < 0).
+ * ------------------------------------------------------------------------------------- */
+int puzzle_merge_pack(const float* w_merged, const uint8_t* m0, const uint8_t* m1,
+                      const uint8_t* s0, const uint8_t* s1, int64_t n, uint16_t* packed_out,
+                      puzzle_pack_stats* stats, puzzle_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * puzzle_unpack -- (a2) Algorithm 1 over a whole tensor.
+ *   packed    u16 [n]   packed words
+ *   pos       0 (expert i: sign bit 15, mask bit 13) or 1 (expert j: bits 14, 12)
+ *   bf16_out  u16 [n]   bf16 bits of W^_pos (Eq. 8); masked-out entries are +0.0 (0x0000)
+ *   Errors: INVALID_ARGUMENT (pos not in {0,1}, null pointer with n > 0, n < 0).
+ * ------------------------------------------------------------------------------------- */
+int puzzle_unpack(const uint16_t* packed, int pos, int64_t n, uint16_t* bf16_out,
+                  puzzle_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * puzzle_merge_experts_pack -- fused Eq. 1-7 merge + pack, for a
+ *   batch of `n_mats` independent matrices (one linear slot of one pair each).
+ *   w_i, w_j        bf16 [n_mats][rows][cols]  the two experts' weights, (out x in)
+ *   norms_i/_j      f32  [n_mats][cols]        ||X||_2 per input column (Eq. 4)
+ *   tau_sim         similarity threshold in [0,1] (Eq. 2; the paper uses 0.4)
+ *   packed_out      u16  [n_mats][rows][cols]  pos 0 = expert i, pos 1 = expert j
+ *   Arithmetic: IEEE f32 exactly as the expressions of Eq. 1-7 are written, 0/0 in
+ *   Eq. 1 := 0 (R4), saliency ties -> expert i (Eq. 5 ">="), then the same RNE + clamp as
+ *   puzzle_merge_pack. Bit-identical to merging with the oracle and packing.
+ *   Errors: INVALID_ARGUMENT (tau outside [0,1], null pointers, negative sizes).
+ * ------------------------------------------------------------------------------------- */
+int puzzle_merge_experts_pack(const uint16_t* w_i, const uint16_t* w_j, const float* norms_i,
+                              const float* norms_j, int64_t n_mats, int64_t rows, int64_t cols,
+                              float tau_sim, uint16_t* packed_out, puzzle_pack_stats* stats,
+                              puzzle_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * One MoE layer whose experts are PuzzleMoE-merged pairs (50% compression).
+ * Weight orientation (out x in) row-major as in HF Mixtral/Qwen (reading R11):
+ *   w13  u16 [n_pairs][2][d_ff][d_model]  packed gate (w1) rows, then up (w3) rows
+ *   w2   u16 [n_pairs][d_model][d_ff]     packed down projection
+ *   expert_slot  i32 [n_experts] (device) = 2*pair + pos  -- the pairing plan
+ * Requirements: n_experts == 2*n_pairs, 2 <= n_experts <= 512; d_model and d_ff multiples
+ * of 64; w13/w2 16-byte aligned.
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_experts;
+  int32_t n_pairs;
+  int32_t d_model;
+  int32_t d_ff;
+  const uint16_t* w13;
+  const uint16_t* w2;
+  const int32_t* expert_slot;
+} puzzle_moe_layer;
+
+/* Kernel path for puzzle_moe_forward_ex. AUTO picks by token count. */
+typedef enum {
+  PUZZLE_PATH_AUTO = 0,
+  PUZZLE_PATH_GEMV = 1,   /* decode shape: register-decode + mma.sync, weights read once per pair */
+  PUZZLE_PATH_TC = 2      /* prefill shape: grouped tcgen05/TMEM GEMM, tiles decoded in shared memory */
+} puzzle_path;
+
+/* Bytes of device workspace puzzle_moe_forward needs for up to max_tokens tokens. */
+size_t puzzle_moe_workspace_size(const puzzle_moe_layer* L, int64_t max_tokens, int top_k);
+
+/* ---------------------------------------------------------------------------------------
+ * puzzle_moe_forward -- the hot path: router top-k + gates (a3), gate/up projections over
+ *   the on-the-fly decoded expert with SwiGLU (a4), down projection (a5), top-k combine
+ *   (a6). Every step runs in this library's kernels; the packed weights are decoded in
+ *   registers / shared memory and never materialised in HBM.
+ *   hidden         bf16 [T][d_model]
+ *   router_logits  f32  [T][n_experts]
+ *   top_k          1 <= top_k <= n_experts; ties in the logits go to the lower expert id
+ *   renormalize    1: gates = softmax over the k selected logits (Mixtral);
+ *                  0: gates = softmax over all experts, taken at the selected (Qwen/DeepSeek)
+ *   residual       bf16 [T][d_model] or NULL; out = residual + sum_j gate_j * FFN_{e_j}(x)
+ *   out            bf16 [T][d_model] (may alias residual; must not alias hidden)
+ *   workspace      device buffer of >= puzzle_moe_workspace_size(L, T, top_k) bytes
+ *   T == 0 is a no-op. Accumulation is fp32; the SwiGLU intermediate is rounded to bf16.
+ * ------------------------------------------------------------------------------------- */
+int puzzle_moe_forward(const puzzle_moe_layer* L, const uint16_t* hidden,
+                       const float* router_logits, int64_t T, int top_k, int renormalize,
+                       const uint16_t* residual, uint16_t* out, void* workspace,
+                       size_t workspace_bytes, puzzle_stream_t stream);
+
+/* Same as puzzle_moe_forward with an explicit kernel path (tests / benchmarks). */
+int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden,
+                          const float* router_logits, int64_t T, int top_k, int renormalize,
+                          const uint16_t* residual, uint16_t* out, void* workspace,
+                          size_t workspace_bytes, int path, puzzle_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Building blocks of puzzle_moe_forward, exported for expert parallelism (the host splits
+ * the layer between route and experts to exchange tokens with NCCL all-to-all).
+ *
+ * puzzle_moe_route -- (a3). For each token: top-k expert ids (ties -> lower id), gates,
+ *   and the grouping of the T*top_k assignments by bucket b = expert_slot[e] (= 2*pair+pos).
+ *   topk_idx     i32 [T][top_k]   selected expert ids
+ *   topk_gate    f32 [T][top_k]   gates
+ *   bucket_off   i32 [2*n_pairs+1] exclusive prefix of per-bucket counts (bucket-major)
+ *   assign_token i32 [T*top_k]    token of assignment a (assignments grouped by bucket)
+ *   assign_of    i32 [T*top_k]    assignment index of (t, j)
+ *   The order of assignments inside one bucket is unspecified (results do not depend on it).
+ * ------------------------------------------------------------------------------------- */
+int puzzle_moe_route(const puzzle_moe_layer* L, const float* router_logits, int64_t T,
+                     int top_k, int renormalize, int32_t* topk_idx, float* topk_gate,
+                     int32_t* bucket_off, int32_t* assign_token, int32_t* assign_of,
+                     puzzle_stream_t stream);
+
+/* puzzle_moe_experts -- (a4)+(a5) over pre-grouped assignments:
+ *   x_rows     bf16 [n_assign][d_model]  activations, already grouped by bucket
+ *   bucket_off i32  [2*n_pairs+1] (device) bucket b owns rows [bucket_off[b], bucket_off[b+1])
+ *   y_rows     f32  [n_assign][d_model]  unweighted expert outputs W2_pos(silu(W1 x)*(W3 x))
+ *   n_assign   host-known upper bound of bucket_off[2P] (rows beyond it are untouched) */
+size_t puzzle_moe_experts_workspace_size(const puzzle_moe_layer* L, int64_t n_assign);
+int puzzle_moe_experts(const puzzle_moe_layer* L, const uint16_t* x_rows,
+                       const int32_t* bucket_off, int64_t n_assign, float* y_rows,
+                       void* workspace, size_t workspace_bytes, int path,
+                       puzzle_stream_t stream);
+
+/* puzzle_moe_combine -- (a6): out[t] = residual[t] + sum_{j<k} topk_gate[t,j] * y_rows[assign_of[t,j]]
+ *   summed in fp32 in slot order j, rounded once to bf16. residual may be NULL. */
+int puzzle_moe_combine(const float* y_rows, const int32_t* assign_of, const float* topk_gate,
+                       int64_t T, int top_k, int d_model, const uint16_t* residual,
+                       uint16_t* out, puzzle_stream_t stream);
+
+/* puzzle_gather_rows -- dst[i] = src[index[i]] for bf16 rows of width `cols` (EP dispatch
+ *   packing / token permutation). */
+int puzzle_gather_rows(const uint16_t* src, const int32_t* index, int64_t n_rows, int64_t cols,
+                       uint16_t* dst, puzzle_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Measurement plumbing (not part of the method). While a profiling window is open, every
+ * kernel the library launches is bracketed by CUDA events recorded on the SAME stream the
+ * kernel is launched on. puzzle_profile_end() synchronises those events and writes one
+ * line per kernel name: "<name> <launches> <total_ms>\n" into buf (truncated to buflen).
+ * Windows are process-global and not thread-safe; returns PUZZLE_ERR_CUDA on event errors.
+ * ------------------------------------------------------------------------------------- */
+int puzzle_profile_begin(void);
+int puzzle_profile_end(char* buf, size_t buflen);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* PUZZLEMOE_H_ */

@@ -1,0 +1,266 @@
+"""B200-native PuzzleMoE packed-expert MoE FFN (arXiv 2511.04805).
+
+Thin Python binding over the C ABI of ``libpuzzlemoe.so`` (declared in
+``include/puzzlemoe.h``). Functions carry the C names without the ``puzzle_`` prefix
+and only marshal torch CUDA tensors (pointer, size, current stream) into the library:
+every step of the path runs in the library's sm_100a kernels. There is no CPU
+fallback -- if the shared library is missing or no CUDA device is present, calls raise.
+
+Build the library with ``python -m paper_2511_04805_b200.build`` (or
+``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpuzzlemoe.so")
+
+PUZZLE_OK = 0
+PATH_AUTO, PATH_GEMV, PATH_TC = 0, 1, 2
+
+EXPORTED_SYMBOLS = (
+    "puzzle_status_string", "puzzle_last_error", "puzzle_abi_version", "puzzle_merge_pack",
+    "puzzle_unpack", "puzzle_merge_experts_pack", "puzzle_moe_workspace_size", "puzzle_moe_forward",
+    "puzzle_moe_forward_ex", "puzzle_moe_route", "puzzle_moe_experts_workspace_size",
+    "puzzle_moe_experts", "puzzle_moe_combine", "puzzle_gather_rows", "puzzle_profile_begin",
+    "puzzle_profile_end",
+)
+
+
+class PuzzleError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: {detail} (status {status})")
+        self.status = status
+
+
+class PackStats(ctypes.Structure):
+    _fields_ = [("rounded_up", ctypes.c_ulonglong), ("saturated", ctypes.c_ulonglong),
+                ("nonfinite", ctypes.c_ulonglong), ("negative", ctypes.c_ulonglong)]
+
+
+class MoELayerDesc(ctypes.Structure):
+    """puzzle_moe_layer."""
+    _fields_ = [("n_experts", ctypes.c_int32), ("n_pairs", ctypes.c_int32), ("d_model", ctypes.c_int32),
+                ("d_ff", ctypes.c_int32), ("w13", ctypes.c_void_p), ("w2", ctypes.c_void_p),
+                ("expert_slot", ctypes.c_void_p)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libpuzzlemoe.so (raises if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run `python -m paper_2511_04805_b200.build` "
+                              "(there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        P, I, I64, SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+        sig = {
+            "puzzle_status_string": ([I], ctypes.c_char_p),
+            "puzzle_last_error": ([], ctypes.c_char_p),
+            "puzzle_abi_version": ([], I),
+            "puzzle_merge_pack": ([P, P, P, P, P, I64, P, P, P], I),
+            "puzzle_unpack": ([P, I, I64, P, P], I),
+            "puzzle_merge_experts_pack": ([P, P, P, P, I64, I64, I64, ctypes.c_float, P, P, P], I),
+            "puzzle_moe_workspace_size": ([P, I64, I], SZ),
+            "puzzle_moe_forward": ([P, P, P, I64, I, I, P, P, P, SZ, P], I),
+            "puzzle_moe_forward_ex": ([P, P, P, I64, I, I, P, P, P, SZ, I, P], I),
+            "puzzle_moe_route": ([P, P, I64, I, I, P, P, P, P, P, P], I),
+            "puzzle_moe_experts_workspace_size": ([P, I64], SZ),
+            "puzzle_moe_experts": ([P, P, P, I64, P, P, SZ, I, P], I),
+            "puzzle_moe_combine": ([P, P, P, I64, I, I, P, P, P], I),
+            "puzzle_gather_rows": ([P, P, I64, I64, P, P], I),
+            "puzzle_profile_begin": ([], I),
+            "puzzle_profile_end": ([ctypes.c_char_p, SZ], I),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+        return lib
+
+
+def _check(rc: int, where: str) -> None:
+    if rc != PUZZLE_OK:
+        lib = load_library()
+        raise PuzzleError(rc, where, f"{lib.puzzle_status_string(rc).decode()}: {lib.puzzle_last_error().decode()}")
+
+
+def _p(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libpuzzlemoe takes CUDA tensors only (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream: torch.cuda.Stream | None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _u16(t: torch.Tensor) -> torch.Tensor:
+    """bf16 / int16 / uint16 tensors share one bit view."""
+    if t.dtype in (torch.bfloat16, torch.int16, torch.uint16, torch.float16):
+        return t
+    raise TypeError(f"expected a 16-bit tensor, got {t.dtype}")
+
+
+# ---------------------------------------------------------------------------- pack / unpack
+def merge_pack(w_merged, m0, m1, s0, s1, out=None, stats=None, stream=None) -> torch.Tensor:
+    """puzzle_merge_pack: f32 magnitudes + uint8 bit-planes -> packed words (int16 tensor)."""
+    assert w_merged.dtype == torch.float32
+    for t in (m0, m1, s0, s1):
+        assert t.dtype == torch.uint8 and t.shape == w_merged.shape
+    out = torch.empty(w_merged.shape, dtype=torch.int16, device=w_merged.device) if out is None else out
+    _check(load_library().puzzle_merge_pack(_p(w_merged), _p(m0), _p(m1), _p(s0), _p(s1), w_merged.numel(),
+                                            _p(out), _p(stats), _stream(stream)), "puzzle_merge_pack")
+    return out
+
+
+def unpack(packed, pos: int, out=None, stream=None) -> torch.Tensor:
+    """puzzle_unpack: Algorithm 1 -> bf16 tensor of expert ``pos``."""
+    packed = _u16(packed)
+    out = torch.empty(packed.shape, dtype=torch.bfloat16, device=packed.device) if out is None else out
+    _check(load_library().puzzle_unpack(_p(packed), int(pos), packed.numel(), _p(out), _stream(stream)),
+           "puzzle_unpack")
+    return out
+
+
+def merge_experts_pack(w_i, w_j, norms_i, norms_j, tau_sim: float = 0.4, out=None, stats=None,
+                       stream=None) -> torch.Tensor:
+    """puzzle_merge_experts_pack: bf16 [B, rows, cols] x2 + f32 norms [B, cols] -> packed."""
+    assert w_i.dtype == torch.bfloat16 and w_j.dtype == torch.bfloat16 and w_i.shape == w_j.shape
+    shp = w_i.shape if w_i.dim() == 3 else (1, *w_i.shape)
+    n_mats, rows, cols = shp
+    assert norms_i.dtype == torch.float32 and norms_i.numel() == n_mats * cols
+    assert norms_j.dtype == torch.float32 and norms_j.numel() == n_mats * cols
+    out = torch.empty(w_i.shape, dtype=torch.int16, device=w_i.device) if out is None else out
+    _check(load_library().puzzle_merge_experts_pack(_p(w_i), _p(w_j), _p(norms_i), _p(norms_j), n_mats, rows,
+                                                    cols, ctypes.c_float(tau_sim), _p(out), _p(stats),
+                                                    _stream(stream)), "puzzle_merge_experts_pack")
+    return out
+
+
+def new_stats(device="cuda") -> torch.Tensor:
+    """Zeroed device puzzle_pack_stats (4 x u64 as int64)."""
+    return torch.zeros(4, dtype=torch.int64, device=device)
+
+
+# ---------------------------------------------------------------------------- MoE layer
+class PackedMoELayer:
+    """Device tensors of one packed MoE layer plus its C descriptor.
+
+    w13: packed [P, 2, d_ff, d_model]; w2: packed [P, d_model, d_ff]; expert_slot: int32 [E]."""
+
+    def __init__(self, w13: torch.Tensor, w2: torch.Tensor, expert_slot: torch.Tensor):
+        P, two, f, d = w13.shape
+        assert two == 2 and tuple(w2.shape) == (P, d, f), (w13.shape, w2.shape)
+        assert expert_slot.dtype == torch.int32 and expert_slot.numel() == 2 * P
+        self.w13, self.w2, self.expert_slot = _u16(w13).contiguous(), _u16(w2).contiguous(), expert_slot.contiguous()
+        self.n_pairs, self.n_experts, self.d_model, self.d_ff = P, 2 * P, d, f
+        self.desc = MoELayerDesc(self.n_experts, P, d, f, self.w13.data_ptr(), self.w2.data_ptr(),
+                                 self.expert_slot.data_ptr())
+        self._ws = None
+
+    @property
+    def packed_bytes(self) -> int:
+        return self.w13.numel() * 2 + self.w2.numel() * 2
+
+    def workspace_size(self, max_tokens: int, top_k: int) -> int:
+        return int(load_library().puzzle_moe_workspace_size(ctypes.byref(self.desc), int(max_tokens), int(top_k)))
+
+    def workspace(self, max_tokens: int, top_k: int) -> torch.Tensor:
+        need = self.workspace_size(max_tokens, top_k)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.w13.device)
+        return self._ws
+
+    def forward(self, hidden, router_logits, top_k: int, renormalize: bool, residual=None, out=None,
+                path: int = PATH_AUTO, workspace=None, stream=None) -> torch.Tensor:
+        """puzzle_moe_forward_ex: bf16 [T, d] hidden, f32 [T, E] logits -> bf16 [T, d]."""
+        T = hidden.shape[0]
+        assert hidden.dtype == torch.bfloat16 and router_logits.dtype == torch.float32
+        out = torch.empty_like(hidden) if out is None else out
+        ws = self.workspace(T, top_k) if workspace is None else workspace
+        _check(load_library().puzzle_moe_forward_ex(
+            ctypes.byref(self.desc), _p(hidden), _p(router_logits), T, int(top_k), int(bool(renormalize)),
+            _p(residual), _p(out), _p(ws), ws.numel(), int(path), _stream(stream)), "puzzle_moe_forward")
+        return out
+
+    __call__ = forward
+
+    def route(self, router_logits, top_k: int, renormalize: bool, stream=None):
+        """puzzle_moe_route -> (topk_idx, topk_gate, bucket_off, assign_token, assign_of)."""
+        T = router_logits.shape[0]
+        dev = router_logits.device
+        idx = torch.empty((T, top_k), dtype=torch.int32, device=dev)
+        gate = torch.empty((T, top_k), dtype=torch.float32, device=dev)
+        off = torch.empty(2 * self.n_pairs + 1, dtype=torch.int32, device=dev)
+        tok = torch.empty(T * top_k, dtype=torch.int32, device=dev)
+        aof = torch.empty(T * top_k, dtype=torch.int32, device=dev)
+        _check(load_library().puzzle_moe_route(ctypes.byref(self.desc), _p(router_logits), T, int(top_k),
+                                               int(bool(renormalize)), _p(idx), _p(gate), _p(off), _p(tok),
+                                               _p(aof), _stream(stream)), "puzzle_moe_route")
+        return idx, gate, off, tok, aof
+
+    def experts(self, x_rows, bucket_off, y_rows=None, path: int = PATH_AUTO, workspace=None, stream=None):
+        """puzzle_moe_experts: grouped bf16 rows -> unweighted f32 expert outputs."""
+        n = x_rows.shape[0]
+        y_rows = torch.empty((n, self.d_model), dtype=torch.float32, device=x_rows.device) if y_rows is None else y_rows
+        if workspace is None:
+            need = int(load_library().puzzle_moe_experts_workspace_size(ctypes.byref(self.desc), n))
+            workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=x_rows.device)
+        _check(load_library().puzzle_moe_experts(ctypes.byref(self.desc), _p(x_rows), _p(bucket_off), n,
+                                                 _p(y_rows), _p(workspace), workspace.numel(), int(path),
+                                                 _stream(stream)), "puzzle_moe_experts")
+        return y_rows
+
+
+def moe_combine(y_rows, assign_of, topk_gate, residual=None, out=None, stream=None) -> torch.Tensor:
+    T, k = topk_gate.shape
+    d = y_rows.shape[1]
+    out = torch.empty((T, d), dtype=torch.bfloat16, device=y_rows.device) if out is None else out
+    _check(load_library().puzzle_moe_combine(_p(y_rows), _p(assign_of), _p(topk_gate), T, k, d, _p(residual),
+                                             _p(out), _stream(stream)), "puzzle_moe_combine")
+    return out
+
+
+def gather_rows(src, index, out=None, stream=None) -> torch.Tensor:
+    n = index.numel()
+    out = torch.empty((n, src.shape[1]), dtype=src.dtype, device=src.device) if out is None else out
+    _check(load_library().puzzle_gather_rows(_p(src), _p(index), n, src.shape[1], _p(out), _stream(stream)),
+           "puzzle_gather_rows")
+    return out
+
+
+class profile_window:
+    """Context manager over puzzle_profile_begin/end: per-kernel CUDA-event timings of every
+    library launch inside the window, recorded on the launching stream.
+    After exit, ``.kernels`` maps kernel name -> (launches, total_ms)."""
+
+    def __enter__(self):
+        _check(load_library().puzzle_profile_begin(), "puzzle_profile_begin")
+        self.kernels = {}
+        return self
+
+    def __exit__(self, *exc):
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(load_library().puzzle_profile_end(buf, len(buf)), "puzzle_profile_end")
+        for line in buf.value.decode().splitlines():
+            name, n, ms = line.split()
+            self.kernels[name] = (int(n), float(ms))
+        return False

@@ -1,0 +1,399 @@
+// extern "C" boundary of libpuzzlemoe: host-side argument validation, workspace layout,
+// kernel-path dispatch. Declared (with citations and contracts) in include/puzzlemoe.h.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pz {
+
+// kernel launchers (pack.cu, route.cu, gemv.cu, gemm_tc.cu)
+int launch_merge_pack(const float*, const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*,
+                      int64_t, uint16_t*, puzzle_pack_stats*, cudaStream_t);
+int launch_unpack(const uint16_t*, int, int64_t, uint16_t*, cudaStream_t);
+int launch_merge_experts_pack(const uint16_t*, const uint16_t*, const float*, const float*, int64_t,
+                              int64_t, int64_t, float, uint16_t*, puzzle_pack_stats*, cudaStream_t);
+int launch_route(const float*, int64_t, int, int, int, const int32_t*, int, int32_t*, float*, int32_t*,
+                 int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int, cudaStream_t);
+int launch_iota(int32_t*, int, int32_t*, cudaStream_t);
+const char* last_error_cstr();
+int launch_combine(const float*, const int32_t*, const float*, int64_t, int, int, const uint16_t*,
+                   uint16_t*, cudaStream_t);
+int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16_t*, cudaStream_t);
+int gemv_nt_for(int64_t T);
+void gemv_splits(int d, int f, int max_active, int* ks13, int* ks2);
+int launch_gemv_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*,
+                        const int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int64_t,
+                        int, int, int, float*, float*, int32_t*, int32_t*, uint16_t*, float*,
+                        cudaStream_t);
+
+namespace {
+thread_local std::string g_last_error;
+
+struct ProfRec {
+  std::string name;
+  cudaEvent_t beg, end;
+};
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t pool_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+void prof_mark_begin(const char* name, cudaStream_t s) {
+  if (!g_prof_on) return;
+  ProfRec r{name, pool_event(), pool_event()};
+  cudaEventRecord(r.beg, s);
+  g_prof.push_back(r);
+}
+
+void prof_mark_end(cudaStream_t s) {
+  if (!g_prof_on || g_prof.empty()) return;
+  cudaEventRecord(g_prof.back().end, s);
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return PUZZLE_OK;
+  return fail(PUZZLE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int num_sms() {
+  static int cached = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      cached = n;
+    else
+      cached = 148;  // B200
+  });
+  return cached;
+}
+
+namespace {
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+int check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(PUZZLE_ERR_CUDA, "no CUDA device: libpuzzlemoe has no CPU fallback");
+  return PUZZLE_OK;
+}
+
+int check_layer(const puzzle_moe_layer* L) {
+  if (!L) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "layer descriptor is NULL");
+  if (!L->w13 || !L->w2 || !L->expert_slot)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "layer weights / expert_slot NULL");
+  if (L->n_pairs < 1 || L->n_experts != 2 * L->n_pairs)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "n_experts must equal 2*n_pairs >= 2 (50% merge)");
+  if (L->n_experts > kMaxExperts) return fail(PUZZLE_ERR_UNSUPPORTED, "n_experts > 512");
+  if (L->d_model < 64 || L->d_ff < 64 || L->d_model % 64 || L->d_ff % 64)
+    return fail(PUZZLE_ERR_UNSUPPORTED, "d_model and d_ff must be positive multiples of 64");
+  if (!al16(L->w13) || !al16(L->w2)) return fail(PUZZLE_ERR_UNSUPPORTED, "weights must be 16-byte aligned");
+  return PUZZLE_OK;
+}
+
+// ---- workspace layout of puzzle_moe_forward / puzzle_moe_experts ----
+struct Plan {
+  int64_t T = 0, n_assign = 0;
+  int k = 0, max_active = 0, nt = 1, ks13 = 1, ks2 = 1;
+};
+
+struct Layout {
+  size_t topk_idx, topk_gate, bucket_off, assign_token, assign_of, active, n_active, cnt13, cnt2, h, y,
+      part13, part2, total;
+};
+
+Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k) {
+  Plan p;
+  p.T = T;
+  p.k = k;
+  p.n_assign = T * k;
+  p.max_active = (int)std::min<int64_t>(L->n_pairs, p.n_assign);
+  p.nt = gemv_nt_for(T);
+  gemv_splits(L->d_model, L->d_ff, std::max(p.max_active, 1), &p.ks13, &p.ks2);
+  return p;
+}
+
+Layout make_layout(const puzzle_moe_layer* L, const Plan& p) {
+  Layout o;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = off;
+    off += align_up(bytes);
+    return at;
+  };
+  const size_t na = (size_t)p.n_assign, P = (size_t)L->n_pairs, d = L->d_model, f = L->d_ff;
+  o.topk_idx = take(na * 4);
+  o.topk_gate = take(na * 4);
+  o.bucket_off = take((2 * P + 1) * 4);
+  o.assign_token = take(na * 4);
+  o.assign_of = take(na * 4);
+  o.active = take(P * 4);
+  o.n_active = take(4);
+  o.cnt13 = take(P * (f / 64) * 4);
+  o.cnt2 = take(P * (d / 64) * 4);
+  o.h = take(na * f * 2);
+  o.y = take(na * d * 4);
+  o.part13 = take(p.ks13 > 1 ? (size_t)p.ks13 * na * 2 * f * 4 : 0);
+  o.part2 = take(p.ks2 > 1 ? (size_t)p.ks2 * na * d * 4 : 0);
+  o.total = off;
+  return o;
+}
+
+size_t workspace_for(const puzzle_moe_layer* L, int64_t max_tokens, int k) {
+  // the split factors depend on min(P, T*k); take the max over every distinct plan
+  size_t best = 0;
+  int64_t knee = (L->n_pairs + k - 1) / k;
+  for (int64_t t = 1; t <= std::min<int64_t>(max_tokens, knee); ++t)
+    best = std::max(best, make_layout(L, make_plan(L, t, k)).total);
+  if (max_tokens > 0) best = std::max(best, make_layout(L, make_plan(L, max_tokens, k)).total);
+  return best;
+}
+
+template <typename T>
+T* at(void* base, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(base) + off);
+}
+
+}  // namespace
+}  // namespace pz
+
+using namespace pz;
+
+extern "C" {
+
+const char* puzzle_status_string(int status) {
+  switch (status) {
+    case PUZZLE_OK: return "PUZZLE_OK";
+    case PUZZLE_ERR_INVALID_ARGUMENT: return "PUZZLE_ERR_INVALID_ARGUMENT";
+    case PUZZLE_ERR_SHAPE_MISMATCH: return "PUZZLE_ERR_SHAPE_MISMATCH";
+    case PUZZLE_ERR_UNSUPPORTED: return "PUZZLE_ERR_UNSUPPORTED";
+    case PUZZLE_ERR_WORKSPACE: return "PUZZLE_ERR_WORKSPACE";
+    case PUZZLE_ERR_CUDA: return "PUZZLE_ERR_CUDA";
+    default: return "PUZZLE_ERR_UNKNOWN";
+  }
+}
+
+const char* puzzle_last_error(void) { return last_error_cstr(); }
+
+int puzzle_abi_version(void) { return (1 << 16) | 0; }
+
+int puzzle_profile_begin(void) {
+  for (auto& r : g_prof) {
+    g_event_pool.push_back(r.beg);
+    g_event_pool.push_back(r.end);
+  }
+  g_prof.clear();
+  g_prof_on = true;
+  return PUZZLE_OK;
+}
+
+int puzzle_profile_end(char* buf, size_t buflen) {
+  g_prof_on = false;
+  std::map<std::string, std::pair<long, double>> agg;
+  std::vector<std::string> order;
+  for (auto& r : g_prof) {
+    if (cudaEventSynchronize(r.end) != cudaSuccess) return fail(PUZZLE_ERR_CUDA, "profile event sync");
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.beg, r.end) != cudaSuccess) return fail(PUZZLE_ERR_CUDA, "profile elapsed");
+    if (!agg.count(r.name)) order.push_back(r.name);
+    agg[r.name].first += 1;
+    agg[r.name].second += ms;
+  }
+  std::string out;
+  for (auto& n : order) {
+    char line[256];
+    snprintf(line, sizeof(line), "%s %ld %.6f\n", n.c_str(), agg[n].first, agg[n].second);
+    out += line;
+  }
+  if (buf && buflen) {
+    size_t n = std::min(buflen - 1, out.size());
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return PUZZLE_OK;
+}
+
+int puzzle_merge_pack(const float* w, const uint8_t* m0, const uint8_t* m1, const uint8_t* s0,
+                      const uint8_t* s1, int64_t n, uint16_t* out, puzzle_pack_stats* stats,
+                      puzzle_stream_t stream) {
+  if (n < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "n < 0");
+  if (n == 0) return PUZZLE_OK;
+  if (!w || !m0 || !m1 || !s0 || !s1 || !out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (int rc = check_device()) return rc;
+  return launch_merge_pack(w, m0, m1, s0, s1, n, out, stats, (cudaStream_t)stream);
+}
+
+int puzzle_unpack(const uint16_t* packed, int pos, int64_t n, uint16_t* out, puzzle_stream_t stream) {
+  if (pos != 0 && pos != 1) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "pos must be 0 or 1");
+  if (n < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "n < 0");
+  if (n == 0) return PUZZLE_OK;
+  if (!packed || !out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (int rc = check_device()) return rc;
+  return launch_unpack(packed, pos, n, out, (cudaStream_t)stream);
+}
+
+int puzzle_merge_experts_pack(const uint16_t* wi, const uint16_t* wj, const float* ni, const float* nj,
+                              int64_t n_mats, int64_t rows, int64_t cols, float tau, uint16_t* out,
+                              puzzle_pack_stats* stats, puzzle_stream_t stream) {
+  if (!(tau >= 0.0f && tau <= 1.0f)) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "tau_sim outside [0,1]");
+  if (n_mats < 0 || rows < 0 || cols < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "negative size");
+  if (n_mats * rows * cols == 0) return PUZZLE_OK;
+  if (!wi || !wj || !ni || !nj || !out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (cols % 8) return fail(PUZZLE_ERR_UNSUPPORTED, "cols must be a multiple of 8");
+  if (!al16(wi) || !al16(wj) || !al16(ni) || !al16(nj) || !al16(out))
+    return fail(PUZZLE_ERR_UNSUPPORTED, "pointers must be 16-byte aligned");
+  if (int rc = check_device()) return rc;
+  return launch_merge_experts_pack(wi, wj, ni, nj, n_mats, rows, cols, tau, out, stats,
+                                   (cudaStream_t)stream);
+}
+
+size_t puzzle_moe_workspace_size(const puzzle_moe_layer* L, int64_t max_tokens, int top_k) {
+  if (check_layer(L) || max_tokens < 0 || top_k < 1 || top_k > L->n_experts) return 0;
+  return workspace_for(L, max_tokens, top_k);
+}
+
+size_t puzzle_moe_experts_workspace_size(const puzzle_moe_layer* L, int64_t n_assign) {
+  // the experts-only call is laid out like a forward with T = n_assign, k = 1
+  if (check_layer(L) || n_assign < 0) return 0;
+  return workspace_for(L, n_assign, 1);
+}
+
+static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout& lay, void* ws,
+                       const uint16_t* x, const int32_t* row_index, const int32_t* bucket_off,
+                       const int32_t* active, const int32_t* n_active, float* y, int path,
+                       cudaStream_t s) {
+  (void)path;
+  return launch_gemv_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, x, row_index, bucket_off,
+                             active, n_active, plan.max_active, plan.n_assign, plan.nt, plan.ks13,
+                             plan.ks2, at<float>(ws, lay.part13), at<float>(ws, lay.part2),
+                             at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2),
+                             at<uint16_t>(ws, lay.h), y, s);
+}
+
+int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits,
+                          int64_t T, int k, int renorm, const uint16_t* residual, uint16_t* out,
+                          void* ws, size_t ws_bytes, int path, puzzle_stream_t stream) {
+  if (int rc = check_layer(L)) return rc;
+  if (T < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "T < 0");
+  if (k < 1 || k > L->n_experts) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "top_k outside [1, n_experts]");
+  if (path < PUZZLE_PATH_AUTO || path > PUZZLE_PATH_TC) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad path");
+  if (T == 0) return PUZZLE_OK;
+  if (!hidden || !logits || !out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL activation pointer");
+  if (hidden == out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "out must not alias hidden");
+  if (!al16(hidden) || !al16(out) || (residual && !al16(residual)))
+    return fail(PUZZLE_ERR_UNSUPPORTED, "activations must be 16-byte aligned");
+  if (int rc = check_device()) return rc;
+  const Plan plan = make_plan(L, T, k);
+  const Layout lay = make_layout(L, plan);
+  if (!ws || ws_bytes < lay.total)
+    return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_moe_workspace_size(L, T, top_k)");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = launch_route(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs,
+                        at<int32_t>(ws, lay.topk_idx), at<float>(ws, lay.topk_gate),
+                        at<int32_t>(ws, lay.bucket_off), at<int32_t>(ws, lay.assign_token),
+                        at<int32_t>(ws, lay.assign_of), at<int32_t>(ws, lay.active),
+                        at<int32_t>(ws, lay.n_active), at<int32_t>(ws, lay.cnt13),
+                        (int)((lay.h - lay.cnt13) / 4), s);
+  if (rc) return rc;
+  rc = run_experts(L, plan, lay, ws, hidden, at<int32_t>(ws, lay.assign_token),
+                   at<int32_t>(ws, lay.bucket_off), at<int32_t>(ws, lay.active),
+                   at<int32_t>(ws, lay.n_active), at<float>(ws, lay.y), path, s);
+  if (rc) return rc;
+  return launch_combine(at<float>(ws, lay.y), at<int32_t>(ws, lay.assign_of), at<float>(ws, lay.topk_gate),
+                        T, k, L->d_model, residual, out, s);
+}
+
+int puzzle_moe_forward(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits, int64_t T,
+                       int k, int renorm, const uint16_t* residual, uint16_t* out, void* ws,
+                       size_t ws_bytes, puzzle_stream_t stream) {
+  return puzzle_moe_forward_ex(L, hidden, logits, T, k, renorm, residual, out, ws, ws_bytes,
+                               PUZZLE_PATH_AUTO, stream);
+}
+
+int puzzle_moe_route(const puzzle_moe_layer* L, const float* logits, int64_t T, int k, int renorm,
+                     int32_t* topk_idx, float* topk_gate, int32_t* bucket_off, int32_t* assign_token,
+                     int32_t* assign_of, puzzle_stream_t stream) {
+  if (int rc = check_layer(L)) return rc;
+  if (T < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "T < 0");
+  if (k < 1 || k > L->n_experts) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "top_k outside [1, n_experts]");
+  if (!logits || !topk_idx || !topk_gate || !bucket_off || !assign_token || !assign_of)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (int rc = check_device()) return rc;
+  return launch_route(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs, topk_idx, topk_gate,
+                      bucket_off, assign_token, assign_of, nullptr, nullptr, nullptr, 0, (cudaStream_t)stream);
+}
+
+int puzzle_moe_experts(const puzzle_moe_layer* L, const uint16_t* x_rows, const int32_t* bucket_off,
+                       int64_t n_assign, float* y_rows, void* ws, size_t ws_bytes, int path,
+                       puzzle_stream_t stream) {
+  if (int rc = check_layer(L)) return rc;
+  if (n_assign < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "n_assign < 0");
+  if (n_assign == 0) return PUZZLE_OK;
+  if (!x_rows || !bucket_off || !y_rows) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!al16(x_rows) || !al16(y_rows)) return fail(PUZZLE_ERR_UNSUPPORTED, "rows must be 16-byte aligned");
+  if (int rc = check_device()) return rc;
+  // Every pair may be touched: plan with T = n_assign, k = 1 (max_active = min(P, n_assign)).
+  Plan plan = make_plan(L, n_assign, 1);
+  plan.nt = gemv_nt_for(std::min<int64_t>(n_assign, 64));
+  const Layout lay = make_layout(L, plan);
+  if (!ws || ws_bytes < lay.total) return fail(PUZZLE_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  // active list = all pairs (empty pairs exit immediately); counters zeroed
+  int rc = cuda_check(cudaMemsetAsync(at<char>(ws, lay.cnt13), 0, lay.h - lay.cnt13, s), "memset");
+  if (rc) return rc;
+  rc = launch_iota(at<int32_t>(ws, lay.active), L->n_pairs, at<int32_t>(ws, lay.n_active), s);
+  if (rc) return rc;
+  plan.max_active = L->n_pairs;
+  return run_experts(L, plan, lay, ws, x_rows, nullptr, bucket_off, at<int32_t>(ws, lay.active),
+                     at<int32_t>(ws, lay.n_active), y_rows, path, s);
+}
+
+int puzzle_moe_combine(const float* y, const int32_t* assign_of, const float* gate, int64_t T, int k,
+                       int d, const uint16_t* residual, uint16_t* out, puzzle_stream_t stream) {
+  if (T < 0 || k < 1 || d < 4 || d % 4) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (T == 0) return PUZZLE_OK;
+  if (!y || !assign_of || !gate || !out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (int rc = check_device()) return rc;
+  return launch_combine(y, assign_of, gate, T, k, d, residual, out, (cudaStream_t)stream);
+}
+
+int puzzle_gather_rows(const uint16_t* src, const int32_t* index, int64_t n_rows, int64_t cols,
+                       uint16_t* dst, puzzle_stream_t stream) {
+  if (n_rows < 0 || cols < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "negative size");
+  if (n_rows == 0) return PUZZLE_OK;
+  if (!src || !index || !dst) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (cols % 8 || !al16(src) || !al16(dst)) return fail(PUZZLE_ERR_UNSUPPORTED, "cols % 8 / alignment");
+  if (int rc = check_device()) return rc;
+  return launch_gather_rows(src, index, n_rows, cols, dst, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Shared device helpers for libpuzzlemoe (sm_100a only). Nothing here is shared with
+// oracle/ (the CPU oracle is an independent statement of the same paper passages).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/puzzlemoe.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libpuzzlemoe targets sm_100a (B200) only"
+#endif
+
+namespace pz {
+
+// ---- host-side error plumbing (thread-local detail string) ----
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_check(cudaError_t e, const char* what);
+int num_sms();
+
+constexpr int kMaxExperts = 512;
+
+// Per-kernel event bracketing while a puzzle_profile window is open (abi.cu).
+void prof_mark_begin(const char* name, cudaStream_t s);
+void prof_mark_end(cudaStream_t s);
+struct ProfScope {
+  cudaStream_t s;
+  ProfScope(const char* name, cudaStream_t st) : s(st) { prof_mark_begin(name, st); }
+  ~ProfScope() { prof_mark_end(s); }
+};
+
+// ---- packed word layout (Algorithm 1) ----
+// bit15 S_i | bit14 S_j | bit13 M_i | bit12 M_j | bits 11..7 e' = e-112 | bits 6..0 mantissa
+
+// f32 -> bf16 round-to-nearest-even in integer arithmetic (reading R3). Integer-only so
+// that FTZ / fast-math settings can never change the result.
+__device__ __forceinline__ uint32_t f32_to_bf16_rne_bits(float x) {
+  uint32_t u = __float_as_uint(x);
+  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+
+// Encode one word from a magnitude already rounded to bf16 bits + 4 header bits.
+// Returns the word; sets *lo / *hi when the exponent was clamped (R1).
+__device__ __forceinline__ uint32_t encode_word(uint32_t h, uint32_t s0, uint32_t s1, uint32_t m0,
+                                                uint32_t m1, uint32_t* lo, uint32_t* hi) {
+  uint32_t e = (h >> 7) & 0xFFu;
+  *lo = e < 112u;
+  *hi = e > 143u;
+  e = e < 112u ? 112u : (e > 143u ? 143u : e);
+  return (s0 << 15) | (s1 << 14) | (m0 << 13) | (m1 << 12) | ((e - 112u) << 7) | (h & 0x7Fu);
+}
+
+// prmt with msb-replicate: for each 16-bit lane, 0xFFFF if bit 15 of the lane is set.
+__device__ __forceinline__ uint32_t lane_msb_mask(uint32_t v) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(r) : "r"(v));
+  return r;
+}
+
+// Two-lane SWAR Algorithm 1: decode both packed words held in `w` for expert `POS`.
+// Per 16-bit lane: mask ? (sign << 15) | ((w & 0x0F80) + (112 << 7)) | (w & 0x7F) : 0.
+// (w & 0x0FFF) + 0x3800 == (w & 0x0F80) + (112 << 7) | (w & 0x7F) since the 0x3800 add
+// never carries out of bits 11..7 (max 0x0FFF + 0x3800 = 0x47FF < 0x8000): no cross-lane carry.
+template <int POS>
+__device__ __forceinline__ uint32_t decode2(uint32_t w, uint32_t base) {
+  const uint32_t sign_src = POS == 0 ? w : (w << 1);         // sign bit 15 (pos 0) / 14 (pos 1)
+  const uint32_t val = (sign_src & 0x80008000u) | base;      // one LOP3
+  const uint32_t mask = lane_msb_mask(w << (2 + POS));       // mask bit 13 / 12 -> bit 15
+  return val & mask;
+}
+__device__ __forceinline__ uint32_t decode_base(uint32_t w) {
+  return (w & 0x0FFF0FFFu) + 0x38003800u;
+}
+template <int POS>
+__device__ __forceinline__ uint32_t decode2(uint32_t w) {
+  return decode2<POS>(w, decode_base(w));
+}
+
+// ---- memory helpers ----
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ldg_v4(const void* p) {
+  uint4 r;
+  asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ---- legacy tensor-core MMA (decode-shape GEMV path) ----
+// D[16x8] += A[16x16] * B[16x8], bf16 inputs, fp32 accumulate.
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                               uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + expf(-g)) * u; }
+
+__device__ __forceinline__ uint16_t f32_to_bf16_bits_rn(float x) {
+  return (uint16_t)f32_to_bf16_rne_bits(x);
+}
+__device__ __forceinline__ float bf16_bits_to_f32(uint32_t h) { return __uint_as_float(h << 16); }
+
+}  // namespace pz

@@ -1,0 +1,56 @@
+"""Test-side helpers: build oracle-packed layers from the seeded generator, upload them,
+and compare GPU outputs with the oracle under the north-star tolerance."""
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+
+import oracle
+import synth
+
+# BASELINE.json north_star: "max abs error <= 2e-2 and relative L2 <= 5e-3 against an
+# fp32-accumulated oracle on bf16 inputs" (our oracle accumulates in f64, R16/R17).
+MAX_ABS = 2e-2
+REL_L2 = 5e-3
+
+
+@functools.lru_cache(maxsize=8)
+def oracle_packed_layer(cfg: synth.MoEConfig, seed: int | None = None, tau: float = 0.4):
+    """Packed w13 [P,2,f,d], w2 [P,d,f] (uint16) merged + packed by the ORACLE from the
+    generator's expert weights, plus expert_slot and pack stats."""
+    _, slot = synth.pairing(cfg, seed)
+    P, d, f = cfg.n_pairs, cfg.d_model, cfg.d_ff
+    w13 = np.empty((P, 2, f, d), np.uint16)
+    w2 = np.empty((P, d, f), np.uint16)
+    stats = np.zeros(4, np.uint64)
+    for p in range(P):
+        for s_idx, slot_name in enumerate(synth.SLOTS):
+            w_i, w_j, n_i, n_j = synth.expert_pair_slot(cfg, p, slot_name, seed)
+            art = oracle.merge(w_i, w_j, n_i, n_j, tau)
+            packed, st = oracle.pack_artifacts(art)
+            stats += st
+            if slot_name == "w1":
+                w13[p, 0] = packed
+            elif slot_name == "w3":
+                w13[p, 1] = packed
+            else:
+                w2[p] = packed
+            del art, w_i, w_j
+    return w13, w2, slot, stats
+
+
+def compare(gpu_out: np.ndarray, ref: np.ndarray) -> dict:
+    g = gpu_out.astype(np.float64)
+    r = ref.astype(np.float64)
+    diff = g - r
+    max_abs = float(np.abs(diff).max()) if diff.size else 0.0
+    denom = float(np.linalg.norm(r)) or 1.0
+    rel = float(np.linalg.norm(diff)) / denom
+    return {"max_abs": max_abs, "rel_l2": rel}
+
+
+def assert_close(gpu_out: np.ndarray, ref: np.ndarray, what: str = ""):
+    m = compare(gpu_out, ref)
+    assert m["max_abs"] <= MAX_ABS and m["rel_l2"] <= REL_L2, f"{what}: {m}"
+    return m

@@ -1,0 +1,78 @@
+"""CPU-side checks of the C-ABI boundary: the library builds/loads and exports every
+symbol include/puzzlemoe.h declares; host-only calls work without a device; argument
+errors are rejected synchronously before any launch; compute calls fail loudly (no CPU
+fallback) when no device exists."""
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "puzzlemoe.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2511_04805_b200 import build
+    build.build()
+    import paper_2511_04805_b200 as pz
+    return pz.load_library()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(puzzle_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for required in ("puzzle_merge_pack", "puzzle_unpack", "puzzle_moe_forward"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    import paper_2511_04805_b200 as pz
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert sorted(pz.EXPORTED_SYMBOLS) == declared_functions()
+
+
+def test_host_only_calls(lib):
+    assert lib.puzzle_abi_version() >> 16 == 1
+    assert lib.puzzle_status_string(0) == b"PUZZLE_OK"
+    assert lib.puzzle_status_string(4) == b"PUZZLE_ERR_WORKSPACE"
+    import paper_2511_04805_b200 as pz
+    desc = pz.MoELayerDesc(8, 4, 4096, 14336, 4096, 4096, 4096)  # fake aligned addresses, never dereferenced
+    ws = lib.puzzle_moe_workspace_size(ctypes.byref(desc), 64, 2)
+    # must at least hold h (bf16) and y (f32) for the 128 assignments
+    assert ws >= 128 * 14336 * 2 + 128 * 4096 * 4
+    bad = pz.MoELayerDesc(8, 4, 4000, 14336, 4096, 4096, 4096)  # d_model % 64 != 0
+    assert lib.puzzle_moe_workspace_size(ctypes.byref(bad), 64, 2) == 0
+
+
+def test_argument_errors_are_synchronous(lib):
+    assert lib.puzzle_unpack(None, 2, 10, None, None) == 1            # pos not in {0,1}
+    assert b"pos" in lib.puzzle_last_error()
+    assert lib.puzzle_unpack(None, 0, 0, None, None) == 0             # n == 0: no-op
+    assert lib.puzzle_merge_pack(None, None, None, None, None, -1, None, None, None) == 1
+    assert lib.puzzle_merge_experts_pack(None, None, None, None, 1, 1, 8, ctypes.c_float(1.5), None, None, None) == 1
+    import paper_2511_04805_b200 as pz
+    desc = pz.MoELayerDesc(7, 4, 4096, 14336, 4096, 4096, 4096)     # E != 2P
+    assert lib.puzzle_moe_forward(ctypes.byref(desc), None, None, 1, 2, 1, None, None, None, 0, None) == 1
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device path")
+def test_compute_without_device_fails_loudly(lib):
+    buf = (ctypes.c_uint16 * 8)()
+    out = (ctypes.c_uint16 * 8)()
+    rc = lib.puzzle_unpack(ctypes.cast(buf, ctypes.c_void_p), 0, 8, ctypes.cast(out, ctypes.c_void_p), None)
+    assert rc == 5 and b"no CUDA device" in lib.puzzle_last_error()
+
+
+def test_binding_rejects_cpu_tensors(lib):
+    import paper_2511_04805_b200 as pz
+    with pytest.raises(ValueError):
+        pz.unpack(torch.zeros(8, dtype=torch.int16), 0)

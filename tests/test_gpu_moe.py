@@ -1,0 +1,125 @@
+"""GPU parity for puzzle_moe_forward (route + gate/up/SwiGLU + down + combine) against the
+f64 oracle FFN, through the C ABI, under the north-star tolerance (tests/helpers.py)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from helpers import assert_close, oracle_packed_layer
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pz():
+    import paper_2511_04805_b200 as pz
+    pz.load_library()
+    return pz
+
+
+def _layer(pz, cfg):
+    w13, w2, slot, _ = oracle_packed_layer(cfg)
+    return pz.PackedMoELayer(torch.from_numpy(w13.view(np.int16)).cuda(),
+                             torch.from_numpy(w2.view(np.int16)).cuda(),
+                             torch.from_numpy(slot).cuda()), (w13, w2, slot)
+
+
+def _run(pz, cfg, T, path, residual=True, skew=0.0, sample=None, seed_shift=0):
+    layer, (w13, w2, slot) = _layer(pz, cfg)
+    hb = synth.hidden_bits(cfg, T, seed=synth.seeds(cfg)["activations"] + seed_shift)
+    lg = synth.router_logits(cfg, T, seed=synth.seeds(cfg)["logits"] + seed_shift, skew=skew)
+    rb = synth.hidden_bits(cfg, T, seed=synth.seeds(cfg)["activations"] + 1000 + seed_shift) if residual else None
+    h_dev = torch.from_numpy(hb.view(np.int16)).cuda().view(torch.bfloat16)
+    l_dev = torch.from_numpy(lg).cuda()
+    r_dev = torch.from_numpy(rb.view(np.int16)).cuda().view(torch.bfloat16) if residual else None
+    out = layer.forward(h_dev, l_dev, cfg.top_k, cfg.renormalize, residual=r_dev, path=path)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    rows = np.arange(T) if sample is None else np.sort(np.random.default_rng(7).choice(T, sample, replace=False))
+    ref = oracle.moe_forward(w13, w2, slot, hb[rows], lg[rows], cfg.top_k, cfg.renormalize,
+                             None if rb is None else rb[rows])
+    return got[rows], ref
+
+
+SMALL = [
+    synth.CONFIGS["tiny"],
+    synth.MoEConfig("small_mix", 5, 256, 512, 8, 2, True),       # several row blocks, split-K
+    synth.MoEConfig("small_fine", 6, 128, 192, 16, 4, False),    # d_ff = 3 x 64 (ragged row blocks)
+    synth.MoEConfig("small_k6", 7, 192, 320, 12, 6, False),
+]
+
+
+@pytest.mark.parametrize("cfg", SMALL, ids=lambda c: c.name)
+@pytest.mark.parametrize("T", [1, 3, 8, 17, 64, 70])
+def test_forward_gemv_small(pz, cfg, T):
+    got, ref = _run(pz, cfg, T, pz.PATH_GEMV)
+    assert_close(got, ref, f"{cfg.name} T={T}")
+
+
+def test_tiny_config_exact_shape(pz):
+    cfg = synth.CONFIGS["tiny"]
+    got, ref = _run(pz, cfg, 8, pz.PATH_AUTO, residual=False)
+    assert_close(got, ref, "tiny")
+
+
+def test_skewed_routing_all_tokens_one_pair(pz):
+    """Every token routed to the same pair (>64 tokens per position: multiple passes)."""
+    cfg = synth.MoEConfig("skew", 8, 128, 256, 8, 2, True)
+    got, ref = _run(pz, cfg, 150, pz.PATH_GEMV, skew=50.0)
+    assert_close(got, ref, "skew")
+
+
+def test_route_outputs(pz):
+    cfg = synth.MoEConfig("route", 9, 64, 64, 64, 6, False)
+    layer, (w13, w2, slot) = _layer(pz, cfg)
+    T = 300
+    lg = synth.router_logits(cfg, T)
+    lg[5, 10] = lg[5, 11] = lg[5].max() + 1.0  # an exact tie -> lower index first
+    idx, gate, off, tok, aof = layer.route(torch.from_numpy(lg).cuda(), cfg.top_k, cfg.renormalize)
+    want_idx, want_gate = oracle.route(lg, cfg.top_k, cfg.renormalize)
+    assert np.array_equal(idx.cpu().numpy(), want_idx)
+    np.testing.assert_allclose(gate.cpu().numpy(), want_gate, rtol=2e-6, atol=1e-7)
+    off = off.cpu().numpy()
+    tok = tok.cpu().numpy()
+    aof = aof.cpu().numpy()
+    buckets = slot[want_idx.reshape(-1)]
+    counts = np.bincount(buckets, minlength=2 * cfg.n_pairs)
+    assert np.array_equal(np.diff(off), counts) and off[0] == 0
+    # assignment (t, j) lands inside its bucket and points back at its token
+    for i, a in enumerate(aof):
+        b = buckets[i]
+        assert off[b] <= a < off[b + 1] and tok[a] == i // cfg.top_k
+    assert len(set(aof.tolist())) == T * cfg.top_k
+
+
+@pytest.mark.parametrize("name", ["qwen15", "deepseek"])
+@pytest.mark.parametrize("T", [1, 16, 64])
+def test_forward_full_size_fine_grained(pz, name, T):
+    cfg = synth.CONFIGS[name]
+    got, ref = _run(pz, cfg, T, pz.PATH_AUTO, sample=min(T, 16))
+    assert_close(got, ref, f"{name} T={T}")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("T", [1, 16, 64])
+def test_forward_full_size_mixtral(pz, T):
+    cfg = synth.CONFIGS["mixtral"]
+    got, ref = _run(pz, cfg, T, pz.PATH_AUTO, sample=min(T, 6))
+    assert_close(got, ref, f"mixtral T={T}")
+
+
+def test_experts_and_combine_building_blocks(pz):
+    """route -> gather -> experts -> combine reproduces forward (the EP decomposition)."""
+    cfg = SMALL[1]
+    layer, (w13, w2, slot) = _layer(pz, cfg)
+    T = 40
+    hb = torch.from_numpy(synth.hidden_bits(cfg, T).view(np.int16)).cuda().view(torch.bfloat16)
+    lg = torch.from_numpy(synth.router_logits(cfg, T)).cuda()
+    full = layer.forward(hb, lg, cfg.top_k, cfg.renormalize)
+    idx, gate, off, tok, aof = layer.route(lg, cfg.top_k, cfg.renormalize)
+    x_rows = pz.gather_rows(hb, tok)
+    y = layer.experts(x_rows, off)
+    out = pz.moe_combine(y, aof, gate)
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)
