@@ -43,6 +43,10 @@ FALLBACK_HBM_GBS = 6650.0     # B200_PROFILING.md fallback (only if MEASURED_PEA
 FALLBACK_BF16_TFLOPS = 1590.0
 
 
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
 def peaks() -> dict:
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -69,14 +73,17 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             import torch
-            bus = torch.cuda.get_device_properties(device_index).pci_bus_id if hasattr(
-                torch.cuda.get_device_properties(device_index), "pci_bus_id") else None
-            if bus:
-                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode() if isinstance(bus, str) else bus)
-            else:
-                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-                idx = int(vis.split(",")[device_index]) if vis and vis.split(",")[0].isdigit() else device_index
-                self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            want = str(getattr(torch.cuda.get_device_properties(device_index), "uuid", "")).lower()
+            self.h = None
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                u = pynvml.nvmlDeviceGetUUID(h)
+                u = (u.decode() if isinstance(u, bytes) else u).lower()
+                if want and want in u:
+                    self.h = h
+                    break
+            if self.h is None:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
             self.nvml = pynvml
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
@@ -349,7 +356,9 @@ def run_ours(args):
     cfg = synth.CONFIGS[args.config]
     T, K, W = args.batch, args.steps, args.warmup
     seed = synth.seeds(cfg)["weights"]
+    log("building layer", cfg.name)
     layer, pack_stats = build_layer_gpu(pz, cfg, seed, device)
+    log("layer built", layer.packed_bytes)
     hidden, logits = make_inputs(cfg, T, seed + 100 * rank + 2, device)
     out = torch.empty_like(hidden)
     ws = layer.workspace(T, cfg.top_k)
@@ -358,7 +367,9 @@ def run_ours(args):
     def step():
         layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
 
+    log("workspace", ws.numel())
     n_touched = touched_pairs(layer, logits, cfg)
+    log("touched pairs", n_touched)
     ab = algorithmic_bytes(cfg, n_touched, T)
     big = ab["w13"] + ab["w2"] > 4 * l2_bytes(device)
     flush_buf = None if big else torch.empty(2 * l2_bytes(device), dtype=torch.uint8, device=device)
@@ -367,6 +378,7 @@ def run_ours(args):
     for _ in range(W):
         step()
     torch.cuda.synchronize()
+    log("warmup done")
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.1)
@@ -383,6 +395,7 @@ def run_ours(args):
     time.sleep(0.05)
     clocks.stop()
     ms = total_ms / K
+    log("timed", ms, prof.kernels)
     if world > 1:
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -427,6 +440,7 @@ def run_ours(args):
         t = torch.tensor([e2e_ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
+    log("e2e", e2e_ms)
     e2e = {"value": T * world / (e2e_ms / 1e3), "unit": "tokens/s",
            "h2d_bytes_per_step": h_host.numel() * 2 + l_host.numel() * 4, "d2h_bytes_per_step": o_host.numel() * 2,
            "ms_per_step": e2e_ms, "api": "PackedMoELayer.forward -> puzzle_moe_forward_ex (host pinned buffers)"}

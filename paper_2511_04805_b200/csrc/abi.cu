@@ -25,6 +25,9 @@ int launch_combine(const float*, const int32_t*, const float*, int64_t, int, int
                    uint16_t*, cudaStream_t);
 int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16_t*, cudaStream_t);
 int gemv_nt_for(int64_t T);
+bool tc_supported(int d, int f);
+int launch_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
+                      uint16_t*, float*, cudaStream_t);
 void gemv_splits(int d, int f, int max_active, int* ks13, int* ks2);
 int launch_gemv_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*,
                         const int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int64_t,
@@ -124,21 +127,31 @@ int check_layer(const puzzle_moe_layer* L) {
 struct Plan {
   int64_t T = 0, n_assign = 0;
   int k = 0, max_active = 0, nt = 1, ks13 = 1, ks2 = 1;
+  int path = PUZZLE_PATH_GEMV;  // resolved (never AUTO)
 };
+
+// Decode shapes (<= 64 tokens) stream each touched pair once through the register-decode
+// GEMV; larger token counts are tensor-bound and go to the tcgen05 grouped GEMM.
+constexpr int64_t kGemvMaxTokens = 64;
 
 struct Layout {
   size_t topk_idx, topk_gate, bucket_off, assign_token, assign_of, active, n_active, cnt13, cnt2, h, y,
-      part13, part2, total;
+      part13, part2, x_perm, total;
 };
 
-Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k) {
+Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   Plan p;
   p.T = T;
   p.k = k;
   p.n_assign = T * k;
   p.max_active = (int)std::min<int64_t>(L->n_pairs, p.n_assign);
-  p.nt = gemv_nt_for(T);
-  gemv_splits(L->d_model, L->d_ff, std::max(p.max_active, 1), &p.ks13, &p.ks2);
+  if (path == PUZZLE_PATH_AUTO)
+    path = (T > kGemvMaxTokens && tc_supported(L->d_model, L->d_ff)) ? PUZZLE_PATH_TC : PUZZLE_PATH_GEMV;
+  p.path = path;
+  if (path == PUZZLE_PATH_GEMV) {
+    p.nt = gemv_nt_for(T);
+    gemv_splits(L->d_model, L->d_ff, std::max(p.max_active, 1), &p.ks13, &p.ks2);
+  }
   return p;
 }
 
@@ -164,17 +177,22 @@ Layout make_layout(const puzzle_moe_layer* L, const Plan& p) {
   o.y = take(na * d * 4);
   o.part13 = take(p.ks13 > 1 ? (size_t)p.ks13 * na * 2 * f * 4 : 0);
   o.part2 = take(p.ks2 > 1 ? (size_t)p.ks2 * na * d * 4 : 0);
+  o.x_perm = take(p.path == PUZZLE_PATH_TC ? na * d * 2 : 0);
   o.total = off;
   return o;
 }
 
 size_t workspace_for(const puzzle_moe_layer* L, int64_t max_tokens, int k) {
-  // the split factors depend on min(P, T*k); take the max over every distinct plan
+  // The GEMV split factors depend on min(P, T*k); take the max over every distinct plan of
+  // either path for any T <= max_tokens.
   size_t best = 0;
   int64_t knee = (L->n_pairs + k - 1) / k;
-  for (int64_t t = 1; t <= std::min<int64_t>(max_tokens, knee); ++t)
-    best = std::max(best, make_layout(L, make_plan(L, t, k)).total);
-  if (max_tokens > 0) best = std::max(best, make_layout(L, make_plan(L, max_tokens, k)).total);
+  for (int path : {(int)PUZZLE_PATH_GEMV, (int)PUZZLE_PATH_TC}) {
+    if (path == PUZZLE_PATH_TC && !tc_supported(L->d_model, L->d_ff)) continue;
+    for (int64_t t = 1; t <= std::min<int64_t>(max_tokens, knee); ++t)
+      best = std::max(best, make_layout(L, make_plan(L, t, k, path)).total);
+    if (max_tokens > 0) best = std::max(best, make_layout(L, make_plan(L, max_tokens, k, path)).total);
+  }
   return best;
 }
 
@@ -289,9 +307,17 @@ size_t puzzle_moe_experts_workspace_size(const puzzle_moe_layer* L, int64_t n_as
 
 static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout& lay, void* ws,
                        const uint16_t* x, const int32_t* row_index, const int32_t* bucket_off,
-                       const int32_t* active, const int32_t* n_active, float* y, int path,
-                       cudaStream_t s) {
-  (void)path;
+                       const int32_t* active, const int32_t* n_active, float* y, cudaStream_t s) {
+  if (plan.path == PUZZLE_PATH_TC) {
+    const uint16_t* rows = x;
+    if (row_index) {  // token permutation into bucket order for the TMA-fed GEMM
+      int rc = launch_gather_rows(x, row_index, plan.n_assign, L->d_model, at<uint16_t>(ws, lay.x_perm), s);
+      if (rc) return rc;
+      rows = at<uint16_t>(ws, lay.x_perm);
+    }
+    return launch_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
+                             at<uint16_t>(ws, lay.h), y, s);
+  }
   return launch_gemv_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, x, row_index, bucket_off,
                              active, n_active, plan.max_active, plan.n_assign, plan.nt, plan.ks13,
                              plan.ks2, at<float>(ws, lay.part13), at<float>(ws, lay.part2),
@@ -312,7 +338,9 @@ int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, con
   if (!al16(hidden) || !al16(out) || (residual && !al16(residual)))
     return fail(PUZZLE_ERR_UNSUPPORTED, "activations must be 16-byte aligned");
   if (int rc = check_device()) return rc;
-  const Plan plan = make_plan(L, T, k);
+  if (path == PUZZLE_PATH_TC && !tc_supported(L->d_model, L->d_ff))
+    return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d_model % 256 == 0 and d_ff % 128 == 0");
+  const Plan plan = make_plan(L, T, k, path);
   const Layout lay = make_layout(L, plan);
   if (!ws || ws_bytes < lay.total)
     return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_moe_workspace_size(L, T, top_k)");
@@ -326,7 +354,7 @@ int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, con
   if (rc) return rc;
   rc = run_experts(L, plan, lay, ws, hidden, at<int32_t>(ws, lay.assign_token),
                    at<int32_t>(ws, lay.bucket_off), at<int32_t>(ws, lay.active),
-                   at<int32_t>(ws, lay.n_active), at<float>(ws, lay.y), path, s);
+                   at<int32_t>(ws, lay.n_active), at<float>(ws, lay.y), s);
   if (rc) return rc;
   return launch_combine(at<float>(ws, lay.y), at<int32_t>(ws, lay.assign_of), at<float>(ws, lay.topk_gate),
                         T, k, L->d_model, residual, out, s);
@@ -361,9 +389,12 @@ int puzzle_moe_experts(const puzzle_moe_layer* L, const uint16_t* x_rows, const 
   if (!x_rows || !bucket_off || !y_rows) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (!al16(x_rows) || !al16(y_rows)) return fail(PUZZLE_ERR_UNSUPPORTED, "rows must be 16-byte aligned");
   if (int rc = check_device()) return rc;
+  if (path < PUZZLE_PATH_AUTO || path > PUZZLE_PATH_TC) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad path");
+  if (path == PUZZLE_PATH_TC && !tc_supported(L->d_model, L->d_ff))
+    return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d_model % 256 == 0 and d_ff % 128 == 0");
   // Every pair may be touched: plan with T = n_assign, k = 1 (max_active = min(P, n_assign)).
-  Plan plan = make_plan(L, n_assign, 1);
-  plan.nt = gemv_nt_for(std::min<int64_t>(n_assign, 64));
+  Plan plan = make_plan(L, n_assign, 1, path);
+  if (plan.path == PUZZLE_PATH_GEMV) plan.nt = gemv_nt_for(std::min<int64_t>(n_assign, 64));
   const Layout lay = make_layout(L, plan);
   if (!ws || ws_bytes < lay.total) return fail(PUZZLE_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
@@ -374,7 +405,7 @@ int puzzle_moe_experts(const puzzle_moe_layer* L, const uint16_t* x_rows, const 
   if (rc) return rc;
   plan.max_active = L->n_pairs;
   return run_experts(L, plan, lay, ws, x_rows, nullptr, bucket_off, at<int32_t>(ws, lay.active),
-                     at<int32_t>(ws, lay.n_active), y_rows, path, s);
+                     at<int32_t>(ws, lay.n_active), y_rows, s);
 }
 
 int puzzle_moe_combine(const float* y, const int32_t* assign_of, const float* gate, int64_t T, int k,

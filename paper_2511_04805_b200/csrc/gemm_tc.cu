@@ -1,0 +1,333 @@
+// Prefill-shape expert kernels (a4)+(a5) on the 5th-generation tensor cores.
+//
+// Grouped GEMM over the 2P (pair, pos) buckets: D[tokens, n] = X_b[tokens, K] . W^_b[n, K]^T
+// with W^_b = Algorithm-1 decode of the pair's packed words for position pos.
+// One persistent CTA per SM walks a static tile list (n-block major, so the CTAs running at
+// the same time share the packed weight tiles in L2; both positions of a pair follow each
+// other so one packed tile serves both experts).
+//
+// Per CTA tile: 256 tokens (two M=128 UMMAs into two TMEM accumulators of 256 fp32
+// columns each = all 512 TMEM columns) x 256 output rows, K in 64-wide stages:
+//   warp 0      TMA producer: X tile [256 x 64] bf16 and the PACKED weight tile [256 x 64]
+//               u16, both 128-byte swizzled, completing on full[s]
+//   warps 2..5  decode warpgroup: Alg. 1 in place on the packed tile (elementwise, so the
+//               swizzled layout is preserved), fence.proxy.async, arrive on dec[s];
+//               after the last k-block of a tile they are the epilogue (TMEM -> registers
+//               -> SwiGLU / fp32 -> global)
+//   warp 1      MMA issuer: one elected lane issues tcgen05.mma (A, B from SMEM
+//               descriptors, D in TMEM), tcgen05.commit frees the stage (empty[s]) and,
+//               after the last k-block, signals tmem_full.
+// w13 variant: the B tile is 128 gate rows + the same 128 up rows (N = 256) so the
+// epilogue sees g and u of one d_ff index in one thread: h = silu(g) * u -> bf16.
+// w2 variant: B = 256 rows of W2 (N = 256 d_model rows), epilogue writes fp32 y.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace pz {
+
+namespace {
+
+constexpr int BM = 256;  // tokens per tile (2 x UMMA M=128)
+constexpr int BN = 256;  // output rows per tile (UMMA N=256)
+constexpr int BK = 64;   // K per stage (= one 128-byte swizzle row of bf16)
+constexpr int kStages = 3;
+constexpr int kABytes = BM * BK * 2;  // 32 KB
+constexpr int kBBytes = BN * BK * 2;  // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 192;         // 6 warps
+constexpr int kDecodeWarps = 4;
+constexpr uint32_t kTmemCols = 512;
+constexpr int kMaxBuckets = 2 * 256;
+
+struct alignas(8) SmemCtl {
+  uint64_t full[kStages];
+  uint64_t dec[kStages];
+  uint64_t empty[kStages];
+  uint64_t tmem_full;
+  uint64_t tmem_empty;
+  uint32_t tmem_base;
+  int32_t n_buckets;
+  int32_t bucket_off[kMaxBuckets + 1];
+  int32_t tile_off[kMaxBuckets + 1];
+};
+
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + sizeof(SmemCtl);
+
+struct TileInfo {
+  int bucket, m_tile, n_block, row0, valid;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const SmemCtl& c, int tile, int mt_total) {
+  TileInfo t;
+  t.n_block = tile / mt_total;
+  const int rem = tile - t.n_block * mt_total;
+  int lo = 0, hi = c.n_buckets - 1;  // last b with tile_off[b] <= rem
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (c.tile_off[mid] <= rem) lo = mid; else hi = mid - 1;
+  }
+  t.bucket = lo;
+  t.m_tile = rem - c.tile_off[lo];
+  t.row0 = c.bucket_off[lo] + t.m_tile * BM;
+  t.valid = min(BM, c.bucket_off[lo + 1] - t.row0);
+  return t;
+}
+
+template <int POS>
+__device__ __forceinline__ void decode_tile(uint8_t* b_tile, int tid) {
+  uint4* p = reinterpret_cast<uint4*>(b_tile);
+#pragma unroll 4
+  for (int i = tid; i < kBBytes / 16; i += kDecodeWarps * 32) {
+    uint4 v = p[i];
+    v.x = decode2<POS>(v.x);
+    v.y = decode2<POS>(v.y);
+    v.z = decode2<POS>(v.z);
+    v.w = decode2<POS>(v.w);
+    p[i] = v;
+  }
+}
+
+template <bool kW13>
+__global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
+    const __grid_constant__ CUtensorMap tmap_a,  // X rows (w13) or h rows (w2): [n_rows][K] bf16
+    const __grid_constant__ CUtensorMap tmap_b,  // packed w13 [P*2*f][d] or w2 [P*d][f] u16
+    const int32_t* __restrict__ bucket_off, int n_buckets, int K, int f, int d, int n_blocks,
+    uint16_t* __restrict__ h_out,  // w13: [n_assign][f] bf16
+    float* __restrict__ y_out) {   // w2:  [n_assign][d] f32
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  SmemCtl& c = *reinterpret_cast<SmemCtl*>(smem + (size_t)kStages * kStageBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- setup: bucket / tile offsets, barriers, TMEM ----
+  for (int i = threadIdx.x; i <= n_buckets; i += blockDim.x) c.bucket_off[i] = bucket_off[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    c.n_buckets = n_buckets;
+    int run = 0;
+    for (int b = 0; b < n_buckets; ++b) {
+      c.tile_off[b] = run;
+      run += (c.bucket_off[b + 1] - c.bucket_off[b] + BM - 1) / BM;
+    }
+    c.tile_off[n_buckets] = run;
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&c.full[s], 1);
+      ptx::mbar_init(&c.dec[s], kDecodeWarps);
+      ptx::mbar_init(&c.empty[s], 1);
+    }
+    ptx::mbar_init(&c.tmem_full, 1);
+    ptx::mbar_init(&c.tmem_empty, kDecodeWarps);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmap_a);
+    ptx::tma_prefetch_desc(&tmap_b);
+  }
+  if (warp == 1) ptx::tmem_alloc<kTmemCols>(&c.tmem_base);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = c.tmem_base;
+  const int mt_total = c.tile_off[n_buckets];
+  const int n_tiles = mt_total * n_blocks;
+  const int nk = K / BK;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const TileInfo t = tile_info(c, tile, mt_total);
+        const int pair = t.bucket >> 1;
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait(&c.empty[stage], phase ^ 1);
+          uint8_t* sa = smem + (size_t)stage * kStageBytes;
+          uint8_t* sb = sa + kABytes;
+          ptx::mbar_arrive_expect_tx(&c.full[stage], kStageBytes);
+          ptx::tma_load_2d(sa, &tmap_a, &c.full[stage], kb * BK, t.row0);
+          if (kW13) {
+            const int gate_row = pair * 2 * f + t.n_block * (BN / 2);
+            ptx::tma_load_2d(sb, &tmap_b, &c.full[stage], kb * BK, gate_row);
+            ptx::tma_load_2d(sb + kBBytes / 2, &tmap_b, &c.full[stage], kb * BK, gate_row + f);
+          } else {
+            ptx::tma_load_2d(sb, &tmap_b, &c.full[stage], kb * BK, pair * d + t.n_block * BN);
+          }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, BN);
+    int stage = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const TileInfo t = tile_info(c, tile, mt_total);
+      const bool two = t.valid > 128;
+      ptx::mbar_wait(&c.tmem_empty, acc_phase ^ 1);
+      ptx::tc_fence_after();
+      for (int kb = 0; kb < nk; ++kb) {
+        ptx::mbar_wait(&c.dec[stage], phase);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = ptx::smem_u32(smem + (size_t)stage * kStageBytes);
+          const uint32_t sb = sa + kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t db = ptx::smem_desc_sw128(sb + k * 32);
+            const uint32_t acc = (kb | k) != 0;
+            ptx::mma_bf16_ss(tmem, ptx::smem_desc_sw128(sa + k * 32), db, idesc, acc);
+            if (two) ptx::mma_bf16_ss(tmem + 256, ptx::smem_desc_sw128(sa + kABytes / 2 + k * 32), db, idesc, acc);
+          }
+          ptx::mma_commit(&c.empty[stage]);
+          if (kb == nk - 1) ptx::mma_commit(&c.tmem_full);
+        }
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+      acc_phase ^= 1;
+    }
+  } else {
+    // ===================== decode warpgroup + epilogue =====================
+    const int tid = threadIdx.x - 64;  // 0..127
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    int stage = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const TileInfo t = tile_info(c, tile, mt_total);
+      const int pos = t.bucket & 1;
+      for (int kb = 0; kb < nk; ++kb) {
+        ptx::mbar_wait(&c.full[stage], phase);
+        uint8_t* sb = smem + (size_t)stage * kStageBytes + kABytes;
+        if (pos == 0) decode_tile<0>(sb, tid); else decode_tile<1>(sb, tid);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&c.dec[stage]);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+      // ---- epilogue ----
+      ptx::mbar_wait(&c.tmem_full, acc_phase);
+      ptx::tc_fence_after();
+      for (int half = 0; half < 2; ++half) {
+        const int m = half * 128 + q * 32 + lane;  // token row within the tile
+        if (half == 1 && t.valid <= 128) break;
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + half * 256;
+        const bool ok = m < t.valid;
+        const int64_t a = t.row0 + m;
+        if (kW13) {
+          for (int j = 0; j < 128; j += 32) {
+            uint32_t g[32], u[32];
+            ptx::tmem_ld_32x32b_x32(tbase + j, g);
+            ptx::tmem_ld_32x32b_x32(tbase + 128 + j, u);
+            ptx::tmem_ld_wait();
+            if (ok) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
+                const float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
+                pk[i] = f32_to_bf16_rne_bits(h0) | (f32_to_bf16_rne_bits(h1) << 16);
+              }
+              uint4* dst = reinterpret_cast<uint4*>(h_out + a * f + t.n_block * (BN / 2) + j);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            }
+          }
+        } else {
+          for (int j = 0; j < BN; j += 32) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(tbase + j, v);
+            ptx::tmem_ld_wait();
+            if (ok) {
+              uint4* dst = reinterpret_cast<uint4*>(y_out + a * d + t.n_block * BN + j);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&c.tmem_empty);
+      acc_phase ^= 1;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+}
+
+// ---------------------------------------------------------------- host: tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D row-major [rows][cols] 16-bit tensor, box [box_rows][64], 128-byte swizzle.
+int make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(PUZZLE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PUZZLE_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return PUZZLE_OK;
+}
+
+}  // namespace
+
+bool tc_supported(int d, int f) { return d % BN == 0 && f % (BN / 2) == 0 && d % BK == 0 && f % BK == 0; }
+
+// x_rows: [n_rows_cap][d] bf16 grouped by bucket; h: [n_rows_cap][f]; y: [n_rows_cap][d]
+int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f, const uint16_t* x_rows,
+                      const int32_t* bucket_off, int64_t n_rows_cap, uint16_t* h, float* y, cudaStream_t stream) {
+  if (!tc_supported(d, f)) return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d % 256 == 0 and d_ff % 128 == 0");
+  if (n_rows_cap == 0) return PUZZLE_OK;
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    cudaFuncSetAttribute(k_tc_experts<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaFuncSetAttribute(k_tc_experts<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  });
+  CUtensorMap ta13, tb13, ta2, tb2;
+  int rc;
+  if ((rc = make_tmap(&ta13, x_rows, n_rows_cap, d, BM))) return rc;
+  if ((rc = make_tmap(&tb13, w13, (int64_t)n_pairs * 2 * f, d, BN / 2))) return rc;
+  if ((rc = make_tmap(&ta2, h, n_rows_cap, f, BM))) return rc;
+  if ((rc = make_tmap(&tb2, w2, (int64_t)n_pairs * d, f, BN))) return rc;
+  const int grid = num_sms();
+  {
+    ProfScope _ps("w13_tc", stream);
+    k_tc_experts<true><<<grid, kThreads, kSmemBytes, stream>>>(ta13, tb13, bucket_off, 2 * n_pairs, d, f, d,
+                                                               f / (BN / 2), h, nullptr);
+  }
+  if ((rc = cuda_check(cudaGetLastError(), "w13_tc launch"))) return rc;
+  {
+    ProfScope _ps("w2_tc", stream);
+    k_tc_experts<false><<<grid, kThreads, kSmemBytes, stream>>>(ta2, tb2, bucket_off, 2 * n_pairs, f, f, d,
+                                                                d / BN, nullptr, y);
+  }
+  return cuda_check(cudaGetLastError(), "w2_tc launch");
+}
+
+}  // namespace pz

@@ -1,0 +1,9 @@
+#!/bin/bash
+# first GPU pass: smoke, gpu tests (fast), bench
+set -x
+cd $GRAFT_REPO_ROOT
+nproc > gpurun_out/nproc.txt
+nvidia-smi > gpurun_out/nvidia_smi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 100 --warmup 5 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log

@@ -123,3 +123,49 @@ def test_experts_and_combine_building_blocks(pz):
     out = pz.moe_combine(y, aof, gate)
     torch.cuda.synchronize()
     assert torch.equal(out, full)
+
+
+TC_SMALL = [
+    synth.MoEConfig("tc_small", 10, 256, 256, 8, 2, True),
+    synth.MoEConfig("tc_fine", 11, 512, 384, 16, 4, False),   # d_ff = 3 x 128: ragged n-blocks
+]
+
+
+@pytest.mark.parametrize("cfg", TC_SMALL, ids=lambda c: c.name)
+@pytest.mark.parametrize("T", [1, 5, 64, 130, 300])
+def test_forward_tc_small(pz, cfg, T):
+    got, ref = _run(pz, cfg, T, pz.PATH_TC)
+    assert_close(got, ref, f"tc {cfg.name} T={T}")
+
+
+def test_forward_tc_skewed_multi_mtile(pz):
+    """>256 tokens in one bucket: several 256-row M tiles, partial last tile with <=128 rows."""
+    cfg = synth.MoEConfig("tc_skew", 12, 256, 256, 8, 2, True)
+    got, ref = _run(pz, cfg, 700, pz.PATH_TC, skew=50.0, sample=64)
+    assert_close(got, ref, "tc skew")
+
+
+def test_tc_matches_gemv_path(pz):
+    cfg = TC_SMALL[0]
+    layer, _ = _layer(pz, cfg)
+    T = 96
+    hb = torch.from_numpy(synth.hidden_bits(cfg, T).view(np.int16)).cuda().view(torch.bfloat16)
+    lg = torch.from_numpy(synth.router_logits(cfg, T)).cuda()
+    a = layer.forward(hb, lg, cfg.top_k, cfg.renormalize, path=pz.PATH_TC).float()
+    b = layer.forward(hb, lg, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV).float()
+    torch.cuda.synchronize()
+    assert (a - b).abs().max().item() <= 2e-2
+
+
+@pytest.mark.parametrize("name,T", [("qwen15", 512), ("deepseek", 256)])
+def test_forward_tc_full_size_fine_grained(pz, name, T):
+    cfg = synth.CONFIGS[name]
+    got, ref = _run(pz, cfg, T, pz.PATH_TC, sample=16)
+    assert_close(got, ref, f"tc {name} T={T}")
+
+
+@pytest.mark.slow
+def test_forward_tc_full_size_mixtral_prefill(pz):
+    cfg = synth.CONFIGS["mixtral"]
+    got, ref = _run(pz, cfg, 4096, pz.PATH_AUTO, sample=4)
+    assert_close(got, ref, "mixtral prefill T=4096")
