@@ -29,10 +29,9 @@ bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
                       uint16_t*, float*, cudaStream_t);
 void gemv_splits(int d, int f, int max_active, int* ks13, int* ks2);
-int launch_gemv_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*,
-                        const int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int64_t,
-                        int, int, int, float*, float*, int32_t*, int32_t*, uint16_t*, float*,
-                        cudaStream_t);
+int launch_gemv_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*,
+                        const int32_t*, const int32_t*, int, int64_t, int, int, int, float*, float*, int32_t*,
+                        int32_t*, int32_t*, uint16_t*, float*, cudaStream_t);
 
 namespace {
 thread_local std::string g_last_error;
@@ -172,12 +171,12 @@ Layout make_layout(const puzzle_moe_layer* L, const Plan& p) {
   o.active = take(P * 4);
   o.n_active = take(4);
   o.cnt13 = take(P * (f / 64) * 4);
-  o.cnt2 = take(P * (d / 64) * 4);
+  o.cnt2 = take(P * (d / 64) * 4 + 2 * 4);  // + the two dynamic-scheduler work counters
   o.h = take(na * f * 2);
   o.y = take(na * d * 4);
   o.part13 = take(p.ks13 > 1 ? (size_t)p.ks13 * na * 2 * f * 4 : 0);
   o.part2 = take(p.ks2 > 1 ? (size_t)p.ks2 * na * d * 4 : 0);
-  o.x_perm = take(p.path == PUZZLE_PATH_TC ? na * d * 2 : 0);
+  o.x_perm = take(na * d * 2);
   o.total = off;
   return o;
 }
@@ -308,21 +307,21 @@ size_t puzzle_moe_experts_workspace_size(const puzzle_moe_layer* L, int64_t n_as
 static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout& lay, void* ws,
                        const uint16_t* x, const int32_t* row_index, const int32_t* bucket_off,
                        const int32_t* active, const int32_t* n_active, float* y, cudaStream_t s) {
-  if (plan.path == PUZZLE_PATH_TC) {
-    const uint16_t* rows = x;
-    if (row_index) {  // token permutation into bucket order for the TMA-fed GEMM
-      int rc = launch_gather_rows(x, row_index, plan.n_assign, L->d_model, at<uint16_t>(ws, lay.x_perm), s);
-      if (rc) return rc;
-      rows = at<uint16_t>(ws, lay.x_perm);
-    }
+  const uint16_t* rows = x;
+  if (row_index) {  // token permutation into bucket order: both paths read rows by TMA
+    int rc = launch_gather_rows(x, row_index, plan.n_assign, L->d_model, at<uint16_t>(ws, lay.x_perm), s);
+    if (rc) return rc;
+    rows = at<uint16_t>(ws, lay.x_perm);
+  }
+  if (plan.path == PUZZLE_PATH_TC)
     return launch_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, s);
-  }
-  return launch_gemv_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, x, row_index, bucket_off,
+  return launch_gemv_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off,
                              active, n_active, plan.max_active, plan.n_assign, plan.nt, plan.ks13,
                              plan.ks2, at<float>(ws, lay.part13), at<float>(ws, lay.part2),
                              at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2),
-                             at<uint16_t>(ws, lay.h), y, s);
+                             at<int32_t>(ws, lay.cnt2) + L->n_pairs * (L->d_model / 64), at<uint16_t>(ws, lay.h), y,
+                             s);
 }
 
 int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits,

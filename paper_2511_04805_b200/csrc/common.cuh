@@ -79,6 +79,29 @@ __device__ __forceinline__ uint32_t decode2(uint32_t w) {
   return decode2<POS>(w, decode_base(w));
 }
 
+// Both positions of one 32-bit register of packed words, arranged so that the SWAR work
+// splits between the ALU pipe (LOP3 / PRMT: 6 ops) and the FMA pipe (IMAD: 4 ops):
+//   b0 = (w & 0x8FFF8FFF) + 0x38003800   sign S_i (bit 15) rides along: no carry leaves a lane
+//   v0 = b0 & msb_mask(w << 2)            mask M_i (bit 13) -> bit 15
+//   b1 = select(0x80008000: w << 1, else b0)   sign S_j (bit 14) -> bit 15
+//   v1 = b1 & msb_mask(w << 3)            mask M_j (bit 12) -> bit 15
+__device__ __forceinline__ uint32_t imul(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t decode_b0(uint32_t w) { return imad(w & 0x8FFF8FFFu, 1u, 0x38003800u); }
+__device__ __forceinline__ uint32_t decode_v0(uint32_t w, uint32_t b0) { return b0 & lane_msb_mask(imul(w, 4u)); }
+__device__ __forceinline__ uint32_t decode_v1(uint32_t w, uint32_t b0) {
+  const uint32_t b1 = (b0 & 0x7FFF7FFFu) | (imul(w, 2u) & 0x80008000u);  // one LOP3
+  return b1 & lane_msb_mask(imul(w, 8u));
+}
+
 // ---- memory helpers ----
 __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
   uint4 r;

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "tmap.cuh"
 
 namespace pz {
 
@@ -262,39 +263,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
   if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
 
-// ---------------------------------------------------------------- host: tensor maps
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
-// 2-D row-major [rows][cols] 16-bit tensor, box [box_rows][64], 128-byte swizzle.
-int make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return fail(PUZZLE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(PUZZLE_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-  return PUZZLE_OK;
-}
-
 }  // namespace
 
 bool tc_supported(int d, int f) { return d % BN == 0 && f % (BN / 2) == 0 && d % BK == 0 && f % BK == 0; }
@@ -311,10 +279,10 @@ int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int 
   });
   CUtensorMap ta13, tb13, ta2, tb2;
   int rc;
-  if ((rc = make_tmap(&ta13, x_rows, n_rows_cap, d, BM))) return rc;
-  if ((rc = make_tmap(&tb13, w13, (int64_t)n_pairs * 2 * f, d, BN / 2))) return rc;
-  if ((rc = make_tmap(&ta2, h, n_rows_cap, f, BM))) return rc;
-  if ((rc = make_tmap(&tb2, w2, (int64_t)n_pairs * d, f, BN))) return rc;
+  if ((rc = make_tmap_2d(&ta13, x_rows, n_rows_cap, d, BM, BK))) return rc;
+  if ((rc = make_tmap_2d(&tb13, w13, (int64_t)n_pairs * 2 * f, d, BN / 2, BK))) return rc;
+  if ((rc = make_tmap_2d(&ta2, h, n_rows_cap, f, BM, BK))) return rc;
+  if ((rc = make_tmap_2d(&tb2, w2, (int64_t)n_pairs * d, f, BN, BK))) return rc;
   const int grid = num_sms();
   {
     ProfScope _ps("w13_tc", stream);

@@ -1,425 +1,414 @@
-// Decode-shape expert kernels (a4)+(a5): the packed weights of each touched pair are
-// streamed from HBM ONCE (128-bit loads, no shared memory), decoded in registers for
-// expert pos 0 and/or pos 1 with the two-lane SWAR form of Algorithm 1, and
-// fed straight into mma.sync m16n8k16 bf16 tensor-core MMAs as the A operand
-// (weights = rows, tokens = columns: "swap-AB" so that 1..64 tokens map onto N = 8 tiles).
+// Decode-shape expert kernels (a4)+(a5), memory-bound: each touched pair's packed words are
+// streamed from HBM ONCE and decoded for expert pos 0 and/or pos 1 (Algorithm 1)
+// in registers, right before mma.sync m16n8k16 bf16 tensor-core MMAs ("swap-AB": weight
+// rows are the M = 16 side, the 1..64 routed tokens the N = 8 side).
 //
-// K-permutation trick: within each 32-wide K sub-chunk, lane (g, tig) loads the 16 bytes
-// at physical k = 8*tig .. 8*tig+7 of rows g and g+8. Physical k 8tig+{0,1}/{2,3} feed
-// MMA#0 fragments a0/a2 (logical k 2tig+{0,1} / 2tig+8+{0,1}); 8tig+{4..7} feed MMA#1. The
-// B fragments (activations) are loaded with the identical permutation, so every dot
-// product sums exactly the same products (in a different order).
+// Warp-specialised, persistent CTAs (one producer warp + 4 consumer warps):
+//   producer  one lane issues TMA (cp.async.bulk.tensor) loads of 64-wide K stages of the
+//             packed weight tile (128 rows: w13 = 64 gate + the same 64 up rows, w2 = 128
+//             d_model rows) and of the tokens' activation rows of both positions into a
+//             4-deep ring of 128-byte-swizzled shared-memory stages (mbarrier full/empty);
+//             bytes in flight cost no registers, so every SM keeps >100 KB of HBM reads
+//             outstanding.
+//   consumers each owns 32 weight rows (two 16-row m-tiles) of the CTA tile; per stage it
+//             reads its fragments from shared memory, SWAR-decodes two words per 32-bit
+//             register, and issues the MMAs for each position that has tokens.
+// K-permutation: inside each 32-wide K sub-chunk, lane (g, tig) takes physical k =
+// 8*tig..8*tig+7 of rows g and g+8; k 8tig+{0..3} feed MMA#0 fragments (a0,a2) and
+// 8tig+{4..7} feed MMA#1. The activation fragments use the identical permutation, so each
+// dot product sums exactly the same products.
+// Work item = (active pair, 64/128-row block, K split); split-K partials are reduced in
+// fixed split order by the last CTA to finish a row block (deterministic).
+#include <algorithm>
+
 #include "common.cuh"
+#include "tc_ptx.cuh"
+#include "tmap.cuh"
 
 namespace pz {
 
 namespace {
 
-constexpr int kWarps = 4;              // warps per CTA
-constexpr int kThreads = kWarps * 32;
-constexpr int kKStep = 64;             // K per main-loop iteration (two 32-wide sub-chunks)
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = 32 * (1 + kConsumerWarps);
+constexpr int kBK = 64;                         // K per stage (128-byte rows)
+constexpr int kRowsPerCta = 128;                // weight rows per CTA tile
+constexpr int kWBytes = kRowsPerCta * kBK * 2;  // 16 KB packed weights per stage
+constexpr int kStages = 4;
+
+template <int NT>
+struct Cfg {
+  static constexpr int kXRows = 8 * NT;             // tokens per position per pass
+  static constexpr int kXBytes = kXRows * kBK * 2;  // per position
+  static constexpr int kStageBytes = kWBytes + 2 * kXBytes;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
+  static_assert(kSmem * 2 <= 227 * 1024, "two CTAs per SM");
+};
 
 struct PairTokens {
   int off0, cnt0, off1, cnt1;
 };
 
-__device__ __forceinline__ PairTokens pair_tokens(const int32_t* bucket_off, int p) {
-  PairTokens r;
-  r.off0 = bucket_off[2 * p];
-  r.off1 = bucket_off[2 * p + 1];
-  r.cnt0 = r.off1 - r.off0;
-  r.cnt1 = bucket_off[2 * p + 2] - r.off1;
-  return r;
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
 }
 
-// Two 16-row m-tiles (gate rows and up rows of the same 16 d_ff indices) per warp.
-// NT = n-tiles (8 tokens each) per expert position per pass.
-template <int NT>
-__global__ void __launch_bounds__(kThreads) k_w13_gemv(
-    const uint16_t* __restrict__ w13, const uint16_t* __restrict__ x,
-    const int32_t* __restrict__ row_index, const int32_t* __restrict__ bucket_off,
-    const int32_t* __restrict__ active_pairs, const int32_t* __restrict__ n_active, int d, int f,
-    int ksplit, int64_t n_assign_cap, float* __restrict__ part, int32_t* __restrict__ counters,
-    uint16_t* __restrict__ h) {
-  const int zslot = blockIdx.z;
-  if (zslot >= *n_active) return;
-  const int p = active_pairs[zslot];
-  const PairTokens pt = pair_tokens(bucket_off, p);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, tig = lane & 3;
-  const int frow_cta = blockIdx.x * (kWarps * 16);
-  const int frow0 = frow_cta + warp * 16;
-  const int kchunk = d / ksplit;
-  const int kbeg = blockIdx.y * kchunk, kend = kbeg + kchunk;
-  const uint16_t* Wg = w13 + ((size_t)p * 2 + 0) * (size_t)f * d + (size_t)(frow0 + g) * d + 8 * tig;
-  const uint16_t* Wu = w13 + ((size_t)p * 2 + 1) * (size_t)f * d + (size_t)(frow0 + g) * d + 8 * tig;
-  const size_t row8 = (size_t)8 * d;
-
-  const int maxcnt = max(pt.cnt0, pt.cnt1);
-  for (int base = 0; base < maxcnt; base += 8 * NT) {
-    const int n0 = min(max(pt.cnt0 - base, 0), 8 * NT);
-    const int n1 = min(max(pt.cnt1 - base, 0), 8 * NT);
-    // activation row pointers for this lane's token (column g of each n-tile)
-    const uint16_t* xp0[NT];
-    const uint16_t* xp1[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      int i0 = min(base + nt * 8 + g, max(pt.cnt0 - 1, 0));
-      int i1 = min(base + nt * 8 + g, max(pt.cnt1 - 1, 0));
-      const int a0 = pt.off0 + i0, a1 = pt.off1 + i1;
-      // rows of empty buckets are never dereferenced (the MMA loop is skipped)
-      const int r0 = pt.cnt0 == 0 ? 0 : (row_index ? row_index[a0] : a0);
-      const int r1 = pt.cnt1 == 0 ? 0 : (row_index ? row_index[a1] : a1);
-      xp0[nt] = x + (size_t)r0 * d + 8 * tig;
-      xp1[nt] = x + (size_t)r1 * d + 8 * tig;
-    }
-    float ag0[NT][4], au0[NT][4], ag1[NT][4], au1[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ag0[nt][q] = au0[nt][q] = ag1[nt][q] = au1[nt][q] = 0.f;
-
-    // software pipeline: weights of iteration k+64 are in flight while k is consumed
-    uint4 wg[2][2], wu[2][2];  // [sub-chunk][row g / row g+8]
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      wg[s][0] = ldg_nc_v4(Wg + kbeg + 32 * s);
-      wg[s][1] = ldg_nc_v4(Wg + row8 + kbeg + 32 * s);
-      wu[s][0] = ldg_nc_v4(Wu + kbeg + 32 * s);
-      wu[s][1] = ldg_nc_v4(Wu + row8 + kbeg + 32 * s);
-    }
-    for (int k0 = kbeg; k0 < kend; k0 += kKStep) {
-      uint4 cg[2][2], cu[2][2];
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          cg[s][r] = wg[s][r];
-          cu[s][r] = wu[s][r];
-        }
-      if (k0 + kKStep < kend) {
-        const int kn = k0 + kKStep;
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          wg[s][0] = ldg_nc_v4(Wg + kn + 32 * s);
-          wg[s][1] = ldg_nc_v4(Wg + row8 + kn + 32 * s);
-          wu[s][0] = ldg_nc_v4(Wu + kn + 32 * s);
-          wu[s][1] = ldg_nc_v4(Wu + row8 + kn + 32 * s);
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int kk = k0 + 32 * s;
-        const uint32_t gl[4] = {cg[s][0].x, cg[s][0].y, cg[s][0].z, cg[s][0].w};
-        const uint32_t gh[4] = {cg[s][1].x, cg[s][1].y, cg[s][1].z, cg[s][1].w};
-        const uint32_t ul[4] = {cu[s][0].x, cu[s][0].y, cu[s][0].z, cu[s][0].w};
-        const uint32_t uh[4] = {cu[s][1].x, cu[s][1].y, cu[s][1].z, cu[s][1].w};
-        uint32_t bgl[4], bgh[4], bul[4], buh[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          bgl[q] = decode_base(gl[q]);
-          bgh[q] = decode_base(gh[q]);
-          bul[q] = decode_base(ul[q]);
-          buh[q] = decode_base(uh[q]);
-        }
-        if (n0 > 0) {
-          // MMA#0 uses words {0,1}; MMA#1 uses words {2,3}
-          const uint32_t g00 = decode2<0>(gl[0], bgl[0]), g01 = decode2<0>(gh[0], bgh[0]);
-          const uint32_t g02 = decode2<0>(gl[1], bgl[1]), g03 = decode2<0>(gh[1], bgh[1]);
-          const uint32_t g10 = decode2<0>(gl[2], bgl[2]), g11 = decode2<0>(gh[2], bgh[2]);
-          const uint32_t g12 = decode2<0>(gl[3], bgl[3]), g13 = decode2<0>(gh[3], bgh[3]);
-          const uint32_t u00 = decode2<0>(ul[0], bul[0]), u01 = decode2<0>(uh[0], buh[0]);
-          const uint32_t u02 = decode2<0>(ul[1], bul[1]), u03 = decode2<0>(uh[1], buh[1]);
-          const uint32_t u10 = decode2<0>(ul[2], bul[2]), u11 = decode2<0>(uh[2], buh[2]);
-          const uint32_t u12 = decode2<0>(ul[3], bul[3]), u13 = decode2<0>(uh[3], buh[3]);
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            if (nt * 8 < n0) {
-              const uint4 xv = ldg_v4(xp0[nt] + kk);
-              mma_bf16_16816(ag0[nt], g00, g01, g02, g03, xv.x, xv.y);
-              mma_bf16_16816(ag0[nt], g10, g11, g12, g13, xv.z, xv.w);
-              mma_bf16_16816(au0[nt], u00, u01, u02, u03, xv.x, xv.y);
-              mma_bf16_16816(au0[nt], u10, u11, u12, u13, xv.z, xv.w);
-            }
-          }
-        }
-        if (n1 > 0) {
-          const uint32_t g00 = decode2<1>(gl[0], bgl[0]), g01 = decode2<1>(gh[0], bgh[0]);
-          const uint32_t g02 = decode2<1>(gl[1], bgl[1]), g03 = decode2<1>(gh[1], bgh[1]);
-          const uint32_t g10 = decode2<1>(gl[2], bgl[2]), g11 = decode2<1>(gh[2], bgh[2]);
-          const uint32_t g12 = decode2<1>(gl[3], bgl[3]), g13 = decode2<1>(gh[3], bgh[3]);
-          const uint32_t u00 = decode2<1>(ul[0], bul[0]), u01 = decode2<1>(uh[0], buh[0]);
-          const uint32_t u02 = decode2<1>(ul[1], bul[1]), u03 = decode2<1>(uh[1], buh[1]);
-          const uint32_t u10 = decode2<1>(ul[2], bul[2]), u11 = decode2<1>(uh[2], buh[2]);
-          const uint32_t u12 = decode2<1>(ul[3], bul[3]), u13 = decode2<1>(uh[3], buh[3]);
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            if (nt * 8 < n1) {
-              const uint4 xv = ldg_v4(xp1[nt] + kk);
-              mma_bf16_16816(ag1[nt], g00, g01, g02, g03, xv.x, xv.y);
-              mma_bf16_16816(ag1[nt], g10, g11, g12, g13, xv.z, xv.w);
-              mma_bf16_16816(au1[nt], u00, u01, u02, u03, xv.x, xv.y);
-              mma_bf16_16816(au1[nt], u10, u11, u12, u13, xv.z, xv.w);
-            }
-          }
-        }
-      }
-    }
-    // ---- epilogue: C fragment c0,c1 = (row g, tokens 2tig, 2tig+1); c2,c3 = row g+8 ----
-    if (ksplit == 1) {
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int tok = nt * 8 + 2 * tig + (q & 1);
-          const int row = frow0 + g + (q >> 1) * 8;
-          if (tok < n0)
-            h[(size_t)(pt.off0 + base + tok) * f + row] = f32_to_bf16_bits_rn(silu_mul(ag0[nt][q], au0[nt][q]));
-          if (tok < n1)
-            h[(size_t)(pt.off1 + base + tok) * f + row] = f32_to_bf16_bits_rn(silu_mul(ag1[nt][q], au1[nt][q]));
-        }
-    } else {
-      float* pk = part + (size_t)blockIdx.y * n_assign_cap * 2 * f;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int tok = nt * 8 + 2 * tig + (q & 1);
-          const int row = frow0 + g + (q >> 1) * 8;
-          if (tok < n0) {
-            float* dst = pk + (size_t)(pt.off0 + base + tok) * 2 * f;
-            dst[row] = ag0[nt][q];
-            dst[f + row] = au0[nt][q];
-          }
-          if (tok < n1) {
-            float* dst = pk + (size_t)(pt.off1 + base + tok) * 2 * f;
-            dst[row] = ag1[nt][q];
-            dst[f + row] = au1[nt][q];
-          }
-        }
-    }
-  }
-  if (ksplit == 1) return;
-  // ---- split-K: the last CTA of this (pair, row block) reduces in fixed split order ----
-  __shared__ int s_last;
-  __threadfence();  // every thread publishes its partial stores before the arrival count
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int idx = p * gridDim.x + blockIdx.x;
-    const int prev = atomicAdd(&counters[idx], 1);
-    s_last = (prev == ksplit - 1);
-    if (s_last) counters[idx] = 0;  // reset for the next call (stream-ordered)
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int nrows = kWarps * 16;
-  const int n_tot = pt.cnt0 + pt.cnt1;  // buckets 2p and 2p+1 are adjacent
-  for (int i = threadIdx.x; i < n_tot * nrows; i += blockDim.x) {
-    const int a = pt.off0 + i / nrows;
-    const int row = frow_cta + i % nrows;
-    float gs = 0.f, us = 0.f;
-    for (int s = 0; s < ksplit; ++s) {
-      const float* src = part + ((size_t)s * n_assign_cap + a) * 2 * f;
-      gs += __ldcg(src + row);
-      us += __ldcg(src + f + row);
-    }
-    h[(size_t)a * f + row] = f32_to_bf16_bits_rn(silu_mul(gs, us));
-  }
+// byte offset of (row, 16-byte chunk) inside a 128-byte-swizzled TMA box with 128-byte rows
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
 }
 
-// Down projection: one 16-row m-tile (d_model rows) per warp, K = d_ff, B = h rows.
-template <int NT>
-__global__ void __launch_bounds__(kThreads) k_w2_gemv(
-    const uint16_t* __restrict__ w2, const uint16_t* __restrict__ h,
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ PairTokens load_pair(const int32_t* bucket_off, int p) {
+  PairTokens pt;
+  pt.off0 = bucket_off[2 * p];
+  pt.off1 = bucket_off[2 * p + 1];
+  pt.cnt0 = pt.off1 - pt.off0;
+  pt.cnt1 = bucket_off[2 * p + 2] - pt.off1;
+  return pt;
+}
+
+// kW13: weights = packed w13 ([P*2f][d]); CTA rows = 64 gate rows + the same 64 up rows.
+// !kW13: weights = packed w2 ([P*d][f]); CTA rows = 128 d_model rows.
+template <int NT, bool kW13>
+__global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
+    const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
     const int32_t* __restrict__ bucket_off, const int32_t* __restrict__ active_pairs,
-    const int32_t* __restrict__ n_active, int d, int f, int ksplit, int64_t n_assign_cap,
-    float* __restrict__ part, int32_t* __restrict__ counters, float* __restrict__ y) {
-  const int zslot = blockIdx.z;
-  if (zslot >= *n_active) return;
-  const int p = active_pairs[zslot];
-  const PairTokens pt = pair_tokens(bucket_off, p);
+    const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb, int ks,
+    int64_t n_assign_cap, float* __restrict__ part, int32_t* __restrict__ counters,
+    int32_t* __restrict__ work_ctr, uint16_t* __restrict__ h_out, float* __restrict__ y_out) {
+  using C = Cfg<NT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * C::kStageBytes);
+  uint64_t* empty = full + kStages;
+  int4* hdr = reinterpret_cast<int4*>(empty + kStages);  // per-stage {item, pass base, kb, 0}
+  int* s_last = reinterpret_cast<int*>(hdr + kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, tig = lane & 3;
-  const int row_cta = blockIdx.x * (kWarps * 16);
-  const int row0 = row_cta + warp * 16;
-  const int kchunk = f / ksplit;
-  const int kbeg = blockIdx.y * kchunk, kend = kbeg + kchunk;
-  const uint16_t* W = w2 + (size_t)p * d * f + (size_t)(row0 + g) * f + 8 * tig;
-  const size_t row8 = (size_t)8 * f;
-
-  const int maxcnt = max(pt.cnt0, pt.cnt1);
-  for (int base = 0; base < maxcnt; base += 8 * NT) {
-    const int n0 = min(max(pt.cnt0 - base, 0), 8 * NT);
-    const int n1 = min(max(pt.cnt1 - base, 0), 8 * NT);
-    const uint16_t* hp0[NT];
-    const uint16_t* hp1[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int i0 = min(base + nt * 8 + g, max(pt.cnt0 - 1, 0));
-      const int i1 = min(base + nt * 8 + g, max(pt.cnt1 - 1, 0));
-      hp0[nt] = h + (size_t)(pt.off0 + i0) * f + 8 * tig;
-      hp1[nt] = h + (size_t)(pt.off1 + i1) * f + 8 * tig;
-    }
-    float a0[NT][4], a1[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) a0[nt][q] = a1[nt][q] = 0.f;
-
-    uint4 w[2][2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      w[s][0] = ldg_nc_v4(W + kbeg + 32 * s);
-      w[s][1] = ldg_nc_v4(W + row8 + kbeg + 32 * s);
-    }
-    for (int k0 = kbeg; k0 < kend; k0 += kKStep) {
-      uint4 c[2][2];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        c[s][0] = w[s][0];
-        c[s][1] = w[s][1];
-      }
-      if (k0 + kKStep < kend) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          w[s][0] = ldg_nc_v4(W + k0 + kKStep + 32 * s);
-          w[s][1] = ldg_nc_v4(W + row8 + k0 + kKStep + 32 * s);
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int kk = k0 + 32 * s;
-        const uint32_t wl[4] = {c[s][0].x, c[s][0].y, c[s][0].z, c[s][0].w};
-        const uint32_t wh[4] = {c[s][1].x, c[s][1].y, c[s][1].z, c[s][1].w};
-        uint32_t bl[4], bh[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          bl[q] = decode_base(wl[q]);
-          bh[q] = decode_base(wh[q]);
-        }
-        if (n0 > 0) {
-          const uint32_t x00 = decode2<0>(wl[0], bl[0]), x01 = decode2<0>(wh[0], bh[0]);
-          const uint32_t x02 = decode2<0>(wl[1], bl[1]), x03 = decode2<0>(wh[1], bh[1]);
-          const uint32_t x10 = decode2<0>(wl[2], bl[2]), x11 = decode2<0>(wh[2], bh[2]);
-          const uint32_t x12 = decode2<0>(wl[3], bl[3]), x13 = decode2<0>(wh[3], bh[3]);
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-            if (nt * 8 < n0) {
-              const uint4 hv = ldg_v4(hp0[nt] + kk);
-              mma_bf16_16816(a0[nt], x00, x01, x02, x03, hv.x, hv.y);
-              mma_bf16_16816(a0[nt], x10, x11, x12, x13, hv.z, hv.w);
-            }
-        }
-        if (n1 > 0) {
-          const uint32_t x00 = decode2<1>(wl[0], bl[0]), x01 = decode2<1>(wh[0], bh[0]);
-          const uint32_t x02 = decode2<1>(wl[1], bl[1]), x03 = decode2<1>(wh[1], bh[1]);
-          const uint32_t x10 = decode2<1>(wl[2], bl[2]), x11 = decode2<1>(wh[2], bh[2]);
-          const uint32_t x12 = decode2<1>(wl[3], bl[3]), x13 = decode2<1>(wh[3], bh[3]);
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-            if (nt * 8 < n1) {
-              const uint4 hv = ldg_v4(hp1[nt] + kk);
-              mma_bf16_16816(a1[nt], x00, x01, x02, x03, hv.x, hv.y);
-              mma_bf16_16816(a1[nt], x10, x11, x12, x13, hv.z, hv.w);
-            }
-        }
-      }
-    }
-    float* dstbase = ksplit == 1 ? y : part + (size_t)blockIdx.y * n_assign_cap * d;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int tok = nt * 8 + 2 * tig + (q & 1);
-        const int row = row0 + g + (q >> 1) * 8;
-        if (tok < n0) dstbase[(size_t)(pt.off0 + base + tok) * d + row] = a0[nt][q];
-        if (tok < n1) dstbase[(size_t)(pt.off1 + base + tok) * d + row] = a1[nt][q];
-      }
-  }
-  if (ksplit == 1) return;
-  __shared__ int s_last;
-  __threadfence();  // every thread publishes its partial stores before the arrival count
-  __syncthreads();
   if (threadIdx.x == 0) {
-    const int idx = p * gridDim.x + blockIdx.x;
-    const int prev = atomicAdd(&counters[idx], 1);
-    s_last = (prev == ksplit - 1);
-    if (s_last) counters[idx] = 0;
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], kConsumerWarps);
+    }
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&tm_w);
+    ptx::tma_prefetch_desc(&tm_x);
   }
   __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int nrows = kWarps * 16;
-  const int n_tot = pt.cnt0 + pt.cnt1;
-  for (int i = threadIdx.x; i < n_tot * nrows; i += blockDim.x) {
-    const int a = pt.off0 + i / nrows;
-    const int row = row_cta + i % nrows;
-    float acc = 0.f;
-    for (int s = 0; s < ksplit; ++s) acc += __ldcg(part + ((size_t)s * n_assign_cap + a) * d + row);
-    y[(size_t)a * d + row] = acc;
+  const int n_active = *n_active_ptr;
+  const int per_pair = n_rb * ks;
+  const int kchunk = K / ks;
+  const int nk = kchunk / kBK;
+
+  if (warp == 0) {
+    // ============================== producer ==============================
+    // Dynamic scheduler: items are claimed with one atomicAdd each, so SMs that run ahead
+    // take more work; every stage carries a header telling the consumers what it holds.
+    if (lane != 0) return;
+    const int n_items = n_active * per_pair;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      const int item = atomicAdd(work_ctr, 1);
+      if (item >= n_items) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        hdr[stage] = make_int4(-1, 0, 0, 0);
+        ptx::mbar_arrive(&full[stage]);  // completes the phase without data: "no more work"
+        break;
+      }
+      const int z = item / per_pair;
+      const int rb = (item / ks) % n_rb, kss = item % ks;
+      const int p = active_pairs[z];
+      const PairTokens pt = load_pair(bucket_off, p);
+      const int maxcnt = max(pt.cnt0, pt.cnt1);
+      const int wrow = kW13 ? p * 2 * f + rb * (kRowsPerCta / 2) : p * d + rb * kRowsPerCta;
+      for (int base = 0; base < maxcnt; base += C::kXRows) {
+        const bool a0 = pt.cnt0 > base, a1 = pt.cnt1 > base;
+        const uint32_t bytes = kWBytes + (a0 ? C::kXBytes : 0) + (a1 ? C::kXBytes : 0);
+        for (int kb = 0; kb < nk; ++kb) {
+          const int kc = kss * kchunk + kb * kBK;
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + (size_t)stage * C::kStageBytes;
+          hdr[stage] = make_int4(item, base, kb, 0);
+          ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+          if (kW13) {
+            ptx::tma_load_2d(st, &tm_w, &full[stage], kc, wrow);
+            ptx::tma_load_2d(st + kWBytes / 2, &tm_w, &full[stage], kc, wrow + f);
+          } else {
+            ptx::tma_load_2d(st, &tm_w, &full[stage], kc, wrow);
+          }
+          if (a0) ptx::tma_load_2d(st + kWBytes, &tm_x, &full[stage], kc, pt.off0 + base);
+          if (a1) ptx::tma_load_2d(st + kWBytes + C::kXBytes, &tm_x, &full[stage], kc, pt.off1 + base);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ============================== consumers ==============================
+  // Warp cw owns ONE m16 tile. w13: tile rows 0..7 = gate rows f0+8cw..+7, rows 8..15 = the
+  // SAME d_ff indices' up rows, so each thread's C fragment holds g (c0,c1) and u (c2,c3)
+  // of one (d_ff index, token) pair and SwiGLU happens in registers. w2: 16 d_model rows.
+  const int cw = warp - 1;
+  const int g = lane >> 2, tig = lane & 3;
+  const uint32_t smem_base = ptx::smem_u32(smem);
+  const int trow_lo = kW13 ? cw * 8 + g : cw * 16 + g;            // tile row of fragment row g
+  const int trow_hi = kW13 ? (kRowsPerCta / 2) + cw * 8 + g : cw * 16 + 8 + g;  // fragment row g+8
+  // per-thread smem offsets (relative to the stage base) of its weight and activation fragments
+  uint32_t off_lo[2], off_hi[2], off_x[2][NT];
+#pragma unroll
+  for (int sub = 0; sub < 2; ++sub) {
+    off_lo[sub] = swz(trow_lo, 4 * sub + tig);
+    off_hi[sub] = swz(trow_hi, 4 * sub + tig);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) off_x[sub][nt] = kWBytes + swz(nt * 8 + g, 4 * sub + tig);
+  }
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    // the first stage of each item names it (or says "no more work")
+    ptx::mbar_wait(&full[stage], phase);
+    const int4 h0 = hdr[stage];
+    if (h0.x < 0) break;
+    const int item = h0.x;
+    const int z = item / per_pair;
+    const int rb = (item / ks) % n_rb, kss = item % ks;
+    const int p = active_pairs[z];
+    const PairTokens pt = load_pair(bucket_off, p);
+    const int maxcnt = max(pt.cnt0, pt.cnt1);
+    // output features of fragment rows g and g+8
+    const int ofeat_lo = kW13 ? rb * (kRowsPerCta / 2) + cw * 8 + g : rb * kRowsPerCta + cw * 16 + g;
+    const int ofeat_hi = kW13 ? ofeat_lo : ofeat_lo + 8;
+    for (int base = 0; base < maxcnt; base += C::kXRows) {
+      const int n0 = min(max(pt.cnt0 - base, 0), C::kXRows);
+      const int n1 = min(max(pt.cnt1 - base, 0), C::kXRows);
+      float acc0[NT][4], acc1[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc0[nt][q] = acc1[nt][q] = 0.f;
+
+      for (int kb = 0; kb < nk; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
+        const uint32_t st = smem_base + (uint32_t)stage * C::kStageBytes;
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+          const uint4 wl = lds128(st + off_lo[sub]);
+          const uint4 wh = lds128(st + off_hi[sub]);
+          const uint32_t Wl[4] = {wl.x, wl.y, wl.z, wl.w}, Wh[4] = {wh.x, wh.y, wh.z, wh.w};
+          uint32_t Bl[4], Bh[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            Bl[i] = decode_b0(Wl[i]);
+            Bh[i] = decode_b0(Wh[i]);
+          }
+          // A fragment: a0 = (row g, k 2tig..), a1 = (row g+8), a2 = (row g, k+8), a3 = (row g+8, k+8)
+#define PZ_POS_BLOCK(DEC, NN, XOFF, ACC)                                                    \
+  if (NN > 0) {                                                                             \
+    uint32_t a[8];                                                                          \
+    _Pragma("unroll") for (int i = 0; i < 4; ++i) {                                        \
+      a[2 * i] = DEC(Wl[i], Bl[i]);                                                         \
+      a[2 * i + 1] = DEC(Wh[i], Bh[i]);                                                     \
+    }                                                                                       \
+    _Pragma("unroll") for (int nt = 0; nt < NT; ++nt) {                                    \
+      if (nt * 8 < NN) {                                                                    \
+        const uint4 xv = lds128(st + XOFF[sub][nt]);                                        \
+        mma_bf16_16816(ACC[nt], a[0], a[1], a[2], a[3], xv.x, xv.y);                        \
+        mma_bf16_16816(ACC[nt], a[4], a[5], a[6], a[7], xv.z, xv.w);                        \
+      }                                                                                     \
+    }                                                                                       \
+  }
+          PZ_POS_BLOCK(decode_v0, n0, off_x, acc0)
+          if (n1 > 0) {
+            // position-1 activations live one X box further
+            uint32_t a[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              a[2 * i] = decode_v1(Wl[i], Bl[i]);
+              a[2 * i + 1] = decode_v1(Wh[i], Bh[i]);
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              if (nt * 8 < n1) {
+                const uint4 xv = lds128(st + off_x[sub][nt] + C::kXBytes);
+                mma_bf16_16816(acc1[nt], a[0], a[1], a[2], a[3], xv.x, xv.y);
+                mma_bf16_16816(acc1[nt], a[4], a[5], a[6], a[7], xv.z, xv.w);
+              }
+            }
+          }
+#undef PZ_POS_BLOCK
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+      // ---- epilogue of this pass: c0,c1 = (row g, tokens 2tig, 2tig+1); c2,c3 = row g+8 ----
+      const bool lo_ok = kW13 || ofeat_lo < d, hi_ok = kW13 || ofeat_hi < d;  // w2 box overhang
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int tok = nt * 8 + 2 * tig + j;
+#pragma unroll
+          for (int ps = 0; ps < 2; ++ps) {
+            const int nn = ps ? n1 : n0;
+            if (tok >= nn) continue;
+            const float lo = ps ? acc1[nt][j] : acc0[nt][j];
+            const float hi = ps ? acc1[nt][2 + j] : acc0[nt][2 + j];
+            const size_t a = (size_t)((ps ? pt.off1 : pt.off0) + base + tok);
+            if (ks == 1) {
+              if (kW13) {
+                h_out[a * f + ofeat_lo] = f32_to_bf16_bits_rn(silu_mul(lo, hi));
+              } else {
+                if (lo_ok) y_out[a * d + ofeat_lo] = lo;
+                if (hi_ok) y_out[a * d + ofeat_hi] = hi;
+              }
+            } else {
+              // partials: w13 -> part[kss][a][0:f] = g, [f:2f] = u ; w2 -> part[kss][a][0:d]
+              const int width = kW13 ? 2 * f : d;
+              float* dst = part + ((size_t)kss * n_assign_cap + a) * width;
+              if (kW13) {
+                dst[ofeat_lo] = lo;
+                dst[f + ofeat_lo] = hi;
+              } else {
+                if (lo_ok) dst[ofeat_lo] = lo;
+                if (hi_ok) dst[ofeat_hi] = hi;
+              }
+            }
+          }
+        }
+    }
+    if (ks > 1) {
+      // ---- the last of the ks CTAs of this (pair, row block) reduces in split order ----
+      __threadfence();
+      named_bar_sync(1, kConsumerWarps * 32);
+      const int ctr = p * n_rb + rb;
+      if (threadIdx.x == 32) {
+        const int prev = atomicAdd(&counters[ctr], 1);
+        *s_last = (prev == ks - 1);
+        if (*s_last) counters[ctr] = 0;  // ready for the next call on this stream
+      }
+      named_bar_sync(1, kConsumerWarps * 32);
+      if (*s_last) {
+        __threadfence();
+        const int row_base = kW13 ? rb * (kRowsPerCta / 2) : rb * kRowsPerCta;
+        const int rows = kW13 ? kRowsPerCta / 2 : min(kRowsPerCta, d - row_base);  // multiple of 4
+        const int q4 = rows / 4;
+        const int n_tot = pt.cnt0 + pt.cnt1;  // buckets 2p and 2p+1 are adjacent
+        const int width = kW13 ? 2 * f : d;
+        for (int i = threadIdx.x - 32; i < n_tot * q4; i += kConsumerWarps * 32) {
+          const size_t a = (size_t)(pt.off0 + i / q4);
+          const int r = row_base + 4 * (i % q4);
+          float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+          const float* src = part + a * width + r;
+          const size_t split_stride = (size_t)n_assign_cap * width;
+#pragma unroll 4
+          for (int s = 0; s < ks; ++s) {
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(src + s * split_stride));
+            s0.x += v.x; s0.y += v.y; s0.z += v.z; s0.w += v.w;
+            if (kW13) {
+              const float4 u = __ldcg(reinterpret_cast<const float4*>(src + s * split_stride + f));
+              s1.x += u.x; s1.y += u.y; s1.z += u.z; s1.w += u.w;
+            }
+          }
+          if (kW13) {
+            uint2 o;
+            o.x = f32_to_bf16_rne_bits(silu_mul(s0.x, s1.x)) | (f32_to_bf16_rne_bits(silu_mul(s0.y, s1.y)) << 16);
+            o.y = f32_to_bf16_rne_bits(silu_mul(s0.z, s1.z)) | (f32_to_bf16_rne_bits(silu_mul(s0.w, s1.w)) << 16);
+            *reinterpret_cast<uint2*>(h_out + a * f + r) = o;
+          } else {
+            *reinterpret_cast<float4*>(y_out + a * d + r) = s0;
+          }
+        }
+      }
+      named_bar_sync(1, kConsumerWarps * 32);
+    }
   }
 }
 
-// Largest split count s <= want with (K / s) % kKStep == 0.
+// Largest split count s <= want with (K / s) % kBK == 0.
 int pick_split(int K, int want) {
   int best = 1;
   for (int s = 1; s <= want; ++s)
-    if (K % (s * kKStep) == 0) best = s;
+    if (K % (s * kBK) == 0) best = s;
   return best;
+}
+
+template <int NT, bool kW13>
+int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* bucket_off, const int32_t* active,
+               const int32_t* n_active, int K, int f, int d, int n_rb, int ks, int max_active, int64_t n_assign_cap,
+               float* part, int32_t* counters, int32_t* work_ctr, uint16_t* h, float* y, cudaStream_t stream) {
+  using C = Cfg<NT>;
+  auto kern = k_gemv_tma<NT, kW13>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+    attr = true;
+  }
+  const int n_items = max_active * n_rb * ks;  // upper bound; the device knows the active count
+  const int grid = std::min(n_items, 2 * num_sms());
+  {
+    ProfScope _ps(kW13 ? "w13_gemv" : "w2_gemv", stream);
+    kern<<<grid, kThreads, C::kSmem, stream>>>(tw, tx, bucket_off, active, n_active, K, f, d, n_rb, ks,
+                                               n_assign_cap, part, counters, work_ctr, h, y);
+  }
+  return cuda_check(cudaGetLastError(), kW13 ? "w13_gemv launch" : "w2_gemv launch");
 }
 
 }  // namespace
 
-int gemv_nt_for(int64_t T) { return T <= 8 ? 1 : (T <= 16 ? 2 : 4); }
+int gemv_nt_for(int64_t T) { return T <= 8 ? 1 : (T <= 16 ? 2 : (T <= 24 ? 3 : 4)); }
 
-// Split-K factor so that (row blocks x splits x active pairs) CTAs give >= ~4 waves.
+// Split-K so that there are >= ~6 work items per resident CTA (2 per SM): the dynamic
+// scheduler's tail is then at most one short item.
 void gemv_splits(int d, int f, int max_active, int* ks13, int* ks2) {
-  const int target_ctas = num_sms() * 4 * 4;  // 4 CTAs of 4 warps per SM, 4 waves
-  const int rb13 = f / (kWarps * 16), rb2 = d / (kWarps * 16);
-  int want13 = (target_ctas + rb13 * max_active - 1) / (rb13 * max_active);
-  int want2 = (target_ctas + rb2 * max_active - 1) / (rb2 * max_active);
-  want13 = want13 < 1 ? 1 : (want13 > 8 ? 8 : want13);
-  want2 = want2 < 1 ? 1 : (want2 > 16 ? 16 : want2);
-  // keep at least 256 of K per split
-  while (want13 > 1 && d / want13 < 256) --want13;
-  while (want2 > 1 && f / want2 < 256) --want2;
+  const int target = num_sms() * 2 * 6;
+  const int items13 = (f / 64) * max_active, items2 = ((d + kRowsPerCta - 1) / kRowsPerCta) * max_active;
+  int want13 = (target + items13 - 1) / items13, want2 = (target + items2 - 1) / items2;
+  want13 = std::min(std::max(want13, 1), 16);
+  want2 = std::min(std::max(want2, 1), 32);
+  while (want13 > 1 && d / want13 < 128) --want13;
+  while (want2 > 1 && f / want2 < 128) --want2;
   *ks13 = pick_split(d, want13);
   *ks2 = pick_split(f, want2);
 }
 
-int launch_gemv_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f,
-                        const uint16_t* x, const int32_t* row_index, const int32_t* bucket_off,
-                        const int32_t* active_pairs, const int32_t* n_active, int max_active,
-                        int64_t n_assign_cap, int nt, int ks13, int ks2, float* part13,
-                        float* part2, int32_t* counters13, int32_t* counters2, uint16_t* h,
-                        float* y, cudaStream_t stream) {
-  (void)n_pairs;
-  if (max_active == 0) return PUZZLE_OK;
-  dim3 g13(f / (kWarps * 16), ks13, max_active);
-  dim3 g2(d / (kWarps * 16), ks2, max_active);
-#define PZ_LAUNCH13(NT)                                                                        \
-  ProfScope _ps13("w13_gemv", stream);                                                         \
-  k_w13_gemv<NT><<<g13, kThreads, 0, stream>>>(w13, x, row_index, bucket_off, active_pairs,    \
-                                               n_active, d, f, ks13, n_assign_cap, part13,     \
-                                               counters13, h)
-#define PZ_LAUNCH2(NT)                                                                               \
-  ProfScope _ps2("w2_gemv", stream);                                                                 \
-  k_w2_gemv<NT><<<g2, kThreads, 0, stream>>>(w2, h, bucket_off, active_pairs, n_active, d, f, ks2, \
-                                             n_assign_cap, part2, counters2, y)
-  if (nt == 1) {
-    { PZ_LAUNCH13(1); }
-    { PZ_LAUNCH2(1); }
-  } else if (nt == 2) {
-    { PZ_LAUNCH13(2); }
-    { PZ_LAUNCH2(2); }
-  } else {
-    { PZ_LAUNCH13(4); }
-    { PZ_LAUNCH2(4); }
-  }
-#undef PZ_LAUNCH13
-#undef PZ_LAUNCH2
-  return cuda_check(cudaGetLastError(), "gemv launch");
+bool gemv_supported(int d, int f) { return d % 64 == 0 && f % 64 == 0; }
+
+// x_rows: [n_assign_cap][d] bf16 in bucket order (TMA source); h: [n_assign_cap][f]; y: [n_assign_cap][d]
+int launch_gemv_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f, const uint16_t* x_rows,
+                        const int32_t* bucket_off, const int32_t* active_pairs, const int32_t* n_active,
+                        int max_active, int64_t n_assign_cap, int nt, int ks13, int ks2, float* part13,
+                        float* part2, int32_t* counters13, int32_t* counters2, int32_t* work_ctrs,
+                        uint16_t* h, float* y, cudaStream_t stream) {
+  if (max_active == 0 || n_assign_cap == 0) return PUZZLE_OK;
+  const int xrows = 8 * nt;
+  CUtensorMap tw13, tx13, tw2, tx2;
+  int rc;
+  if ((rc = make_tmap_2d(&tw13, w13, (int64_t)n_pairs * 2 * f, d, 64, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx13, x_rows, n_assign_cap, d, xrows, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tw2, w2, (int64_t)n_pairs * d, f, kRowsPerCta, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx2, h, n_assign_cap, f, xrows, kBK))) return rc;
+  const int rb13 = f / 64, rb2 = (d + kRowsPerCta - 1) / kRowsPerCta;
+#define PZ_GO(NT)                                                                                             \
+  do {                                                                                                        \
+    if ((rc = launch_one<NT, true>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, ks13,        \
+                                   max_active, n_assign_cap, part13, counters13, work_ctrs, h, y, stream))) \
+      return rc;                                                                                              \
+    return launch_one<NT, false>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, ks2, max_active, \
+                                 n_assign_cap, part2, counters2, work_ctrs + 1, h, y, stream);               \
+  } while (0)
+  if (nt == 1) PZ_GO(1);
+  if (nt == 2) PZ_GO(2);
+  if (nt == 3) PZ_GO(3);
+  PZ_GO(4);
+#undef PZ_GO
 }
 
 }  // namespace pz
