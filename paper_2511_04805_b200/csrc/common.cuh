@@ -97,8 +97,14 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
 }
 __device__ __forceinline__ uint32_t decode_b0(uint32_t w) { return imad(w & 0x8FFF8FFFu, 1u, 0x38003800u); }
 __device__ __forceinline__ uint32_t decode_v0(uint32_t w, uint32_t b0) { return b0 & lane_msb_mask(imul(w, 4u)); }
+__device__ __forceinline__ uint32_t lop3_select_sign(uint32_t from_sign, uint32_t rest) {
+  // (from_sign & 0x80008000) | (rest & 0x7FFF7FFF) in one LOP3 (LUT 0xE2 = B ? A : C)
+  uint32_t r;
+  asm("lop3.b32 %0, %1, 0x80008000, %2, 0xE2;" : "=r"(r) : "r"(from_sign), "r"(rest));
+  return r;
+}
 __device__ __forceinline__ uint32_t decode_v1(uint32_t w, uint32_t b0) {
-  const uint32_t b1 = (b0 & 0x7FFF7FFFu) | (imul(w, 2u) & 0x80008000u);  // one LOP3
+  const uint32_t b1 = lop3_select_sign(imul(w, 2u), b0);
   return b1 & lane_msb_mask(imul(w, 8u));
 }
 

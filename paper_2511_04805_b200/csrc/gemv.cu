@@ -73,6 +73,74 @@ __device__ __forceinline__ PairTokens load_pair(const int32_t* bucket_off, int p
   return pt;
 }
 
+// Multipliers kept in registers (values unknown to ptxas) so the SWAR shifts / adds of the
+// decode are emitted as IMAD on the FMA pipe instead of SHF / IADD3 on the ALU pipe.
+struct Muls {
+  uint32_t one, two, four, eight;
+};
+
+// One 32-wide K sub-step of one warp: decode the 8 packed registers of its m16 tile for the
+// active position(s) and issue D[16 x 8N] += A[16 x 32] X for the first N n-tiles.
+// MODE bit 0 = position 0 has tokens, bit 1 = position 1. Unpredicated, fully unrolled MMAs;
+// both positions' MMAs are interleaved so consecutive HMMAs are independent.
+// A fragment: a[2i] = (row g, k-pair i), a[2i+1] = (row g+8, k-pair i); registers 0..3 feed
+// k16-half 0, registers 4..7 half 1 (see the K-permutation note at the top).
+template <int NT, int N, int MODE>
+__device__ __forceinline__ void sub_step(float (&acc0)[NT][4], float (&acc1)[NT][4], const uint4& wl,
+                                         const uint4& wh, uint32_t xs0, uint32_t xs1, const Muls& mu) {
+  const uint32_t W[8] = {wl.x, wh.x, wl.y, wh.y, wl.z, wh.z, wl.w, wh.w};
+  uint32_t a0[8], a1[8];
+  uint4 x0[N], x1[N];
+  if (MODE & 1) {
+#pragma unroll
+    for (int t = 0; t < N; ++t) x0[t] = lds128(xs0 + t * 1024);
+  }
+  if (MODE & 2) {
+#pragma unroll
+    for (int t = 0; t < N; ++t) x1[t] = lds128(xs1 + t * 1024);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    // b0 = (w & 0x8FFF8FFF) + 0x38003800: exponent rebuilt, sign S_i riding in bit 15
+    const uint32_t b0 = imad(W[i] & 0x8FFF8FFFu, mu.one, 0x38003800u);
+    if (MODE & 1) a0[i] = b0 & lane_msb_mask(imul(W[i], mu.four));                    // mask M_i
+    if (MODE & 2)
+      a1[i] = lop3_select_sign(imul(W[i], mu.two), b0) & lane_msb_mask(imul(W[i], mu.eight));  // S_j, M_j
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int t = 0; t < N; ++t) {
+      if (MODE & 1)
+        mma_bf16_16816(acc0[t], a0[4 * h], a0[4 * h + 1], a0[4 * h + 2], a0[4 * h + 3], h ? x0[t].z : x0[t].x,
+                       h ? x0[t].w : x0[t].y);
+      if (MODE & 2)
+        mma_bf16_16816(acc1[t], a1[4 * h], a1[4 * h + 1], a1[4 * h + 2], a1[4 * h + 3], h ? x1[t].z : x1[t].x,
+                       h ? x1[t].w : x1[t].y);
+    }
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void sub_dispatch(float (&acc0)[NT][4], float (&acc1)[NT][4], const uint4& wl,
+                                             const uint4& wh, uint32_t xs0, uint32_t xs1, int nta0, int nta1,
+                                             const Muls& mu) {
+  const int mode = (nta0 > 0) | ((nta1 > 0) << 1);
+  const int n = max(nta0, nta1);  // both active: empty tiles of the shorter position are harmless
+#define PZ_CASE(NN)                                                                          \
+  if (n == NN) {                                                                             \
+    if (mode == 3) sub_step<NT, NN, 3>(acc0, acc1, wl, wh, xs0, xs1, mu);                    \
+    else if (mode == 1) sub_step<NT, NN, 1>(acc0, acc1, wl, wh, xs0, xs1, mu);               \
+    else sub_step<NT, NN, 2>(acc0, acc1, wl, wh, xs0, xs1, mu);                              \
+    return;                                                                                  \
+  }
+  if (NT >= 4) PZ_CASE((NT >= 4 ? 4 : 1))
+  if (NT >= 3) PZ_CASE((NT >= 3 ? 3 : 1))
+  if (NT >= 2) PZ_CASE((NT >= 2 ? 2 : 1))
+  PZ_CASE(1)
+#undef PZ_CASE
+}
+
 // kW13: weights = packed w13 ([P*2f][d]); CTA rows = 64 gate rows + the same 64 up rows.
 // !kW13: weights = packed w2 ([P*d][f]); CTA rows = 128 d_model rows.
 template <int NT, bool kW13>
@@ -81,7 +149,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
     const int32_t* __restrict__ bucket_off, const int32_t* __restrict__ active_pairs,
     const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb, int ks,
     int64_t n_assign_cap, float* __restrict__ part, int32_t* __restrict__ counters,
-    int32_t* __restrict__ work_ctr, uint16_t* __restrict__ h_out, float* __restrict__ y_out) {
+    int32_t* __restrict__ work_ctr, uint16_t* __restrict__ h_out, float* __restrict__ y_out,
+    uint32_t mul_one) {
   using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -157,7 +226,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
   // of one (d_ff index, token) pair and SwiGLU happens in registers. w2: 16 d_model rows.
   const int cw = warp - 1;
   const int g = lane >> 2, tig = lane & 3;
-  const uint32_t smem_base = ptx::smem_u32(smem);
+  const uint32_t smem_base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;  // == smem, shared window
+  const Muls mu{mul_one, mul_one * 2u, mul_one * 4u, mul_one * 8u};
   const int trow_lo = kW13 ? cw * 8 + g : cw * 16 + g;            // tile row of fragment row g
   const int trow_hi = kW13 ? (kRowsPerCta / 2) + cw * 8 + g : cw * 16 + 8 + g;  // fragment row g+8
   // per-thread smem offsets (relative to the stage base) of its weight and activation fragments
@@ -188,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
     for (int base = 0; base < maxcnt; base += C::kXRows) {
       const int n0 = min(max(pt.cnt0 - base, 0), C::kXRows);
       const int n1 = min(max(pt.cnt1 - base, 0), C::kXRows);
+      const int nta0 = (n0 + 7) >> 3, nta1 = (n1 + 7) >> 3;  // n-tiles with tokens (warp-uniform)
       float acc0[NT][4], acc1[NT][4];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
@@ -197,53 +268,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
       for (int kb = 0; kb < nk; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         const uint32_t st = smem_base + (uint32_t)stage * C::kStageBytes;
-#pragma unroll
-        for (int sub = 0; sub < 2; ++sub) {
-          const uint4 wl = lds128(st + off_lo[sub]);
-          const uint4 wh = lds128(st + off_hi[sub]);
-          const uint32_t Wl[4] = {wl.x, wl.y, wl.z, wl.w}, Wh[4] = {wh.x, wh.y, wh.z, wh.w};
-          uint32_t Bl[4], Bh[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            Bl[i] = decode_b0(Wl[i]);
-            Bh[i] = decode_b0(Wh[i]);
-          }
-          // A fragment: a0 = (row g, k 2tig..), a1 = (row g+8), a2 = (row g, k+8), a3 = (row g+8, k+8)
-#define PZ_POS_BLOCK(DEC, NN, XOFF, ACC)                                                    \
-  if (NN > 0) {                                                                             \
-    uint32_t a[8];                                                                          \
-    _Pragma("unroll") for (int i = 0; i < 4; ++i) {                                        \
-      a[2 * i] = DEC(Wl[i], Bl[i]);                                                         \
-      a[2 * i + 1] = DEC(Wh[i], Bh[i]);                                                     \
-    }                                                                                       \
-    _Pragma("unroll") for (int nt = 0; nt < NT; ++nt) {                                    \
-      if (nt * 8 < NN) {                                                                    \
-        const uint4 xv = lds128(st + XOFF[sub][nt]);                                        \
-        mma_bf16_16816(ACC[nt], a[0], a[1], a[2], a[3], xv.x, xv.y);                        \
-        mma_bf16_16816(ACC[nt], a[4], a[5], a[6], a[7], xv.z, xv.w);                        \
-      }                                                                                     \
-    }                                                                                       \
-  }
-          PZ_POS_BLOCK(decode_v0, n0, off_x, acc0)
-          if (n1 > 0) {
-            // position-1 activations live one X box further
-            uint32_t a[8];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              a[2 * i] = decode_v1(Wl[i], Bl[i]);
-              a[2 * i + 1] = decode_v1(Wh[i], Bh[i]);
-            }
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              if (nt * 8 < n1) {
-                const uint4 xv = lds128(st + off_x[sub][nt] + C::kXBytes);
-                mma_bf16_16816(acc1[nt], a[0], a[1], a[2], a[3], xv.x, xv.y);
-                mma_bf16_16816(acc1[nt], a[4], a[5], a[6], a[7], xv.z, xv.w);
-              }
-            }
-          }
-#undef PZ_POS_BLOCK
-        }
+        // both sub-steps' weight fragments are requested up front (LDS latency overlap)
+        const uint4 wl0 = lds128(st + off_lo[0]), wh0 = lds128(st + off_hi[0]);
+        const uint4 wl1 = lds128(st + off_lo[1]), wh1 = lds128(st + off_hi[1]);
+        sub_dispatch<NT>(acc0, acc1, wl0, wh0, st + off_x[0][0], st + off_x[0][0] + C::kXBytes, nta0, nta1, mu);
+        sub_dispatch<NT>(acc0, acc1, wl1, wh1, st + off_x[1][0], st + off_x[1][0] + C::kXBytes, nta0, nta1, mu);
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&empty[stage]);
         if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -356,7 +385,7 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
   {
     ProfScope _ps(kW13 ? "w13_gemv" : "w2_gemv", stream);
     kern<<<grid, kThreads, C::kSmem, stream>>>(tw, tx, bucket_off, active, n_active, K, f, d, n_rb, ks,
-                                               n_assign_cap, part, counters, work_ctr, h, y);
+                                               n_assign_cap, part, counters, work_ctr, h, y, 1u);
   }
   return cuda_check(cudaGetLastError(), kW13 ? "w13_gemv launch" : "w2_gemv launch");
 }
