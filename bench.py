@@ -512,11 +512,14 @@ def packer_rates(pz, layer, device):
 
 
 def sweep(pz, args, device, pk):
-    """Secondary decode configs (BASELINE.json configs[1] batches and configs[3] shapes)."""
+    """Secondary configs: decode batches of BASELINE.json configs[1] and configs[3] shapes
+    (HBM-bound, GB/s of packed weights), and prefill of configs[2] / configs[3] on the tcgen05
+    path (tensor-bound, TFLOP/s of the dense-equivalent 2*3*d*f*T*k)."""
     import torch
     res = []
     for name, T in (("mixtral", 1), ("mixtral", 16), ("qwen15", 1), ("qwen15", 16), ("qwen15", 64),
-                    ("deepseek", 1), ("deepseek", 16), ("deepseek", 64)):
+                    ("deepseek", 1), ("deepseek", 16), ("deepseek", 64),
+                    ("mixtral", 4096), ("qwen15", 4096), ("deepseek", 4096)):
         cfg = synth.CONFIGS[name]
         try:
             layer, _ = build_layer_gpu(pz, cfg, synth.seeds(cfg)["weights"], device)
@@ -530,11 +533,22 @@ def sweep(pz, args, device, pk):
             for _ in range(5):
                 step()
             torch.cuda.synchronize()
-            K = 50
-            ms = timed_steps(step, K, lambda: flush_buf.zero_()) / K
+            K = 50 if T <= 64 else 20
+            with pz.profile_window() as prof:
+                ms = timed_steps(step, K, lambda: flush_buf.zero_()) / K
+            kern = {k: round(t / n, 5) for k, (n, t) in prof.kernels.items()}
             gbs = (ab["w13"] + ab["w2"]) / (ms / 1e3) / 1e9
-            res.append({"config": name, "batch": T, "tokens_per_s": T / (ms / 1e3), "ms_per_step": ms,
-                        "touched_pairs": nt, "weight_gbs": gbs, "frac_hbm": gbs / pk["hbm_gbs"]})
+            row = {"config": name, "batch": T, "tokens_per_s": T / (ms / 1e3), "ms_per_step": ms,
+                   "touched_pairs": nt, "kernel_avg_ms": kern}
+            if T <= 64:
+                row.update({"weight_gbs": gbs, "frac_hbm": gbs / pk["hbm_gbs"]})
+            else:
+                flops = 2 * 3 * cfg.d_model * cfg.d_ff * T * cfg.top_k
+                tc_ms = sum(v for k, v in kern.items() if k.endswith("_tc"))
+                row.update({"path": "tcgen05", "tflops_step": flops / (ms / 1e3) / 1e12,
+                            "tflops_tc_kernels": flops / (tc_ms / 1e3) / 1e12 if tc_ms else None,
+                            "frac_bf16_peak": flops / (tc_ms / 1e3) / 1e12 / pk["bf16_tflops"] if tc_ms else None})
+            res.append(row)
             del layer, flush_buf
             torch.cuda.empty_cache()
         except Exception as e:  # pragma: no cover

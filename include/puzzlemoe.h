@@ -181,11 +181,14 @@ int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden,
  *   assign_token i32 [T*top_k]    token of assignment a (assignments grouped by bucket)
  *   assign_of    i32 [T*top_k]    assignment index of (t, j)
  *   The order of assignments inside one bucket is unspecified (results do not depend on it).
+ *   workspace: device scratch of >= puzzle_moe_route_workspace_size(L) bytes (used when
+ *   T*top_k > 4096; batches up to that size route inside one CTA).
  * ------------------------------------------------------------------------------------- */
+size_t puzzle_moe_route_workspace_size(const puzzle_moe_layer* L);
 int puzzle_moe_route(const puzzle_moe_layer* L, const float* router_logits, int64_t T,
                      int top_k, int renormalize, int32_t* topk_idx, float* topk_gate,
                      int32_t* bucket_off, int32_t* assign_token, int32_t* assign_of,
-                     puzzle_stream_t stream);
+                     void* workspace, size_t workspace_bytes, puzzle_stream_t stream);
 
 /* puzzle_moe_experts -- (a4)+(a5) over pre-grouped assignments:
  *   x_rows     bf16 [n_assign][d_model]  activations, already grouped by bucket

@@ -28,7 +28,7 @@ EXPORTED_SYMBOLS = (
     "puzzle_unpack", "puzzle_merge_experts_pack", "puzzle_moe_workspace_size", "puzzle_moe_forward",
     "puzzle_moe_forward_ex", "puzzle_moe_route", "puzzle_moe_experts_workspace_size",
     "puzzle_moe_experts", "puzzle_moe_combine", "puzzle_gather_rows", "puzzle_profile_begin",
-    "puzzle_profile_end",
+    "puzzle_profile_end", "puzzle_moe_route_workspace_size",
 )
 
 
@@ -75,7 +75,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_moe_workspace_size": ([P, I64, I], SZ),
             "puzzle_moe_forward": ([P, P, P, I64, I, I, P, P, P, SZ, P], I),
             "puzzle_moe_forward_ex": ([P, P, P, I64, I, I, P, P, P, SZ, I, P], I),
-            "puzzle_moe_route": ([P, P, I64, I, I, P, P, P, P, P, P], I),
+            "puzzle_moe_route": ([P, P, I64, I, I, P, P, P, P, P, P, SZ, P], I),
+            "puzzle_moe_route_workspace_size": ([P], SZ),
             "puzzle_moe_experts_workspace_size": ([P, I64], SZ),
             "puzzle_moe_experts": ([P, P, P, I64, P, P, SZ, I, P], I),
             "puzzle_moe_combine": ([P, P, P, I64, I, I, P, P, P], I),
@@ -212,9 +213,11 @@ class PackedMoELayer:
         off = torch.empty(2 * self.n_pairs + 1, dtype=torch.int32, device=dev)
         tok = torch.empty(T * top_k, dtype=torch.int32, device=dev)
         aof = torch.empty(T * top_k, dtype=torch.int32, device=dev)
+        need = int(load_library().puzzle_moe_route_workspace_size(ctypes.byref(self.desc)))
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
         _check(load_library().puzzle_moe_route(ctypes.byref(self.desc), _p(router_logits), T, int(top_k),
                                                int(bool(renormalize)), _p(idx), _p(gate), _p(off), _p(tok),
-                                               _p(aof), _stream(stream)), "puzzle_moe_route")
+                                               _p(aof), _p(ws), ws.numel(), _stream(stream)), "puzzle_moe_route")
         return idx, gate, off, tok, aof
 
     def experts(self, x_rows, bucket_off, y_rows=None, path: int = PATH_AUTO, workspace=None, stream=None):

@@ -18,7 +18,8 @@ int launch_unpack(const uint16_t*, int, int64_t, uint16_t*, cudaStream_t);
 int launch_merge_experts_pack(const uint16_t*, const uint16_t*, const float*, const float*, int64_t,
                               int64_t, int64_t, float, uint16_t*, puzzle_pack_stats*, cudaStream_t);
 int launch_route(const float*, int64_t, int, int, int, const int32_t*, int, int32_t*, float*, int32_t*,
-                 int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int, cudaStream_t);
+                 int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int, int32_t*, const uint16_t*, int, uint16_t*,
+                 bool*, cudaStream_t);
 int launch_iota(int32_t*, int, int32_t*, cudaStream_t);
 const char* last_error_cstr();
 int launch_combine(const float*, const int32_t*, const float*, int64_t, int, int, const uint16_t*,
@@ -135,7 +136,7 @@ constexpr int64_t kGemvMaxTokens = 64;
 
 struct Layout {
   size_t topk_idx, topk_gate, bucket_off, assign_token, assign_of, active, n_active, cnt13, cnt2, h, y,
-      part13, part2, x_perm, total;
+      part13, part2, x_perm, route_scratch, total;
 };
 
 Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
@@ -177,6 +178,7 @@ Layout make_layout(const puzzle_moe_layer* L, const Plan& p) {
   o.part13 = take(p.ks13 > 1 ? (size_t)p.ks13 * na * 2 * f * 4 : 0);
   o.part2 = take(p.ks2 > 1 ? (size_t)p.ks2 * na * d * 4 : 0);
   o.x_perm = take(na * d * 2);
+  o.route_scratch = take(2 * 2 * P * 4);
   o.total = off;
   return o;
 }
@@ -344,16 +346,19 @@ int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, con
   if (!ws || ws_bytes < lay.total)
     return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_moe_workspace_size(L, T, top_k)");
   cudaStream_t s = (cudaStream_t)stream;
+  bool rows_written = false;
   int rc = launch_route(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs,
                         at<int32_t>(ws, lay.topk_idx), at<float>(ws, lay.topk_gate),
                         at<int32_t>(ws, lay.bucket_off), at<int32_t>(ws, lay.assign_token),
                         at<int32_t>(ws, lay.assign_of), at<int32_t>(ws, lay.active),
                         at<int32_t>(ws, lay.n_active), at<int32_t>(ws, lay.cnt13),
-                        (int)((lay.h - lay.cnt13) / 4), s);
+                        (int)((lay.h - lay.cnt13) / 4), at<int32_t>(ws, lay.route_scratch), hidden, L->d_model,
+                        at<uint16_t>(ws, lay.x_perm), &rows_written, s);
   if (rc) return rc;
-  rc = run_experts(L, plan, lay, ws, hidden, at<int32_t>(ws, lay.assign_token),
-                   at<int32_t>(ws, lay.bucket_off), at<int32_t>(ws, lay.active),
-                   at<int32_t>(ws, lay.n_active), at<float>(ws, lay.y), s);
+  // rows already in bucket order (fused into the large-batch scatter) or gathered now
+  rc = run_experts(L, plan, lay, ws, rows_written ? at<uint16_t>(ws, lay.x_perm) : hidden,
+                   rows_written ? nullptr : at<int32_t>(ws, lay.assign_token), at<int32_t>(ws, lay.bucket_off),
+                   at<int32_t>(ws, lay.active), at<int32_t>(ws, lay.n_active), at<float>(ws, lay.y), s);
   if (rc) return rc;
   return launch_combine(at<float>(ws, lay.y), at<int32_t>(ws, lay.assign_of), at<float>(ws, lay.topk_gate),
                         T, k, L->d_model, residual, out, s);
@@ -366,17 +371,26 @@ int puzzle_moe_forward(const puzzle_moe_layer* L, const uint16_t* hidden, const 
                                PUZZLE_PATH_AUTO, stream);
 }
 
+size_t puzzle_moe_route_workspace_size(const puzzle_moe_layer* L) {
+  if (check_layer(L)) return 0;
+  return (size_t)2 * 2 * L->n_pairs * sizeof(int32_t);
+}
+
 int puzzle_moe_route(const puzzle_moe_layer* L, const float* logits, int64_t T, int k, int renorm,
                      int32_t* topk_idx, float* topk_gate, int32_t* bucket_off, int32_t* assign_token,
-                     int32_t* assign_of, puzzle_stream_t stream) {
+                     int32_t* assign_of, void* workspace, size_t workspace_bytes, puzzle_stream_t stream) {
   if (int rc = check_layer(L)) return rc;
   if (T < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "T < 0");
   if (k < 1 || k > L->n_experts) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "top_k outside [1, n_experts]");
   if (!logits || !topk_idx || !topk_gate || !bucket_off || !assign_token || !assign_of)
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (int rc = check_device()) return rc;
+  if (T == 0) return PUZZLE_OK;
+  if (workspace_bytes < puzzle_moe_route_workspace_size(L) || (!workspace && workspace_bytes))
+    return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_moe_route_workspace_size(L)");
   return launch_route(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs, topk_idx, topk_gate,
-                      bucket_off, assign_token, assign_of, nullptr, nullptr, nullptr, 0, (cudaStream_t)stream);
+                      bucket_off, assign_token, assign_of, nullptr, nullptr, nullptr, 0,
+                      static_cast<int32_t*>(workspace), nullptr, L->d_model, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 int puzzle_moe_experts(const puzzle_moe_layer* L, const uint16_t* x_rows, const int32_t* bucket_off,

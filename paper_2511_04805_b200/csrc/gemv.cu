@@ -392,7 +392,7 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
 
 }  // namespace
 
-int gemv_nt_for(int64_t T) { return T <= 8 ? 1 : (T <= 16 ? 2 : (T <= 24 ? 3 : 4)); }
+int gemv_nt_for(int64_t T) { return T <= 8 ? 1 : (T <= 16 ? 2 : (T <= 128 ? 3 : 4)); }
 
 // Split-K so that there are >= ~6 work items per resident CTA (2 per SM): the dynamic
 // scheduler's tail is then at most one short item.

@@ -70,10 +70,10 @@ def test_skewed_routing_all_tokens_one_pair(pz):
     assert_close(got, ref, "skew")
 
 
-def test_route_outputs(pz):
+@pytest.mark.parametrize("T", [300, 1000])  # 1000 x 6 > 4096: the multi-CTA routing path
+def test_route_outputs(pz, T):
     cfg = synth.MoEConfig("route", 9, 64, 64, 64, 6, False)
     layer, (w13, w2, slot) = _layer(pz, cfg)
-    T = 300
     lg = synth.router_logits(cfg, T)
     lg[5, 10] = lg[5, 11] = lg[5].max() + 1.0  # an exact tie -> lower index first
     idx, gate, off, tok, aof = layer.route(torch.from_numpy(lg).cuda(), cfg.top_k, cfg.renormalize)
@@ -138,6 +138,13 @@ TC_SMALL = [
 def test_forward_tc_small(pz, cfg, T):
     got, ref = _run(pz, cfg, T, pz.PATH_TC)
     assert_close(got, ref, f"tc {cfg.name} T={T}")
+
+
+def test_forward_tc_large_batch_routing(pz):
+    """T*k > 4096: multi-CTA routing with the bucket-order row copy fused into the scatter."""
+    cfg = TC_SMALL[1]
+    got, ref = _run(pz, cfg, 1100, pz.PATH_TC, sample=48)
+    assert_close(got, ref, "tc large-batch routing")
 
 
 def test_forward_tc_skewed_multi_mtile(pz):
