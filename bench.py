@@ -363,9 +363,21 @@ def run_ours(args):
     out = torch.empty_like(hidden)
     ws = layer.workspace(T, cfg.top_k)
     stream = torch.cuda.current_stream()
+    ep = None
+    if world > 1:
+        # expert parallelism: this rank keeps only its pairs (or d_ff slice) of the layer
+        from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_packed
+        part = Partition(cfg.n_pairs, world)
+        w13_l, w2_l = shard_packed(layer.w13, layer.w2, part, rank)
+        local = pz.PackedMoELayer(w13_l, w2_l, torch.arange(2 * w13_l.shape[0], dtype=torch.int32, device=device))
+        routing = pz.RoutingLayer(cfg.n_pairs, cfg.d_model, cfg.d_ff, layer.expert_slot, w13_l)
+        ep = ExpertParallelMoE(part, rank, routing, local, cfg.d_model)
 
     def step():
-        layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+        if ep is not None:
+            ep.forward(hidden, logits, cfg.top_k, cfg.renormalize)
+        else:
+            layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
 
     log("workspace", ws.numel())
     n_touched = touched_pairs(layer, logits, cfg)
@@ -379,6 +391,15 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     log("warmup done")
+    graph = None
+    if not args.no_graph and ep is None:  # EP needs host-side split sizes: eager
+        # the whole forward (route .. combine) replayed as one CUDA graph: no host launch gaps
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(W):
+            graph.replay()
+        torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.1)
@@ -386,12 +407,20 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    with pz.profile_window() as prof:
-        total_ms = timed_steps(step, K, flush)
+    if graph is not None:
+        total_ms = timed_steps(graph.replay, K, flush)
+    else:
+        with pz.profile_window() as prof:
+            total_ms = timed_steps(step, K, flush)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t1 = time.perf_counter()
+    if graph is not None:
+        # per-kernel durations: the same K steps launched eagerly with library events on
+        # the launching stream (graph replays carry no per-kernel events)
+        with pz.profile_window() as prof:
+            timed_steps(step, K, flush)
     time.sleep(0.05)
     clocks.stop()
     ms = total_ms / K
@@ -429,8 +458,11 @@ def run_ours(args):
     def e2e_step():
         h_dev.copy_(h_host, non_blocking=True)
         l_dev.copy_(l_host, non_blocking=True)
-        layer.forward(h_dev, l_dev, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
-        o_host.copy_(out, non_blocking=True)
+        if ep is not None:
+            o_host.copy_(ep.forward(h_dev, l_dev, cfg.top_k, cfg.renormalize), non_blocking=True)
+        else:
+            layer.forward(h_dev, l_dev, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+            o_host.copy_(out, non_blocking=True)
 
     for _ in range(W):
         e2e_step()
@@ -452,9 +484,11 @@ def run_ours(args):
                                    + (" (BASELINE.json configs[1])" if cfg.name == "mixtral" else ""),
                        "d_model": cfg.d_model, "d_ff": cfg.d_ff, "n_experts": cfg.n_experts,
                        "n_pairs": cfg.n_pairs, "top_k": cfg.top_k, "batch_per_gpu": T,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": f"ep{world} (pairs sharded, NCCL all-to-all dispatch/combine, "
+                                      f"{T} tokens per rank)" if world > 1 else "single",
                        "l2": "inputs larger than L2 (packed layer %.2f GB)" % (layer.packed_bytes / 1e9) if big
-                       else "L2 flushed between timed steps"},
+                       else "L2 flushed between timed steps",
+                       "launch": "CUDA graph replay of the whole forward" if graph is not None else "eager"},
             "roofline": roof, "step_weight_gbs": step_gbs, "gpu_launches": gpu_launches,
             "kernels": kern, "e2e": e2e}
     if rank == 0:
@@ -526,7 +560,16 @@ def sweep(pz, args, device, pk):
             hidden, logits = make_inputs(cfg, T, synth.seeds(cfg)["activations"], device)
             out = torch.empty_like(hidden)
             ws = layer.workspace(T, cfg.top_k)
-            step = lambda: layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+            eager = lambda: layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+            eager()
+            torch.cuda.synchronize()
+            if args.no_graph:
+                step = eager
+            else:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    eager()
+                step = g.replay
             nt = touched_pairs(layer, logits, cfg)
             ab = algorithmic_bytes(cfg, nt, T)
             flush_buf = torch.empty(2 * l2_bytes(device), dtype=torch.uint8, device=device)
@@ -534,8 +577,9 @@ def sweep(pz, args, device, pk):
                 step()
             torch.cuda.synchronize()
             K = 50 if T <= 64 else 20
+            ms = timed_steps(step, K, lambda: flush_buf.zero_()) / K
             with pz.profile_window() as prof:
-                ms = timed_steps(step, K, lambda: flush_buf.zero_()) / K
+                timed_steps(eager, K, lambda: flush_buf.zero_())
             kern = {k: round(t / n, 5) for k, (n, t) in prof.kernels.items()}
             gbs = (ab["w13"] + ab["w2"]) / (ms / 1e3) / 1e9
             row = {"config": name, "batch": T, "tokens_per_s": T / (ms / 1e3), "ms_per_step": ms,
@@ -566,6 +610,7 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--no-extra", action="store_true", help="skip the unpacked baseline / sweep / packer lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)

@@ -51,6 +51,8 @@ def _load():
             lib.oracle_unpack.argtypes = [P, I, I64, P]
             lib.oracle_route.argtypes = [P, I64, I, I, I, P, P]
             lib.oracle_moe_forward.argtypes = [P, P, P, I, I, I, P, P, I64, I, I, I, P, P]
+            lib.oracle_expert_ffn.argtypes = [P, P, I, I, I, I, P, I64, P]
+            lib.oracle_expert_ffn.restype = I
             lib.oracle_num_threads.restype = I
             lib.oracle_set_num_threads.argtypes = [I]
             for name in ("oracle_bf16_round", "oracle_merge", "oracle_pack", "oracle_unpack",
@@ -183,3 +185,16 @@ def moe_forward(w13, w2, expert_slot, hidden_bits, logits, k: int, renormalize: 
     if rc != 0:
         raise ValueError(f"oracle_moe_forward failed rc={rc}")
     return out
+
+
+def expert_ffn(w13, w2, pair: int, pos: int, x_bits) -> np.ndarray:
+    """f64 [n, d] = W2_pos (silu(W1_pos x) * (W3_pos x)) for rows already routed to expert
+    (pair, pos); no gate, no residual."""
+    w13 = _c(w13, np.uint16)
+    w2 = _c(w2, np.uint16)
+    P, two, f, d = w13.shape
+    xb = _c(x_bits, np.uint16).reshape(-1, d)
+    y = np.empty((xb.shape[0], d), np.float64)
+    if _load().oracle_expert_ffn(_ptr(w13), _ptr(w2), int(pair), int(pos), d, f, _ptr(xb), xb.shape[0], _ptr(y)) != 0:
+        raise ValueError("bad expert position")
+    return y

@@ -284,6 +284,40 @@ int oracle_moe_forward(const uint16_t* w13, const uint16_t* w2, const int32_t* e
   return err;
 }
 
+/* ------------------------------------------------------------------------ */
+/* O5c. One expert of one pair on rows that are already routed to it:       */
+/*      y[n] = W2_pos (silu(W1_pos x[n]) * (W3_pos x[n])), f64, no gate.     */
+/*      (The EP tests' CPU stand-in for the expert kernels.)                  */
+/* ------------------------------------------------------------------------ */
+int oracle_expert_ffn(const uint16_t* w13, const uint16_t* w2, int pair, int pos, int d, int f,
+                      const uint16_t* x_rows, int64_t n, double* y) {
+  if (pos != 0 && pos != 1) return 1;
+  const uint16_t* W1 = w13 + ((size_t)pair * 2 + 0) * (size_t)f * d;
+  const uint16_t* W3 = w13 + ((size_t)pair * 2 + 1) * (size_t)f * d;
+  const uint16_t* W2 = w2 + (size_t)pair * (size_t)d * f;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t t = 0; t < n; ++t) {
+    double* h = (double*)malloc(sizeof(double) * (size_t)f);
+    const uint16_t* x = x_rows + t * d;
+    for (int r = 0; r < f; ++r) {
+      double g = 0.0, u = 0.0;
+      for (int c = 0; c < d; ++c) {
+        double xc = bf16_to_double(x[c]);
+        g += bf16_to_double(decode_word(W1[(size_t)r * d + c], pos)) * xc;
+        u += bf16_to_double(decode_word(W3[(size_t)r * d + c], pos)) * xc;
+      }
+      h[r] = g / (1.0 + exp(-g)) * u;
+    }
+    for (int r = 0; r < d; ++r) {
+      double acc = 0.0;
+      for (int c = 0; c < f; ++c) acc += bf16_to_double(decode_word(W2[(size_t)r * f + c], pos)) * h[c];
+      y[t * d + r] = acc;
+    }
+    free(h);
+  }
+  return 0;
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

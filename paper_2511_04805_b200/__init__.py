@@ -206,19 +206,7 @@ class PackedMoELayer:
 
     def route(self, router_logits, top_k: int, renormalize: bool, stream=None):
         """puzzle_moe_route -> (topk_idx, topk_gate, bucket_off, assign_token, assign_of)."""
-        T = router_logits.shape[0]
-        dev = router_logits.device
-        idx = torch.empty((T, top_k), dtype=torch.int32, device=dev)
-        gate = torch.empty((T, top_k), dtype=torch.float32, device=dev)
-        off = torch.empty(2 * self.n_pairs + 1, dtype=torch.int32, device=dev)
-        tok = torch.empty(T * top_k, dtype=torch.int32, device=dev)
-        aof = torch.empty(T * top_k, dtype=torch.int32, device=dev)
-        need = int(load_library().puzzle_moe_route_workspace_size(ctypes.byref(self.desc)))
-        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
-        _check(load_library().puzzle_moe_route(ctypes.byref(self.desc), _p(router_logits), T, int(top_k),
-                                               int(bool(renormalize)), _p(idx), _p(gate), _p(off), _p(tok),
-                                               _p(aof), _p(ws), ws.numel(), _stream(stream)), "puzzle_moe_route")
-        return idx, gate, off, tok, aof
+        return _route(self.desc, self.n_pairs, router_logits, top_k, renormalize, stream)
 
     def experts(self, x_rows, bucket_off, y_rows=None, path: int = PATH_AUTO, workspace=None, stream=None):
         """puzzle_moe_experts: grouped bf16 rows -> unweighted f32 expert outputs."""
@@ -231,6 +219,39 @@ class PackedMoELayer:
                                                  _p(y_rows), _p(workspace), workspace.numel(), int(path),
                                                  _stream(stream)), "puzzle_moe_experts")
         return y_rows
+
+
+class RoutingLayer:
+    """Routing-only view of a layer for expert parallelism: GLOBAL n_experts / n_pairs /
+    expert_slot (puzzle_moe_route reads nothing else); `anchor` is any 16-byte aligned 16-bit
+    device tensor standing in for the weight pointers, which routing never dereferences."""
+
+    def __init__(self, n_pairs: int, d_model: int, d_ff: int, expert_slot: torch.Tensor, anchor: torch.Tensor):
+        assert expert_slot.dtype == torch.int32 and expert_slot.numel() == 2 * n_pairs
+        self.expert_slot, self.anchor = expert_slot.contiguous(), anchor
+        self.n_pairs = n_pairs
+        self.desc = MoELayerDesc(2 * n_pairs, n_pairs, d_model, d_ff, anchor.data_ptr(), anchor.data_ptr(),
+                                 self.expert_slot.data_ptr())
+
+    def route(self, router_logits, top_k: int, renormalize: bool, stream=None):
+        return _route(self.desc, self.n_pairs, router_logits, top_k, renormalize, stream)
+
+
+def _route(desc, n_pairs, router_logits, top_k, renormalize, stream=None):
+    """puzzle_moe_route -> (topk_idx, topk_gate, bucket_off, assign_token, assign_of)."""
+    T = router_logits.shape[0]
+    dev = router_logits.device
+    idx = torch.empty((T, top_k), dtype=torch.int32, device=dev)
+    gate = torch.empty((T, top_k), dtype=torch.float32, device=dev)
+    off = torch.empty(2 * n_pairs + 1, dtype=torch.int32, device=dev)
+    tok = torch.empty(T * top_k, dtype=torch.int32, device=dev)
+    aof = torch.empty(T * top_k, dtype=torch.int32, device=dev)
+    need = int(load_library().puzzle_moe_route_workspace_size(ctypes.byref(desc)))
+    ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+    _check(load_library().puzzle_moe_route(ctypes.byref(desc), _p(router_logits), T, int(top_k),
+                                           int(bool(renormalize)), _p(idx), _p(gate), _p(off), _p(tok),
+                                           _p(aof), _p(ws), ws.numel(), _stream(stream)), "puzzle_moe_route")
+    return idx, gate, off, tok, aof
 
 
 def moe_combine(y_rows, assign_of, topk_gate, residual=None, out=None, stream=None) -> torch.Tensor:

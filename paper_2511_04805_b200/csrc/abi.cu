@@ -59,6 +59,8 @@ cudaEvent_t pool_event() {
 
 void prof_mark_begin(const char* name, cudaStream_t s) {
   if (!g_prof_on) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;  // graph capture
   ProfRec r{name, pool_event(), pool_event()};
   cudaEventRecord(r.beg, s);
   g_prof.push_back(r);
@@ -66,6 +68,8 @@ void prof_mark_begin(const char* name, cudaStream_t s) {
 
 void prof_mark_end(cudaStream_t s) {
   if (!g_prof_on || g_prof.empty()) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
   cudaEventRecord(g_prof.back().end, s);
 }
 

@@ -1,0 +1,185 @@
+"""Expert parallelism: PuzzleMoE merged pairs sharded over the GPUs of one node,
+tokens dispatched to the pair owners and back with all-to-all (NCCL over NVLink in production,
+gloo in the CPU tests).
+
+Partition (the unit is a merged PAIR, so both experts of a pair stay co-resident and each
+packed tile is still read once):
+  world <= P : rank r owns pairs [floor(r P / G), floor((r+1) P / G)).
+  world >  P : world % P == 0; each pair is split along d_ff into G/P slices (SwiGLU is
+               elementwise in d_ff, so every slice computes an exact partial of W2 h; the
+               partials are summed by the combine on the token's home rank).
+
+Per layer (every rank holds T_local tokens of its own):
+  1. route (a3) against the global pairing -> top-k, gates, global buckets (pair-major),
+  2. rows gathered into bucket order (the buckets of a rank's pairs are contiguous),
+  3. per-bucket counts exchanged (all_to_all), rows dispatched (all_to_all, variable splits),
+  4. received rows regrouped into the owner's local bucket order, local experts (a4)+(a5),
+  5. outputs un-permuted and sent home (all_to_all), combine (a6) with the home gates.
+Every data-path step runs in libpuzzlemoe kernels (route, gather, experts, combine); torch
+supplies the collectives and the host-side split sizes (one D2H copy of the bucket counts).
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+@dataclasses.dataclass(frozen=True)
+class Partition:
+    n_pairs: int
+    world: int
+
+    @property
+    def slices(self) -> int:
+        """d_ff slices per pair (1 unless world > n_pairs)."""
+        if self.world <= self.n_pairs:
+            return 1
+        if self.world % self.n_pairs:
+            raise ValueError("expert parallelism with world > n_pairs needs world % n_pairs == 0")
+        return self.world // self.n_pairs
+
+    def pairs_of(self, rank: int) -> tuple[int, int]:
+        """[first, last) global pair ids held (whole pairs, or one pair's d_ff slice)."""
+        if self.slices == 1:
+            return (rank * self.n_pairs) // self.world, ((rank + 1) * self.n_pairs) // self.world
+        p = rank // self.slices
+        return p, p + 1
+
+    def slice_of(self, rank: int) -> int:
+        return rank % self.slices
+
+    def owners(self, pair: int) -> list[int]:
+        if self.slices == 1:
+            return [r for r in range(self.world) if self.pairs_of(r)[0] <= pair < self.pairs_of(r)[1]]
+        return [pair * self.slices + j for j in range(self.slices)]
+
+
+def shard_packed(w13: torch.Tensor, w2: torch.Tensor, part: Partition, rank: int):
+    """Packed weights this rank holds: w13 [P,2,f,d] -> [p1-p0, 2, f/S, d]; w2 [P,d,f] ->
+    [p1-p0, d, f/S] (a d_ff slice of a packed tensor is still a valid packed tensor: the
+    decode is elementwise)."""
+    p0, p1 = part.pairs_of(rank)
+    S = part.slices
+    f = w13.shape[2]
+    if f % S or (f // S) % 64:
+        raise ValueError("d_ff / slices must be a multiple of 64")
+    fs = f // S
+    j = part.slice_of(rank)
+    w13_l = w13[p0:p1, :, j * fs:(j + 1) * fs, :].contiguous()
+    w2_l = w2[p0:p1, :, j * fs:(j + 1) * fs].contiguous()
+    return w13_l, w2_l
+
+
+class CudaOps:
+    """Device ops of the EP data path: libpuzzlemoe kernels."""
+
+    def __init__(self):
+        import paper_2511_04805_b200 as pz
+        self.pz = pz
+
+    def route(self, route_layer, logits, k, renorm):
+        return route_layer.route(logits, k, renorm)
+
+    def gather_rows(self, src, index):
+        if src.dtype == torch.float32:  # 4-byte rows move as pairs of 16-bit columns
+            return self.pz.gather_rows(src.view(torch.int16), index).view(torch.float32)
+        return self.pz.gather_rows(src, index)
+
+    def experts(self, local_layer, x_rows, bucket_off):
+        return local_layer.experts(x_rows, bucket_off)
+
+    def combine(self, y, assign_of, gate, residual):
+        return self.pz.moe_combine(y, assign_of, gate, residual=residual)
+
+
+class ExpertParallelMoE:
+    """One MoE layer sharded by merged pairs over `world` ranks of `group`.
+
+    route_layer: a layer descriptor whose routing metadata (n_experts, n_pairs, expert_slot)
+                 is GLOBAL (route reads no weights); local_layer: this rank's packed shard."""
+
+    def __init__(self, part: Partition, rank: int, route_layer, local_layer, d_model: int, group=None, ops=None):
+        self.part, self.rank, self.world = part, rank, part.world
+        self.route_layer, self.local_layer = route_layer, local_layer
+        self.d = d_model
+        self.group = group
+        self.ops = ops if ops is not None else CudaOps()
+        # local bucket b_local = 2 * (pair - p0) + pos
+        self.p0, self.p1 = part.pairs_of(rank)
+        self.n_local_buckets = 2 * (self.p1 - self.p0)
+
+    def _a2a(self, out, inp, out_splits, in_splits):
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+
+    def forward(self, hidden, logits, top_k: int, renormalize: bool, residual=None):
+        ops, part, G, r = self.ops, self.part, self.world, self.rank
+        dev = hidden.device
+        T = hidden.shape[0]
+        topk_idx, gate, bucket_off, assign_token, assign_of = ops.route(self.route_layer, logits, top_k, renormalize)
+        off = bucket_off.cpu().numpy().astype(np.int64)  # the one D2H sync (split sizes)
+        counts = np.diff(off)
+        # ---- dispatch plan: rows for rank q = its pairs' buckets (duplicated for d_ff slices)
+        send_index, send_split, send_counts = [], [], []
+        for q in range(G):
+            qa, qb = part.pairs_of(q)
+            lo, hi = off[2 * qa], off[2 * qb]
+            send_index.append(np.arange(lo, hi, dtype=np.int64))
+            send_split.append(int(hi - lo))
+            send_counts.append(counts[2 * qa:2 * qb])
+        send_index = np.concatenate(send_index) if send_index else np.zeros(0, np.int64)
+        x_perm = ops.gather_rows(hidden, assign_token)                   # bucket order
+        if part.slices == 1:
+            send_buf = x_perm                                            # already rank-major
+        else:
+            send_buf = ops.gather_rows(x_perm, torch.from_numpy(send_index.astype(np.int32)).to(dev))
+        # ---- per-bucket counts: each rank learns [source][local bucket] counts
+        lb = [2 * (part.pairs_of(q)[1] - part.pairs_of(q)[0]) for q in range(G)]
+        c_send = torch.from_numpy(np.concatenate(send_counts).astype(np.int64)) if send_counts else torch.zeros(0, dtype=torch.int64)
+        c_recv = torch.empty(G * lb[r], dtype=torch.int64)
+        if dev.type == "cuda" and dist.get_backend(self.group) == "nccl":
+            c_send_d, c_recv_d = c_send.to(dev), c_recv.to(dev)
+            self._a2a(c_recv_d, c_send_d, [lb[r]] * G, lb)
+            c_recv = c_recv_d.cpu()
+        else:
+            self._a2a(c_recv, c_send, [lb[r]] * G, lb)
+        rc = c_recv.numpy().reshape(G, lb[r])                             # [source][local bucket]
+        recv_split = rc.sum(1).astype(np.int64)
+        # ---- rows to the owners
+        x_recv = torch.empty((int(recv_split.sum()), self.d), dtype=hidden.dtype, device=dev)
+        self._a2a(x_recv, send_buf, [int(v) for v in recv_split], send_split)
+        # ---- regroup by local bucket: (bucket, source) order
+        src_base = np.concatenate([[0], np.cumsum(recv_split)[:-1]]).astype(np.int64)
+        within = np.concatenate([np.zeros((G, 1), np.int64), np.cumsum(rc, 1)[:, :-1]], 1)
+        regroup = [src_base[s] + within[s, b] + np.arange(rc[s, b], dtype=np.int64)
+                   for b in range(lb[r]) for s in range(G)]
+        regroup = np.concatenate(regroup) if regroup else np.zeros(0, np.int64)
+        local_off = np.concatenate([[0], np.cumsum(rc.sum(0))]).astype(np.int32)
+        n_local = int(local_off[-1])
+        if n_local > 0:
+            x_local = ops.gather_rows(x_recv, torch.from_numpy(regroup.astype(np.int32)).to(dev))
+            y_local = ops.experts(self.local_layer, x_local, torch.from_numpy(local_off).to(dev))
+            inv = np.empty_like(regroup)
+            inv[regroup] = np.arange(regroup.size)
+            y_recv = ops.gather_rows(y_local, torch.from_numpy(inv.astype(np.int32)).to(dev))
+        else:
+            y_recv = torch.empty((0, self.d), dtype=torch.float32, device=dev)
+        # ---- outputs home, aligned with send_buf rows
+        y_back = torch.empty((int(sum(send_split)), self.d), dtype=torch.float32, device=dev)
+        self._a2a(y_back, y_recv, send_split, [int(v) for v in recv_split])
+        # ---- combine: every (t, j) sums its S partial rows with the full gate
+        S = part.slices
+        if S == 1:
+            return ops.combine(y_back, assign_of, gate, residual)
+        # row of assignment a's s-th copy inside send_buf / y_back
+        pos_of = np.empty((off[-1], S), np.int64)
+        seen = np.zeros(off[-1], np.int64)
+        for i, a in enumerate(send_index):
+            pos_of[a, seen[a]] = i
+            seen[a] += 1
+        aof = assign_of.cpu().numpy().astype(np.int64).reshape(T, top_k)
+        aof_s = pos_of[aof].reshape(T, top_k * S).astype(np.int32)
+        gate_s = gate.reshape(T, top_k, 1).expand(T, top_k, S).reshape(T, top_k * S).contiguous()
+        return ops.combine(y_back, torch.from_numpy(aof_s).to(dev).reshape(-1), gate_s, residual)

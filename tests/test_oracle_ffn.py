@@ -137,3 +137,21 @@ def test_topk_combination_and_permutation_equivariance():
     perm = rng.permutation(T)
     out_p = oracle.moe_forward(w13, w2, slot, hb[perm], logits[perm], 2, False)
     assert np.array_equal(out_p, out[perm])
+
+
+def test_expert_ffn_matches_forward_and_dense():
+    """oracle.expert_ffn on rows routed to one expert == the dense f64 FFN of the Eq. 8
+    reconstruction, and == moe_forward for a top-1 renormalised route (gate 1)."""
+    cfg = synth.CONFIGS["tiny"]
+    rng = np.random.default_rng(9)
+    w13, w2, _ = _merged_pair(cfg, rng)
+    hb = synth.hidden_bits(cfg, 5, seed=21)
+    x = oracle.bf16_bits_to_f32(hb)
+    for pos in (0, 1):
+        y = oracle.expert_ffn(w13, w2, 0, pos, hb)
+        w1, w3, w2d = (oracle.bf16_bits_to_f32(oracle.unpack(w, pos)) for w in (w13[0, 0], w13[0, 1], w2[0]))
+        np.testing.assert_allclose(y, _dense_ffn_f64(x, w1, w3, w2d).numpy(), rtol=1e-12, atol=1e-13)
+        logits = np.zeros((5, 2), np.float32)
+        logits[:, pos] = 1.0  # expert `pos` is at position pos with expert_slot = [0, 1]
+        out = oracle.moe_forward(w13, w2, np.array([0, 1], np.int32), hb, logits, 1, True)
+        np.testing.assert_allclose(out, y, rtol=1e-12, atol=1e-13)
