@@ -13,10 +13,10 @@
 //   consumers each owns 32 weight rows (two 16-row m-tiles) of the CTA tile; per stage it
 //             reads its fragments from shared memory, SWAR-decodes two words per 32-bit
 //             register, and issues the MMAs for each position that has tokens.
-// K-permutation: inside each 32-wide K sub-chunk, lane (g, tig) takes physical k =
-// 8*tig..8*tig+7 of rows g and g+8; k 8tig+{0..3} feed MMA#0 fragments (a0,a2) and
-// 8tig+{4..7} feed MMA#1. The activation fragments use the identical permutation, so each
-// dot product sums exactly the same products.
+// K-permutation: in sub-step s (of 2 per 64-wide stage), lane (g, tig) takes the 8 physical
+// k of 16-byte chunk 2*tig+s of rows g and g+8; its first 4 k feed MMA#0 fragments (a0,a2),
+// the last 4 feed MMA#1. The activation fragments use the identical permutation, so each dot
+// product sums exactly the same products (bank-conflict-free under the 128-byte swizzle).
 // Work item = (active pair, 64/128-row block, K split); split-K partials are reduced in
 // fixed split order by the last CTA to finish a row block (deterministic).
 #include <algorithm>
@@ -234,10 +234,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
   uint32_t off_lo[2], off_hi[2], off_x[2][NT];
 #pragma unroll
   for (int sub = 0; sub < 2; ++sub) {
-    off_lo[sub] = swz(trow_lo, 4 * sub + tig);
-    off_hi[sub] = swz(trow_hi, 4 * sub + tig);
+    // sub-step `sub` of lane tig reads 16-byte chunk 2*tig + sub of its rows: within every
+    // 8-lane LDS phase (rows g, g+1) the chunks {2t+s} ^ g and {2t+s} ^ (g+1) are 8 distinct
+    // bank groups under the 128-byte swizzle -> conflict-free (4*sub + tig would be 2-way)
+    off_lo[sub] = swz(trow_lo, 2 * tig + sub);
+    off_hi[sub] = swz(trow_hi, 2 * tig + sub);
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) off_x[sub][nt] = kWBytes + swz(nt * 8 + g, 4 * sub + tig);
+    for (int nt = 0; nt < NT; ++nt) off_x[sub][nt] = kWBytes + swz(nt * 8 + g, 2 * tig + sub);
   }
   int stage = 0;
   uint32_t phase = 0;

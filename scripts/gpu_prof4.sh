@@ -2,5 +2,5 @@
 cd $GRAFT_REPO_ROOT
 CMD="python bench.py --steps 5 --warmup 3 --no-extra --no-cpu"
 $CMD > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_gemv_tma -s 2 -c 2 -o gpurun_out/prof_gemv5 $CMD > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_gemv_tma -s 2 -c 2 -o gpurun_out/prof_gemv6 $CMD > gpurun_out/ncu_full.log 2>&1
 echo done
