@@ -20,6 +20,7 @@
 // Work item = (active pair, 64/128-row block, K split); split-K partials are reduced in
 // fixed split order by the last CTA to finish a row block (deterministic).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -395,20 +396,33 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
 
 }  // namespace
 
-int gemv_nt_for(int64_t T) { return T <= 8 ? 1 : (T <= 16 ? 2 : (T <= 128 ? 3 : 4)); }
+namespace {
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+}  // namespace
+
+// PUZZLE_GEMV_NT / PUZZLE_GEMV_KS13 / PUZZLE_GEMV_KS2 / PUZZLE_GEMV_ITEMS_PER_CTA override the
+// heuristics below (tuning experiments only; results are identical up to fp32 summation order).
+int gemv_nt_for(int64_t T) {
+  const int forced = env_int("PUZZLE_GEMV_NT", 0);
+  if (forced >= 1 && forced <= 4) return forced;
+  return T <= 8 ? 1 : (T <= 16 ? 2 : (T <= 128 ? 3 : 4));
+}
 
 // Split-K so that there are >= ~6 work items per resident CTA (2 per SM): the dynamic
 // scheduler's tail is then at most one short item.
 void gemv_splits(int d, int f, int max_active, int* ks13, int* ks2) {
-  const int target = num_sms() * 2 * 6;
+  const int target = num_sms() * 2 * env_int("PUZZLE_GEMV_ITEMS_PER_CTA", 6);
   const int items13 = (f / 64) * max_active, items2 = ((d + kRowsPerCta - 1) / kRowsPerCta) * max_active;
   int want13 = (target + items13 - 1) / items13, want2 = (target + items2 - 1) / items2;
   want13 = std::min(std::max(want13, 1), 16);
   want2 = std::min(std::max(want2, 1), 32);
   while (want13 > 1 && d / want13 < 128) --want13;
   while (want2 > 1 && f / want2 < 128) --want2;
-  *ks13 = pick_split(d, want13);
-  *ks2 = pick_split(f, want2);
+  *ks13 = pick_split(d, env_int("PUZZLE_GEMV_KS13", want13));
+  *ks2 = pick_split(f, env_int("PUZZLE_GEMV_KS2", want2));
 }
 
 bool gemv_supported(int d, int f) { return d % 64 == 0 && f % 64 == 0; }
