@@ -39,8 +39,8 @@ constexpr int kStages = 3;
 constexpr int kABytes = BM * BK * 2;  // 32 KB
 constexpr int kBBytes = BN * BK * 2;  // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kThreads = 192;         // 6 warps
-constexpr int kDecodeWarps = 4;
+constexpr int kDecodeWarps = 8;       // also the epilogue warps (2 per TMEM lane quarter)
+constexpr int kThreads = 64 + 32 * kDecodeWarps;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kMaxBuckets = 2 * 256;
 
@@ -53,7 +53,8 @@ struct alignas(8) SmemCtl {
   uint32_t tmem_base;
   int32_t n_buckets;
   int32_t bucket_off[kMaxBuckets + 1];
-  int32_t tile_off[kMaxBuckets + 1];
+  int32_t mtiles[kMaxBuckets];          // M tiles of each bucket
+  int32_t pair_off[kMaxBuckets / 2 + 1];  // first tile of each pair (pair-major tile order)
 };
 
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + sizeof(SmemCtl);
@@ -62,19 +63,25 @@ struct TileInfo {
   int bucket, m_tile, n_block, row0, valid;
 };
 
-__device__ __forceinline__ TileInfo tile_info(const SmemCtl& c, int tile, int mt_total) {
+// Tile order: pair-major, then n-block, then (pos, m-tile). The CTAs of one wave therefore
+// work on a band of n-blocks of ONE pair: the pair's activation rows and that band of its
+// packed weight tiles are re-read from L2, not HBM.
+__device__ __forceinline__ TileInfo tile_info(const SmemCtl& c, int tile, int n_blocks) {
   TileInfo t;
-  t.n_block = tile / mt_total;
-  const int rem = tile - t.n_block * mt_total;
-  int lo = 0, hi = c.n_buckets - 1;  // last b with tile_off[b] <= rem
+  int lo = 0, hi = c.n_buckets / 2 - 1;  // last pair with pair_off[p] <= tile
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (c.tile_off[mid] <= rem) lo = mid; else hi = mid - 1;
+    if (c.pair_off[mid] <= tile) lo = mid; else hi = mid - 1;
   }
-  t.bucket = lo;
-  t.m_tile = rem - c.tile_off[lo];
-  t.row0 = c.bucket_off[lo] + t.m_tile * BM;
-  t.valid = min(BM, c.bucket_off[lo + 1] - t.row0);
+  const int p = lo;
+  const int m0 = c.mtiles[2 * p], m01 = m0 + c.mtiles[2 * p + 1];
+  const int rem = tile - c.pair_off[p];
+  t.n_block = rem / m01;
+  const int r2 = rem - t.n_block * m01;
+  t.bucket = 2 * p + (r2 >= m0);
+  t.m_tile = r2 >= m0 ? r2 - m0 : r2;
+  t.row0 = c.bucket_off[t.bucket] + t.m_tile * BM;
+  t.valid = min(BM, c.bucket_off[t.bucket + 1] - t.row0);
   return t;
 }
 
@@ -110,11 +117,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
   if (threadIdx.x == 0) {
     c.n_buckets = n_buckets;
     int run = 0;
-    for (int b = 0; b < n_buckets; ++b) {
-      c.tile_off[b] = run;
-      run += (c.bucket_off[b + 1] - c.bucket_off[b] + BM - 1) / BM;
+    for (int b = 0; b < n_buckets; ++b) c.mtiles[b] = (c.bucket_off[b + 1] - c.bucket_off[b] + BM - 1) / BM;
+    for (int p = 0; p < n_buckets / 2; ++p) {
+      c.pair_off[p] = run;
+      run += n_blocks * (c.mtiles[2 * p] + c.mtiles[2 * p + 1]);
     }
-    c.tile_off[n_buckets] = run;
+    c.pair_off[n_buckets / 2] = run;
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&c.full[s], 1);
       ptx::mbar_init(&c.dec[s], kDecodeWarps);
@@ -133,8 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = c.tmem_base;
-  const int mt_total = c.tile_off[n_buckets];
-  const int n_tiles = mt_total * n_blocks;
+  const int n_tiles = c.pair_off[n_buckets / 2];
   const int nk = K / BK;
 
   if (warp == 0) {
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const TileInfo t = tile_info(c, tile, mt_total);
+        const TileInfo t = tile_info(c, tile, n_blocks);
         const int pair = t.bucket >> 1;
         for (int kb = 0; kb < nk; ++kb) {
           ptx::mbar_wait(&c.empty[stage], phase ^ 1);
@@ -168,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo t = tile_info(c, tile, mt_total);
+      const TileInfo t = tile_info(c, tile, n_blocks);
       const bool two = t.valid > 128;
       ptx::mbar_wait(&c.tmem_empty, acc_phase ^ 1);
       ptx::tc_fence_after();
@@ -195,12 +202,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     }
   } else {
     // ===================== decode warpgroup + epilogue =====================
-    const int tid = threadIdx.x - 64;  // 0..127
-    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    const int tid = threadIdx.x - 64;      // 0 .. 32*kDecodeWarps-1
+    const int q = warp & 3;                // TMEM lane quarter this warp may access
+    const int ch = (warp - 2) >> 2;        // which half of the columns (2 warps per quarter)
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo t = tile_info(c, tile, mt_total);
+      const TileInfo t = tile_info(c, tile, n_blocks);
       const int pos = t.bucket & 1;
       for (int kb = 0; kb < nk; ++kb) {
         ptx::mbar_wait(&c.full[stage], phase);
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
         const bool ok = m < t.valid;
         const int64_t a = t.row0 + m;
         if (kW13) {
-          for (int j = 0; j < 128; j += 32) {
+          for (int j = ch * 64; j < ch * 64 + 64; j += 32) {
             uint32_t g[32], u[32];
             ptx::tmem_ld_32x32b_x32(tbase + j, g);
             ptx::tmem_ld_32x32b_x32(tbase + 128 + j, u);
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
             }
           }
         } else {
-          for (int j = 0; j < BN; j += 32) {
+          for (int j = ch * 128; j < ch * 128 + 128; j += 32) {
             uint32_t v[32];
             ptx::tmem_ld_32x32b_x32(tbase + j, v);
             ptx::tmem_ld_wait();
