@@ -85,18 +85,40 @@ __device__ __forceinline__ TileInfo tile_info(const SmemCtl& c, int tile, int n_
   return t;
 }
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Algorithm 1 in place on one packed B stage (shared-space address `b_tile`): elementwise, so
+// the TMA's swizzled layout is preserved. Shifts/adds on the FMA pipe (register multipliers).
 template <int POS>
-__device__ __forceinline__ void decode_tile(uint8_t* b_tile, int tid) {
-  uint4* p = reinterpret_cast<uint4*>(b_tile);
-#pragma unroll 4
-  for (int i = tid; i < kBBytes / 16; i += kDecodeWarps * 32) {
-    uint4 v = p[i];
-    v.x = decode2<POS>(v.x);
-    v.y = decode2<POS>(v.y);
-    v.z = decode2<POS>(v.z);
-    v.w = decode2<POS>(v.w);
-    p[i] = v;
+__device__ __forceinline__ uint32_t dec_word(uint32_t w, uint32_t one, uint32_t two, uint32_t four, uint32_t eight) {
+  const uint32_t b0 = imad(w & 0x8FFF8FFFu, one, 0x38003800u);
+  if (POS == 0) return b0 & lane_msb_mask(imul(w, four));
+  return lop3_select_sign(imul(w, two), b0) & lane_msb_mask(imul(w, eight));
+}
+template <int POS>
+__device__ __forceinline__ void decode_tile(uint32_t b_tile, int tid, uint32_t one) {
+  const uint32_t two = one * 2u, four = one * 4u, eight = one * 8u;
+  constexpr int kPer = kBBytes / 16 / (kDecodeWarps * 32);  // uint4 per thread per stage
+  uint4 v[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) v[j] = lds128(b_tile + (uint32_t)(tid + j * kDecodeWarps * 32) * 16u);
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    v[j].x = dec_word<POS>(v[j].x, one, two, four, eight);
+    v[j].y = dec_word<POS>(v[j].y, one, two, four, eight);
+    v[j].z = dec_word<POS>(v[j].z, one, two, four, eight);
+    v[j].w = dec_word<POS>(v[j].w, one, two, four, eight);
   }
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) sts128(b_tile + (uint32_t)(tid + j * kDecodeWarps * 32) * 16u, v[j]);
 }
 
 template <bool kW13>
@@ -105,10 +127,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     const __grid_constant__ CUtensorMap tmap_b,  // packed w13 [P*2*f][d] or w2 [P*d][f] u16
     const int32_t* __restrict__ bucket_off, int n_buckets, int K, int f, int d, int n_blocks,
     uint16_t* __restrict__ h_out,  // w13: [n_assign][f] bf16
-    float* __restrict__ y_out) {   // w2:  [n_assign][d] f32
+    float* __restrict__ y_out,     // w2:  [n_assign][d] f32
+    uint32_t mul_one) {            // = 1, opaque to ptxas (keeps decode shifts on the FMA pipe)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   SmemCtl& c = *reinterpret_cast<SmemCtl*>(smem + (size_t)kStages * kStageBytes);
+  const uint32_t smem_base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;  // shared-window address of smem
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // ---- setup: bucket / tile offsets, barriers, TMEM ----
@@ -212,8 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       const int pos = t.bucket & 1;
       for (int kb = 0; kb < nk; ++kb) {
         ptx::mbar_wait(&c.full[stage], phase);
-        uint8_t* sb = smem + (size_t)stage * kStageBytes + kABytes;
-        if (pos == 0) decode_tile<0>(sb, tid); else decode_tile<1>(sb, tid);
+        const uint32_t sb = smem_base + (uint32_t)stage * kStageBytes + kABytes;
+        if (pos == 0) decode_tile<0>(sb, tid, mul_one); else decode_tile<1>(sb, tid, mul_one);
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&c.dec[stage]);
@@ -295,13 +319,13 @@ int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int 
   {
     ProfScope _ps("w13_tc", stream);
     k_tc_experts<true><<<grid, kThreads, kSmemBytes, stream>>>(ta13, tb13, bucket_off, 2 * n_pairs, d, f, d,
-                                                               f / (BN / 2), h, nullptr);
+                                                               f / (BN / 2), h, nullptr, 1u);
   }
   if ((rc = cuda_check(cudaGetLastError(), "w13_tc launch"))) return rc;
   {
     ProfScope _ps("w2_tc", stream);
     k_tc_experts<false><<<grid, kThreads, kSmemBytes, stream>>>(ta2, tb2, bucket_off, 2 * n_pairs, f, f, d,
-                                                                d / BN, nullptr, y);
+                                                                d / BN, nullptr, y, 1u);
   }
   return cuda_check(cudaGetLastError(), "w2_tc launch");
 }
