@@ -25,7 +25,7 @@ const char* last_error_cstr();
 int launch_combine(const float*, const int32_t*, const float*, int64_t, int, int, const uint16_t*,
                    uint16_t*, cudaStream_t);
 int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16_t*, cudaStream_t);
-int gemv_nt_for(int64_t T);
+int gemv_nt_for(int64_t T, int k, int E);
 bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
                       uint16_t*, float*, cudaStream_t);
@@ -153,7 +153,7 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
     path = (T > kGemvMaxTokens && tc_supported(L->d_model, L->d_ff)) ? PUZZLE_PATH_TC : PUZZLE_PATH_GEMV;
   p.path = path;
   if (path == PUZZLE_PATH_GEMV) {
-    p.nt = gemv_nt_for(T);
+    p.nt = gemv_nt_for(T, k, L->n_experts);
     gemv_splits(L->d_model, L->d_ff, std::max(p.max_active, 1), &p.ks13, &p.ks2);
   }
   return p;
@@ -411,7 +411,7 @@ int puzzle_moe_experts(const puzzle_moe_layer* L, const uint16_t* x_rows, const 
     return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d_model % 256 == 0 and d_ff % 128 == 0");
   // Every pair may be touched: plan with T = n_assign, k = 1 (max_active = min(P, n_assign)).
   Plan plan = make_plan(L, n_assign, 1, path);
-  if (plan.path == PUZZLE_PATH_GEMV) plan.nt = gemv_nt_for(std::min<int64_t>(n_assign, 64));
+  if (plan.path == PUZZLE_PATH_GEMV) plan.nt = gemv_nt_for(std::min<int64_t>(n_assign, 64), 2, 2);
   const Layout lay = make_layout(L, plan);
   if (!ws || ws_bytes < lay.total) return fail(PUZZLE_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = (cudaStream_t)stream;

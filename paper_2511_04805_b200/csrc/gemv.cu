@@ -20,6 +20,7 @@
 // Work item = (active pair, 64/128-row block, K split); split-K partials are reduced in
 // fixed split order by the last CTA to finish a row block (deterministic).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -405,16 +406,22 @@ int env_int(const char* name, int dflt) {
 
 // PUZZLE_GEMV_NT / PUZZLE_GEMV_KS13 / PUZZLE_GEMV_KS2 / PUZZLE_GEMV_ITEMS_PER_CTA override the
 // heuristics below (tuning experiments only; results are identical up to fp32 summation order).
-int gemv_nt_for(int64_t T) {
+// n-tiles (8 tokens each) per position per pass: sized for a typical bucket of a uniform
+// router, mean mu = T*k/E tokens, so that a second pass (re-reading the item's weights from L2)
+// is rare: ceil((mu + 1.5 sqrt(mu) + 1) / 8), capped by the batch itself.
+int gemv_nt_for(int64_t T, int k, int E) {
   const int forced = env_int("PUZZLE_GEMV_NT", 0);
   if (forced >= 1 && forced <= 4) return forced;
-  return T <= 8 ? 1 : (T <= 16 ? 2 : (T <= 128 ? 3 : 4));
+  const double mu = (double)T * k / E;
+  int nt = (int)ceil((mu + 1.5 * sqrt(mu) + 1.0) / 8.0);
+  nt = std::min(nt, (int)((T + 7) / 8));
+  return std::max(1, std::min(nt, 4));
 }
 
 // Split-K so that there are >= ~6 work items per resident CTA (2 per SM): the dynamic
 // scheduler's tail is then at most one short item.
 void gemv_splits(int d, int f, int max_active, int* ks13, int* ks2) {
-  const int target = num_sms() * 2 * env_int("PUZZLE_GEMV_ITEMS_PER_CTA", 6);
+  const int target = num_sms() * 2 * env_int("PUZZLE_GEMV_ITEMS_PER_CTA", 2);
   const int items13 = (f / 64) * max_active, items2 = ((d + kRowsPerCta - 1) / kRowsPerCta) * max_active;
   int want13 = (target + items13 - 1) / items13, want2 = (target + items2 - 1) / items2;
   want13 = std::min(std::max(want13, 1), 16);
