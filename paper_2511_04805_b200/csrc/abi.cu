@@ -29,7 +29,7 @@ int gemv_nt_for(int64_t T, int k, int E);
 bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
                       uint16_t*, float*, cudaStream_t);
-void gemv_splits(int d, int f, int max_active, int* ks13, int* ks2);
+void gemv_splits(int d, int f, int max_active, int64_t n_assign, int* ks13, int* ks2);
 int launch_gemv_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*,
                         const int32_t*, const int32_t*, int, int64_t, int, int, int, float*, float*, int32_t*,
                         int32_t*, int32_t*, uint16_t*, float*, cudaStream_t);
@@ -154,7 +154,7 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   p.path = path;
   if (path == PUZZLE_PATH_GEMV) {
     p.nt = gemv_nt_for(T, k, L->n_experts);
-    gemv_splits(L->d_model, L->d_ff, std::max(p.max_active, 1), &p.ks13, &p.ks2);
+    gemv_splits(L->d_model, L->d_ff, std::max(p.max_active, 1), p.n_assign, &p.ks13, &p.ks2);
   }
   return p;
 }

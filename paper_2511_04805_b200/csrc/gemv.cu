@@ -184,8 +184,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
     const int n_items = n_active * per_pair;
     int stage = 0;
     uint32_t phase = 0;
+    // the claim of the NEXT item is issued before the current one streams, so the atomic's
+    // round trip overlaps the TMA traffic instead of draining the ring
+    int next = atomicAdd(work_ctr, 1);
     for (;;) {
-      const int item = atomicAdd(work_ctr, 1);
+      const int item = next;
+      if (item < n_items) next = atomicAdd(work_ctr, 1);
       if (item >= n_items) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         hdr[stage] = make_int4(-1, 0, 0, 0);
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
         const uint32_t bytes = kWBytes + (a0 ? C::kXBytes : 0) + (a1 ? C::kXBytes : 0);
         for (int kb = 0; kb < nk; ++kb) {
           const int kc = kss * kchunk + kb * kBK;
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_wait_sleep(&empty[stage], phase ^ 1, 2000);
           uint8_t* st = smem + (size_t)stage * C::kStageBytes;
           hdr[stage] = make_int4(item, base, kb, 0);
           ptx::mbar_arrive_expect_tx(&full[stage], bytes);
@@ -418,10 +422,13 @@ int gemv_nt_for(int64_t T, int k, int E) {
   return std::max(1, std::min(nt, 4));
 }
 
-// Split-K so that there are >= ~6 work items per resident CTA (2 per SM): the dynamic
-// scheduler's tail is then at most one short item.
-void gemv_splits(int d, int f, int max_active, int* ks13, int* ks2) {
-  const int target = num_sms() * 2 * env_int("PUZZLE_GEMV_ITEMS_PER_CTA", 2);
+// Split-K so that each resident CTA (2 per SM) gets several work items: the dynamic scheduler's
+// tail is at most one item. Partials cost n_assign * ks * width floats, so small batches (where
+// they are negligible) split finer than large ones.
+void gemv_splits(int d, int f, int max_active, int64_t n_assign, int* ks13, int* ks2) {
+  (void)n_assign;  // (finer splits for small batches measured slower: per-item overheads dominate)
+  const int per_cta = env_int("PUZZLE_GEMV_ITEMS_PER_CTA", 2);
+  const int target = num_sms() * 2 * per_cta;
   const int items13 = (f / 64) * max_active, items2 = ((d + kRowsPerCta - 1) / kRowsPerCta) * max_active;
   int want13 = (target + items13 - 1) / items13, want2 = (target + items2 - 1) / items2;
   want13 = std::min(std::max(want13, 1), 16);

@@ -41,6 +41,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Same, but the waiting thread may be suspended by the hardware for up to `ns` nanoseconds per
+// probe instead of re-issuing it (for producers that mostly wait on slow consumers).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+  }
+}
 
 // ---------------------------------------------------------------- proxies / fences
 // generic-proxy shared-memory writes -> visible to the async proxy (tensor core / TMA)
