@@ -43,7 +43,7 @@ struct Cfg {
   static constexpr int kXRows = 8 * NT;             // tokens per position per pass
   static constexpr int kXBytes = kXRows * kBK * 2;  // per position
   static constexpr int kStageBytes = kWBytes + 2 * kXBytes;
-  static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256 + 4 * (2 * kMaxExperts + 8);
   static_assert(kSmem * 2 <= 227 * 1024, "two CTAs per SM");
 };
 
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
     const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb, int ks,
     int64_t n_assign_cap, float* __restrict__ part, int32_t* __restrict__ counters,
     int32_t* __restrict__ work_ctr, uint16_t* __restrict__ h_out, float* __restrict__ y_out,
-    uint32_t mul_one) {
+    uint32_t mul_one, int n_bucket_pairs) {
   using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
   uint64_t* empty = full + kStages;
   int4* hdr = reinterpret_cast<int4*>(empty + kStages);  // per-stage {item, pass base, kb, 0}
   int* s_last = reinterpret_cast<int*>(hdr + kStages);
+  int32_t* s_off = s_last + 4;                   // bucket_off[0 .. 2P], cached once
+  int32_t* s_active = s_off + kMaxExperts + 1;   // active_pairs[0 .. n_active)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -170,8 +172,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
     ptx::tma_prefetch_desc(&tm_w);
     ptx::tma_prefetch_desc(&tm_x);
   }
-  __syncthreads();
+  // routing metadata in shared memory: per-item lookups stay on-chip (no dependent global
+  // loads between one item's last TMA and the next item's first)
   const int n_active = *n_active_ptr;
+  for (int i = threadIdx.x; i < n_active; i += blockDim.x) s_active[i] = active_pairs[i];
+  for (int i = threadIdx.x; i <= 2 * n_bucket_pairs; i += blockDim.x) s_off[i] = bucket_off[i];
+  __syncthreads();
   const int per_pair = n_rb * ks;
   const int kchunk = K / ks;
   const int nk = kchunk / kBK;
@@ -198,8 +204,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
       }
       const int z = item / per_pair;
       const int rb = (item / ks) % n_rb, kss = item % ks;
-      const int p = active_pairs[z];
-      const PairTokens pt = load_pair(bucket_off, p);
+      const int p = s_active[z];
+      const PairTokens pt = load_pair(s_off, p);
       const int maxcnt = max(pt.cnt0, pt.cnt1);
       const int wrow = kW13 ? p * 2 * f + rb * (kRowsPerCta / 2) : p * d + rb * kRowsPerCta;
       for (int base = 0; base < maxcnt; base += C::kXRows) {
@@ -258,8 +264,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
     const int item = h0.x;
     const int z = item / per_pair;
     const int rb = (item / ks) % n_rb, kss = item % ks;
-    const int p = active_pairs[z];
-    const PairTokens pt = load_pair(bucket_off, p);
+    const int p = s_active[z];
+    const PairTokens pt = load_pair(s_off, p);
     const int maxcnt = max(pt.cnt0, pt.cnt1);
     // output features of fragment rows g and g+8
     const int ofeat_lo = kW13 ? rb * (kRowsPerCta / 2) + cw * 8 + g : rb * kRowsPerCta + cw * 16 + g;
@@ -324,17 +330,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
     }
     if (ks > 1) {
       // ---- the last of the ks CTAs of this (pair, row block) reduces in split order ----
-      __threadfence();
+      // (the barrier orders every consumer's partial stores before thread 32's gpu-scope
+      //  fence, which is cumulative, so one fence publishes them all)
       named_bar_sync(1, kConsumerWarps * 32);
       const int ctr = p * n_rb + rb;
       if (threadIdx.x == 32) {
+        __threadfence();
         const int prev = atomicAdd(&counters[ctr], 1);
         *s_last = (prev == ks - 1);
         if (*s_last) counters[ctr] = 0;  // ready for the next call on this stream
       }
+      if (threadIdx.x == 32 && *s_last) __threadfence();  // acquire side of the counter
       named_bar_sync(1, kConsumerWarps * 32);
       if (*s_last) {
-        __threadfence();
         const int row_base = kW13 ? rb * (kRowsPerCta / 2) : rb * kRowsPerCta;
         const int rows = kW13 ? kRowsPerCta / 2 : min(kRowsPerCta, d - row_base);  // multiple of 4
         const int q4 = rows / 4;
@@ -381,7 +389,8 @@ int pick_split(int K, int want) {
 template <int NT, bool kW13>
 int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* bucket_off, const int32_t* active,
                const int32_t* n_active, int K, int f, int d, int n_rb, int ks, int max_active, int64_t n_assign_cap,
-               float* part, int32_t* counters, int32_t* work_ctr, uint16_t* h, float* y, cudaStream_t stream) {
+               float* part, int32_t* counters, int32_t* work_ctr, uint16_t* h, float* y, int n_pairs,
+               cudaStream_t stream) {
   using C = Cfg<NT>;
   auto kern = k_gemv_tma<NT, kW13>;
   static bool attr = false;
@@ -394,7 +403,7 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
   {
     ProfScope _ps(kW13 ? "w13_gemv" : "w2_gemv", stream);
     kern<<<grid, kThreads, C::kSmem, stream>>>(tw, tx, bucket_off, active, n_active, K, f, d, n_rb, ks,
-                                               n_assign_cap, part, counters, work_ctr, h, y, 1u);
+                                               n_assign_cap, part, counters, work_ctr, h, y, 1u, n_pairs);
   }
   return cuda_check(cudaGetLastError(), kW13 ? "w13_gemv launch" : "w2_gemv launch");
 }
@@ -459,10 +468,11 @@ int launch_gemv_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, in
 #define PZ_GO(NT)                                                                                             \
   do {                                                                                                        \
     if ((rc = launch_one<NT, true>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, ks13,        \
-                                   max_active, n_assign_cap, part13, counters13, work_ctrs, h, y, stream))) \
+                                   max_active, n_assign_cap, part13, counters13, work_ctrs, h, y, n_pairs,     \
+                                   stream)))                                                                  \
       return rc;                                                                                              \
     return launch_one<NT, false>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, ks2, max_active, \
-                                 n_assign_cap, part2, counters2, work_ctrs + 1, h, y, stream);               \
+                                 n_assign_cap, part2, counters2, work_ctrs + 1, h, y, n_pairs, stream);      \
   } while (0)
   if (nt == 1) PZ_GO(1);
   if (nt == 2) PZ_GO(2);
