@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/puzzlemoe.h"
 
@@ -31,6 +32,30 @@ struct ProfScope {
   ProfScope(const char* name, cudaStream_t st) : s(st) { prof_mark_begin(name, st); }
   ~ProfScope() { prof_mark_end(s); }
 };
+
+// ---- Programmatic Dependent Launch (the forward's kernel chain) ----
+// A kernel launched with launch_pdl may start (prologue: barrier init, descriptor prefetch)
+// while its predecessor on the stream is still finishing; pdl_wait() blocks until every
+// prerequisite grid has completed and its writes are visible (a no-op for a normal launch).
+// pdl_trigger() lets the NEXT kernel's CTAs start launching early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---- packed word layout (Algorithm 1) ----
 // bit15 S_i | bit14 S_j | bit13 M_i | bit12 M_j | bits 11..7 e' = e-112 | bits 6..0 mantissa

@@ -136,6 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // ---- setup: bucket / tile offsets, barriers, TMEM ----
+  pdl_wait();
+  pdl_trigger();
   for (int i = threadIdx.x; i <= n_buckets; i += blockDim.x) c.bucket_off[i] = bucket_off[i];
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -318,14 +320,16 @@ int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int 
   const int grid = num_sms();
   {
     ProfScope _ps("w13_tc", stream);
-    k_tc_experts<true><<<grid, kThreads, kSmemBytes, stream>>>(ta13, tb13, bucket_off, 2 * n_pairs, d, f, d,
-                                                               f / (BN / 2), h, nullptr, 1u);
+    cudaError_t e = launch_pdl(k_tc_experts<true>, dim3(grid), dim3(kThreads), kSmemBytes, stream, ta13, tb13,
+                               bucket_off, 2 * n_pairs, d, f, d, f / (BN / 2), h, (float*)nullptr, 1u);
+    if (e != cudaSuccess) return cuda_check(e, "w13_tc launch");
   }
   if ((rc = cuda_check(cudaGetLastError(), "w13_tc launch"))) return rc;
   {
     ProfScope _ps("w2_tc", stream);
-    k_tc_experts<false><<<grid, kThreads, kSmemBytes, stream>>>(ta2, tb2, bucket_off, 2 * n_pairs, f, f, d,
-                                                                d / BN, nullptr, y, 1u);
+    cudaError_t e = launch_pdl(k_tc_experts<false>, dim3(grid), dim3(kThreads), kSmemBytes, stream, ta2, tb2,
+                               bucket_off, 2 * n_pairs, f, f, d, d / BN, (uint16_t*)nullptr, y, 1u);
+    if (e != cudaSuccess) return cuda_check(e, "w2_tc launch");
   }
   return cuda_check(cudaGetLastError(), "w2_tc launch");
 }

@@ -172,6 +172,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tma(
     ptx::tma_prefetch_desc(&tm_w);
     ptx::tma_prefetch_desc(&tm_x);
   }
+  pdl_wait();     // route / gather / previous projection complete and visible
+  pdl_trigger();  // the next kernel may begin its prologue as CTAs of this one retire
   // routing metadata in shared memory: per-item lookups stay on-chip (no dependent global
   // loads between one item's last TMA and the next item's first)
   const int n_active = *n_active_ptr;
@@ -402,8 +404,9 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
   const int grid = std::min(n_items, 2 * num_sms());
   {
     ProfScope _ps(kW13 ? "w13_gemv" : "w2_gemv", stream);
-    kern<<<grid, kThreads, C::kSmem, stream>>>(tw, tx, bucket_off, active, n_active, K, f, d, n_rb, ks,
-                                               n_assign_cap, part, counters, work_ctr, h, y, 1u, n_pairs);
+    cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kThreads), C::kSmem, stream, tw, tx, bucket_off, active, n_active,
+                               K, f, d, n_rb, ks, n_assign_cap, part, counters, work_ctr, h, y, 1u, n_pairs);
+    if (e != cudaSuccess) return cuda_check(e, kW13 ? "w13_gemv launch" : "w2_gemv launch");
   }
   return cuda_check(cudaGetLastError(), kW13 ? "w13_gemv launch" : "w2_gemv launch");
 }

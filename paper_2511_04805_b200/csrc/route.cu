@@ -128,6 +128,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_route_small(
   __shared__ int32_t s_off[kMaxExperts + 1];
   __shared__ int32_t s_bucket[kSmallMaxAssign];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  pdl_wait();  // the previous forward may still be using this workspace
+  pdl_trigger();
   // split-K arrival counters / scheduler counters of the expert kernels that follow
   for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero_ptr[i] = 0;
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_slot[e] = expert_slot[e];
@@ -175,6 +177,8 @@ __global__ void __launch_bounds__(kBigThreads) k_route_topk(const float* __restr
   __shared__ int32_t s_count[kMaxExperts];
   __shared__ int32_t s_slot[kMaxExperts];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_trigger();
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_slot[e] = expert_slot[e];
   for (int b = threadIdx.x; b < n_buckets; b += blockDim.x) s_count[b] = 0;
   __syncthreads();
@@ -203,6 +207,8 @@ __global__ void __launch_bounds__(64) k_route_scan(const int32_t* __restrict__ g
   __shared__ int32_t s_count[kMaxExperts];
   __shared__ int32_t s_off[kMaxExperts + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_trigger();
   for (int b = threadIdx.x; b < n_buckets; b += blockDim.x) s_count[b] = g_count[b];
   __syncthreads();
   if (warp == 0) {
@@ -227,6 +233,8 @@ __global__ void __launch_bounds__(kBigThreads) k_route_scatter(
   __shared__ int32_t s_count[kMaxExperts];
   __shared__ int32_t s_base[kMaxExperts];
   __shared__ int32_t s_slotof[kScatterChunk];
+  pdl_wait();
+  pdl_trigger();
   for (int b = threadIdx.x; b < n_buckets; b += blockDim.x) s_count[b] = 0;
   __syncthreads();
   const int64_t i0 = (int64_t)blockIdx.x * kScatterChunk;
@@ -265,6 +273,8 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y,
                                                  uint16_t* __restrict__ out) {
   const int64_t t = blockIdx.y;
   const int c4 = blockIdx.x * blockDim.x + threadIdx.x;  // index of a 4-column group
+  pdl_wait();
+  pdl_trigger();
   if (c4 * 4 >= d) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (residual != nullptr) {
@@ -291,6 +301,8 @@ __global__ void __launch_bounds__(256) k_gather_rows(const uint16_t* __restrict_
                                                      const int32_t* __restrict__ index, int64_t n_rows,
                                                      int64_t cols, uint16_t* __restrict__ dst) {
   const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  pdl_wait();
+  pdl_trigger();
   if (i >= n_rows) return;
   const int lane = threadIdx.x & 31;
   const int64_t s = index[i];
@@ -331,9 +343,10 @@ int launch_route(const float* logits, int64_t T, int E, int k, int renorm, const
   if (route_is_small(T, k)) {
     {
       ProfScope _ps("route", stream);
-      k_route_small<<<1, kSmallThreads, 0, stream>>>(logits, (int)T, E, k, renorm, expert_slot, nb, topk_idx,
-                                                     topk_gate, bucket_off, assign_token, assign_of, active_pairs,
-                                                     n_active, zero_ptr, n_zero);
+      cudaError_t e = launch_pdl(k_route_small, dim3(1), dim3(kSmallThreads), 0, stream, logits, (int)T, E, k, renorm,
+                                 expert_slot, nb, topk_idx, topk_gate, bucket_off, assign_token, assign_of,
+                                 active_pairs, n_active, zero_ptr, n_zero);
+      if (e != cudaSuccess) return cuda_check(e, "route launch");
     }
     return cuda_check(cudaGetLastError(), "route launch");
   }
@@ -347,18 +360,26 @@ int launch_route(const float* logits, int64_t T, int E, int k, int renorm, const
   const int per_cta = kTokensPerWarp * (kBigThreads / 32);
   {
     ProfScope _ps("route_topk", stream);
-    k_route_topk<<<(unsigned)((T + per_cta - 1) / per_cta), kBigThreads, 0, stream>>>(
-        logits, (int)T, E, k, renorm, expert_slot, nb, topk_idx, topk_gate, g_count);
+    if ((rc = cuda_check(launch_pdl(k_route_topk, dim3((unsigned)((T + per_cta - 1) / per_cta)), dim3(kBigThreads), 0,
+                                    stream, logits, (int)T, E, k, renorm, expert_slot, nb, topk_idx, topk_gate, g_count),
+                         "route_topk launch")))
+      return rc;
   }
   {
     ProfScope _ps("route_scan", stream);
-    k_route_scan<<<1, 64, 0, stream>>>(g_count, nb, bucket_off, cursor, active_pairs, n_active);
+    if ((rc = cuda_check(launch_pdl(k_route_scan, dim3(1), dim3(64), 0, stream, (const int32_t*)g_count, nb, bucket_off,
+                                    cursor, active_pairs, n_active),
+                         "route_scan launch")))
+      return rc;
   }
   const int64_t n_assign = T * k;
   {
     ProfScope _ps("route_scatter", stream);
-    k_route_scatter<<<(unsigned)((n_assign + kScatterChunk - 1) / kScatterChunk), kBigThreads, 0, stream>>>(
-        topk_idx, n_assign, k, expert_slot, nb, cursor, assign_token, assign_of, hidden, d, x_perm);
+    if ((rc = cuda_check(launch_pdl(k_route_scatter, dim3((unsigned)((n_assign + kScatterChunk - 1) / kScatterChunk)),
+                                    dim3(kBigThreads), 0, stream, (const int32_t*)topk_idx, n_assign, k, expert_slot, nb,
+                                    cursor, assign_token, assign_of, hidden, d, x_perm),
+                         "route_scatter launch")))
+      return rc;
   }
   if (rows_written) *rows_written = x_perm != nullptr && hidden != nullptr;
   return cuda_check(cudaGetLastError(), "route launch");
@@ -371,7 +392,8 @@ int launch_combine(const float* y, const int32_t* assign_of, const float* gate, 
   dim3 grid((unsigned)((d / 4 + threads - 1) / threads), (unsigned)T);
   {
     ProfScope _ps("combine", stream);
-    k_combine<<<grid, threads, 0, stream>>>(y, assign_of, gate, k, d, residual, out);
+    cudaError_t e = launch_pdl(k_combine, grid, dim3(threads), 0, stream, y, assign_of, gate, k, d, residual, out);
+    if (e != cudaSuccess) return cuda_check(e, "combine launch");
   }
   return cuda_check(cudaGetLastError(), "combine launch");
 }
@@ -381,7 +403,9 @@ int launch_gather_rows(const uint16_t* src, const int32_t* index, int64_t n_rows
   if (n_rows == 0) return PUZZLE_OK;
   {
     ProfScope _ps("gather_rows", stream);
-    k_gather_rows<<<(unsigned)((n_rows + 7) / 8), 256, 0, stream>>>(src, index, n_rows, cols, dst);
+    cudaError_t e = launch_pdl(k_gather_rows, dim3((unsigned)((n_rows + 7) / 8)), dim3(256), 0, stream, src, index, n_rows,
+                               cols, dst);
+    if (e != cudaSuccess) return cuda_check(e, "gather launch");
   }
   return cuda_check(cudaGetLastError(), "gather launch");
 }
