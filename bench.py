@@ -502,6 +502,12 @@ def run_ours(args):
                 line["aux"]["unpacked_bf16_baseline"] = {"error": repr(e)}
             line["aux"]["packer"] = packer_rates(pz, layer, device)
             line["aux"]["sweep"] = sweep(pz, args, device, pk)
+            try:
+                del layer
+                torch.cuda.empty_cache()
+                line["aux"]["stack32"] = stack_runs(pz, args, device, pk)
+            except Exception as e:  # pragma: no cover
+                line["aux"]["stack32"] = {"error": repr(e)}
         if world == 1 and not args.no_cpu:
             try:
                 line["cpu_baseline"] = cpu_oracle_timing(cfg, T)
@@ -597,6 +603,63 @@ def sweep(pz, args, device, pk):
             torch.cuda.empty_cache()
         except Exception as e:  # pragma: no cover
             res.append({"config": name, "batch": T, "error": repr(e)})
+    return res
+
+
+def stack_runs(pz, args, device, pk):
+    """BASELINE.json configs[4] on one B200: the 32-layer Mixtral-8x7B MoE stack at 50%
+    compression (45.1 GB packed), x_{l+1} = x_l + MoE_l(x_l) with fixed per-layer router
+    logits, batch-64 decode (graph replay) and 8192-token prefill."""
+    import torch
+    cfg = synth.CONFIGS["mixtral"]
+    n_layers = 32
+    layers = []
+    for l in range(n_layers):
+        layer, _ = build_layer_gpu(pz, cfg, 90000 + l, device)
+        layers.append(layer)
+    res = []
+    for T in (64, 8192):
+        g = torch.Generator(device=device)
+        g.manual_seed(777 + T)
+        x0 = torch.randn((T, cfg.d_model), generator=g, device=device).to(torch.bfloat16)
+        logits = [torch.randn((T, cfg.n_experts), generator=g, device=device) for _ in range(n_layers)]
+        bufs = [torch.empty_like(x0), torch.empty_like(x0)]
+        ws = [layer.workspace(T, cfg.top_k) for layer in layers[:1]][0]
+        need = max(layer.workspace_size(T, cfg.top_k) for layer in layers)
+        if ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=device)
+
+        def step():
+            x = x0
+            for l, layer in enumerate(layers):
+                out = bufs[l % 2]
+                layer.forward(x, logits[l], cfg.top_k, cfg.renormalize, residual=x, out=out, workspace=ws)
+                x = out
+            return x
+
+        step()
+        torch.cuda.synchronize()
+        run = step
+        if T <= 64 and not args.no_graph:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                step()
+            run = gr.replay
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        K = 20 if T <= 64 else 5
+        ms = timed_steps(run, K) / K
+        row = {"config": "mixtral_stack32", "batch": T, "ms_per_step": ms, "tokens_per_s": T / (ms / 1e3),
+               "layers": n_layers, "packed_gb": sum(l.packed_bytes for l in layers) / 1e9}
+        if T <= 64:
+            row["weight_gbs"] = row["packed_gb"] * 1e9 / (ms / 1e3) / 1e9  # upper bound: all pairs touched at B=64
+        else:
+            fl = 2 * 3 * cfg.d_model * cfg.d_ff * T * cfg.top_k * n_layers
+            row["tflops_step"] = fl / (ms / 1e3) / 1e12
+        res.append(row)
+    del layers
+    torch.cuda.empty_cache()
     return res
 
 

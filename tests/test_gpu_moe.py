@@ -178,3 +178,28 @@ def test_forward_tc_full_size_mixtral_prefill(pz):
     cfg = synth.CONFIGS["mixtral"]
     got, ref = _run(pz, cfg, 4096, pz.PATH_AUTO, sample=4)
     assert_close(got, ref, "mixtral prefill T=4096")
+
+
+def test_residual_stack_matches_chained_oracle(pz):
+    """BASELINE.json config 5 in miniature: x_{l+1} = x_l + MoE_l(x_l) over 3 layers with
+    per-layer logits; the oracle chain is independent (its own bf16-rounded outputs feed it)."""
+    base = synth.MoEConfig("stack", 40, 128, 256, 8, 2, True)
+    T, n_layers = 24, 3
+    x_bits = synth.hidden_bits(base, T, seed=500)
+    x_dev = torch.from_numpy(x_bits.view(np.int16)).cuda().view(torch.bfloat16)
+    ref_bits = x_bits
+    for l in range(n_layers):
+        cfg = synth.MoEConfig(f"stack{l}", 41 + l, 128, 256, 8, 2, True)
+        layer, (w13, w2, slot) = _layer(pz, cfg)
+        lg = synth.router_logits(cfg, T, seed=600 + l)
+        x_dev = layer.forward(x_dev, torch.from_numpy(lg).cuda(), cfg.top_k, cfg.renormalize, residual=x_dev)
+        ref = oracle.moe_forward(w13, w2, slot, ref_bits, lg, cfg.top_k, cfg.renormalize, ref_bits)
+        ref_bits = synth.to_bf16_bits(ref.astype(np.float32))
+    torch.cuda.synchronize()
+    got = x_dev.float().cpu().numpy().astype(np.float64)
+    ref = oracle.bf16_bits_to_f32(ref_bits).astype(np.float64)
+    # DESIGN.md R19: both chains round every layer's output to bf16 independently, so besides
+    # the single-layer bound each layer may contribute one bf16 ulp of |x| (~2^-8 relative)
+    ulp = np.abs(ref) * 2.0 ** -8
+    assert np.all(np.abs(got - ref) <= 2e-2 + n_layers * ulp), np.max(np.abs(got - ref) - n_layers * ulp)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 5e-3
