@@ -33,6 +33,9 @@ void gemv_splits(int d, int f, int max_active, int64_t n_assign, int* ks13, int*
 int launch_gemv_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*,
                         const int32_t*, const int32_t*, int, int64_t, int, int, int, float*, float*, int32_t*,
                         int32_t*, int32_t*, uint16_t*, float*, cudaStream_t);
+int launch_gemv_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*,
+                           const int32_t*, const int32_t*, int, int64_t, int, int, int, float*, float*, int32_t*,
+                           int32_t*, int32_t*, uint16_t*, float*, cudaStream_t);
 
 namespace {
 thread_local std::string g_last_error;
@@ -322,7 +325,14 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
   if (plan.path == PUZZLE_PATH_TC)
     return launch_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, s);
-  return launch_gemv_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off,
+  // decode shapes: tcgen05 with the decoded weights staged in TMEM (gemv_tc.cu); the
+  // register-decode mma.sync kernel (gemv.cu) stays selectable for A/B measurements
+  static const bool use_mma = [] {
+    const char* v = getenv("PUZZLE_GEMV_IMPL");
+    return v && std::string(v) == "mma";
+  }();
+  auto launch = use_mma ? launch_gemv_experts : launch_gemv_tc_experts;
+  return launch(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off,
                              active, n_active, plan.max_active, plan.n_assign, plan.nt, plan.ks13,
                              plan.ks2, at<float>(ws, lay.part13), at<float>(ws, lay.part2),
                              at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2),

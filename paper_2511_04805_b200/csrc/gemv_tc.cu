@@ -1,0 +1,512 @@
+// Decode-shape expert kernels (a4)+(a5) on the 5th-generation tensor cores, weights on the
+// M side ("swap-AB"): D[weight rows x tokens] = W^_pos[rows, K] . X_pos[tokens, K]^T, where
+// W^_pos is the Algorithm-1 decode of the pair's packed words. Each touched pair's
+// packed words are streamed from HBM ONCE and decoded for position 0 and/or 1.
+//
+// Warp-specialised, persistent CTAs (2 per SM, 256 TMEM columns each):
+//   warp 0     producer: one lane claims work items with an atomic (dynamic scheduler) and
+//              issues TMA loads, per 64-wide K stage, of the PACKED 128-row weight tile into a
+//              4-deep W ring and of the tokens' activation rows of both positions (16-row
+//              boxes, <= 32 tokens each per pass) into a 5-deep X ring (128-byte swizzle).
+//              The W ring is released by the decoders as soon as they hold the words in
+//              registers, the X ring by the MMAs' commit, so HBM reads are never held up by
+//              the tensor-core round trip.
+//   warps 2-9  decoders: warp (q = warp % 4, kh) owns tile rows 32q..32q+31 (= the TMEM lanes
+//              it may access) and K half kh of a stage: 4 x LDS.128 (conflict-free under the
+//              swizzle), SWAR Algorithm 1 for the active position(s), tcgen05.st of the bf16
+//              rows into a TMEM A buffer (lane = row, column = k pair). After the last stage of
+//              a pass they are the epilogue (tcgen05.ld of the fp32 accumulators).
+//   warp 1     MMA issuer: one lane issues tcgen05.mma.kind::f16 with A from TMEM and B (the
+//              tokens, N = 16 or 32) from a shared-memory descriptor, accumulators in TMEM.
+// w13 tile rows: quarter q holds 16 gate rows (features f0+16q ..+15) then the same 16
+// features' up rows, so g and u of one d_ff index sit in lanes i and i+16 of ONE warp and
+// SwiGLU needs only a shuffle. w2 tile rows: 128 consecutive d_model rows.
+// TMEM columns: A buffer j (of 3), position p at 64 j + 32 p (64 bf16 k = 32 columns);
+// accumulators of position p at 192 + 32 p (32 fp32 token columns).
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+#include "tmap.cuh"
+
+namespace pz {
+
+namespace {
+
+constexpr int kDecWarps = 8;
+constexpr int kThreads = 64 + 32 * kDecWarps;  // warp 0 producer, warp 1 MMA, warps 2..9 decoders
+constexpr int kBK = 64;                          // K per stage (one 128-byte swizzle row)
+constexpr int kRows = 128;                       // weight rows per tile (UMMA M)
+constexpr int kWBytes = kRows * kBK * 2;         // 16 KB packed words per stage
+constexpr int kNX = 32;                          // tokens per position per pass (UMMA N <= 32)
+constexpr int kBox = 16;                         // rows per TMA box (activations, w13 halves)
+constexpr int kBoxBytes = kBox * kBK * 2;        // 2 KB
+constexpr int kXPos = kNX * kBK * 2;             // 4 KB per position
+constexpr int kXBytes = 2 * kXPos;               // X stage: both positions
+constexpr int kWStages = 4;
+constexpr int kXStages = 5;
+constexpr int kAStages = 3;
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kAccCol = 64 * kAStages;      // 192
+
+struct alignas(16) Ctl {
+  int4 whdr[kWStages];  // {item, pass base, kb, 0}; item -1 = no more work
+  int4 xhdr[kXStages];
+  uint64_t wfull[kWStages], wempty[kWStages], xfull[kXStages], xempty[kXStages];
+  uint64_t a_full[kAStages], a_empty[kAStages], acc_full, acc_empty;
+  uint32_t tmem_base;
+  int s_last;
+  int32_t s_off[kMaxExperts + 1];     // bucket_off[0 .. 2P]
+  int32_t s_active[kMaxExperts / 2];  // active_pairs[0 .. n_active)
+};
+
+constexpr size_t kSmem = 1024 + (size_t)kWStages * kWBytes + (size_t)kXStages * kXBytes + sizeof(Ctl);
+static_assert(2 * (kSmem + 1024) <= 228 * 1024, "two CTAs per SM");
+
+struct PairTokens {
+  int off0, cnt0, off1, cnt1;
+};
+
+__device__ __forceinline__ PairTokens load_pair(const int32_t* off, int p) {
+  PairTokens pt;
+  pt.off0 = off[2 * p];
+  pt.off1 = off[2 * p + 1];
+  pt.cnt0 = pt.off1 - pt.off0;
+  pt.cnt1 = off[2 * p + 2] - pt.off1;
+  return pt;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int4 lds_int4(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+// byte offset of (row, 16-byte chunk) inside a 128-byte-swizzled tile with 128-byte rows
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct Muls {
+  uint32_t one, two, four, eight;
+};
+
+__device__ __forceinline__ uint32_t comp(const uint4& v, int j) { return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w; }
+
+// Exact bf16x2 product (one operand is +-2^k or +-0, no overflow / subnormal): the decode's
+// sign and mask application on the FMA pipe instead of the integer ALU.
+__device__ __forceinline__ uint32_t bf16x2_mul(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// Ring cursor: slot index + mbarrier phase parity.
+struct Ring {
+  int i;
+  uint32_t ph;
+  template <int N>
+  __device__ __forceinline__ void next() {
+    if (++i == N) { i = 0; ph ^= 1; }
+  }
+};
+
+// Pass parameters shared by the MMA warp and the decoders (derived from a stage header).
+struct Pass {
+  int item, base, rb, kss, p;
+  PairTokens pt;
+  int n0, n1;  // tokens of position 0 / 1 in this pass (0 .. kNX)
+};
+
+__device__ __forceinline__ Pass make_pass(const Ctl& c, int4 h, int per_pair, int ks, int n_rb) {
+  Pass s;
+  s.item = h.x;
+  s.base = h.y;
+  const int z = h.x / per_pair;
+  s.rb = (h.x / ks) % n_rb;
+  s.kss = h.x % ks;
+  s.p = c.s_active[z];
+  s.pt = load_pair(c.s_off, s.p);
+  s.n0 = min(max(s.pt.cnt0 - s.base, 0), kNX);
+  s.n1 = min(max(s.pt.cnt1 - s.base, 0), kNX);
+  return s;
+}
+
+// One pass of the decoders over nk stages for the active position(s) (MODE bit 0 = pos 0,
+// bit 1 = pos 1): decode this thread's 32 packed words per stage (16 registers, k = 32 kh ..
+// 32 kh + 31 of its row) and store the bf16 rows into the TMEM A buffer: register r of chunk
+// i -> column 16 kh + 4 i + r (k pair 32 kh + 8 i + 2 r).
+template <int MODE>
+__device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t lane_tmem, const uint32_t (&w_off)[4],
+                                            int kh, int nk, Ring& w, Ring& a, const Muls& mu) {
+  const int lane = threadIdx.x & 31;
+  for (int kb = 0; kb < nk; ++kb) {
+    if (kb) ptx::mbar_wait(&c.wfull[w.i], w.ph);
+    const uint32_t st = smem_w + (uint32_t)w.i * kWBytes;
+    uint4 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = lds128(st + w_off[i]);
+    uint32_t d0[16], d1[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t x = comp(v[i], j);
+        // |W^| * 2^63: exponent field e' + 112 + 63 (never carries out of a lane)
+        const uint32_t mag = imad(x & 0x0FFF0FFFu, mu.one, 0x57805780u);
+        // sign S_i (bit 15) + mask M_i (bit 13) = +-2^-63 or +-0 as bf16: one exact product
+        if (MODE & 1) d0[4 * i + j] = bf16x2_mul(mag, x & 0xA000A000u);
+        // S_j (bit 14) and M_j (bit 12) shifted to bits 15 / 13
+        if (MODE & 2) d1[4 * i + j] = bf16x2_mul(mag, imul(x, mu.two) & 0xA000A000u);
+      }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&c.wempty[w.i]);  // packed words consumed: the slot may refill
+    w.next<kWStages>();
+    ptx::mbar_wait(&c.a_empty[a.i], a.ph ^ 1);
+    ptx::tc_fence_after();
+    const uint32_t t0 = lane_tmem + 64u * a.i + 16u * kh;
+    if (MODE & 1) ptx::tmem_st_32x32b_x16(t0, d0);
+    if (MODE & 2) ptx::tmem_st_32x32b_x16(t0 + 32u, d1);
+    ptx::tmem_st_wait();
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&c.a_full[a.i]);
+    a.next<kAStages>();
+  }
+}
+
+template <bool kW13>
+__global__ void __launch_bounds__(kThreads, 2) k_gemv_tc(
+    const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+    const int32_t* __restrict__ bucket_off, const int32_t* __restrict__ active_pairs,
+    const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb, int ks, int64_t n_assign_cap,
+    float* __restrict__ part, int32_t* __restrict__ counters, int32_t* __restrict__ work_ctr,
+    uint16_t* __restrict__ h_out, float* __restrict__ y_out, uint32_t mul_one, int n_bucket_pairs) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t smem_w = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;  // == smem, shared window
+  const uint32_t smem_x = smem_w + kWStages * kWBytes;
+  Ctl& c = *reinterpret_cast<Ctl*>(smem + (size_t)kWStages * kWBytes + (size_t)kXStages * kXBytes);
+  const uint32_t whdr_s = ptx::smem_u32(&c.whdr[0]), xhdr_s = ptx::smem_u32(&c.xhdr[0]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWStages; ++s) {
+      ptx::mbar_init(&c.wfull[s], 1);
+      ptx::mbar_init(&c.wempty[s], kDecWarps);
+    }
+    for (int s = 0; s < kXStages; ++s) {
+      ptx::mbar_init(&c.xfull[s], 1);
+      ptx::mbar_init(&c.xempty[s], 1);
+    }
+    for (int j = 0; j < kAStages; ++j) {
+      ptx::mbar_init(&c.a_full[j], kDecWarps);
+      ptx::mbar_init(&c.a_empty[j], 1);
+    }
+    ptx::mbar_init(&c.acc_full, 1);
+    ptx::mbar_init(&c.acc_empty, kDecWarps);
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&tm_w);
+    ptx::tma_prefetch_desc(&tm_x);
+  }
+  if (warp == 1) ptx::tmem_alloc<kTmemCols>(&c.tmem_base);
+  pdl_wait();     // route / gather / previous projection complete and visible
+  pdl_trigger();  // the next kernel may begin its prologue as CTAs of this one retire
+  const int n_active = *n_active_ptr;
+  for (int i = threadIdx.x; i < n_active; i += blockDim.x) c.s_active[i] = active_pairs[i];
+  for (int i = threadIdx.x; i <= 2 * n_bucket_pairs; i += blockDim.x) c.s_off[i] = bucket_off[i];
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = c.tmem_base;
+  const int per_pair = n_rb * ks;
+  const int kchunk = K / ks;
+  const int nk = kchunk / kBK;
+
+  if (warp == 0) {
+    // ============================== producer ==============================
+    if (lane != 0) return;
+    const int n_items = n_active * per_pair;
+    Ring w{0, 0}, x{0, 0};
+    int next = atomicAdd(work_ctr, 1);  // the next claim overlaps the current item's stream
+    for (;;) {
+      const int item = next;
+      if (item < n_items) next = atomicAdd(work_ctr, 1);
+      if (item >= n_items) {
+        ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
+        ptx::mbar_wait(&c.xempty[x.i], x.ph ^ 1);
+        c.whdr[w.i] = make_int4(-1, 0, 0, 0);
+        c.xhdr[x.i] = make_int4(-1, 0, 0, 0);
+        ptx::mbar_arrive(&c.wfull[w.i]);  // completes the phase without data: "no more work"
+        ptx::mbar_arrive(&c.xfull[x.i]);
+        break;
+      }
+      const int z = item / per_pair;
+      const int rb = (item / ks) % n_rb, kss = item % ks;
+      const int p = c.s_active[z];
+      const PairTokens pt = load_pair(c.s_off, p);
+      const int maxcnt = max(pt.cnt0, pt.cnt1);
+      const int wrow = kW13 ? p * 2 * f + rb * (kRows / 2) : p * d + rb * kRows;
+      for (int base = 0; base < maxcnt; base += kNX) {
+        const int l0 = (min(max(pt.cnt0 - base, 0), kNX) + kBox - 1) / kBox;
+        const int l1 = (min(max(pt.cnt1 - base, 0), kNX) + kBox - 1) / kBox;
+        const uint32_t xbytes = (uint32_t)(l0 + l1) * kBoxBytes;
+        for (int kb = 0; kb < nk; ++kb) {
+          const int kc = kss * kchunk + kb * kBK;
+          const int4 hv = make_int4(item, base, kb, 0);
+          ptx::mbar_wait_sleep(&c.wempty[w.i], w.ph ^ 1, 500);
+          c.whdr[w.i] = hv;
+          uint8_t* sw = smem + (size_t)w.i * kWBytes;
+          ptx::mbar_arrive_expect_tx(&c.wfull[w.i], kWBytes);
+          if (kW13) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // quarter q: 16 gate rows, then the same features' up rows
+              ptx::tma_load_2d(sw + q * 2 * kBoxBytes, &tm_w, &c.wfull[w.i], kc, wrow + kBox * q);
+              ptx::tma_load_2d(sw + q * 2 * kBoxBytes + kBoxBytes, &tm_w, &c.wfull[w.i], kc, wrow + f + kBox * q);
+            }
+          } else {
+            ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
+          }
+          w.next<kWStages>();
+          ptx::mbar_wait_sleep(&c.xempty[x.i], x.ph ^ 1, 500);
+          c.xhdr[x.i] = hv;
+          uint8_t* sx = smem + (size_t)kWStages * kWBytes + (size_t)x.i * kXBytes;
+          ptx::mbar_arrive_expect_tx(&c.xfull[x.i], xbytes);
+          for (int i = 0; i < l0; ++i)
+            ptx::tma_load_2d(sx + i * kBoxBytes, &tm_x, &c.xfull[x.i], kc, pt.off0 + base + kBox * i);
+          for (int i = 0; i < l1; ++i)
+            ptx::tma_load_2d(sx + kXPos + i * kBoxBytes, &tm_x, &c.xfull[x.i], kc, pt.off1 + base + kBox * i);
+          x.next<kXStages>();
+        }
+      }
+    }
+    return;
+  }
+
+  if (warp == 1) {
+    // ============================== MMA issuer ==============================
+    Ring x{0, 0}, a{0, 0};
+    uint32_t accph = 0;
+    for (;;) {
+      ptx::mbar_wait(&c.xfull[x.i], x.ph);
+      const int4 h = lds_int4(xhdr_s + 16u * x.i);
+      if (h.x < 0) break;
+      const Pass s = make_pass(c, h, per_pair, ks, n_rb);
+      const uint32_t id0 = ptx::idesc_bf16_f32(128, (uint32_t)((s.n0 + 15) & ~15));
+      const uint32_t id1 = ptx::idesc_bf16_f32(128, (uint32_t)((s.n1 + 15) & ~15));
+      ptx::mbar_wait(&c.acc_empty, accph ^ 1);  // the previous pass's epilogue drained TMEM
+      ptx::tc_fence_after();
+      for (int kb = 0; kb < nk; ++kb) {
+        if (kb) ptx::mbar_wait(&c.xfull[x.i], x.ph);
+        ptx::mbar_wait(&c.a_full[a.i], a.ph);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t xs = smem_x + (uint32_t)x.i * kXBytes;
+          const uint32_t ta = tmem + 64u * a.i;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint32_t acc = (kb | kk) != 0;
+            if (s.n0 > 0) ptx::mma_bf16_ts(tmem + kAccCol, ta + 8 * kk, ptx::smem_desc_sw128(xs + 32 * kk), id0, acc);
+            if (s.n1 > 0)
+              ptx::mma_bf16_ts(tmem + kAccCol + 32, ta + 32 + 8 * kk, ptx::smem_desc_sw128(xs + kXPos + 32 * kk), id1,
+                               acc);
+          }
+          ptx::mma_commit(&c.a_empty[a.i]);
+          ptx::mma_commit(&c.xempty[x.i]);
+          if (kb == nk - 1) ptx::mma_commit(&c.acc_full);
+        }
+        __syncwarp();
+        x.next<kXStages>();
+        a.next<kAStages>();
+      }
+      accph ^= 1;
+    }
+  } else {
+    // ============================== decoders + epilogue ==============================
+    const int dtid = threadIdx.x - 64;
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int kh = (warp - 2) >> 2;  // K half of a stage; position handled in the epilogue
+    const int row = 32 * q + lane;   // tile row == TMEM lane
+    const uint32_t lane_tmem = tmem + ((uint32_t)(32 * q) << 16);
+    const Muls mu{mul_one, mul_one * 2u, mul_one * 4u, mul_one * 8u};
+    uint32_t w_off[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w_off[i] = swz(row, 4 * kh + i);
+    Ring w{0, 0}, a{0, 0};
+    uint32_t accph = 0;
+    for (;;) {
+      ptx::mbar_wait(&c.wfull[w.i], w.ph);
+      const int4 h = lds_int4(whdr_s + 16u * w.i);
+      if (h.x < 0) break;
+      const Pass s = make_pass(c, h, per_pair, ks, n_rb);
+      if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu);
+      else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu);
+      else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu);
+
+      // ---- epilogue of this pass: warp (q, pos = kh) reads its rows' accumulators ----
+      ptx::mbar_wait(&c.acc_full, accph);
+      accph ^= 1;
+      ptx::tc_fence_after();
+      const int pos = kh;
+      const int np = pos ? s.n1 : s.n0;
+      const int offp = (pos ? s.pt.off1 : s.pt.off0) + s.base;
+      const uint32_t acc_t = lane_tmem + kAccCol + 32u * pos;
+      for (int c0 = 0; c0 < np; c0 += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld_32x32b_x16(acc_t + c0, r);
+        ptx::tmem_ld_wait();
+        if (kW13) {
+          const bool up = lane >= 16;  // lanes 16..31 of every quarter hold the up rows
+          const int feat = s.rb * (kRows / 2) + 16 * q + (lane & 15);  // d_ff index of this row
+          if (ks == 1) {
+            // exchange g <-> u with the partner lane; gate lanes finish tokens c0..c0+7,
+            // up lanes tokens c0+8..c0+15
+            float o[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __shfl_xor_sync(0xffffffffu, __uint_as_float(r[i]), 16);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float g = up ? o[8 + j] : __uint_as_float(r[j]);
+              const float u = up ? __uint_as_float(r[8 + j]) : o[j];
+              const int tok = c0 + (up ? 8 : 0) + j;
+              if (tok < np) h_out[(size_t)(offp + tok) * f + feat] = f32_to_bf16_bits_rn(silu_mul(g, u));
+            }
+          } else {
+            // partials: part[kss][a][0:f] = g, [f:2f] = u
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < np)
+                part[((size_t)s.kss * n_assign_cap + offp + c0 + i) * (2 * f) + (up ? f : 0) + feat] =
+                    __uint_as_float(r[i]);
+          }
+        } else {
+          const int r_out = s.rb * kRows + row;  // d_model row (the last block may overhang d)
+          if (r_out < d) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < np) {
+                const size_t aa = (size_t)(offp + c0 + i);
+                float* dst = ks == 1 ? y_out + aa * d : part + ((size_t)s.kss * n_assign_cap + aa) * d;
+                dst[r_out] = __uint_as_float(r[i]);
+              }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&c.acc_empty);
+
+      if (ks > 1 && s.base + kNX >= max(s.pt.cnt0, s.pt.cnt1)) {
+        // ---- the last of the ks CTAs of this (pair, row block) reduces in split order ----
+        // (the barrier orders every decoder's partial stores before thread 64's gpu-scope
+        //  fence, which is cumulative, so one fence publishes them all)
+        named_bar_sync(1, kDecWarps * 32);
+        const int ctr = s.p * n_rb + s.rb;
+        if (dtid == 0) {
+          __threadfence();
+          const int prev = atomicAdd(&counters[ctr], 1);
+          c.s_last = (prev == ks - 1);
+          if (c.s_last) counters[ctr] = 0;  // ready for the next call on this stream
+        }
+        if (dtid == 0 && c.s_last) __threadfence();  // acquire side of the counter
+        named_bar_sync(1, kDecWarps * 32);
+        if (c.s_last) {
+          const int row_base = kW13 ? s.rb * (kRows / 2) : s.rb * kRows;
+          const int rows = kW13 ? kRows / 2 : min(kRows, d - row_base);  // multiple of 4
+          const int q4 = rows / 4;
+          const int n_tot = s.pt.cnt0 + s.pt.cnt1;  // buckets 2p and 2p+1 are adjacent
+          const int width = kW13 ? 2 * f : d;
+          const size_t split_stride = (size_t)n_assign_cap * width;
+          for (int i = dtid; i < n_tot * q4; i += kDecWarps * 32) {
+            const size_t aa = (size_t)(s.pt.off0 + i / q4);
+            const int r = row_base + 4 * (i % q4);
+            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+            const float* src = part + aa * width + r;
+#pragma unroll 4
+            for (int sp = 0; sp < ks; ++sp) {
+              const float4 v4 = __ldcg(reinterpret_cast<const float4*>(src + sp * split_stride));
+              s0.x += v4.x; s0.y += v4.y; s0.z += v4.z; s0.w += v4.w;
+              if (kW13) {
+                const float4 u = __ldcg(reinterpret_cast<const float4*>(src + sp * split_stride + f));
+                s1.x += u.x; s1.y += u.y; s1.z += u.z; s1.w += u.w;
+              }
+            }
+            if (kW13) {
+              uint2 o;
+              o.x = f32_to_bf16_rne_bits(silu_mul(s0.x, s1.x)) | (f32_to_bf16_rne_bits(silu_mul(s0.y, s1.y)) << 16);
+              o.y = f32_to_bf16_rne_bits(silu_mul(s0.z, s1.z)) | (f32_to_bf16_rne_bits(silu_mul(s0.w, s1.w)) << 16);
+              *reinterpret_cast<uint2*>(h_out + aa * f + r) = o;
+            } else {
+              *reinterpret_cast<float4*>(y_out + aa * d + r) = s0;
+            }
+          }
+        }
+        named_bar_sync(1, kDecWarps * 32);
+      }
+    }
+  }
+  // MMA warp + decoders: every MMA has completed (the last epilogue waited on it) and every
+  // tcgen05.ld has been waited on -> release TMEM
+  ptx::tc_fence_before();
+  named_bar_sync(3, 32 + kDecWarps * 32);
+  ptx::tc_fence_after();
+  if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+}
+
+template <bool kW13>
+int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* bucket_off, const int32_t* active,
+               const int32_t* n_active, int K, int f, int d, int n_rb, int ks, int max_active, int64_t n_assign_cap,
+               float* part, int32_t* counters, int32_t* work_ctr, uint16_t* h, float* y, int n_pairs,
+               cudaStream_t stream) {
+  auto kern = k_gemv_tc<kW13>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    attr = true;
+  }
+  const int n_items = max_active * n_rb * ks;  // upper bound; the device knows the active count
+  const int grid = std::min(n_items, 2 * num_sms());
+  {
+    ProfScope _ps(kW13 ? "w13_gemv" : "w2_gemv", stream);
+    cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kThreads), kSmem, stream, tw, tx, bucket_off, active, n_active,
+                               K, f, d, n_rb, ks, n_assign_cap, part, counters, work_ctr, h, y, 1u, n_pairs);
+    if (e != cudaSuccess) return cuda_check(e, kW13 ? "w13_gemv launch" : "w2_gemv launch");
+  }
+  return cuda_check(cudaGetLastError(), kW13 ? "w13_gemv launch" : "w2_gemv launch");
+}
+
+}  // namespace
+
+// Same contract as launch_gemv_experts (gemv.cu); `nt` is unused (up to 32 tokens per position
+// per pass; more -> further passes over the same weights).
+int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f,
+                           const uint16_t* x_rows, const int32_t* bucket_off, const int32_t* active_pairs,
+                           const int32_t* n_active, int max_active, int64_t n_assign_cap, int nt, int ks13, int ks2,
+                           float* part13, float* part2, int32_t* counters13, int32_t* counters2, int32_t* work_ctrs,
+                           uint16_t* h, float* y, cudaStream_t stream) {
+  (void)nt;
+  if (max_active == 0 || n_assign_cap == 0) return PUZZLE_OK;
+  CUtensorMap tw13, tx13, tw2, tx2;
+  int rc;
+  if ((rc = make_tmap_2d(&tw13, w13, (int64_t)n_pairs * 2 * f, d, kBox, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx13, x_rows, n_assign_cap, d, kBox, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tw2, w2, (int64_t)n_pairs * d, f, kRows, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx2, h, n_assign_cap, f, kBox, kBK))) return rc;
+  const int rb13 = f / (kRows / 2), rb2 = (d + kRows - 1) / kRows;
+  if ((rc = launch_one<true>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, ks13, max_active,
+                             n_assign_cap, part13, counters13, work_ctrs, h, y, n_pairs, stream)))
+    return rc;
+  return launch_one<false>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, ks2, max_active, n_assign_cap,
+                           part2, counters2, work_ctrs + 1, h, y, n_pairs, stream);
+}
+
+}  // namespace pz
