@@ -18,7 +18,9 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpuzzlemoe.so")
+# PUZZLE_LIB points at an alternative build of the same library (tuning variants built by
+# scripts/build_variant.py); by default the in-tree build is loaded.
+LIB_PATH = os.environ.get("PUZZLE_LIB") or os.path.join(_HERE, "libpuzzlemoe.so")
 
 PUZZLE_OK = 0
 PATH_AUTO, PATH_GEMV, PATH_TC = 0, 1, 2

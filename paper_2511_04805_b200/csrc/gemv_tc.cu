@@ -6,21 +6,25 @@
 // Warp-specialised, persistent CTAs (2 per SM, 256 TMEM columns each):
 //   warp 0     producer: one lane claims work items with an atomic (dynamic scheduler) and
 //              issues TMA loads, per 64-wide K stage, of the PACKED 128-row weight tile into a
-//              4-deep W ring and of the tokens' activation rows of both positions (16-row
-//              boxes, <= 32 tokens each per pass) into a 5-deep X ring (128-byte swizzle).
-//              The W ring is released by the decoders as soon as they hold the words in
-//              registers, the X ring by the MMAs' commit, so HBM reads are never held up by
-//              the tensor-core round trip.
+//              4-deep W ring and of the tokens' activation rows of both positions (one 32-row
+//              box each per pass) into a 5-deep X ring (128-byte swizzle): <= 4 TMA
+//              instructions per stage (each costs the issuing thread tens of ns). It polls
+//              both rings, so weight loads never wait for an activation slot: the W ring is
+//              released by the decoders as soon as they hold the words in registers, the X
+//              ring by the MMAs' commit.
 //   warps 2-9  decoders: warp (q = warp % 4, kh) owns tile rows 32q..32q+31 (= the TMEM lanes
 //              it may access) and K half kh of a stage: 4 x LDS.128 (conflict-free under the
 //              swizzle), SWAR Algorithm 1 for the active position(s), tcgen05.st of the bf16
-//              rows into a TMEM A buffer (lane = row, column = k pair). After the last stage of
+//              rows into TMEM A buffer j (lane = row, column = k pair). After the last stage of
 //              a pass they are the epilogue (tcgen05.ld of the fp32 accumulators).
-//   warp 1     MMA issuer: one lane issues tcgen05.mma.kind::f16 with A from TMEM and B (the
-//              tokens, N = 16 or 32) from a shared-memory descriptor, accumulators in TMEM.
-// w13 tile rows: quarter q holds 16 gate rows (features f0+16q ..+15) then the same 16
-// features' up rows, so g and u of one d_ff index sit in lanes i and i+16 of ONE warp and
-// SwiGLU needs only a shuffle. w2 tile rows: 128 consecutive d_model rows.
+//   warps 1,10 MMA issuers, one per position: tcgen05.mma.kind::f16 (A from TMEM, B = the
+//              tokens, N = 16 or 32, from a shared-memory descriptor, accumulators in TMEM);
+//              two instruction streams, since one thread's MMAs retire ~57 ns apart at these
+//              N (scripts/micro/umma_rate.cu). Commits release the A buffer and the X slot.
+// w13: TMEM lane quarter q holds 16 gate rows (features f0+16q ..+15) then the same 16
+// features' up rows (the decoders pick the rows from the gate / up halves of the stage), so g
+// and u of one d_ff index sit in lanes i and i+16 of ONE warp and SwiGLU needs only a shuffle.
+// w2 tile rows: 128 consecutive d_model rows.
 // TMEM columns: A buffer j (of 3), position p at 64 j + 32 p (64 bf16 k = 32 columns);
 // accumulators of position p at 192 + 32 p (32 fp32 token columns).
 #include <algorithm>
@@ -35,26 +39,51 @@ namespace pz {
 namespace {
 
 constexpr int kDecWarps = 8;
-constexpr int kThreads = 64 + 32 * kDecWarps;  // warp 0 producer, warp 1 MMA, warps 2..9 decoders
+// warp 0 producer, warp 1 MMA (position 0), warps 2..9 decoders, warp 10 MMA (position 1)
+constexpr int kThreads = 96 + 32 * kDecWarps;
 constexpr int kBK = 64;                          // K per stage (one 128-byte swizzle row)
 constexpr int kRows = 128;                       // weight rows per tile (UMMA M)
 constexpr int kWBytes = kRows * kBK * 2;         // 16 KB packed words per stage
 constexpr int kNX = 32;                          // tokens per position per pass (UMMA N <= 32)
-constexpr int kBox = 16;                         // rows per TMA box (activations, w13 halves)
-constexpr int kBoxBytes = kBox * kBK * 2;        // 2 KB
+constexpr int kXBox = 32;                        // token rows per activation TMA box (= kNX)
 constexpr int kXPos = kNX * kBK * 2;             // 4 KB per position
 constexpr int kXBytes = 2 * kXPos;               // X stage: both positions
-constexpr int kWStages = 4;
-constexpr int kXStages = 5;
-constexpr int kAStages = 3;
+#ifndef PZ_TC_WST  // W ring depth (tuning knob)
+#define PZ_TC_WST 4
+#endif
+#ifndef PZ_TC_XST  // X ring depth (tuning knob)
+#define PZ_TC_XST 5
+#endif
+constexpr int kWStages = PZ_TC_WST;
+constexpr int kXStages = PZ_TC_XST;
+constexpr int kAStages = 3;  // TMEM A buffers
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kAccCol = 64 * kAStages;      // 192
+
+#ifdef PZ_TRACE  // pipeline timeline of one CTA (tuning builds only; scripts/trace_gemv.py)
+__device__ unsigned long long g_trace[8][4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PZ_TR(ev, idx) \
+  if (kW13 && blockIdx.x == PZ_TRACE && (idx) < 4096) g_trace[ev][idx] = gtimer()
+#define PZ_TRD(ev, idx) \
+  if (kW13 && blockIdx.x == PZ_TRACE && (idx) < 4096 && threadIdx.x == 64) g_trace[ev][idx] = gtimer()
+#else
+#define PZ_TR(ev, idx)
+#define PZ_TRD(ev, idx)
+#endif
 
 struct alignas(16) Ctl {
   int4 whdr[kWStages];  // {item, pass base, kb, 0}; item -1 = no more work
   int4 xhdr[kXStages];
-  uint64_t wfull[kWStages], wempty[kWStages], xfull[kXStages], xempty[kXStages];
-  uint64_t a_full[kAStages], a_empty[kAStages], acc_full, acc_empty;
+  int4 sq[8];           // producer: stages whose W is issued and X is not yet (X load params)
+  int4 sqh[8];          //   ... and their stage headers
+  uint64_t wfull[kWStages], wempty[kWStages], xfull[kXStages], xempty[kXStages], a_full[kAStages],
+      a_empty[kAStages];
+  uint64_t acc_full, acc_empty;
   uint32_t tmem_base;
   int s_last;
   int32_t s_off[kMaxExperts + 1];     // bucket_off[0 .. 2P]
@@ -148,10 +177,14 @@ __device__ __forceinline__ Pass make_pass(const Ctl& c, int4 h, int per_pair, in
 // i -> column 16 kh + 4 i + r (k pair 32 kh + 8 i + 2 r).
 template <int MODE>
 __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t lane_tmem, const uint32_t (&w_off)[4],
-                                            int kh, int nk, Ring& w, Ring& a, const Muls& mu) {
+                                            int kh, int nk, Ring& w, Ring& a, const Muls& mu, int& tcount,
+                                            bool kW13) {
   const int lane = threadIdx.x & 31;
+  (void)tcount;
+  (void)kW13;
   for (int kb = 0; kb < nk; ++kb) {
     if (kb) ptx::mbar_wait(&c.wfull[w.i], w.ph);
+    PZ_TRD(2, tcount);
     const uint32_t st = smem_w + (uint32_t)w.i * kWBytes;
     uint4 v[4];
 #pragma unroll
@@ -172,7 +205,8 @@ __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t la
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&c.wempty[w.i]);  // packed words consumed: the slot may refill
     w.next<kWStages>();
-    ptx::mbar_wait(&c.a_empty[a.i], a.ph ^ 1);
+    ptx::mbar_wait(&c.a_empty[a.i], a.ph ^ 1);  // the MMAs that read A buffer a.i have completed
+    PZ_TRD(3, tcount);
     ptx::tc_fence_after();
     const uint32_t t0 = lane_tmem + 64u * a.i + 16u * kh;
     if (MODE & 1) ptx::tmem_st_32x32b_x16(t0, d0);
@@ -181,12 +215,14 @@ __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t la
     ptx::tc_fence_before();
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&c.a_full[a.i]);
+    PZ_TRD(4, tcount);
+    ++tcount;
     a.next<kAStages>();
   }
 }
 
 template <bool kW13>
-__global__ void __launch_bounds__(kThreads, 2) k_gemv_tc(
+__global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 11 warps: <= 6 warps per SM sub-partition
     const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
     const int32_t* __restrict__ bucket_off, const int32_t* __restrict__ active_pairs,
     const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb, int ks, int64_t n_assign_cap,
@@ -204,15 +240,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tc(
       ptx::mbar_init(&c.wfull[s], 1);
       ptx::mbar_init(&c.wempty[s], kDecWarps);
     }
-    for (int s = 0; s < kXStages; ++s) {
-      ptx::mbar_init(&c.xfull[s], 1);
-      ptx::mbar_init(&c.xempty[s], 1);
+    for (int j = 0; j < kXStages; ++j) {
+      ptx::mbar_init(&c.xfull[j], 1);
+      ptx::mbar_init(&c.xempty[j], 2);  // commits of both MMA warps
     }
     for (int j = 0; j < kAStages; ++j) {
       ptx::mbar_init(&c.a_full[j], kDecWarps);
-      ptx::mbar_init(&c.a_empty[j], 1);
+      ptx::mbar_init(&c.a_empty[j], 2);
     }
-    ptx::mbar_init(&c.acc_full, 1);
+    ptx::mbar_init(&c.acc_full, 2);
     ptx::mbar_init(&c.acc_empty, kDecWarps);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tm_w);
@@ -234,97 +270,132 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tc(
 
   if (warp == 0) {
     // ============================== producer ==============================
+    // W side: walks items (claimed with an atomic) / passes / k-blocks, one TMA stage per
+    // free W slot, and queues each stage in sq; X side: loads the activation rows of the
+    // oldest queued stage into the next free X slot. Both are polled, neither blocks the other.
     if (lane != 0) return;
     const int n_items = n_active * per_pair;
     Ring w{0, 0}, x{0, 0};
-    int next = atomicAdd(work_ctr, 1);  // the next claim overlaps the current item's stream
-    for (;;) {
-      const int item = next;
-      if (item < n_items) next = atomicAdd(work_ctr, 1);
-      if (item >= n_items) {
-        ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
-        ptx::mbar_wait(&c.xempty[x.i], x.ph ^ 1);
-        c.whdr[w.i] = make_int4(-1, 0, 0, 0);
-        c.xhdr[x.i] = make_int4(-1, 0, 0, 0);
-        ptx::mbar_arrive(&c.wfull[w.i]);  // completes the phase without data: "no more work"
-        ptx::mbar_arrive(&c.xfull[x.i]);
-        break;
-      }
+    int tw = 0, tx = 0;  // stages issued on the W / X side
+    int tcount = 0;
+    (void)tcount;
+    int item = atomicAdd(work_ctr, 1), base = 0, kb = 0;
+    int next = item < n_items ? atomicAdd(work_ctr, 1) : n_items;  // claim overlaps the stream
+    int wrow = 0, maxcnt = 0, kss = 0, off0 = 0, off1 = 0, l0 = 0, l1 = 0;
+    auto load_item = [&]() {
       const int z = item / per_pair;
-      const int rb = (item / ks) % n_rb, kss = item % ks;
+      const int rb = (item / ks) % n_rb;
+      kss = item % ks;
       const int p = c.s_active[z];
       const PairTokens pt = load_pair(c.s_off, p);
-      const int maxcnt = max(pt.cnt0, pt.cnt1);
-      const int wrow = kW13 ? p * 2 * f + rb * (kRows / 2) : p * d + rb * kRows;
-      for (int base = 0; base < maxcnt; base += kNX) {
-        const int l0 = (min(max(pt.cnt0 - base, 0), kNX) + kBox - 1) / kBox;
-        const int l1 = (min(max(pt.cnt1 - base, 0), kNX) + kBox - 1) / kBox;
-        const uint32_t xbytes = (uint32_t)(l0 + l1) * kBoxBytes;
-        for (int kb = 0; kb < nk; ++kb) {
-          const int kc = kss * kchunk + kb * kBK;
-          const int4 hv = make_int4(item, base, kb, 0);
-          ptx::mbar_wait_sleep(&c.wempty[w.i], w.ph ^ 1, 500);
-          c.whdr[w.i] = hv;
-          uint8_t* sw = smem + (size_t)w.i * kWBytes;
-          ptx::mbar_arrive_expect_tx(&c.wfull[w.i], kWBytes);
-          if (kW13) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {  // quarter q: 16 gate rows, then the same features' up rows
-              ptx::tma_load_2d(sw + q * 2 * kBoxBytes, &tm_w, &c.wfull[w.i], kc, wrow + kBox * q);
-              ptx::tma_load_2d(sw + q * 2 * kBoxBytes + kBoxBytes, &tm_w, &c.wfull[w.i], kc, wrow + f + kBox * q);
-            }
+      maxcnt = max(pt.cnt0, pt.cnt1);
+      off0 = pt.off0;
+      off1 = pt.off1;
+      wrow = kW13 ? p * 2 * f + rb * (kRows / 2) : p * d + rb * kRows;
+      l0 = pt.cnt0 > 0;  // one activation box per active position
+      l1 = pt.cnt1 > 0;
+    };
+    if (item < n_items) load_item();
+    bool w_done = item >= n_items;
+    while (!w_done || tx < tw) {
+      if (!w_done && tw - tx < 8 && ptx::mbar_test(&c.wempty[w.i], w.ph ^ 1)) {
+        const int kc = kss * kchunk + kb * kBK;
+        PZ_TR(0, tw);
+        c.whdr[w.i] = make_int4(item, base, kb, 0);
+        c.sqh[tw & 7] = make_int4(item, base, kb, 0);
+        // for the X side: item, pass base, k column, row offsets of both positions + box counts
+        c.sq[tw & 7] = make_int4(item, kc, (off0 + base) | (l0 << 28), (off1 + base) | (l1 << 28));
+        uint8_t* sw = smem + (size_t)w.i * kWBytes;
+        ptx::mbar_arrive_expect_tx(&c.wfull[w.i], kWBytes);
+        if (kW13) {  // 64 gate rows, then the same features' 64 up rows
+          ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
+          ptx::tma_load_2d(sw + kWBytes / 2, &tm_w, &c.wfull[w.i], kc, wrow + f);
+        } else {
+          ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
+        }
+        w.next<kWStages>();
+        ++tw;
+        if (++kb == nk) {  // next pass of this item, or the next item
+          kb = 0;
+          base += kNX;
+          if (base < maxcnt) {  // box counts of the later pass
+            const int z = item / per_pair;
+            const PairTokens pt = load_pair(c.s_off, c.s_active[z]);
+            l0 = pt.cnt0 > base;
+            l1 = pt.cnt1 > base;
           } else {
-            ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
+            base = 0;
+            item = next;
+            if (item < n_items) {
+              next = atomicAdd(work_ctr, 1);
+              load_item();
+            } else {
+              w_done = true;
+            }
           }
-          w.next<kWStages>();
-          ptx::mbar_wait_sleep(&c.xempty[x.i], x.ph ^ 1, 500);
-          c.xhdr[x.i] = hv;
-          uint8_t* sx = smem + (size_t)kWStages * kWBytes + (size_t)x.i * kXBytes;
-          ptx::mbar_arrive_expect_tx(&c.xfull[x.i], xbytes);
-          for (int i = 0; i < l0; ++i)
-            ptx::tma_load_2d(sx + i * kBoxBytes, &tm_x, &c.xfull[x.i], kc, pt.off0 + base + kBox * i);
-          for (int i = 0; i < l1; ++i)
-            ptx::tma_load_2d(sx + kXPos + i * kBoxBytes, &tm_x, &c.xfull[x.i], kc, pt.off1 + base + kBox * i);
-          x.next<kXStages>();
         }
       }
+      if (tx < tw && ptx::mbar_test(&c.xempty[x.i], x.ph ^ 1)) {
+        const int4 q = c.sq[tx & 7];
+        const int ql0 = (int)((uint32_t)q.z >> 28), ql1 = (int)((uint32_t)q.w >> 28);
+        const int r0 = q.z & 0x0FFFFFFF, r1 = q.w & 0x0FFFFFFF;
+        PZ_TR(1, tx);
+        c.xhdr[x.i] = c.sqh[tx & 7];
+        uint8_t* sx = smem + (size_t)kWStages * kWBytes + (size_t)x.i * kXBytes;
+        ptx::mbar_arrive_expect_tx(&c.xfull[x.i], (uint32_t)(ql0 + ql1) * kXPos);
+        if (ql0) ptx::tma_load_2d(sx, &tm_x, &c.xfull[x.i], q.y, r0);
+        if (ql1) ptx::tma_load_2d(sx + kXPos, &tm_x, &c.xfull[x.i], q.y, r1);
+        x.next<kXStages>();
+        ++tx;
+      }
     }
+    // "no more work": complete one more phase of each ring without data
+    ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
+    c.whdr[w.i] = make_int4(-1, 0, 0, 0);
+    ptx::mbar_arrive(&c.wfull[w.i]);
+    ptx::mbar_wait(&c.xempty[x.i], x.ph ^ 1);
+    c.xhdr[x.i] = make_int4(-1, 0, 0, 0);
+    ptx::mbar_arrive(&c.xfull[x.i]);
     return;
   }
 
-  if (warp == 1) {
-    // ============================== MMA issuer ==============================
+  if (warp == 1 || warp == 2 + kDecWarps) {
+    // ============================== MMA issuers ==============================
+    // warp 1 issues position 0's MMAs, the last warp position 1's: two instruction streams,
+    // since one thread's tcgen05.mma retire ~57 ns apart at these N (scripts/micro/umma_rate.cu)
+    const int mypos = warp == 1 ? 0 : 1;
     Ring x{0, 0}, a{0, 0};
     uint32_t accph = 0;
+    int tcount = 0;
+    (void)tcount;
     for (;;) {
       ptx::mbar_wait(&c.xfull[x.i], x.ph);
       const int4 h = lds_int4(xhdr_s + 16u * x.i);
       if (h.x < 0) break;
       const Pass s = make_pass(c, h, per_pair, ks, n_rb);
-      const uint32_t id0 = ptx::idesc_bf16_f32(128, (uint32_t)((s.n0 + 15) & ~15));
-      const uint32_t id1 = ptx::idesc_bf16_f32(128, (uint32_t)((s.n1 + 15) & ~15));
+      const int np = mypos ? s.n1 : s.n0;
+      const uint32_t idp = ptx::idesc_bf16_f32(128, (uint32_t)((np + 15) & ~15));
+      const uint32_t acc_col = tmem + kAccCol + 32u * mypos;
       ptx::mbar_wait(&c.acc_empty, accph ^ 1);  // the previous pass's epilogue drained TMEM
       ptx::tc_fence_after();
       for (int kb = 0; kb < nk; ++kb) {
         if (kb) ptx::mbar_wait(&c.xfull[x.i], x.ph);
+        if (mypos == 0) PZ_TR(6, tcount);
         ptx::mbar_wait(&c.a_full[a.i], a.ph);
+        if (mypos == 0) PZ_TR(5, tcount);
         ptx::tc_fence_after();
-        if (lane == 0) {
-          const uint32_t xs = smem_x + (uint32_t)x.i * kXBytes;
-          const uint32_t ta = tmem + 64u * a.i;
+        const uint32_t xs = smem_x + (uint32_t)x.i * kXBytes + (uint32_t)(kXPos * mypos);
+        const uint32_t ta = tmem + 64u * a.i + 32u * mypos;
+        if (np > 0) {
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint32_t acc = (kb | kk) != 0;
-            if (s.n0 > 0) ptx::mma_bf16_ts(tmem + kAccCol, ta + 8 * kk, ptx::smem_desc_sw128(xs + 32 * kk), id0, acc);
-            if (s.n1 > 0)
-              ptx::mma_bf16_ts(tmem + kAccCol + 32, ta + 32 + 8 * kk, ptx::smem_desc_sw128(xs + kXPos + 32 * kk), id1,
-                               acc);
-          }
-          ptx::mma_commit(&c.a_empty[a.i]);
-          ptx::mma_commit(&c.xempty[x.i]);
-          if (kb == nk - 1) ptx::mma_commit(&c.acc_full);
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            ptx::mma_bf16_ts_elect(acc_col, ta + 8 * kk, ptx::smem_desc_sw128(xs + 32 * kk), idp, (kb | kk) != 0);
         }
-        __syncwarp();
+        ptx::mma_commit_elect(&c.a_empty[a.i]);  // A buffer free once these MMAs complete
+        ptx::mma_commit_elect(&c.xempty[x.i]);   // X slot likewise
+        if (kb == nk - 1) ptx::mma_commit_elect(&c.acc_full);
+        if (mypos == 0) PZ_TR(7, tcount);
+        ++tcount;
         x.next<kXStages>();
         a.next<kAStages>();
       }
@@ -336,21 +407,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tc(
     const int q = warp & 3;          // TMEM lane quarter this warp may access
     const int kh = (warp - 2) >> 2;  // K half of a stage; position handled in the epilogue
     const int row = 32 * q + lane;   // tile row == TMEM lane
+    // shared-memory row this thread decodes. w13: the stage holds 64 gate rows then the same
+    // features' 64 up rows; lanes 0-15 of quarter q take gate rows 16q.., lanes 16-31 the up
+    // rows of the same features, so g and u of one d_ff index land in lanes i, i+16 of one warp
+    const int srow = kW13 ? (lane < 16 ? 16 * q + lane : 64 + 16 * q + lane - 16) : row;
     const uint32_t lane_tmem = tmem + ((uint32_t)(32 * q) << 16);
     const Muls mu{mul_one, mul_one * 2u, mul_one * 4u, mul_one * 8u};
     uint32_t w_off[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) w_off[i] = swz(row, 4 * kh + i);
-    Ring w{0, 0}, a{0, 0};
+    for (int i = 0; i < 4; ++i) w_off[i] = swz(srow, 4 * kh + i);
+    Ring w{0, 0}, a{0, 0};  // a: TMEM A buffer (== X slot) ring
     uint32_t accph = 0;
+    int tcount = 0;
     for (;;) {
       ptx::mbar_wait(&c.wfull[w.i], w.ph);
       const int4 h = lds_int4(whdr_s + 16u * w.i);
       if (h.x < 0) break;
       const Pass s = make_pass(c, h, per_pair, ks, n_rb);
-      if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu);
-      else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu);
-      else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu);
+      if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu, tcount, kW13);
+      else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu, tcount, kW13);
+      else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu, tcount, kW13);
 
       // ---- epilogue of this pass: warp (q, pos = kh) reads its rows' accumulators ----
       ptx::mbar_wait(&c.acc_full, accph);
@@ -457,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gemv_tc(
   // MMA warp + decoders: every MMA has completed (the last epilogue waited on it) and every
   // tcgen05.ld has been waited on -> release TMEM
   ptx::tc_fence_before();
-  named_bar_sync(3, 32 + kDecWarps * 32);
+  named_bar_sync(3, 64 + kDecWarps * 32);
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
@@ -497,10 +573,10 @@ int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs,
   if (max_active == 0 || n_assign_cap == 0) return PUZZLE_OK;
   CUtensorMap tw13, tx13, tw2, tx2;
   int rc;
-  if ((rc = make_tmap_2d(&tw13, w13, (int64_t)n_pairs * 2 * f, d, kBox, kBK))) return rc;
-  if ((rc = make_tmap_2d(&tx13, x_rows, n_assign_cap, d, kBox, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tw13, w13, (int64_t)n_pairs * 2 * f, d, kRows / 2, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx13, x_rows, n_assign_cap, d, kXBox, kBK))) return rc;
   if ((rc = make_tmap_2d(&tw2, w2, (int64_t)n_pairs * d, f, kRows, kBK))) return rc;
-  if ((rc = make_tmap_2d(&tx2, h, n_assign_cap, f, kBox, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx2, h, n_assign_cap, f, kXBox, kBK))) return rc;
   const int rb13 = f / (kRows / 2), rb2 = (d + kRows - 1) / kRows;
   if ((rc = launch_one<true>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, ks13, max_active,
                              n_assign_cap, part13, counters13, work_ctrs, h, y, n_pairs, stream)))
@@ -508,5 +584,11 @@ int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs,
   return launch_one<false>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, ks2, max_active, n_assign_cap,
                            part2, counters2, work_ctrs + 1, h, y, n_pairs, stream);
 }
+
+#ifdef PZ_TRACE
+extern "C" __attribute__((visibility("default"))) int puzzle_debug_trace(void* dst, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(dst, g_trace, bytes);
+}
+#endif
 
 }  // namespace pz

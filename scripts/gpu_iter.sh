@@ -1,11 +1,13 @@
 #!/bin/bash
-# iteration: gpu tests (fast subset first), then bench
+# one iteration: GPU parity tests, headline bench (+ variants), pipeline traces (trace* variants)
 cd $GRAFT_REPO_ROOT
-[ -x scripts/micro/hmma_rate ] && ./scripts/micro/hmma_rate > gpurun_out/hmma_rate.txt 2>&1
-timeout 300 python -X faulthandler -m pytest tests/test_gpu_moe.py -x -q -k "gemv_small or tiny or skew or building" > gpurun_out/t1.log 2>&1; echo "rc=$?" >> gpurun_out/t1.log
-if tail -1 gpurun_out/t1.log | grep -q "rc=0"; then
-  timeout 900 python -X faulthandler bench.py --steps 200 --warmup 10 --no-cpu > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
-  if [ "$FULL" = "1" ]; then
-    timeout 900 python -X faulthandler -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/t2.log 2>&1; echo "rc=$?" >> gpurun_out/t2.log
-  fi
+if [ "${SKIP_TESTS:-0}" = 0 ]; then
+timeout 600 python -X faulthandler -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/t_it.log 2>&1; echo "rc=$?" >> gpurun_out/t_it.log
 fi
+timeout 200 python bench.py --steps 100 --warmup 5 --no-extra --no-cpu > gpurun_out/v_default.log 2>&1
+for d in build/variants/*/; do n=$(basename $d)
+  case $n in
+    trace*) PUZZLE_LIB=$d/libpuzzlemoe.so timeout 300 python scripts/trace_gemv.py mixtral 64 > gpurun_out/$n.log 2>&1 ;;
+    *) PUZZLE_LIB=$d/libpuzzlemoe.so timeout 200 python bench.py --steps 100 --warmup 5 --no-extra --no-cpu > gpurun_out/v_$n.log 2>&1 ;;
+  esac
+done
