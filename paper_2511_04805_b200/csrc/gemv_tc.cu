@@ -4,14 +4,14 @@
 // packed words are streamed from HBM ONCE and decoded for position 0 and/or 1.
 //
 // Warp-specialised, persistent CTAs (2 per SM, 256 TMEM columns each):
-//   warp 0     producer: one lane claims work items with an atomic (dynamic scheduler) and
-//              issues TMA loads, per 64-wide K stage, of the PACKED 128-row weight tile into a
-//              4-deep W ring and of the tokens' activation rows of both positions (one 32-row
-//              box each per pass) into a 5-deep X ring (128-byte swizzle): <= 4 TMA
-//              instructions per stage (each costs the issuing thread tens of ns). It polls
-//              both rings, so weight loads never wait for an activation slot: the W ring is
-//              released by the decoders as soon as they hold the words in registers, the X
-//              ring by the MMAs' commit.
+//   warp 0     W producer: one lane claims work items with an atomic (dynamic scheduler)
+//              and issues the TMA loads of each 64-wide K stage of the PACKED 128-row weight
+//              tile (2 boxes) into a 4-deep W ring, released by the decoders as soon as they
+//              hold the words in registers; every stage is queued for
+//   warp 11    X producer: one lane loads the tokens' activation rows of both positions (one
+//              32-row box each per pass) into a 5-deep X ring, released by the MMAs' commit.
+//              (Two producer threads: each TMA instruction costs its issuing thread tens of
+//              ns, and weight loads must never wait behind activation slots.)
 //   warps 2-9  decoders: warp (q = warp % 4, kh) owns tile rows 32q..32q+31 (= the TMEM lanes
 //              it may access) and K half kh of a stage: 4 x LDS.128 (conflict-free under the
 //              swizzle), SWAR Algorithm 1 for the active position(s), tcgen05.st of the bf16
@@ -39,8 +39,9 @@ namespace pz {
 namespace {
 
 constexpr int kDecWarps = 8;
-// warp 0 producer, warp 1 MMA (position 0), warps 2..9 decoders, warp 10 MMA (position 1)
-constexpr int kThreads = 96 + 32 * kDecWarps;
+// warp 0 W producer, warp 1 MMA (position 0), warps 2..9 decoders, warp 10 MMA (position 1),
+// warp 11 X producer
+constexpr int kThreads = 128 + 32 * kDecWarps;
 constexpr int kBK = 64;                          // K per stage (one 128-byte swizzle row)
 constexpr int kRows = 128;                       // weight rows per tile (UMMA M)
 constexpr int kWBytes = kRows * kBK * 2;         // 16 KB packed words per stage
@@ -57,6 +58,7 @@ constexpr int kXBytes = 2 * kXPos;               // X stage: both positions
 constexpr int kWStages = PZ_TC_WST;
 constexpr int kXStages = PZ_TC_XST;
 constexpr int kAStages = 3;  // TMEM A buffers
+constexpr int kSq = 8;       // stage queue W producer -> X producer
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kAccCol = 64 * kAStages;      // 192
 
@@ -79,10 +81,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct alignas(16) Ctl {
   int4 whdr[kWStages];  // {item, pass base, kb, 0}; item -1 = no more work
   int4 xhdr[kXStages];
-  int4 sq[8];           // producer: stages whose W is issued and X is not yet (X load params)
-  int4 sqh[8];          //   ... and their stage headers
+  int4 sq[kSq];         // W producer -> X producer: {k column, row0 | active0 << 28, row1 | ...}
+  int4 sqh[kSq];        //   ... and the stage headers
   uint64_t wfull[kWStages], wempty[kWStages], xfull[kXStages], xempty[kXStages], a_full[kAStages],
       a_empty[kAStages];
+  uint64_t sqfull[kSq], sqempty[kSq];
   uint64_t acc_full, acc_empty;
   uint32_t tmem_base;
   int s_last;
@@ -222,7 +225,7 @@ __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t la
 }
 
 template <bool kW13>
-__global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 11 warps: <= 6 warps per SM sub-partition
+__global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM sub-partition
     const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
     const int32_t* __restrict__ bucket_off, const int32_t* __restrict__ active_pairs,
     const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb, int ks, int64_t n_assign_cap,
@@ -248,6 +251,10 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 11 warps: <= 6 warps per
       ptx::mbar_init(&c.a_full[j], kDecWarps);
       ptx::mbar_init(&c.a_empty[j], 2);
     }
+    for (int j = 0; j < kSq; ++j) {
+      ptx::mbar_init(&c.sqfull[j], 1);
+      ptx::mbar_init(&c.sqempty[j], 1);
+    }
     ptx::mbar_init(&c.acc_full, 2);
     ptx::mbar_init(&c.acc_empty, kDecWarps);
     ptx::fence_mbar_init();
@@ -269,93 +276,90 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 11 warps: <= 6 warps per
   const int nk = kchunk / kBK;
 
   if (warp == 0) {
-    // ============================== producer ==============================
-    // W side: walks items (claimed with an atomic) / passes / k-blocks, one TMA stage per
-    // free W slot, and queues each stage in sq; X side: loads the activation rows of the
-    // oldest queued stage into the next free X slot. Both are polled, neither blocks the other.
+    // ============================== W producer ==============================
+    // walks items (claimed with an atomic) / passes / k-blocks: one TMA stage of packed words
+    // per free W slot; each stage is also queued (sq) for the X producer
     if (lane != 0) return;
     const int n_items = n_active * per_pair;
-    Ring w{0, 0}, x{0, 0};
-    int tw = 0, tx = 0;  // stages issued on the W / X side
-    int tcount = 0;
-    (void)tcount;
-    int item = atomicAdd(work_ctr, 1), base = 0, kb = 0;
+    Ring w{0, 0}, sq{0, 0};
+    int tw = 0;
+    (void)tw;
+    int item = atomicAdd(work_ctr, 1);
     int next = item < n_items ? atomicAdd(work_ctr, 1) : n_items;  // claim overlaps the stream
-    int wrow = 0, maxcnt = 0, kss = 0, off0 = 0, off1 = 0, l0 = 0, l1 = 0;
-    auto load_item = [&]() {
+    while (item < n_items) {
       const int z = item / per_pair;
-      const int rb = (item / ks) % n_rb;
-      kss = item % ks;
-      const int p = c.s_active[z];
-      const PairTokens pt = load_pair(c.s_off, p);
-      maxcnt = max(pt.cnt0, pt.cnt1);
-      off0 = pt.off0;
-      off1 = pt.off1;
-      wrow = kW13 ? p * 2 * f + rb * (kRows / 2) : p * d + rb * kRows;
-      l0 = pt.cnt0 > 0;  // one activation box per active position
-      l1 = pt.cnt1 > 0;
-    };
-    if (item < n_items) load_item();
-    bool w_done = item >= n_items;
-    while (!w_done || tx < tw) {
-      if (!w_done && tw - tx < 8 && ptx::mbar_test(&c.wempty[w.i], w.ph ^ 1)) {
-        const int kc = kss * kchunk + kb * kBK;
-        PZ_TR(0, tw);
-        c.whdr[w.i] = make_int4(item, base, kb, 0);
-        c.sqh[tw & 7] = make_int4(item, base, kb, 0);
-        // for the X side: item, pass base, k column, row offsets of both positions + box counts
-        c.sq[tw & 7] = make_int4(item, kc, (off0 + base) | (l0 << 28), (off1 + base) | (l1 << 28));
-        uint8_t* sw = smem + (size_t)w.i * kWBytes;
-        ptx::mbar_arrive_expect_tx(&c.wfull[w.i], kWBytes);
-        if (kW13) {  // 64 gate rows, then the same features' 64 up rows
-          ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
-          ptx::tma_load_2d(sw + kWBytes / 2, &tm_w, &c.wfull[w.i], kc, wrow + f);
-        } else {
-          ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
-        }
-        w.next<kWStages>();
-        ++tw;
-        if (++kb == nk) {  // next pass of this item, or the next item
-          kb = 0;
-          base += kNX;
-          if (base < maxcnt) {  // box counts of the later pass
-            const int z = item / per_pair;
-            const PairTokens pt = load_pair(c.s_off, c.s_active[z]);
-            l0 = pt.cnt0 > base;
-            l1 = pt.cnt1 > base;
+      const int rb = (item / ks) % n_rb, kss = item % ks;
+      const PairTokens pt = load_pair(c.s_off, c.s_active[z]);
+      const int maxcnt = max(pt.cnt0, pt.cnt1);
+      const int wrow = kW13 ? c.s_active[z] * 2 * f + rb * (kRows / 2) : c.s_active[z] * d + rb * kRows;
+      for (int base = 0; base < maxcnt; base += kNX) {
+        // X-side parameters: one activation box per active position (flag in bit 28)
+        const int r0 = (pt.off0 + base) | ((pt.cnt0 > base) << 28);
+        const int r1 = (pt.off1 + base) | ((pt.cnt1 > base) << 28);
+        for (int kb = 0; kb < nk; ++kb) {
+          const int kc = kss * kchunk + kb * kBK;
+          const int4 hv = make_int4(item, base, kb, 0);
+          ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
+          PZ_TR(0, tw);
+          c.whdr[w.i] = hv;
+          uint8_t* sw = smem + (size_t)w.i * kWBytes;
+          ptx::mbar_arrive_expect_tx(&c.wfull[w.i], kWBytes);
+          if (kW13) {  // 64 gate rows, then the same features' 64 up rows
+            ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
+            ptx::tma_load_2d(sw + kWBytes / 2, &tm_w, &c.wfull[w.i], kc, wrow + f);
           } else {
-            base = 0;
-            item = next;
-            if (item < n_items) {
-              next = atomicAdd(work_ctr, 1);
-              load_item();
-            } else {
-              w_done = true;
-            }
+            ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
           }
+          w.next<kWStages>();
+          ++tw;
+          ptx::mbar_wait(&c.sqempty[sq.i], sq.ph ^ 1);
+          c.sqh[sq.i] = hv;
+          c.sq[sq.i] = make_int4(kc, r0, r1, 0);
+          ptx::mbar_arrive(&c.sqfull[sq.i]);
+          sq.next<kSq>();
         }
       }
-      if (tx < tw && ptx::mbar_test(&c.xempty[x.i], x.ph ^ 1)) {
-        const int4 q = c.sq[tx & 7];
-        const int ql0 = (int)((uint32_t)q.z >> 28), ql1 = (int)((uint32_t)q.w >> 28);
-        const int r0 = q.z & 0x0FFFFFFF, r1 = q.w & 0x0FFFFFFF;
-        PZ_TR(1, tx);
-        c.xhdr[x.i] = c.sqh[tx & 7];
-        uint8_t* sx = smem + (size_t)kWStages * kWBytes + (size_t)x.i * kXBytes;
-        ptx::mbar_arrive_expect_tx(&c.xfull[x.i], (uint32_t)(ql0 + ql1) * kXPos);
-        if (ql0) ptx::tma_load_2d(sx, &tm_x, &c.xfull[x.i], q.y, r0);
-        if (ql1) ptx::tma_load_2d(sx + kXPos, &tm_x, &c.xfull[x.i], q.y, r1);
-        x.next<kXStages>();
-        ++tx;
-      }
+      item = next;
+      if (item < n_items) next = atomicAdd(work_ctr, 1);
     }
-    // "no more work": complete one more phase of each ring without data
+    // "no more work": complete one more phase of the W ring and the queue without data
     ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
     c.whdr[w.i] = make_int4(-1, 0, 0, 0);
     ptx::mbar_arrive(&c.wfull[w.i]);
-    ptx::mbar_wait(&c.xempty[x.i], x.ph ^ 1);
-    c.xhdr[x.i] = make_int4(-1, 0, 0, 0);
-    ptx::mbar_arrive(&c.xfull[x.i]);
+    ptx::mbar_wait(&c.sqempty[sq.i], sq.ph ^ 1);
+    c.sqh[sq.i] = make_int4(-1, 0, 0, 0);
+    ptx::mbar_arrive(&c.sqfull[sq.i]);
+    return;
+  }
+
+  if (warp == 3 + kDecWarps) {
+    // ============================== X producer ==============================
+    // the activation rows of each queued stage into the next free X slot
+    if (lane != 0) return;
+    Ring sq{0, 0}, x{0, 0};
+    int tx = 0;
+    (void)tx;
+    for (;;) {
+      ptx::mbar_wait(&c.sqfull[sq.i], sq.ph);
+      const int4 h = c.sqh[sq.i];
+      const int4 q = c.sq[sq.i];
+      ptx::mbar_arrive(&c.sqempty[sq.i]);
+      sq.next<kSq>();
+      ptx::mbar_wait(&c.xempty[x.i], x.ph ^ 1);
+      c.xhdr[x.i] = h;
+      if (h.x < 0) {
+        ptx::mbar_arrive(&c.xfull[x.i]);  // "no more work"
+        break;
+      }
+      PZ_TR(1, tx);
+      ++tx;
+      const bool a0 = (q.y >> 28) & 1, a1 = (q.z >> 28) & 1;
+      uint8_t* sx = smem + (size_t)kWStages * kWBytes + (size_t)x.i * kXBytes;
+      ptx::mbar_arrive_expect_tx(&c.xfull[x.i], (uint32_t)(a0 + a1) * kXPos);
+      if (a0) ptx::tma_load_2d(sx, &tm_x, &c.xfull[x.i], q.x, q.y & 0x0FFFFFFF);
+      if (a1) ptx::tma_load_2d(sx + kXPos, &tm_x, &c.xfull[x.i], q.x, q.z & 0x0FFFFFFF);
+      x.next<kXStages>();
+    }
     return;
   }
 
