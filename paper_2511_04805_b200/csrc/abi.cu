@@ -20,22 +20,19 @@ int launch_merge_experts_pack(const uint16_t*, const uint16_t*, const float*, co
 int launch_route(const float*, int64_t, int, int, int, const int32_t*, int, int32_t*, float*, int32_t*,
                  int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int, int32_t*, const uint16_t*, int, uint16_t*,
                  bool*, cudaStream_t);
-int launch_iota(int32_t*, int, int32_t*, cudaStream_t);
+int launch_active_pairs(const int32_t*, int, int32_t*, int32_t*, cudaStream_t);
 const char* last_error_cstr();
 int launch_combine(const float*, const int32_t*, const float*, int64_t, int, int, const uint16_t*,
                    uint16_t*, cudaStream_t);
 int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16_t*, cudaStream_t);
-int gemv_nt_for(int64_t T, int k, int E);
 bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
                       uint16_t*, float*, cudaStream_t);
-void gemv_splits(int d, int f, int max_active, int64_t n_assign, int* ks13, int* ks2);
-int launch_gemv_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*,
-                        const int32_t*, const int32_t*, int, int64_t, int, int, int, float*, float*, int32_t*,
-                        int32_t*, int32_t*, uint16_t*, float*, cudaStream_t);
+int gemv_tc_max_ctas();
+bool gemv_supported(int d, int f);
 int launch_gemv_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*,
-                           const int32_t*, const int32_t*, int, int64_t, int, int, int, float*, float*, int32_t*,
-                           int32_t*, int32_t*, uint16_t*, float*, cudaStream_t);
+                           const int32_t*, const int32_t*, int, int64_t, int, float*, int32_t*, int32_t*,
+                           uint16_t*, float*, cudaStream_t);
 
 namespace {
 thread_local std::string g_last_error;
@@ -133,17 +130,18 @@ int check_layer(const puzzle_moe_layer* L) {
 // ---- workspace layout of puzzle_moe_forward / puzzle_moe_experts ----
 struct Plan {
   int64_t T = 0, n_assign = 0;
-  int k = 0, max_active = 0, nt = 1, ks13 = 1, ks2 = 1;
+  int k = 0, max_active = 0;
+  int slot_tok = 0;  // GEMV path: assignments of one pair, bound for the stream-K partial slots
   int path = PUZZLE_PATH_GEMV;  // resolved (never AUTO)
 };
 
-// Decode shapes (<= 64 tokens) stream each touched pair once through the register-decode
-// GEMV; larger token counts are tensor-bound and go to the tcgen05 grouped GEMM.
+// Decode shapes (<= 64 tokens) stream each touched pair once through the decode-shape kernels
+// (gemv_tc.cu); larger token counts are tensor-bound and go to the tcgen05 grouped GEMM.
 constexpr int64_t kGemvMaxTokens = 64;
 
 struct Layout {
-  size_t topk_idx, topk_gate, bucket_off, assign_token, assign_of, active, n_active, cnt13, cnt2, h, y,
-      part13, part2, x_perm, route_scratch, total;
+  size_t topk_idx, topk_gate, bucket_off, assign_token, assign_of, active, n_active, cnt13, cnt2, h, y, part,
+      x_perm, route_scratch, total;
 };
 
 Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
@@ -155,10 +153,7 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   if (path == PUZZLE_PATH_AUTO)
     path = (T > kGemvMaxTokens && tc_supported(L->d_model, L->d_ff)) ? PUZZLE_PATH_TC : PUZZLE_PATH_GEMV;
   p.path = path;
-  if (path == PUZZLE_PATH_GEMV) {
-    p.nt = gemv_nt_for(T, k, L->n_experts);
-    gemv_splits(L->d_model, L->d_ff, std::max(p.max_active, 1), p.n_assign, &p.ks13, &p.ks2);
-  }
+  if (path == PUZZLE_PATH_GEMV) p.slot_tok = (int)std::min<int64_t>(p.n_assign, 2 * T);  // <= 2 experts per token
   return p;
 }
 
@@ -179,11 +174,11 @@ Layout make_layout(const puzzle_moe_layer* L, const Plan& p) {
   o.active = take(P * 4);
   o.n_active = take(4);
   o.cnt13 = take(P * (f / 64) * 4);
-  o.cnt2 = take(P * (d / 64) * 4 + 2 * 4);  // + the two dynamic-scheduler work counters
+  o.cnt2 = take(P * (d / 64) * 4);
   o.h = take(na * f * 2);
   o.y = take(na * d * 4);
-  o.part13 = take(p.ks13 > 1 ? (size_t)p.ks13 * na * 2 * f * 4 : 0);
-  o.part2 = take(p.ks2 > 1 ? (size_t)p.ks2 * na * d * 4 : 0);
+  // stream-K partial slots of the decode kernels: 2 per CTA x slot_tok x 128 fp32
+  o.part = take(p.path == PUZZLE_PATH_GEMV ? (size_t)2 * gemv_tc_max_ctas() * p.slot_tok * 128 * 4 : 0);
   o.x_perm = take(na * d * 2);
   o.route_scratch = take(2 * 2 * P * 4);
   o.total = off;
@@ -325,19 +320,9 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
   if (plan.path == PUZZLE_PATH_TC)
     return launch_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, s);
-  // decode shapes: tcgen05 with the decoded weights staged in TMEM (gemv_tc.cu); the
-  // register-decode mma.sync kernel (gemv.cu) stays selectable for A/B measurements
-  static const bool use_mma = [] {
-    const char* v = getenv("PUZZLE_GEMV_IMPL");
-    return v && std::string(v) == "mma";
-  }();
-  auto launch = use_mma ? launch_gemv_experts : launch_gemv_tc_experts;
-  return launch(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off,
-                             active, n_active, plan.max_active, plan.n_assign, plan.nt, plan.ks13,
-                             plan.ks2, at<float>(ws, lay.part13), at<float>(ws, lay.part2),
-                             at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2),
-                             at<int32_t>(ws, lay.cnt2) + L->n_pairs * (L->d_model / 64), at<uint16_t>(ws, lay.h), y,
-                             s);
+  return launch_gemv_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
+                                n_active, plan.max_active, plan.n_assign, plan.slot_tok, at<float>(ws, lay.part),
+                                at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);
 }
 
 int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits,
@@ -421,14 +406,13 @@ int puzzle_moe_experts(const puzzle_moe_layer* L, const uint16_t* x_rows, const 
     return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d_model % 256 == 0 and d_ff % 128 == 0");
   // Every pair may be touched: plan with T = n_assign, k = 1 (max_active = min(P, n_assign)).
   Plan plan = make_plan(L, n_assign, 1, path);
-  if (plan.path == PUZZLE_PATH_GEMV) plan.nt = gemv_nt_for(std::min<int64_t>(n_assign, 64), 2, 2);
   const Layout lay = make_layout(L, plan);
   if (!ws || ws_bytes < lay.total) return fail(PUZZLE_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
-  // active list = all pairs (empty pairs exit immediately); counters zeroed
+  // active list = the pairs with rows; counters zeroed
   int rc = cuda_check(cudaMemsetAsync(at<char>(ws, lay.cnt13), 0, lay.h - lay.cnt13, s), "memset");
   if (rc) return rc;
-  rc = launch_iota(at<int32_t>(ws, lay.active), L->n_pairs, at<int32_t>(ws, lay.n_active), s);
+  rc = launch_active_pairs(bucket_off, L->n_pairs, at<int32_t>(ws, lay.active), at<int32_t>(ws, lay.n_active), s);
   if (rc) return rc;
   plan.max_active = L->n_pairs;
   return run_experts(L, plan, lay, ws, x_rows, nullptr, bucket_off, at<int32_t>(ws, lay.active),

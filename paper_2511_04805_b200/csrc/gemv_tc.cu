@@ -36,6 +36,8 @@
 
 namespace pz {
 
+int gemv_tc_max_ctas();
+
 namespace {
 
 constexpr int kDecWarps = 8;
@@ -59,6 +61,7 @@ constexpr int kWStages = PZ_TC_WST;
 constexpr int kXStages = PZ_TC_XST;
 constexpr int kAStages = 3;  // TMEM A buffers
 constexpr int kSq = 8;       // stage queue W producer -> X producer
+constexpr int kMinStages = 8;  // stream-K: minimum stages per CTA
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kAccCol = 64 * kAStages;      // 192
 
@@ -153,39 +156,50 @@ struct Ring {
   }
 };
 
-// Pass parameters shared by the MMA warp and the decoders (derived from a stage header).
+// Stream-K partition: the S = (active pairs x row blocks) x nk stages are cut into G
+// contiguous ranges, CTA g taking stages [b_g, b_{g+1}), b_g = ceil(g S / G). A work item
+// (pair, row block) that straddles a cut is computed in pieces whose fp32 partials are summed,
+// in CTA order, by the piece that finishes last.
+struct StreamK {
+  int S, G;
+  __device__ __forceinline__ int begin(int g) const { return (int)(((int64_t)g * S + G - 1) / G); }
+  __device__ __forceinline__ int owner(int s) const { return (int)(((int64_t)s * G) / S); }
+};
+
+// Stage header {item, pass base, kb, kb0 << 16 | kb1}: the stage is k-block kb of the piece
+// [kb0, kb1) of work item `item`, for the tokens [base, base + kNX) of each position.
 struct Pass {
-  int item, base, rb, kss, p;
+  int item, base, kb0, kb1, rb, p;
   PairTokens pt;
   int n0, n1;  // tokens of position 0 / 1 in this pass (0 .. kNX)
 };
 
-__device__ __forceinline__ Pass make_pass(const Ctl& c, int4 h, int per_pair, int ks, int n_rb) {
+__device__ __forceinline__ Pass make_pass(const Ctl& c, int4 h, int n_rb) {
   Pass s;
   s.item = h.x;
   s.base = h.y;
-  const int z = h.x / per_pair;
-  s.rb = (h.x / ks) % n_rb;
-  s.kss = h.x % ks;
-  s.p = c.s_active[z];
+  s.kb0 = h.w >> 16;
+  s.kb1 = h.w & 0xFFFF;
+  s.rb = h.x % n_rb;
+  s.p = c.s_active[h.x / n_rb];
   s.pt = load_pair(c.s_off, s.p);
   s.n0 = min(max(s.pt.cnt0 - s.base, 0), kNX);
   s.n1 = min(max(s.pt.cnt1 - s.base, 0), kNX);
   return s;
 }
 
-// One pass of the decoders over nk stages for the active position(s) (MODE bit 0 = pos 0,
-// bit 1 = pos 1): decode this thread's 32 packed words per stage (16 registers, k = 32 kh ..
-// 32 kh + 31 of its row) and store the bf16 rows into the TMEM A buffer: register r of chunk
-// i -> column 16 kh + 4 i + r (k pair 32 kh + 8 i + 2 r).
+// One pass of the decoders over the piece's stages for the active position(s) (MODE bit 0 =
+// pos 0, bit 1 = pos 1): decode this thread's 32 packed words per stage (16 registers, k =
+// 32 kh .. 32 kh + 31 of its row) and store the bf16 rows into the TMEM A buffer: register r
+// of chunk i -> column 16 kh + 4 i + r (k pair 32 kh + 8 i + 2 r).
 template <int MODE>
 __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t lane_tmem, const uint32_t (&w_off)[4],
-                                            int kh, int nk, Ring& w, Ring& a, const Muls& mu, int& tcount,
+                                            int kh, int n_stages, Ring& w, Ring& a, const Muls& mu, int& tcount,
                                             bool kW13) {
   const int lane = threadIdx.x & 31;
   (void)tcount;
   (void)kW13;
-  for (int kb = 0; kb < nk; ++kb) {
+  for (int kb = 0; kb < n_stages; ++kb) {
     if (kb) ptx::mbar_wait(&c.wfull[w.i], w.ph);
     PZ_TRD(2, tcount);
     const uint32_t st = smem_w + (uint32_t)w.i * kWBytes;
@@ -224,13 +238,15 @@ __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t la
   }
 }
 
+// part: 2 slots per CTA ([g][0] = its first piece, [g][1] = its last piece), each
+// slot_tok x 128 fp32 (token of the pair x tile row; w13 rows 0-63 = g, 64-127 = u).
 template <bool kW13>
 __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM sub-partition
     const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
     const int32_t* __restrict__ bucket_off, const int32_t* __restrict__ active_pairs,
-    const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb, int ks, int64_t n_assign_cap,
-    float* __restrict__ part, int32_t* __restrict__ counters, int32_t* __restrict__ work_ctr,
-    uint16_t* __restrict__ h_out, float* __restrict__ y_out, uint32_t mul_one, int n_bucket_pairs) {
+    const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb, int slot_tok,
+    float* __restrict__ part, int32_t* __restrict__ counters, uint16_t* __restrict__ h_out,
+    float* __restrict__ y_out, uint32_t mul_one, int n_bucket_pairs) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_w = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;  // == smem, shared window
@@ -271,34 +287,36 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = c.tmem_base;
-  const int per_pair = n_rb * ks;
-  const int kchunk = K / ks;
-  const int nk = kchunk / kBK;
+  const int nk = K / kBK;
+  StreamK sk;
+  sk.S = n_active * n_rb * nk;
+  sk.G = max(1, min((int)gridDim.x, sk.S / kMinStages));  // >= kMinStages stages per CTA
+  const int g = blockIdx.x;
+  const int s_begin = g < sk.G ? sk.begin(g) : 0, s_end = g < sk.G ? sk.begin(g + 1) : 0;
 
   if (warp == 0) {
     // ============================== W producer ==============================
-    // walks items (claimed with an atomic) / passes / k-blocks: one TMA stage of packed words
-    // per free W slot; each stage is also queued (sq) for the X producer
+    // walks this CTA's stage range piece by piece (a piece = the part of one work item in the
+    // range), pass by pass: one TMA stage of packed words per free W slot; each stage is also
+    // queued (sq) for the X producer
     if (lane != 0) return;
-    const int n_items = n_active * per_pair;
     Ring w{0, 0}, sq{0, 0};
     int tw = 0;
     (void)tw;
-    int item = atomicAdd(work_ctr, 1);
-    int next = item < n_items ? atomicAdd(work_ctr, 1) : n_items;  // claim overlaps the stream
-    while (item < n_items) {
-      const int z = item / per_pair;
-      const int rb = (item / ks) % n_rb, kss = item % ks;
-      const PairTokens pt = load_pair(c.s_off, c.s_active[z]);
+    for (int s0 = s_begin; s0 < s_end;) {
+      const int item = s0 / nk, kb0 = s0 % nk, kb1 = min(nk, kb0 + (s_end - s0));
+      s0 += kb1 - kb0;
+      const int rb = item % n_rb, p = c.s_active[item / n_rb];
+      const PairTokens pt = load_pair(c.s_off, p);
       const int maxcnt = max(pt.cnt0, pt.cnt1);
-      const int wrow = kW13 ? c.s_active[z] * 2 * f + rb * (kRows / 2) : c.s_active[z] * d + rb * kRows;
+      const int wrow = kW13 ? p * 2 * f + rb * (kRows / 2) : p * d + rb * kRows;
       for (int base = 0; base < maxcnt; base += kNX) {
         // X-side parameters: one activation box per active position (flag in bit 28)
         const int r0 = (pt.off0 + base) | ((pt.cnt0 > base) << 28);
         const int r1 = (pt.off1 + base) | ((pt.cnt1 > base) << 28);
-        for (int kb = 0; kb < nk; ++kb) {
-          const int kc = kss * kchunk + kb * kBK;
-          const int4 hv = make_int4(item, base, kb, 0);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int kc = kb * kBK;
+          const int4 hv = make_int4(item, base, kb, (kb0 << 16) | kb1);
           ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
           PZ_TR(0, tw);
           c.whdr[w.i] = hv;
@@ -319,8 +337,6 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           sq.next<kSq>();
         }
       }
-      item = next;
-      if (item < n_items) next = atomicAdd(work_ctr, 1);
     }
     // "no more work": complete one more phase of the W ring and the queue without data
     ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
@@ -365,8 +381,8 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
 
   if (warp == 1 || warp == 2 + kDecWarps) {
     // ============================== MMA issuers ==============================
-    // warp 1 issues position 0's MMAs, the last warp position 1's: two instruction streams,
-    // since one thread's tcgen05.mma retire ~57 ns apart at these N (scripts/micro/umma_rate.cu)
+    // warp 1 issues position 0's MMAs, warp 10 position 1's: two instruction streams, since
+    // one thread's tcgen05.mma retire ~57 ns apart at these N (scripts/micro/umma_rate.cu)
     const int mypos = warp == 1 ? 0 : 1;
     Ring x{0, 0}, a{0, 0};
     uint32_t accph = 0;
@@ -376,14 +392,14 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       ptx::mbar_wait(&c.xfull[x.i], x.ph);
       const int4 h = lds_int4(xhdr_s + 16u * x.i);
       if (h.x < 0) break;
-      const Pass s = make_pass(c, h, per_pair, ks, n_rb);
+      const Pass s = make_pass(c, h, n_rb);
       const int np = mypos ? s.n1 : s.n0;
       const uint32_t idp = ptx::idesc_bf16_f32(128, (uint32_t)((np + 15) & ~15));
       const uint32_t acc_col = tmem + kAccCol + 32u * mypos;
       ptx::mbar_wait(&c.acc_empty, accph ^ 1);  // the previous pass's epilogue drained TMEM
       ptx::tc_fence_after();
-      for (int kb = 0; kb < nk; ++kb) {
-        if (kb) ptx::mbar_wait(&c.xfull[x.i], x.ph);
+      for (int kb = s.kb0; kb < s.kb1; ++kb) {
+        if (kb != s.kb0) ptx::mbar_wait(&c.xfull[x.i], x.ph);
         if (mypos == 0) PZ_TR(6, tcount);
         ptx::mbar_wait(&c.a_full[a.i], a.ph);
         if (mypos == 0) PZ_TR(5, tcount);
@@ -393,11 +409,12 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         if (np > 0) {
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk)
-            ptx::mma_bf16_ts_elect(acc_col, ta + 8 * kk, ptx::smem_desc_sw128(xs + 32 * kk), idp, (kb | kk) != 0);
+            ptx::mma_bf16_ts_elect(acc_col, ta + 8 * kk, ptx::smem_desc_sw128(xs + 32 * kk), idp,
+                                   (kb != s.kb0) | (kk != 0));
         }
         ptx::mma_commit_elect(&c.a_empty[a.i]);  // A buffer free once these MMAs complete
         ptx::mma_commit_elect(&c.xempty[x.i]);   // X slot likewise
-        if (kb == nk - 1) ptx::mma_commit_elect(&c.acc_full);
+        if (kb == s.kb1 - 1) ptx::mma_commit_elect(&c.acc_full);
         if (mypos == 0) PZ_TR(7, tcount);
         ++tcount;
         x.next<kXStages>();
@@ -415,69 +432,67 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     // features' 64 up rows; lanes 0-15 of quarter q take gate rows 16q.., lanes 16-31 the up
     // rows of the same features, so g and u of one d_ff index land in lanes i, i+16 of one warp
     const int srow = kW13 ? (lane < 16 ? 16 * q + lane : 64 + 16 * q + lane - 16) : row;
+    // partial-slot row of this thread: w13 g rows 0-63 / u rows 64-127 by feature, w2 the tile row
+    const int prow = kW13 ? (lane < 16 ? 16 * q + lane : 64 + 16 * q + lane - 16) : row;
     const uint32_t lane_tmem = tmem + ((uint32_t)(32 * q) << 16);
     const Muls mu{mul_one, mul_one * 2u, mul_one * 4u, mul_one * 8u};
     uint32_t w_off[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) w_off[i] = swz(srow, 4 * kh + i);
-    Ring w{0, 0}, a{0, 0};  // a: TMEM A buffer (== X slot) ring
+    Ring w{0, 0}, a{0, 0};
     uint32_t accph = 0;
     int tcount = 0;
+    const int first_item = s_begin / nk;  // pieces of this CTA: [g][0] = first, [g][1] = last
     for (;;) {
       ptx::mbar_wait(&c.wfull[w.i], w.ph);
       const int4 h = lds_int4(whdr_s + 16u * w.i);
       if (h.x < 0) break;
-      const Pass s = make_pass(c, h, per_pair, ks, n_rb);
-      if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu, tcount, kW13);
-      else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu, tcount, kW13);
-      else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, nk, w, a, mu, tcount, kW13);
+      const Pass s = make_pass(c, h, n_rb);
+      const int n_st = s.kb1 - s.kb0;
+      if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13);
+      else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13);
+      else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13);
 
       // ---- epilogue of this pass: warp (q, pos = kh) reads its rows' accumulators ----
       ptx::mbar_wait(&c.acc_full, accph);
       accph ^= 1;
       ptx::tc_fence_after();
+      const bool whole = s.kb0 == 0 && s.kb1 == nk;  // the item is not split: final outputs
       const int pos = kh;
       const int np = pos ? s.n1 : s.n0;
-      const int offp = (pos ? s.pt.off1 : s.pt.off0) + s.base;
+      const int offp = (pos ? s.pt.off1 : s.pt.off0) + s.base;  // first assignment of this warp
+      float* slot = part + (size_t)(2 * g + (s.item == first_item ? 0 : 1)) * slot_tok * kRows;
       const uint32_t acc_t = lane_tmem + kAccCol + 32u * pos;
       for (int c0 = 0; c0 < np; c0 += 16) {
         uint32_t r[16];
         ptx::tmem_ld_32x32b_x16(acc_t + c0, r);
         ptx::tmem_ld_wait();
-        if (kW13) {
-          const bool up = lane >= 16;  // lanes 16..31 of every quarter hold the up rows
+        if (!whole) {
+          const int t0 = offp - s.pt.off0 + c0;  // token index within the pair's assignments
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < np) slot[(size_t)(t0 + i) * kRows + prow] = __uint_as_float(r[i]);
+        } else if (kW13) {
+          // exchange g <-> u with the partner lane; gate lanes finish tokens c0..c0+7,
+          // up lanes tokens c0+8..c0+15
+          const bool up = lane >= 16;
           const int feat = s.rb * (kRows / 2) + 16 * q + (lane & 15);  // d_ff index of this row
-          if (ks == 1) {
-            // exchange g <-> u with the partner lane; gate lanes finish tokens c0..c0+7,
-            // up lanes tokens c0+8..c0+15
-            float o[16];
+          float o[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __shfl_xor_sync(0xffffffffu, __uint_as_float(r[i]), 16);
+          for (int i = 0; i < 16; ++i) o[i] = __shfl_xor_sync(0xffffffffu, __uint_as_float(r[i]), 16);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float g = up ? o[8 + j] : __uint_as_float(r[j]);
-              const float u = up ? __uint_as_float(r[8 + j]) : o[j];
-              const int tok = c0 + (up ? 8 : 0) + j;
-              if (tok < np) h_out[(size_t)(offp + tok) * f + feat] = f32_to_bf16_bits_rn(silu_mul(g, u));
-            }
-          } else {
-            // partials: part[kss][a][0:f] = g, [f:2f] = u
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (c0 + i < np)
-                part[((size_t)s.kss * n_assign_cap + offp + c0 + i) * (2 * f) + (up ? f : 0) + feat] =
-                    __uint_as_float(r[i]);
+          for (int j = 0; j < 8; ++j) {
+            const float gv = up ? o[8 + j] : __uint_as_float(r[j]);
+            const float uv = up ? __uint_as_float(r[8 + j]) : o[j];
+            const int tok = c0 + (up ? 8 : 0) + j;
+            if (tok < np) h_out[(size_t)(offp + tok) * f + feat] = f32_to_bf16_bits_rn(silu_mul(gv, uv));
           }
         } else {
           const int r_out = s.rb * kRows + row;  // d_model row (the last block may overhang d)
           if (r_out < d) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if (c0 + i < np) {
-                const size_t aa = (size_t)(offp + c0 + i);
-                float* dst = ks == 1 ? y_out + aa * d : part + ((size_t)s.kss * n_assign_cap + aa) * d;
-                dst[r_out] = __uint_as_float(r[i]);
-              }
+              if (c0 + i < np) y_out[(size_t)(offp + c0 + i) * d + r_out] = __uint_as_float(r[i]);
           }
         }
       }
@@ -485,48 +500,46 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&c.acc_empty);
 
-      if (ks > 1 && s.base + kNX >= max(s.pt.cnt0, s.pt.cnt1)) {
-        // ---- the last of the ks CTAs of this (pair, row block) reduces in split order ----
+      if (!whole && s.base + kNX >= max(s.pt.cnt0, s.pt.cnt1)) {
+        // ---- last pass of a piece: the last of the item's pieces sums them in CTA order ----
         // (the barrier orders every decoder's partial stores before thread 64's gpu-scope
         //  fence, which is cumulative, so one fence publishes them all)
+        const int g_first = sk.owner(s.item * nk), g_last = sk.owner(s.item * nk + nk - 1);
         named_bar_sync(1, kDecWarps * 32);
-        const int ctr = s.p * n_rb + s.rb;
         if (dtid == 0) {
           __threadfence();
-          const int prev = atomicAdd(&counters[ctr], 1);
-          c.s_last = (prev == ks - 1);
-          if (c.s_last) counters[ctr] = 0;  // ready for the next call on this stream
+          const int prev = atomicAdd(&counters[s.item], 1);
+          c.s_last = (prev == g_last - g_first);
+          if (c.s_last) counters[s.item] = 0;  // ready for the next call on this stream
         }
         if (dtid == 0 && c.s_last) __threadfence();  // acquire side of the counter
         named_bar_sync(1, kDecWarps * 32);
         if (c.s_last) {
-          const int row_base = kW13 ? s.rb * (kRows / 2) : s.rb * kRows;
-          const int rows = kW13 ? kRows / 2 : min(kRows, d - row_base);  // multiple of 4
-          const int q4 = rows / 4;
+          const int r0 = s.rb * (kW13 ? kRows / 2 : kRows);
+          const int cols = kW13 ? kRows / 2 : min(kRows, d - r0);  // outputs of this tile, multiple of 4
+          const int q4 = cols / 4;
           const int n_tot = s.pt.cnt0 + s.pt.cnt1;  // buckets 2p and 2p+1 are adjacent
-          const int width = kW13 ? 2 * f : d;
-          const size_t split_stride = (size_t)n_assign_cap * width;
           for (int i = dtid; i < n_tot * q4; i += kDecWarps * 32) {
-            const size_t aa = (size_t)(s.pt.off0 + i / q4);
-            const int r = row_base + 4 * (i % q4);
+            const int t = i / q4, cq = 4 * (i % q4);
             float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
-            const float* src = part + aa * width + r;
-#pragma unroll 4
-            for (int sp = 0; sp < ks; ++sp) {
-              const float4 v4 = __ldcg(reinterpret_cast<const float4*>(src + sp * split_stride));
+            for (int gg = g_first; gg <= g_last; ++gg) {
+              const int sl = 2 * gg + (s.item == sk.begin(gg) / nk ? 0 : 1);
+              const float* src = part + ((size_t)sl * slot_tok + t) * kRows + cq;
+              const float4 v4 = __ldcg(reinterpret_cast<const float4*>(src));
               s0.x += v4.x; s0.y += v4.y; s0.z += v4.z; s0.w += v4.w;
               if (kW13) {
-                const float4 u = __ldcg(reinterpret_cast<const float4*>(src + sp * split_stride + f));
+                const float4 u = __ldcg(reinterpret_cast<const float4*>(src + kRows / 2));
                 s1.x += u.x; s1.y += u.y; s1.z += u.z; s1.w += u.w;
               }
             }
+            const size_t aa = (size_t)(s.pt.off0 + t);
             if (kW13) {
               uint2 o;
               o.x = f32_to_bf16_rne_bits(silu_mul(s0.x, s1.x)) | (f32_to_bf16_rne_bits(silu_mul(s0.y, s1.y)) << 16);
               o.y = f32_to_bf16_rne_bits(silu_mul(s0.z, s1.z)) | (f32_to_bf16_rne_bits(silu_mul(s0.w, s1.w)) << 16);
-              *reinterpret_cast<uint2*>(h_out + aa * f + r) = o;
+              *reinterpret_cast<uint2*>(h_out + aa * f + r0 + cq) = o;
             } else {
-              *reinterpret_cast<float4*>(y_out + aa * d + r) = s0;
+              *reinterpret_cast<float4*>(y_out + aa * d + r0 + cq) = s0;
             }
           }
         }
@@ -534,7 +547,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       }
     }
   }
-  // MMA warp + decoders: every MMA has completed (the last epilogue waited on it) and every
+  // MMA warps + decoders: every MMA has completed (the last epilogue waited on it) and every
   // tcgen05.ld has been waited on -> release TMEM
   ptx::tc_fence_before();
   named_bar_sync(3, 64 + kDecWarps * 32);
@@ -544,21 +557,22 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
 
 template <bool kW13>
 int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* bucket_off, const int32_t* active,
-               const int32_t* n_active, int K, int f, int d, int n_rb, int ks, int max_active, int64_t n_assign_cap,
-               float* part, int32_t* counters, int32_t* work_ctr, uint16_t* h, float* y, int n_pairs,
-               cudaStream_t stream) {
+               const int32_t* n_active, int K, int f, int d, int n_rb, int max_active, int slot_tok, float* part,
+               int32_t* counters, uint16_t* h, float* y, int n_pairs, cudaStream_t stream) {
   auto kern = k_gemv_tc<kW13>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     attr = true;
   }
-  const int n_items = max_active * n_rb * ks;  // upper bound; the device knows the active count
-  const int grid = std::min(n_items, 2 * num_sms());
+  // stream-K grid: every resident CTA slot, but >= kMinStages stages each (the device
+  // recomputes the partition from the actual number of active pairs)
+  const int64_t S = (int64_t)max_active * n_rb * (K / kBK);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gemv_tc_max_ctas(), S / kMinStages));
   {
     ProfScope _ps(kW13 ? "w13_gemv" : "w2_gemv", stream);
     cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kThreads), kSmem, stream, tw, tx, bucket_off, active, n_active,
-                               K, f, d, n_rb, ks, n_assign_cap, part, counters, work_ctr, h, y, 1u, n_pairs);
+                               K, f, d, n_rb, slot_tok, part, counters, h, y, 1u, n_pairs);
     if (e != cudaSuccess) return cuda_check(e, kW13 ? "w13_gemv launch" : "w2_gemv launch");
   }
   return cuda_check(cudaGetLastError(), kW13 ? "w13_gemv launch" : "w2_gemv launch");
@@ -566,14 +580,18 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
 
 }  // namespace
 
-// Same contract as launch_gemv_experts (gemv.cu); `nt` is unused (up to 32 tokens per position
-// per pass; more -> further passes over the same weights).
+// Resident CTA slots of the decode kernels (2 per SM): bounds the stream-K grid and the
+// partial-slot workspace.
+int gemv_tc_max_ctas() { return 2 * num_sms(); }
+bool gemv_supported(int d, int f) { return d % 64 == 0 && f % 64 == 0 && d <= 65535 * 64 && f <= 65535 * 64; }
+
+// x_rows: [n_assign_cap][d] bf16 in bucket order (TMA source); h: [n_assign_cap][f];
+// y: [n_assign_cap][d]; part: 2 * gemv_tc_max_ctas() * slot_tok * 128 floats, slot_tok >= the
+// assignments of any one pair; counters13 / counters2: >= n_pairs * row blocks, zero.
 int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f,
                            const uint16_t* x_rows, const int32_t* bucket_off, const int32_t* active_pairs,
-                           const int32_t* n_active, int max_active, int64_t n_assign_cap, int nt, int ks13, int ks2,
-                           float* part13, float* part2, int32_t* counters13, int32_t* counters2, int32_t* work_ctrs,
-                           uint16_t* h, float* y, cudaStream_t stream) {
-  (void)nt;
+                           const int32_t* n_active, int max_active, int64_t n_assign_cap, int slot_tok, float* part,
+                           int32_t* counters13, int32_t* counters2, uint16_t* h, float* y, cudaStream_t stream) {
   if (max_active == 0 || n_assign_cap == 0) return PUZZLE_OK;
   CUtensorMap tw13, tx13, tw2, tx2;
   int rc;
@@ -582,11 +600,11 @@ int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs,
   if ((rc = make_tmap_2d(&tw2, w2, (int64_t)n_pairs * d, f, kRows, kBK))) return rc;
   if ((rc = make_tmap_2d(&tx2, h, n_assign_cap, f, kXBox, kBK))) return rc;
   const int rb13 = f / (kRows / 2), rb2 = (d + kRows - 1) / kRows;
-  if ((rc = launch_one<true>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, ks13, max_active,
-                             n_assign_cap, part13, counters13, work_ctrs, h, y, n_pairs, stream)))
+  if ((rc = launch_one<true>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, max_active, slot_tok,
+                             part, counters13, h, y, n_pairs, stream)))
     return rc;
-  return launch_one<false>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, ks2, max_active, n_assign_cap,
-                           part2, counters2, work_ctrs + 1, h, y, n_pairs, stream);
+  return launch_one<false>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, max_active, slot_tok, part,
+                           counters2, h, y, n_pairs, stream);
 }
 
 #ifdef PZ_TRACE

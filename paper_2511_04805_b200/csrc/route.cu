@@ -311,19 +311,34 @@ __global__ void __launch_bounds__(256) k_gather_rows(const uint16_t* __restrict_
   for (int64_t c = lane; c < cols / 8; c += 32) dp[c] = sp[c];
 }
 
-__global__ void k_iota(int32_t* v, int n, int32_t* count) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = i;
-  if (threadIdx.x == 0) *count = n;
+// Pairs with at least one routed row, ascending (the experts-only entry point, whose buckets
+// come from the caller). One block of 256 threads, P <= 256.
+__global__ void k_active_pairs(const int32_t* __restrict__ off, int n_pairs, int32_t* __restrict__ active,
+                               int32_t* __restrict__ count) {
+  __shared__ int warp_cnt[8];
+  const int p = threadIdx.x, lane = p & 31, w = p >> 5;
+  const bool has = p < n_pairs && off[2 * p + 2] > off[2 * p];
+  const unsigned b = __ballot_sync(0xffffffffu, has);
+  if (lane == 0) warp_cnt[w] = __popc(b);
+  __syncthreads();
+  int base = 0;
+  for (int i = 0; i < w; ++i) base += warp_cnt[i];
+  if (has) active[base + __popc(b & ((1u << lane) - 1u))] = p;
+  if (p == 0) {
+    int t = 0;
+    for (int i = 0; i < 8; ++i) t += warp_cnt[i];
+    *count = t;
+  }
 }
 
 }  // namespace
 
-int launch_iota(int32_t* v, int n, int32_t* count, cudaStream_t stream) {
+int launch_active_pairs(const int32_t* bucket_off, int n_pairs, int32_t* active, int32_t* count, cudaStream_t stream) {
   {
-    ProfScope _ps("iota", stream);
-    k_iota<<<1, 256, 0, stream>>>(v, n, count);
+    ProfScope _ps("active_pairs", stream);
+    k_active_pairs<<<1, 256, 0, stream>>>(bucket_off, n_pairs, active, count);
   }
-  return cuda_check(cudaGetLastError(), "iota launch");
+  return cuda_check(cudaGetLastError(), "active_pairs launch");
 }
 
 bool route_is_small(int64_t T, int k) { return T * k <= kSmallMaxAssign; }
