@@ -67,6 +67,7 @@ constexpr uint32_t kAccCol = 64 * kAStages;      // 192
 
 #ifdef PZ_TRACE  // pipeline timeline of one CTA (tuning builds only; scripts/trace_gemv.py)
 __device__ unsigned long long g_trace[8][4096];
+__device__ unsigned long long g_cta[2][1024][4];  // [kernel][cta] {start, first W issue, producer done, end}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -277,6 +278,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     ptx::tma_prefetch_desc(&tm_w);
     ptx::tma_prefetch_desc(&tm_x);
   }
+#ifdef PZ_TRACE
+  if (threadIdx.x == 0) g_cta[kW13][blockIdx.x][0] = gtimer();
+#endif
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(&c.tmem_base);
   pdl_wait();     // route / gather / previous projection complete and visible
   pdl_trigger();  // the next kernel may begin its prologue as CTAs of this one retire
@@ -319,6 +323,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           const int4 hv = make_int4(item, base, kb, (kb0 << 16) | kb1);
           ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
           PZ_TR(0, tw);
+#ifdef PZ_TRACE
+          if (tw == 0) g_cta[kW13][blockIdx.x][1] = gtimer();
+#endif
           c.whdr[w.i] = hv;
           uint8_t* sw = smem + (size_t)w.i * kWBytes;
           ptx::mbar_arrive_expect_tx(&c.wfull[w.i], kWBytes);
@@ -338,6 +345,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         }
       }
     }
+#ifdef PZ_TRACE
+    g_cta[kW13][blockIdx.x][2] = gtimer();
+#endif
     // "no more work": complete one more phase of the W ring and the queue without data
     ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
     c.whdr[w.i] = make_int4(-1, 0, 0, 0);
@@ -553,6 +563,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   named_bar_sync(3, 64 + kDecWarps * 32);
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+#ifdef PZ_TRACE
+  if (threadIdx.x == 32) g_cta[kW13][blockIdx.x][3] = gtimer();
+#endif
 }
 
 template <bool kW13>
@@ -610,6 +623,9 @@ int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs,
 #ifdef PZ_TRACE
 extern "C" __attribute__((visibility("default"))) int puzzle_debug_trace(void* dst, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(dst, g_trace, bytes);
+}
+extern "C" __attribute__((visibility("default"))) int puzzle_debug_cta(void* dst, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(dst, g_cta, bytes);
 }
 #endif
 

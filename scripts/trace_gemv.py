@@ -53,3 +53,17 @@ mid = n // 2
 print("middle stages:")
 for t in range(mid, min(mid + 12, n)):
     print(t, " ".join(f"{names[e]}={ev[e, t]/1e3:7.2f}" for e in (0, 1, 2, 3, 4, 6, 5, 7)))
+
+cta = np.zeros((2, 1024, 4), np.uint64)
+lib.puzzle_debug_cta.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+assert lib.puzzle_debug_cta(cta.ctypes.data, cta.nbytes) == 0
+for kname, k in (("w13", 1), ("w2", 0)):
+    v = cta[k].astype(np.int64)
+    n = int((v[:, 3] > 0).sum())
+    v = v[:n]
+    t0 = v[:, 0].min()
+    v = v - t0
+    print(f"{kname}: {n} CTAs; start spread {v[:,0].max()/1e3:.1f} us; first W issue med {np.median(v[:,1])/1e3:.1f} "
+          f"max {v[:,1].max()/1e3:.1f}; producer done min {v[:,2].min()/1e3:.1f} med {np.median(v[:,2])/1e3:.1f} "
+          f"max {v[:,2].max()/1e3:.1f}; end min {v[:,3].min()/1e3:.1f} med {np.median(v[:,3])/1e3:.1f} max {v[:,3].max()/1e3:.1f} us")
+    print("  end-time percentiles (us):", [round(float(np.percentile(v[:,3], q))/1e3, 1) for q in (0, 10, 25, 50, 75, 90, 99, 100)])
