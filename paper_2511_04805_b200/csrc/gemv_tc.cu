@@ -90,6 +90,7 @@ struct alignas(16) Ctl {
   uint64_t wfull[kWStages], wempty[kWStages], xfull[kXStages], xempty[kXStages], a_full[kAStages],
       a_empty[kAStages];
   uint64_t sqfull[kSq], sqempty[kSq];
+  uint64_t pdone;  // decoders -> X producer: partials of this CTA's first (signalling) piece stored
   uint64_t acc_full, acc_empty;
   uint32_t tmem_base;
   int s_last;
@@ -159,13 +160,22 @@ struct Ring {
 
 // Stream-K partition: the S = (active pairs x row blocks) x nk stages are cut into G
 // contiguous ranges, CTA g taking stages [b_g, b_{g+1}), b_g = ceil(g S / G). A work item
-// (pair, row block) that straddles a cut is computed in pieces whose fp32 partials are summed,
-// in CTA order, by the piece that finishes last.
+// (pair, row block) that straddles a cut is computed in pieces (one per CTA it spans) whose
+// fp32 partials are summed in CTA order by the CTA owning the item's first stage: there the
+// piece is the LAST of that CTA's range, while every other piece is the FIRST of its CTA's
+// range, finished long before. Those signal with a counter (their X producer thread does the
+// fence + atomic, off the decoders' path); the reducer waits for the count at its range end.
 struct StreamK {
   int S, G;
   __device__ __forceinline__ int begin(int g) const { return (int)(((int64_t)g * S + G - 1) / G); }
   __device__ __forceinline__ int owner(int s) const { return (int)(((int64_t)s * G) / S); }
 };
+
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // Stage header {item, pass base, kb, kb0 << 16 | kb1}: the stage is k-block kb of the piece
 // [kb0, kb1) of work item `item`, for the tokens [base, base + kNX) of each position.
@@ -272,6 +282,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       ptx::mbar_init(&c.sqfull[j], 1);
       ptx::mbar_init(&c.sqempty[j], 1);
     }
+    ptx::mbar_init(&c.pdone, kDecWarps);
     ptx::mbar_init(&c.acc_full, 2);
     ptx::mbar_init(&c.acc_empty, kDecWarps);
     ptx::fence_mbar_init();
@@ -365,7 +376,21 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     Ring sq{0, 0}, x{0, 0};
     int tx = 0;
     (void)tx;
+    // this CTA's first piece signals its item's reducer when the item is split and started
+    // in an earlier CTA's range
+    int sig_item = s_begin < s_end && s_begin % nk != 0 ? s_begin / nk : -1;
+    if (sig_item >= 0) {  // (an active pair always has rows; an empty one would never signal)
+      const PairTokens pt = load_pair(c.s_off, c.s_active[sig_item / n_rb]);
+      if (pt.cnt0 + pt.cnt1 == 0) sig_item = -1;
+    }
+    bool signalled = sig_item < 0;
+    auto signal = [&]() {
+      __threadfence();  // cumulative: orders the decoders' partial stores (acquired via pdone)
+      atomicAdd(&counters[sig_item], 1);
+      signalled = true;
+    };
     for (;;) {
+      if (!signalled && ptx::mbar_test(&c.pdone, 0)) signal();
       ptx::mbar_wait(&c.sqfull[sq.i], sq.ph);
       const int4 h = c.sqh[sq.i];
       const int4 q = c.sq[sq.i];
@@ -377,6 +402,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         ptx::mbar_arrive(&c.xfull[x.i]);  // "no more work"
         break;
       }
+      if (!signalled && ptx::mbar_test(&c.pdone, 0)) signal();
       PZ_TR(1, tx);
       ++tx;
       const bool a0 = (q.y >> 28) & 1, a1 = (q.z >> 28) & 1;
@@ -385,6 +411,10 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       if (a0) ptx::tma_load_2d(sx, &tm_x, &c.xfull[x.i], q.x, q.y & 0x0FFFFFFF);
       if (a1) ptx::tma_load_2d(sx + kXPos, &tm_x, &c.xfull[x.i], q.x, q.z & 0x0FFFFFFF);
       x.next<kXStages>();
+    }
+    if (!signalled) {
+      ptx::mbar_wait(&c.pdone, 0);
+      signal();
     }
     return;
   }
@@ -510,21 +540,22 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&c.acc_empty);
 
-      if (!whole && s.base + kNX >= max(s.pt.cnt0, s.pt.cnt1)) {
-        // ---- last pass of a piece: the last of the item's pieces sums them in CTA order ----
-        // (the barrier orders every decoder's partial stores before thread 64's gpu-scope
-        //  fence, which is cumulative, so one fence publishes them all)
+      if (!whole && s.base + kNX >= max(s.pt.cnt0, s.pt.cnt1)) {  // last pass of a split piece
         const int g_first = sk.owner(s.item * nk), g_last = sk.owner(s.item * nk + nk - 1);
-        named_bar_sync(1, kDecWarps * 32);
-        if (dtid == 0) {
-          __threadfence();
-          const int prev = atomicAdd(&counters[s.item], 1);
-          c.s_last = (prev == g_last - g_first);
-          if (c.s_last) counters[s.item] = 0;  // ready for the next call on this stream
-        }
-        if (dtid == 0 && c.s_last) __threadfence();  // acquire side of the counter
-        named_bar_sync(1, kDecWarps * 32);
-        if (c.s_last) {
+        if (g != g_first) {
+          // a signalling piece: the X producer publishes it (fence + counter)
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&c.pdone);
+        } else {
+          // the reducer (this CTA's last piece): wait for the other pieces' signals, then sum
+          // the partials in CTA order (own slot included)
+          named_bar_sync(1, kDecWarps * 32);
+          if (dtid == 0) {
+            __threadfence();
+            while (ld_acquire_gpu(&counters[s.item]) < g_last - g_first) __nanosleep(64);
+            counters[s.item] = 0;  // ready for the next call on this stream
+          }
+          named_bar_sync(1, kDecWarps * 32);
           const int r0 = s.rb * (kW13 ? kRows / 2 : kRows);
           const int cols = kW13 ? kRows / 2 : min(kRows, d - r0);  // outputs of this tile, multiple of 4
           const int q4 = cols / 4;
@@ -552,8 +583,8 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
               *reinterpret_cast<float4*>(y_out + aa * d + r0 + cq) = s0;
             }
           }
+          named_bar_sync(1, kDecWarps * 32);
         }
-        named_bar_sync(1, kDecWarps * 32);
       }
     }
   }

@@ -49,7 +49,7 @@ print("A free seen - mma issued 3 stages ago  med ns", med(ev[3, 3:] - ev[7, :-3
 print("first 24 stages (us):")
 for t in range(min(24, n)):
     print(t, " ".join(f"{names[e]}={ev[e, t]/1e3:7.2f}" for e in (0, 1, 2, 3, 4, 6, 5, 7)))
-mid = n // 2
+mid = int(sys.argv[3]) if len(sys.argv) > 3 else n // 2
 print("middle stages:")
 for t in range(mid, min(mid + 12, n)):
     print(t, " ".join(f"{names[e]}={ev[e, t]/1e3:7.2f}" for e in (0, 1, 2, 3, 4, 6, 5, 7)))
