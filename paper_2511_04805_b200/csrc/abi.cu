@@ -21,6 +21,10 @@ int launch_route(const float*, int64_t, int, int, int, const int32_t*, int, int3
                  int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int, int32_t*, const uint16_t*, int, uint16_t*,
                  bool*, cudaStream_t);
 int launch_active_pairs(const int32_t*, int, int32_t*, int32_t*, cudaStream_t);
+int64_t route_dec_scratch_ints(int64_t T, int k, int n_pairs);
+int launch_route_dec(const float*, int64_t, int, int, int, const int32_t*, int, int32_t*, float*, int32_t*, int32_t*,
+                     int32_t*, int32_t*, int32_t*, int32_t*, int, int32_t*, const uint16_t*, int, uint16_t*,
+                     cudaStream_t);
 const char* last_error_cstr();
 int launch_combine(const float*, const int32_t*, const float*, int64_t, int, int, const uint16_t*,
                    uint16_t*, cudaStream_t);
@@ -180,7 +184,9 @@ Layout make_layout(const puzzle_moe_layer* L, const Plan& p) {
   // stream-K partial slots of the decode kernels: 2 per CTA x slot_tok x 128 fp32
   o.part = take(p.path == PUZZLE_PATH_GEMV ? (size_t)2 * gemv_tc_max_ctas() * p.slot_tok * 128 * 4 : 0);
   o.x_perm = take(na * d * 2);
-  o.route_scratch = take(2 * 2 * P * 4);
+  o.route_scratch = take((size_t)std::max<int64_t>(2 * 2 * (int64_t)P, p.T <= kGemvMaxTokens
+                                                                          ? route_dec_scratch_ints(p.T, p.k, (int)P)
+                                                                          : 0) * 4);
   o.total = off;
   return o;
 }
@@ -346,13 +352,24 @@ int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, con
     return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_moe_workspace_size(L, T, top_k)");
   cudaStream_t s = (cudaStream_t)stream;
   bool rows_written = false;
-  int rc = launch_route(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs,
+  int rc;
+  if (T <= kGemvMaxTokens) {  // decode batches: two-grid routing with the row gather fused
+    rc = launch_route_dec(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs,
+                          at<int32_t>(ws, lay.topk_idx), at<float>(ws, lay.topk_gate), at<int32_t>(ws, lay.bucket_off),
+                          at<int32_t>(ws, lay.assign_token), at<int32_t>(ws, lay.assign_of),
+                          at<int32_t>(ws, lay.active), at<int32_t>(ws, lay.n_active), at<int32_t>(ws, lay.cnt13),
+                          (int)((lay.h - lay.cnt13) / 4), at<int32_t>(ws, lay.route_scratch), hidden, L->d_model,
+                          at<uint16_t>(ws, lay.x_perm), s);
+    rows_written = true;
+  } else {
+  rc = launch_route(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs,
                         at<int32_t>(ws, lay.topk_idx), at<float>(ws, lay.topk_gate),
                         at<int32_t>(ws, lay.bucket_off), at<int32_t>(ws, lay.assign_token),
                         at<int32_t>(ws, lay.assign_of), at<int32_t>(ws, lay.active),
                         at<int32_t>(ws, lay.n_active), at<int32_t>(ws, lay.cnt13),
                         (int)((lay.h - lay.cnt13) / 4), at<int32_t>(ws, lay.route_scratch), hidden, L->d_model,
                         at<uint16_t>(ws, lay.x_perm), &rows_written, s);
+  }
   if (rc) return rc;
   // rows already in bucket order (fused into the large-batch scatter) or gathered now
   rc = run_experts(L, plan, lay, ws, rows_written ? at<uint16_t>(ws, lay.x_perm) : hidden,

@@ -51,6 +51,9 @@ constexpr int kNX = 32;                          // tokens per position per pass
 constexpr int kXBox = 32;                        // token rows per activation TMA box (= kNX)
 constexpr int kXPos = kNX * kBK * 2;             // 4 KB per position
 constexpr int kXBytes = 2 * kXPos;               // X stage: both positions
+#ifndef PZ_TC_DEFER  // decoders drain a pass's accumulators after two stages of the next pass
+#define PZ_TC_DEFER 0
+#endif
 #ifndef PZ_TC_WST  // W ring depth (tuning knob)
 #define PZ_TC_WST 4
 #endif
@@ -68,6 +71,7 @@ constexpr uint32_t kAccCol = 64 * kAStages;      // 192
 #ifdef PZ_TRACE  // pipeline timeline of one CTA (tuning builds only; scripts/trace_gemv.py)
 __device__ unsigned long long g_trace[8][4096];
 __device__ unsigned long long g_cta[2][1024][4];  // [kernel][cta] {start, first W issue, producer done, end}
+__device__ unsigned long long g_after_wait[2][1024];  // [kernel][cta] pdl_wait returned
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -203,10 +207,10 @@ __device__ __forceinline__ Pass make_pass(const Ctl& c, int4 h, int n_rb) {
 // pos 0, bit 1 = pos 1): decode this thread's 32 packed words per stage (16 registers, k =
 // 32 kh .. 32 kh + 31 of its row) and store the bf16 rows into the TMEM A buffer: register r
 // of chunk i -> column 16 kh + 4 i + r (k pair 32 kh + 8 i + 2 r).
-template <int MODE>
+template <int MODE, class Epi>
 __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t lane_tmem, const uint32_t (&w_off)[4],
                                             int kh, int n_stages, Ring& w, Ring& a, const Muls& mu, int& tcount,
-                                            bool kW13) {
+                                            bool kW13, int ep_at, Epi&& epi) {
   const int lane = threadIdx.x & 31;
   (void)tcount;
   (void)kW13;
@@ -246,6 +250,7 @@ __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t la
     PZ_TRD(4, tcount);
     ++tcount;
     a.next<kAStages>();
+    if (kb == ep_at) epi();  // the previous pass's epilogue, once the tensor pipe has work queued
   }
 }
 
@@ -294,6 +299,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
 #endif
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(&c.tmem_base);
   pdl_wait();     // route / gather / previous projection complete and visible
+#ifdef PZ_TRACE
+  if (threadIdx.x == 0) g_after_wait[kW13][blockIdx.x] = gtimer();
+#endif
   pdl_trigger();  // the next kernel may begin its prologue as CTAs of this one retire
   const int n_active = *n_active_ptr;
   for (int i = threadIdx.x; i < n_active; i += blockDim.x) c.s_active[i] = active_pairs[i];
@@ -483,17 +491,8 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     uint32_t accph = 0;
     int tcount = 0;
     const int first_item = s_begin / nk;  // pieces of this CTA: [g][0] = first, [g][1] = last
-    for (;;) {
-      ptx::mbar_wait(&c.wfull[w.i], w.ph);
-      const int4 h = lds_int4(whdr_s + 16u * w.i);
-      if (h.x < 0) break;
-      const Pass s = make_pass(c, h, n_rb);
-      const int n_st = s.kb1 - s.kb0;
-      if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13);
-      else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13);
-      else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13);
-
-      // ---- epilogue of this pass: warp (q, pos = kh) reads its rows' accumulators ----
+    // ---- epilogue of pass s: warp (q, pos = kh) reads its rows' accumulators ----
+    auto finish = [&](const Pass& s) {
       ptx::mbar_wait(&c.acc_full, accph);
       accph ^= 1;
       ptx::tc_fence_after();
@@ -586,7 +585,33 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           named_bar_sync(1, kDecWarps * 32);
         }
       }
+    };
+    Pass pend;
+    bool have_pend = false;
+    auto flush = [&]() {
+      if (have_pend) finish(pend);
+      have_pend = false;
+    };
+    for (;;) {
+      ptx::mbar_wait(&c.wfull[w.i], w.ph);
+      const int4 h = lds_int4(whdr_s + 16u * w.i);
+      if (h.x < 0) break;
+      const Pass s = make_pass(c, h, n_rb);
+      const int n_st = s.kb1 - s.kb0;
+      // PZ_TC_DEFER: drain the previous pass after two stages of this one (its last MMAs have
+      // completed by then; the A ring lets the decoders run ahead meanwhile)
+      const int ep_at = PZ_TC_DEFER ? min(1, n_st - 1) : -1;
+      if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      if (PZ_TC_DEFER) {
+        pend = s;
+        have_pend = true;
+      } else {
+        finish(s);
+      }
     }
+    flush();
   }
   // MMA warps + decoders: every MMA has completed (the last epilogue waited on it) and every
   // tcgen05.ld has been waited on -> release TMEM
@@ -657,6 +682,9 @@ extern "C" __attribute__((visibility("default"))) int puzzle_debug_trace(void* d
 }
 extern "C" __attribute__((visibility("default"))) int puzzle_debug_cta(void* dst, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(dst, g_cta, bytes);
+}
+extern "C" __attribute__((visibility("default"))) int puzzle_debug_wait(void* dst, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(dst, g_after_wait, bytes);
 }
 #endif
 

@@ -1,9 +1,8 @@
 // (a3) routing: top-k, gates, grouping of assignments by (pair, pos) bucket;
 // (a6) combine; plus a bf16 row gather used for token permutation / EP packing.
 //
-// Top-k is warp-per-token: each lane holds E/32 logits in registers, k rounds of a shuffle
-// argmax (ties -> lower expert id, R13) pick the experts, gates come from one more shuffle
-// sum. Small batches (decode) run the whole routing in ONE CTA (histogram, warp scan,
+// Top-k is warp-per-token: each lane holds E/32 logits in registers and ranks them against
+// all E logits (ties -> lower expert id, R13); gates come from two shuffle reductions. Small batches (decode) run the whole routing in ONE CTA (histogram, warp scan,
 // scatter in shared memory); large batches (prefill) use a grid of top-k CTAs, a one-CTA
 // scan, and a grid of scatter CTAs that also copy each token row to its bucket slot (the
 // TMA source of the expert kernels).
@@ -11,73 +10,79 @@
 
 namespace pz {
 
+#ifdef PZ_TRACE  // step timeline (tuning builds only): [kernel][min start, max end] in globaltimer ns
+__device__ unsigned long long g_rt[4][2];  // route, gather, combine, route_topk
+__device__ __forceinline__ void rt_stamp(int kid, bool end) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (end) atomicMax(&g_rt[kid][1], t);
+  else atomicMin(&g_rt[kid][0], t);
+}
+#define PZ_RT(kid, end) \
+  if (threadIdx.x == 0) rt_stamp(kid, end)
+extern "C" __attribute__((visibility("default"))) int puzzle_debug_rt(void* dst, size_t bytes, int reset) {
+  if (reset) {
+    unsigned long long init[4][2];
+    for (int i = 0; i < 4; ++i) { init[i][0] = ~0ull; init[i][1] = 0; }
+    return (int)cudaMemcpyToSymbol(g_rt, init, sizeof(init));
+  }
+  return (int)cudaMemcpyFromSymbol(dst, g_rt, bytes);
+}
+#else
+#define PZ_RT(kid, end)
+#endif
+
 namespace {
 
 constexpr int kMaxTopK = 16;
-constexpr int kMaxLogitsPerLane = kMaxExperts / 32;  // 16
 constexpr int kSmallThreads = 1024;
 constexpr int kSmallMaxAssign = 4096;  // single-CTA path keeps the assignment list in smem
+constexpr int64_t kDecMaxTokens = 64;   // two-grid decode routing
 
-// (v, e) ranks above (v2, e2): larger logit, or equal logit and lower expert id.
-__device__ __forceinline__ bool ranks_above(float v, int e, float v2, int e2) {
-  return v > v2 || (v == v2 && e < e2);
-}
-
-// One warp routes token t: lane j < k receives the j-th selected expert and its gate.
+// One warp routes token t. Rank selection: lane l holds the logits of experts 32 i + l
+// (i < PER); each counts how many of the E logits rank above each of its own (larger logit,
+// or equal logit and lower expert id, R13) from 32 PER independent shuffles -- no serial
+// k-round argmax. (Padding slots hold -inf and never rank above a real logit.)
+// The j-th largest (rank j < k) is selected as slot j; emit(rank, expert, gate) is called by
+// the lane holding it. Gates: softmax over the k selected (renormalize) or over all E.
+template <int PER, class Emit>
 __device__ __forceinline__ void warp_topk(const float* __restrict__ lg, int E, int k, int renorm, int lane,
-                                          int* sel_out, float* gate_out) {
-  float v[kMaxLogitsPerLane];
-  const int per = (E + 31) / 32;
+                                          Emit&& emit) {
+  float v[PER];
+  int rank[PER];
 #pragma unroll
-  for (int i = 0; i < kMaxLogitsPerLane; ++i) {
+  for (int i = 0; i < PER; ++i) {
     const int e = i * 32 + lane;
-    v[i] = (i < per && e < E) ? lg[e] : -INFINITY;
+    v[i] = e < E ? lg[e] : -INFINITY;
+    rank[i] = 0;
   }
-  float m_all = -INFINITY;  // the first selected logit = max over all experts
-  float sel_v = 0.f;
-  int sel_e = -1;
-  uint32_t taken = 0;  // bit i: v[i] already selected
-  for (int j = 0; j < k; ++j) {
-    float bv = -INFINITY;
-    int be = 0x7fffffff;
 #pragma unroll
-    for (int i = 0; i < kMaxLogitsPerLane; ++i) {
-      const int e = i * 32 + lane;
-      if (i < per && e < E && !((taken >> i) & 1u) && (be == 0x7fffffff || ranks_above(v[i], e, bv, be))) {
-        bv = v[i];
-        be = e;
-      }
-    }
+  for (int i2 = 0; i2 < PER; ++i2)
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      const int oe = __shfl_xor_sync(0xffffffffu, be, off);
-      if (oe != 0x7fffffff && (be == 0x7fffffff || ranks_above(ov, oe, bv, be))) {
-        bv = ov;
-        be = oe;
-      }
+    for (int src = 0; src < 32; ++src) {
+      const float x = __shfl_sync(0xffffffffu, v[i2], src);  // logit of expert 32 i2 + src
+      const int e2 = i2 * 32 + src;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) rank[i] += (x > v[i]) | ((x == v[i]) & (e2 < i * 32 + lane));
     }
-    if ((be & 31) == lane) taken |= 1u << (be >> 5);
-    if (j == 0) m_all = bv;
-    if (lane == j) {
-      sel_v = bv;
-      sel_e = be;
-    }
-  }
+  float m = -INFINITY;  // the largest logit (rank 0)
+#pragma unroll
+  for (int i = 0; i < PER; ++i) m = fmaxf(m, v[i]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
   float s = 0.f;
-  if (renorm) {
-    s = lane < k ? expf(sel_v - m_all) : 0.f;
-  } else {
 #pragma unroll
-    for (int i = 0; i < kMaxLogitsPerLane; ++i) {
-      const int e = i * 32 + lane;
-      if (i < per && e < E) s += expf(v[i] - m_all);
-    }
+  for (int i = 0; i < PER; ++i) {
+    const int e = i * 32 + lane;
+    if (e < E && (renorm ? rank[i] < k : true)) s += expf(v[i] - m);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  *sel_out = sel_e;
-  *gate_out = lane < k ? expf(sel_v - m_all) / s : 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int e = i * 32 + lane;
+    if (e < E && rank[i] < k) emit(rank[i], e, expf(v[i] - m) / s);
+  }
 }
 
 // Exclusive scan of s_count[0..n) by one warp into s_off[0..n].
@@ -117,6 +122,7 @@ __device__ __forceinline__ void warp_active(const int32_t* s_count, int n_pairs,
 }
 
 // ------------------------------------------------------------ small batches: one CTA
+template <int PER>
 __global__ void __launch_bounds__(kSmallThreads) k_route_small(
     const float* __restrict__ logits, int T, int E, int k, int renorm, const int32_t* __restrict__ expert_slot,
     int n_buckets, int32_t* __restrict__ topk_idx, float* __restrict__ topk_gate,
@@ -129,6 +135,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_route_small(
   __shared__ int32_t s_bucket[kSmallMaxAssign];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   pdl_wait();  // the previous forward may still be using this workspace
+  PZ_RT(0, false);
   pdl_trigger();
   // split-K arrival counters / scheduler counters of the expert kernels that follow
   for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero_ptr[i] = 0;
@@ -136,16 +143,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_route_small(
   for (int b = threadIdx.x; b < n_buckets; b += blockDim.x) s_count[b] = 0;
   __syncthreads();
   for (int t = warp; t < T; t += nwarps) {
-    int sel;
-    float gate;
-    warp_topk(logits + (size_t)t * E, E, k, renorm, lane, &sel, &gate);
-    if (lane < k) {
-      topk_idx[t * k + lane] = sel;
-      topk_gate[t * k + lane] = gate;
-      const int b = s_slot[sel];
-      s_bucket[t * k + lane] = b;
+    warp_topk<PER>(logits + (size_t)t * E, E, k, renorm, lane, [&](int j, int e, float gate) {
+      topk_idx[t * k + j] = e;
+      topk_gate[t * k + j] = gate;
+      const int b = s_slot[e];
+      s_bucket[t * k + j] = b;
       atomicAdd(&s_count[b], 1);
-    }
+    });
   }
   __syncthreads();
   if (warp == 0) {
@@ -162,6 +166,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_route_small(
     assign_token[a] = i / k;
     assign_of[i] = a;
   }
+  PZ_RT(0, true);
 }
 
 // ------------------------------------------------------------ large batches: three grids
@@ -169,6 +174,7 @@ constexpr int kBigThreads = 256;
 constexpr int kTokensPerWarp = 4;
 
 // top-k per token + per-CTA histogram folded into the global bucket counts
+template <int PER>
 __global__ void __launch_bounds__(kBigThreads) k_route_topk(const float* __restrict__ logits, int T, int E, int k,
                                                             int renorm, const int32_t* __restrict__ expert_slot,
                                                             int n_buckets, int32_t* __restrict__ topk_idx,
@@ -185,14 +191,11 @@ __global__ void __launch_bounds__(kBigThreads) k_route_topk(const float* __restr
   const int per_cta = kTokensPerWarp * (kBigThreads / 32);
   const int t_end = min(T, (int)(blockIdx.x + 1) * per_cta);
   for (int t = blockIdx.x * per_cta + warp; t < t_end; t += kBigThreads / 32) {
-    int sel;
-    float gate;
-    warp_topk(logits + (size_t)t * E, E, k, renorm, lane, &sel, &gate);
-    if (lane < k) {
-      topk_idx[(size_t)t * k + lane] = sel;
-      topk_gate[(size_t)t * k + lane] = gate;
-      atomicAdd(&s_count[s_slot[sel]], 1);
-    }
+    warp_topk<PER>(logits + (size_t)t * E, E, k, renorm, lane, [&](int j, int e, float gate) {
+      topk_idx[(size_t)t * k + j] = e;
+      topk_gate[(size_t)t * k + j] = gate;
+      atomicAdd(&s_count[s_slot[e]], 1);
+    });
   }
   __syncthreads();
   for (int b = threadIdx.x; b < n_buckets; b += blockDim.x)
@@ -265,6 +268,103 @@ __global__ void __launch_bounds__(kBigThreads) k_route_scatter(
   }
 }
 
+// ------------------------------------------------------------ decode batches: two grids
+// (T <= kDecMaxTokens) Every step is spread over many SMs and no zero-initialised global state
+// is needed (the workspace is caller memory): the top-k grid writes per-CTA bucket histograms and
+// each assignment's bucket + its position inside its CTA's share; the scatter grid scans the
+// histograms redundantly in every CTA (a few hundred ints), places each assignment and copies
+// its token row to the slot (the TMA source of the expert kernels).
+constexpr int kDecThreads = 256;  // one token per warp in the top-k grid, one assignment per warp in the scatter
+constexpr int kDecTokensPerCta = kDecThreads / 32;
+
+template <int PER>
+__global__ void __launch_bounds__(kDecThreads) k_route_dec_topk(
+    const float* __restrict__ logits, int T, int E, int k, int renorm, const int32_t* __restrict__ expert_slot,
+    int n_buckets, int32_t* __restrict__ topk_idx, float* __restrict__ topk_gate, int32_t* __restrict__ hist,
+    int32_t* __restrict__ bpos, int32_t* __restrict__ zero_ptr, int n_zero) {
+  __shared__ int32_t s_count[kMaxExperts];
+  __shared__ int32_t s_slot[kMaxExperts];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();  // the previous forward may still be using this workspace
+  PZ_RT(3, false);
+  pdl_trigger();
+  // split-piece counters of the expert kernels that follow
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_zero; i += gridDim.x * blockDim.x) zero_ptr[i] = 0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_slot[e] = expert_slot[e];
+  for (int b = threadIdx.x; b < n_buckets; b += blockDim.x) s_count[b] = 0;
+  __syncthreads();
+  const int t = blockIdx.x * kDecTokensPerCta + warp;
+  if (t < T) {
+    warp_topk<PER>(logits + (size_t)t * E, E, k, renorm, lane, [&](int j, int e, float gate) {
+      topk_idx[t * k + j] = e;
+      topk_gate[t * k + j] = gate;
+      const int b = s_slot[e];
+      bpos[t * k + j] = b | (atomicAdd(&s_count[b], 1) << 16);  // bucket | position in this CTA
+    });
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < n_buckets; b += blockDim.x) hist[blockIdx.x * n_buckets + b] = s_count[b];
+  PZ_RT(3, true);
+}
+
+__global__ void __launch_bounds__(kDecThreads) k_route_dec_scatter(
+    const int32_t* __restrict__ hist, int n_hist, const int32_t* __restrict__ bpos, int n_assign, int k,
+    int n_buckets, int32_t* __restrict__ bucket_off, int32_t* __restrict__ assign_token,
+    int32_t* __restrict__ assign_of, int32_t* __restrict__ active_pairs, int32_t* __restrict__ n_active,
+    const uint16_t* __restrict__ hidden, int d, uint16_t* __restrict__ x_perm) {
+  extern __shared__ int32_t s_pre[];  // [n_hist][n_buckets] exclusive prefix over top-k CTAs
+  __shared__ int32_t s_tot[kMaxExperts];
+  __shared__ int32_t s_off[kMaxExperts + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();
+  PZ_RT(0, false);
+  pdl_trigger();
+  for (int b = threadIdx.x; b < n_buckets; b += blockDim.x) {
+    int run = 0;
+    for (int c = 0; c < n_hist; ++c) {
+      const int v = hist[c * n_buckets + b];
+      s_pre[c * n_buckets + b] = run;
+      run += v;
+    }
+    s_tot[b] = run;
+  }
+  __syncthreads();
+  if (warp == 0) warp_scan(s_tot, s_off, n_buckets, lane);
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    if (warp == 0) {
+      for (int b = lane; b <= n_buckets; b += 32) bucket_off[b] = s_off[b];
+    } else if (warp == 1 && active_pairs != nullptr) {
+      warp_active(s_tot, n_buckets / 2, active_pairs, n_active, lane);
+    }
+  }
+  const int i = blockIdx.x * (kDecThreads / 32) + warp;  // assignment of this warp
+  if (i < n_assign) {
+    const int t = i / k, c = t / kDecTokensPerCta;
+    const int bp = bpos[i], b = bp & 0xFFFF;
+    const int a = s_off[b] + s_pre[c * n_buckets + b] + (bp >> 16);
+    if (lane == 0) {
+      assign_token[a] = t;
+      assign_of[i] = a;
+    }
+    if (x_perm != nullptr) {  // the token row into its slot, 8 x 16 B in flight per lane
+      const uint4* src = reinterpret_cast<const uint4*>(hidden + (size_t)t * d);
+      uint4* dst = reinterpret_cast<uint4*>(x_perm + (size_t)a * d);
+      const int n16 = d / 8;
+      for (int c0 = 0; c0 < n16; c0 += 32 * 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c0 + 32 * u + lane < n16) v[u] = src[c0 + 32 * u + lane];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c0 + 32 * u + lane < n16) dst[c0 + 32 * u + lane] = v[u];
+      }
+    }
+  }
+  PZ_RT(0, true);
+}
+
 // out[t] = residual[t] + sum_j gate[t,j] * y[assign_of[t,j]], fp32 in slot order, one bf16 rounding.
 __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y,
                                                  const int32_t* __restrict__ assign_of,
@@ -274,6 +374,7 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y,
   const int64_t t = blockIdx.y;
   const int c4 = blockIdx.x * blockDim.x + threadIdx.x;  // index of a 4-column group
   pdl_wait();
+  PZ_RT(2, false);
   pdl_trigger();
   if (c4 * 4 >= d) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -294,6 +395,7 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y,
   o.x = f32_to_bf16_rne_bits(acc.x) | (f32_to_bf16_rne_bits(acc.y) << 16);
   o.y = f32_to_bf16_rne_bits(acc.z) | (f32_to_bf16_rne_bits(acc.w) << 16);
   *reinterpret_cast<uint2*>(out + t * d + c4 * 4) = o;
+  PZ_RT(2, true);
 }
 
 // dst[i] = src[index[i]] for bf16 rows; cols % 8 == 0 (16-byte chunks); one warp per row.
@@ -302,6 +404,7 @@ __global__ void __launch_bounds__(256) k_gather_rows(const uint16_t* __restrict_
                                                      int64_t cols, uint16_t* __restrict__ dst) {
   const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   pdl_wait();
+  PZ_RT(1, false);
   pdl_trigger();
   if (i >= n_rows) return;
   const int lane = threadIdx.x & 31;
@@ -309,6 +412,8 @@ __global__ void __launch_bounds__(256) k_gather_rows(const uint16_t* __restrict_
   const uint4* sp = reinterpret_cast<const uint4*>(src + s * cols);
   uint4* dp = reinterpret_cast<uint4*>(dst + i * cols);
   for (int64_t c = lane; c < cols / 8; c += 32) dp[c] = sp[c];
+  __syncwarp();
+  if (lane == 0) PZ_RT(1, true);
 }
 
 // Pairs with at least one routed row, ascending (the experts-only entry point, whose buckets
@@ -341,7 +446,55 @@ int launch_active_pairs(const int32_t* bucket_off, int n_pairs, int32_t* active,
   return cuda_check(cudaGetLastError(), "active_pairs launch");
 }
 
+// logits per lane of the warp top-k, rounded up to a power of two
+static int per_lane(int E) {
+  int per = 1;
+  while (per * 32 < E) per *= 2;
+  return per;
+}
+
 bool route_is_small(int64_t T, int k) { return T * k <= kSmallMaxAssign; }
+
+// Decode-batch routing scratch: per-CTA histograms + packed bucket positions (ints).
+int64_t route_dec_scratch_ints(int64_t T, int k, int n_pairs) {
+  return ((T + kDecTokensPerCta - 1) / kDecTokensPerCta) * 2 * n_pairs + T * k;
+}
+
+// Routing + fused row gather for T <= kDecMaxTokens: two multi-CTA kernels (see above).
+int launch_route_dec(const float* logits, int64_t T, int E, int k, int renorm, const int32_t* expert_slot,
+                     int n_pairs, int32_t* topk_idx, float* topk_gate, int32_t* bucket_off, int32_t* assign_token,
+                     int32_t* assign_of, int32_t* active_pairs, int32_t* n_active, int32_t* zero_ptr, int n_zero,
+                     int32_t* scratch, const uint16_t* hidden, int d, uint16_t* x_perm, cudaStream_t stream) {
+  if (k > kMaxTopK) return fail(PUZZLE_ERR_UNSUPPORTED, "top_k > 16 is not supported by the route kernel");
+  if (E > kMaxExperts) return fail(PUZZLE_ERR_UNSUPPORTED, "n_experts > 512");
+  if (T > kDecMaxTokens) return fail(PUZZLE_ERR_UNSUPPORTED, "decode routing takes <= 64 tokens");
+  const int nb = 2 * n_pairs;
+  const int n_hist = (int)((T + kDecTokensPerCta - 1) / kDecTokensPerCta);
+  int32_t* hist = scratch;
+  int32_t* bpos = scratch + (int64_t)n_hist * nb;
+  const int per = per_lane(E);
+  auto topk = per == 1 ? k_route_dec_topk<1> : per == 2 ? k_route_dec_topk<2> : per == 4 ? k_route_dec_topk<4>
+            : per == 8 ? k_route_dec_topk<8> : k_route_dec_topk<16>;
+  int rc;
+  {
+    ProfScope _ps("route_topk", stream);
+    if ((rc = cuda_check(launch_pdl(topk, dim3(n_hist), dim3(kDecThreads), 0, stream, logits, (int)T, E, k, renorm,
+                                    expert_slot, nb, topk_idx, topk_gate, hist, bpos, zero_ptr, n_zero),
+                         "route_topk launch")))
+      return rc;
+  }
+  const int n_assign = (int)(T * k);
+  {
+    ProfScope _ps("route_scatter", stream);
+    if ((rc = cuda_check(launch_pdl(k_route_dec_scatter, dim3((n_assign + kDecThreads / 32 - 1) / (kDecThreads / 32)),
+                                    dim3(kDecThreads), (size_t)n_hist * nb * sizeof(int32_t), stream,
+                                    (const int32_t*)hist, n_hist, (const int32_t*)bpos, n_assign, k, nb, bucket_off,
+                                    assign_token, assign_of, active_pairs, n_active, hidden, d, x_perm),
+                         "route_scatter launch")))
+      return rc;
+  }
+  return PUZZLE_OK;
+}
 
 // scratch: >= 2 * n_buckets int32 (global counts + cursors), used by the large-batch path only.
 // hidden / x_perm (optional): the large-batch scatter also writes the bucket-ordered rows and
@@ -358,7 +511,10 @@ int launch_route(const float* logits, int64_t T, int E, int k, int renorm, const
   if (route_is_small(T, k)) {
     {
       ProfScope _ps("route", stream);
-      cudaError_t e = launch_pdl(k_route_small, dim3(1), dim3(kSmallThreads), 0, stream, logits, (int)T, E, k, renorm,
+      const int per = per_lane(E);
+      auto kern = per == 1 ? k_route_small<1> : per == 2 ? k_route_small<2> : per == 4 ? k_route_small<4>
+                : per == 8 ? k_route_small<8> : k_route_small<16>;
+      cudaError_t e = launch_pdl(kern, dim3(1), dim3(kSmallThreads), 0, stream, logits, (int)T, E, k, renorm,
                                  expert_slot, nb, topk_idx, topk_gate, bucket_off, assign_token, assign_of,
                                  active_pairs, n_active, zero_ptr, n_zero);
       if (e != cudaSuccess) return cuda_check(e, "route launch");
@@ -375,7 +531,10 @@ int launch_route(const float* logits, int64_t T, int E, int k, int renorm, const
   const int per_cta = kTokensPerWarp * (kBigThreads / 32);
   {
     ProfScope _ps("route_topk", stream);
-    if ((rc = cuda_check(launch_pdl(k_route_topk, dim3((unsigned)((T + per_cta - 1) / per_cta)), dim3(kBigThreads), 0,
+    const int per = per_lane(E);
+    auto kern = per == 1 ? k_route_topk<1> : per == 2 ? k_route_topk<2> : per == 4 ? k_route_topk<4>
+              : per == 8 ? k_route_topk<8> : k_route_topk<16>;
+    if ((rc = cuda_check(launch_pdl(kern, dim3((unsigned)((T + per_cta - 1) / per_cta)), dim3(kBigThreads), 0,
                                     stream, logits, (int)T, E, k, renorm, expert_slot, nb, topk_idx, topk_gate, g_count),
                          "route_topk launch")))
       return rc;

@@ -1,0 +1,71 @@
+"""GPU timeline of one CUDA-graph replay of the forward (needs a PZ_TRACE build of route.cu and
+gemv_tc.cu: python scripts/build_variant.py trace route.cu,gemv_tc.cu -DPZ_TRACE=5; run with
+PUZZLE_LIB=...). Prints each kernel's [first CTA start, pdl_wait return, last CTA end] in us
+relative to the route kernel's start."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import synth  # noqa: E402
+import paper_2511_04805_b200 as pz  # noqa: E402
+
+cfg = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "mixtral"]
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+dev = torch.device("cuda:0")
+layer, _ = bench.build_layer_gpu(pz, cfg, 1, dev)
+hidden, logits = bench.make_inputs(cfg, T, 2, dev)
+out = torch.empty_like(hidden)
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    for _ in range(3):
+        layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out)
+lib = pz.load_library()
+for name in ("puzzle_debug_rt", "puzzle_debug_cta", "puzzle_debug_wait"):
+    getattr(lib, name).restype = ctypes.c_int
+lib.puzzle_debug_rt.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+lib.puzzle_debug_cta.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+lib.puzzle_debug_wait.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+for _ in range(5):
+    g.replay()
+torch.cuda.synchronize()
+rt = np.zeros((4, 2), np.uint64)
+cta = np.zeros((2, 1024, 4), np.uint64)
+wt = np.zeros((2, 1024), np.uint64)
+assert lib.puzzle_debug_rt(None, 0, 1) == 0
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+with torch.cuda.stream(s):
+    ev0.record(s)
+    g.replay()
+    ev1.record(s)
+torch.cuda.synchronize()
+assert lib.puzzle_debug_rt(rt.ctypes.data, rt.nbytes, 0) == 0
+assert lib.puzzle_debug_cta(cta.ctypes.data, cta.nbytes) == 0
+assert lib.puzzle_debug_wait(wt.ctypes.data, wt.nbytes) == 0
+t0 = int(min(rt[0, 0], rt[3, 0]))
+print(f"{cfg.name} T={T}: graph replay {ev0.elapsed_time(ev1) * 1e3:.1f} us (events)")
+def us(x):
+    return (int(x) - t0) / 1e3
+if int(rt[3, 1]) > 0:
+    print(f"  topk    start {us(rt[3,0]):7.2f}  end {us(rt[3,1]):7.2f}")
+print(f"  route   start {us(rt[0,0]):7.2f}  end {us(rt[0,1]):7.2f}   (single-CTA route, or the decode scatter+gather)")
+if int(rt[1, 1]) > 0:
+    print(f"  gather  start {us(rt[1,0]):7.2f}  end {us(rt[1,1]):7.2f}")
+for name, k in (("w13", 1), ("w2", 0)):
+    v = cta[k]
+    n = int((v[:, 3] > 0).sum())
+    starts = v[:n, 0].astype(np.int64)
+    waits = wt[k, :n].astype(np.int64)
+    ends = v[:n, 3].astype(np.int64)
+    print(f"  {name:6s}  start {(starts.min() - t0)/1e3:7.2f}  wait-ret min {(waits.min() - t0)/1e3:7.2f} "
+          f"max {(waits.max() - t0)/1e3:7.2f}  end min {(ends.min() - t0)/1e3:7.2f} med {(np.median(ends) - t0)/1e3:7.2f} "
+          f"max {(ends.max() - t0)/1e3:7.2f}   ({n} CTAs)")
+print(f"  combine start {us(rt[2,0]):7.2f}  end {us(rt[2,1]):7.2f}")
