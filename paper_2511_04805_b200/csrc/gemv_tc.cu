@@ -72,6 +72,7 @@ constexpr uint32_t kAccCol = 64 * kAStages;      // 192
 __device__ unsigned long long g_trace[8][4096];
 __device__ unsigned long long g_cta[2][1024][4];  // [kernel][cta] {start, first W issue, producer done, end}
 __device__ unsigned long long g_after_wait[2][1024];  // [kernel][cta] pdl_wait returned
+__device__ unsigned int g_smid[2][1024];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -300,7 +301,12 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(&c.tmem_base);
   pdl_wait();     // route / gather / previous projection complete and visible
 #ifdef PZ_TRACE
-  if (threadIdx.x == 0) g_after_wait[kW13][blockIdx.x] = gtimer();
+  if (threadIdx.x == 0) {
+    g_after_wait[kW13][blockIdx.x] = gtimer();
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_smid[kW13][blockIdx.x] = smid;
+  }
 #endif
   pdl_trigger();  // the next kernel may begin its prologue as CTAs of this one retire
   const int n_active = *n_active_ptr;
@@ -685,6 +691,9 @@ extern "C" __attribute__((visibility("default"))) int puzzle_debug_cta(void* dst
 }
 extern "C" __attribute__((visibility("default"))) int puzzle_debug_wait(void* dst, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(dst, g_after_wait, bytes);
+}
+extern "C" __attribute__((visibility("default"))) int puzzle_debug_smid(void* dst, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(dst, g_smid, bytes);
 }
 #endif
 

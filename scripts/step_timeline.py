@@ -69,3 +69,35 @@ for name, k in (("w13", 1), ("w2", 0)):
           f"max {(waits.max() - t0)/1e3:7.2f}  end min {(ends.min() - t0)/1e3:7.2f} med {(np.median(ends) - t0)/1e3:7.2f} "
           f"max {(ends.max() - t0)/1e3:7.2f}   ({n} CTAs)")
 print(f"  combine start {us(rt[2,0]):7.2f}  end {us(rt[2,1]):7.2f}")
+
+if len(sys.argv) > 3:
+    sm = np.zeros((2, 1024), np.uint32)
+    lib.puzzle_debug_smid.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    assert lib.puzzle_debug_smid(sm.ctypes.data, sm.nbytes) == 0
+    for name, k in (("w13", 1), ("w2", 0)):
+        v = cta[k]
+        n = int((v[:, 3] > 0).sum())
+        dur = (v[:n, 3].astype(np.int64) - wt[k, :n].astype(np.int64)) / 1e3
+        smid = sm[k, :n]
+        print(f"{name}: duration after wait: mean {dur.mean():.1f} std {dur.std():.1f} min {dur.min():.1f} max {dur.max():.1f}")
+        # per SM: the two CTAs on it
+        per_sm = {}
+        for i in range(n):
+            per_sm.setdefault(int(smid[i]), []).append(float(dur[i]))
+        sm_mean = np.array([np.mean(per_sm[s]) for s in sorted(per_sm)])
+        print(f"  per-SM mean duration: min {sm_mean.min():.1f} max {sm_mean.max():.1f}; CTAs per SM "
+              f"{sorted(set(len(x) for x in per_sm.values()))}")
+        order = np.argsort(sm_mean)
+        keys = sorted(per_sm)
+        print("  slowest SMs:", [(keys[i], round(sm_mean[i], 1)) for i in order[-8:]])
+        print("  fastest SMs:", [(keys[i], round(sm_mean[i], 1)) for i in order[:8]])
+        # by CTA index halves
+        print(f"  CTA idx < {n//2}: mean {dur[:n//2].mean():.1f}; >= : mean {dur[n//2:].mean():.1f}")
+        # within-SM difference
+        diffs = [abs(x[0] - x[1]) for x in per_sm.values() if len(x) == 2]
+        print(f"  |CTA a - CTA b| on the same SM: mean {np.mean(diffs):.1f} max {np.max(diffs):.1f}")
+        # dump durations in SM order for a correlation by GPC (SM id // 16 approx)
+        gpc = {}
+        for s_, d_ in per_sm.items():
+            gpc.setdefault(s_ // 18, []).append(np.mean(d_))
+        print("  by SM-id block of 18:", {k2: round(float(np.mean(v2)), 1) for k2, v2 in sorted(gpc.items())})
