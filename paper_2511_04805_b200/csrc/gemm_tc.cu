@@ -30,6 +30,26 @@
 
 namespace pz {
 
+#ifdef PZ_TRACE  // pipeline timeline of one CTA (tuning builds only; scripts/trace_tc.py)
+__device__ unsigned long long g_tct[6][4096];  // 0 TMA issue, 1 decode done, 2 MMA issued, 3 epi start, 4 epi end
+__device__ unsigned long long g_tcc[2][1024][2];  // [kernel][cta] {start after wait, end}
+__device__ __forceinline__ unsigned long long tc_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PZ_TT(ev, idx) \
+  if (kW13 && blockIdx.x == PZ_TRACE && (idx) < 4096) g_tct[ev][idx] = tc_gtimer()
+extern "C" __attribute__((visibility("default"))) int puzzle_debug_tc(void* dst, size_t bytes, void* dst2,
+                                                                    size_t bytes2) {
+  int rc = (int)cudaMemcpyFromSymbol(dst, g_tct, bytes);
+  if (rc) return rc;
+  return (int)cudaMemcpyFromSymbol(dst2, g_tcc, bytes2);
+}
+#else
+#define PZ_TT(ev, idx)
+#endif
+
 namespace {
 
 constexpr int BM = 256;  // tokens per tile (2 x UMMA M=128)
@@ -137,6 +157,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
 
   // ---- setup: bucket / tile offsets, barriers, TMEM ----
   pdl_wait();
+#ifdef PZ_TRACE
+  if (threadIdx.x == 0) g_tcc[kW13][blockIdx.x][0] = tc_gtimer();
+#endif
   pdl_trigger();
   for (int i = threadIdx.x; i <= n_buckets; i += blockDim.x) c.bucket_off[i] = bucket_off[i];
   __syncthreads();
@@ -175,11 +198,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int tcount = 0;
+      (void)tcount;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const TileInfo t = tile_info(c, tile, n_blocks);
         const int pair = t.bucket >> 1;
         for (int kb = 0; kb < nk; ++kb) {
           ptx::mbar_wait(&c.empty[stage], phase ^ 1);
+          PZ_TT(0, tcount);
+          ++tcount;
           uint8_t* sa = smem + (size_t)stage * kStageBytes;
           uint8_t* sb = sa + kABytes;
           ptx::mbar_arrive_expect_tx(&c.full[stage], kStageBytes);
@@ -200,6 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, BN);
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
+    int tcount = 0;
+    (void)tcount;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const TileInfo t = tile_info(c, tile, n_blocks);
       const bool two = t.valid > 128;
@@ -220,7 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
           }
           ptx::mma_commit(&c.empty[stage]);
           if (kb == nk - 1) ptx::mma_commit(&c.tmem_full);
+          PZ_TT(2, tcount);
         }
+        ++tcount;
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
@@ -233,6 +264,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     const int ch = (warp - 2) >> 2;        // which half of the columns (2 warps per quarter)
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
+    int tcount = 0, tiles_done = 0;
+    (void)tcount;
+    (void)tiles_done;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const TileInfo t = tile_info(c, tile, n_blocks);
       const int pos = t.bucket & 1;
@@ -243,9 +277,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&c.dec[stage]);
+        if (threadIdx.x == 64) PZ_TT(1, tcount);
+        ++tcount;
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
       // ---- epilogue ----
+      if (threadIdx.x == 64) PZ_TT(3, tiles_done);
       ptx::mbar_wait(&c.tmem_full, acc_phase);
       ptx::tc_fence_after();
       for (int half = 0; half < 2; ++half) {
@@ -289,12 +326,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&c.tmem_empty);
+      if (threadIdx.x == 64) PZ_TT(4, tiles_done);
+      ++tiles_done;
       acc_phase ^= 1;
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+#ifdef PZ_TRACE
+  if (threadIdx.x == 0) g_tcc[kW13][blockIdx.x][1] = tc_gtimer();
+#endif
 }
 
 }  // namespace
