@@ -446,6 +446,17 @@ def run_ours(args):
                 "units_per_launch": n_touched, "unit_bytes": per_launch_bytes[dom] // max(n_touched, 1),
                 "peak_source": pk["source"],
                 "step_share": kern[dom]["total_ms"] / max(sum(v["total_ms"] for v in kern.values()), 1e-9)}
+    elif dom in ("w13_tc", "w2_tc"):
+        # prefill: tensor-bound; algorithmic flops = dense-equivalent FFN flops of the routed
+        # assignments (unit: one assignment's 2*(2f)*d (w13) or 2*d*f (w2) flop)
+        n_assign = T * cfg.top_k
+        unit = 2 * 2 * cfg.d_ff * cfg.d_model if dom == "w13_tc" else 2 * cfg.d_model * cfg.d_ff
+        achieved = unit * n_assign / (kern[dom]["avg_ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops"], "traffic": ncu_traffic(cfg.name, T, dom),
+                "algorithmic_flops_per_launch": unit * n_assign, "units_per_launch": n_assign, "unit_flops": unit,
+                "peak_source": pk["source"],
+                "step_share": kern[dom]["total_ms"] / max(sum(v["total_ms"] for v in kern.values()), 1e-9)}
     step_gbs = (ab["w13"] + ab["w2"]) / (ms / 1e3) / 1e9
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region

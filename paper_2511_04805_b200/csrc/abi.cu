@@ -31,7 +31,7 @@ int launch_combine(const float*, const int32_t*, const float*, int64_t, int, int
 int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16_t*, cudaStream_t);
 bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
-                      uint16_t*, float*, cudaStream_t);
+                      uint16_t*, float*, int32_t*, cudaStream_t);
 int gemv_tc_max_ctas();
 bool gemv_supported(int d, int f);
 int launch_gemv_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*,
@@ -325,7 +325,7 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
   }
   if (plan.path == PUZZLE_PATH_TC)
     return launch_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
-                             at<uint16_t>(ws, lay.h), y, s);
+                             at<uint16_t>(ws, lay.h), y, at<int32_t>(ws, lay.cnt13), s);  // cnt13: zeroed per call
   return launch_gemv_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
                                 n_active, plan.max_active, plan.n_assign, plan.slot_tok, at<float>(ws, lay.part),
                                 at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);

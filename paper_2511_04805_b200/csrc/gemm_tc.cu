@@ -65,6 +65,8 @@ constexpr uint32_t kTmemCols = 512;
 constexpr int kMaxBuckets = 2 * 256;
 
 struct alignas(8) SmemCtl {
+  int32_t hdr[kStages];  // tile of each stage (-1 = no more work), written by the producer
+  int32_t pad_;
   uint64_t full[kStages];
   uint64_t dec[kStages];
   uint64_t empty[kStages];
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     const int32_t* __restrict__ bucket_off, int n_buckets, int K, int f, int d, int n_blocks,
     uint16_t* __restrict__ h_out,  // w13: [n_assign][f] bf16
     float* __restrict__ y_out,     // w2:  [n_assign][d] f32
+    int32_t* __restrict__ work_ctr,  // zero on entry: tiles are claimed with an atomic
     uint32_t mul_one) {            // = 1, opaque to ptxas (keeps decode shifts on the FMA pipe)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -200,13 +203,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       uint32_t phase = 0;
       int tcount = 0;
       (void)tcount;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      // tiles are claimed dynamically (their costs differ: ragged M tiles, pairs with one
+      // position); the next claim overlaps the current tile's stream
+#ifndef PZ_TC_STATIC  // 1: static round-robin tile assignment (A/B experiments)
+#define PZ_TC_STATIC 0
+#endif
+      int next = PZ_TC_STATIC ? (int)blockIdx.x : atomicAdd(work_ctr, 1);
+      for (;;) {
+        const int tile = next;
+        if (tile >= n_tiles) break;
+        next = PZ_TC_STATIC ? next + (int)gridDim.x : atomicAdd(work_ctr, 1);
         const TileInfo t = tile_info(c, tile, n_blocks);
         const int pair = t.bucket >> 1;
         for (int kb = 0; kb < nk; ++kb) {
           ptx::mbar_wait(&c.empty[stage], phase ^ 1);
           PZ_TT(0, tcount);
           ++tcount;
+          c.hdr[stage] = tile;
           uint8_t* sa = smem + (size_t)stage * kStageBytes;
           uint8_t* sb = sa + kABytes;
           ptx::mbar_arrive_expect_tx(&c.full[stage], kStageBytes);
@@ -221,6 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
+      ptx::mbar_wait(&c.empty[stage], phase ^ 1);  // "no more work": a phase without data
+      c.hdr[stage] = -1;
+      ptx::mbar_arrive(&c.full[stage]);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
@@ -229,13 +245,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     uint32_t phase = 0, acc_phase = 0;
     int tcount = 0;
     (void)tcount;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (;;) {
+      ptx::mbar_wait(&c.dec[stage], phase);  // the tile's first stage (or "no more work")
+      const int tile = c.hdr[stage];
+      if (tile < 0) break;
       const TileInfo t = tile_info(c, tile, n_blocks);
       const bool two = t.valid > 128;
       ptx::mbar_wait(&c.tmem_empty, acc_phase ^ 1);
       ptx::tc_fence_after();
       for (int kb = 0; kb < nk; ++kb) {
-        ptx::mbar_wait(&c.dec[stage], phase);
+        if (kb) ptx::mbar_wait(&c.dec[stage], phase);
         ptx::tc_fence_after();
         if (lane == 0) {
           const uint32_t sa = ptx::smem_u32(smem + (size_t)stage * kStageBytes);
@@ -267,7 +286,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     int tcount = 0, tiles_done = 0;
     (void)tcount;
     (void)tiles_done;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (;;) {
+      ptx::mbar_wait(&c.full[stage], phase);  // the tile's first stage (or "no more work")
+      const int tile = c.hdr[stage];
+      if (tile < 0) {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&c.dec[stage]);  // pass the end on to the MMA warp
+        break;
+      }
       const TileInfo t = tile_info(c, tile, n_blocks);
       const int pos = t.bucket & 1;
       for (int kb = 0; kb < nk; ++kb) {
@@ -344,8 +370,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
 bool tc_supported(int d, int f) { return d % BN == 0 && f % (BN / 2) == 0 && d % BK == 0 && f % BK == 0; }
 
 // x_rows: [n_rows_cap][d] bf16 grouped by bucket; h: [n_rows_cap][f]; y: [n_rows_cap][d]
+// work_ctrs: 2 ints, zero on entry (tile claim counters of the w13 and the w2 launch).
 int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f, const uint16_t* x_rows,
-                      const int32_t* bucket_off, int64_t n_rows_cap, uint16_t* h, float* y, cudaStream_t stream) {
+                      const int32_t* bucket_off, int64_t n_rows_cap, uint16_t* h, float* y, int32_t* work_ctrs,
+                      cudaStream_t stream) {
   if (!tc_supported(d, f)) return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d % 256 == 0 and d_ff % 128 == 0");
   if (n_rows_cap == 0) return PUZZLE_OK;
   static std::once_flag attr_once;
@@ -363,14 +391,14 @@ int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int 
   {
     ProfScope _ps("w13_tc", stream);
     cudaError_t e = launch_pdl(k_tc_experts<true>, dim3(grid), dim3(kThreads), kSmemBytes, stream, ta13, tb13,
-                               bucket_off, 2 * n_pairs, d, f, d, f / (BN / 2), h, (float*)nullptr, 1u);
+                               bucket_off, 2 * n_pairs, d, f, d, f / (BN / 2), h, (float*)nullptr, work_ctrs, 1u);
     if (e != cudaSuccess) return cuda_check(e, "w13_tc launch");
   }
   if ((rc = cuda_check(cudaGetLastError(), "w13_tc launch"))) return rc;
   {
     ProfScope _ps("w2_tc", stream);
     cudaError_t e = launch_pdl(k_tc_experts<false>, dim3(grid), dim3(kThreads), kSmemBytes, stream, ta2, tb2,
-                               bucket_off, 2 * n_pairs, f, f, d, d / BN, (uint16_t*)nullptr, y, 1u);
+                               bucket_off, 2 * n_pairs, f, f, d, d / BN, (uint16_t*)nullptr, y, work_ctrs + 1, 1u);
     if (e != cudaSuccess) return cuda_check(e, "w2_tc launch");
   }
   return cuda_check(cudaGetLastError(), "w2_tc launch");
