@@ -52,6 +52,9 @@ extern "C" __attribute__((visibility("default"))) int puzzle_debug_tc(void* dst,
 
 namespace {
 
+#ifndef PZ_TC_DEFER_EPI  // 0: epilogue right after a tile's last stage (A/B experiments)
+#define PZ_TC_DEFER_EPI 1
+#endif
 constexpr int BM = 256;  // tokens per tile (2 x UMMA M=128)
 constexpr int BN = 256;  // output rows per tile (UMMA N=256)
 constexpr int BK = 64;   // K per stage (= one 128-byte swizzle row of bf16)
@@ -71,7 +74,7 @@ struct alignas(8) SmemCtl {
   uint64_t dec[kStages];
   uint64_t empty[kStages];
   uint64_t tmem_full;
-  uint64_t tmem_empty;
+  uint64_t tmem_empty[2];  // accumulator of M-block 0 / 1 drained (released one after the other)
   uint32_t tmem_base;
   int32_t n_buckets;
   int32_t bucket_off[kMaxBuckets + 1];
@@ -181,7 +184,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       ptx::mbar_init(&c.empty[s], 1);
     }
     ptx::mbar_init(&c.tmem_full, 1);
-    ptx::mbar_init(&c.tmem_empty, kDecodeWarps);
+    ptx::mbar_init(&c.tmem_empty[0], kDecodeWarps);
+    ptx::mbar_init(&c.tmem_empty[1], kDecodeWarps);
     ptx::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -251,19 +255,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       if (tile < 0) break;
       const TileInfo t = tile_info(c, tile, n_blocks);
       const bool two = t.valid > 128;
-      ptx::mbar_wait(&c.tmem_empty, acc_phase ^ 1);
+      ptx::mbar_wait(&c.tmem_empty[0], acc_phase ^ 1);  // M-block 0's accumulator drained
       ptx::tc_fence_after();
       for (int kb = 0; kb < nk; ++kb) {
         if (kb) ptx::mbar_wait(&c.dec[stage], phase);
         ptx::tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(smem + (size_t)stage * kStageBytes);
+        const uint32_t sb = sa + kABytes;
+        if (kb == 0) {
+          // stage 0: M-block 0 first, then (once the epilogue has drained it) M-block 1
+          if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              ptx::mma_bf16_ss(tmem, ptx::smem_desc_sw128(sa + k * 32), ptx::smem_desc_sw128(sb + k * 32), idesc,
+                               k != 0);
+          }
+          __syncwarp();
+          ptx::mbar_wait(&c.tmem_empty[1], acc_phase ^ 1);
+          ptx::tc_fence_after();
+        }
         if (lane == 0) {
-          const uint32_t sa = ptx::smem_u32(smem + (size_t)stage * kStageBytes);
-          const uint32_t sb = sa + kABytes;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t db = ptx::smem_desc_sw128(sb + k * 32);
             const uint32_t acc = (kb | k) != 0;
-            ptx::mma_bf16_ss(tmem, ptx::smem_desc_sw128(sa + k * 32), db, idesc, acc);
+            if (kb) ptx::mma_bf16_ss(tmem, ptx::smem_desc_sw128(sa + k * 32), db, idesc, acc);
             if (two) ptx::mma_bf16_ss(tmem + 256, ptx::smem_desc_sw128(sa + kABytes / 2 + k * 32), db, idesc, acc);
           }
           ptx::mma_commit(&c.empty[stage]);
@@ -286,6 +302,59 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     int tcount = 0, tiles_done = 0;
     (void)tcount;
     (void)tiles_done;
+    // ---- epilogue of tile e: drains M-block 0 then 1, releasing each as soon as it is read ----
+    auto epilogue = [&](const TileInfo& e) {
+      if (threadIdx.x == 64) PZ_TT(3, tiles_done);
+      ptx::mbar_wait(&c.tmem_full, acc_phase);
+      ptx::tc_fence_after();
+      for (int half = 0; half < 2; ++half) {
+        const int m = half * 128 + q * 32 + lane;  // token row within the tile
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + half * 256;
+        const bool ok = m < e.valid;
+        const int64_t a = e.row0 + m;
+        if (half == 0 || e.valid > 128) {
+          if (kW13) {
+            for (int j = ch * 64; j < ch * 64 + 64; j += 32) {
+              uint32_t g[32], u[32];
+              ptx::tmem_ld_32x32b_x32(tbase + j, g);
+              ptx::tmem_ld_32x32b_x32(tbase + 128 + j, u);
+              ptx::tmem_ld_wait();
+              if (ok) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
+                  const float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
+                  pk[i] = f32_to_bf16_rne_bits(h0) | (f32_to_bf16_rne_bits(h1) << 16);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(h_out + a * f + e.n_block * (BN / 2) + j);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+              }
+            }
+          } else {
+            for (int j = ch * 128; j < ch * 128 + 128; j += 32) {
+              uint32_t v[32];
+              ptx::tmem_ld_32x32b_x32(tbase + j, v);
+              ptx::tmem_ld_wait();
+              if (ok) {
+                uint4* dst = reinterpret_cast<uint4*>(y_out + a * d + e.n_block * BN + j);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              }
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&c.tmem_empty[half]);
+      }
+      if (threadIdx.x == 64) PZ_TT(4, tiles_done);
+      ++tiles_done;
+      acc_phase ^= 1;
+    };
+    TileInfo pend{};
+    bool have_pend = false;
     for (;;) {
       ptx::mbar_wait(&c.full[stage], phase);  // the tile's first stage (or "no more work")
       const int tile = c.hdr[stage];
@@ -306,56 +375,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
         if (threadIdx.x == 64) PZ_TT(1, tcount);
         ++tcount;
         if (++stage == kStages) { stage = 0; phase ^= 1; }
-      }
-      // ---- epilogue ----
-      if (threadIdx.x == 64) PZ_TT(3, tiles_done);
-      ptx::mbar_wait(&c.tmem_full, acc_phase);
-      ptx::tc_fence_after();
-      for (int half = 0; half < 2; ++half) {
-        const int m = half * 128 + q * 32 + lane;  // token row within the tile
-        if (half == 1 && t.valid <= 128) break;
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + half * 256;
-        const bool ok = m < t.valid;
-        const int64_t a = t.row0 + m;
-        if (kW13) {
-          for (int j = ch * 64; j < ch * 64 + 64; j += 32) {
-            uint32_t g[32], u[32];
-            ptx::tmem_ld_32x32b_x32(tbase + j, g);
-            ptx::tmem_ld_32x32b_x32(tbase + 128 + j, u);
-            ptx::tmem_ld_wait();
-            if (ok) {
-              uint32_t pk[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
-                const float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
-                pk[i] = f32_to_bf16_rne_bits(h0) | (f32_to_bf16_rne_bits(h1) << 16);
-              }
-              uint4* dst = reinterpret_cast<uint4*>(h_out + a * f + t.n_block * (BN / 2) + j);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-            }
-          }
-        } else {
-          for (int j = ch * 128; j < ch * 128 + 128; j += 32) {
-            uint32_t v[32];
-            ptx::tmem_ld_32x32b_x32(tbase + j, v);
-            ptx::tmem_ld_wait();
-            if (ok) {
-              uint4* dst = reinterpret_cast<uint4*>(y_out + a * d + t.n_block * BN + j);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
-          }
+        // the previous tile's epilogue once this tile's first stage is decoded: its last MMAs
+        // have completed by then, and this tile's first MMAs (M-block 0) can start as soon as
+        // M-block 0 is drained
+        if (kb == 0 && have_pend) {
+          epilogue(pend);
+          have_pend = false;
         }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&c.tmem_empty);
-      if (threadIdx.x == 64) PZ_TT(4, tiles_done);
-      ++tiles_done;
-      acc_phase ^= 1;
+      pend = t;
+      have_pend = true;
+      if (!PZ_TC_DEFER_EPI) {
+        epilogue(pend);
+        have_pend = false;
+      }
     }
+    if (have_pend) epilogue(pend);
   }
   ptx::tc_fence_before();
   __syncthreads();
