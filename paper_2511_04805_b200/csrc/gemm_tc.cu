@@ -63,7 +63,7 @@ constexpr int kABytes = BM * BK * 2;  // 32 KB
 constexpr int kBBytes = BN * BK * 2;  // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kDecodeWarps = 8;       // also the epilogue warps (2 per TMEM lane quarter)
-constexpr int kThreads = 64 + 32 * kDecodeWarps;
+constexpr int kThreads = 96 + 32 * kDecodeWarps;  // + warp 10: second MMA issuer
 constexpr uint32_t kTmemCols = 512;
 constexpr int kMaxBuckets = 2 * 256;
 
@@ -181,9 +181,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&c.full[s], 1);
       ptx::mbar_init(&c.dec[s], kDecodeWarps);
-      ptx::mbar_init(&c.empty[s], 1);
+      ptx::mbar_init(&c.empty[s], 2);  // a commit from each MMA issuer
     }
-    ptx::mbar_init(&c.tmem_full, 1);
+    ptx::mbar_init(&c.tmem_full, 2);
     ptx::mbar_init(&c.tmem_empty[0], kDecodeWarps);
     ptx::mbar_init(&c.tmem_empty[1], kDecodeWarps);
     ptx::fence_mbar_init();
@@ -242,8 +242,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       c.hdr[stage] = -1;
       ptx::mbar_arrive(&c.full[stage]);
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
+  } else if (warp == 1 || warp == 2 + kDecodeWarps) {
+    // ===================== MMA issuers =====================
+    // warp 1 issues M-block 0's MMAs, the last warp M-block 1's: two instruction streams
+    // (one thread's tcgen05.mma retire one after the other; scripts/micro/umma_rate.cu)
+    const int mblk = warp == 1 ? 0 : 1;
     constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, BN);
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
@@ -254,37 +257,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       const int tile = c.hdr[stage];
       if (tile < 0) break;
       const TileInfo t = tile_info(c, tile, n_blocks);
-      const bool two = t.valid > 128;
-      ptx::mbar_wait(&c.tmem_empty[0], acc_phase ^ 1);  // M-block 0's accumulator drained
+      const bool active = mblk == 0 || t.valid > 128;
+      ptx::mbar_wait(&c.tmem_empty[mblk], acc_phase ^ 1);  // this M-block's accumulator drained
       ptx::tc_fence_after();
       for (int kb = 0; kb < nk; ++kb) {
         if (kb) ptx::mbar_wait(&c.dec[stage], phase);
         ptx::tc_fence_after();
-        const uint32_t sa = ptx::smem_u32(smem + (size_t)stage * kStageBytes);
-        const uint32_t sb = sa + kABytes;
-        if (kb == 0) {
-          // stage 0: M-block 0 first, then (once the epilogue has drained it) M-block 1
-          if (lane == 0) {
+        if (lane == 0) {
+          const uint32_t sa = ptx::smem_u32(smem + (size_t)stage * kStageBytes) + (uint32_t)(mblk * (kABytes / 2));
+          const uint32_t sb = ptx::smem_u32(smem + (size_t)stage * kStageBytes) + kABytes;
+          if (active) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              ptx::mma_bf16_ss(tmem, ptx::smem_desc_sw128(sa + k * 32), ptx::smem_desc_sw128(sb + k * 32), idesc,
-                               k != 0);
+              ptx::mma_bf16_ss(tmem + 256u * mblk, ptx::smem_desc_sw128(sa + k * 32), ptx::smem_desc_sw128(sb + k * 32),
+                               idesc, (kb | k) != 0);
           }
-          __syncwarp();
-          ptx::mbar_wait(&c.tmem_empty[1], acc_phase ^ 1);
-          ptx::tc_fence_after();
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t db = ptx::smem_desc_sw128(sb + k * 32);
-            const uint32_t acc = (kb | k) != 0;
-            if (kb) ptx::mma_bf16_ss(tmem, ptx::smem_desc_sw128(sa + k * 32), db, idesc, acc);
-            if (two) ptx::mma_bf16_ss(tmem + 256, ptx::smem_desc_sw128(sa + kABytes / 2 + k * 32), db, idesc, acc);
-          }
-          ptx::mma_commit(&c.empty[stage]);
+          ptx::mma_commit(&c.empty[stage]);  // (an issuer with nothing pending arrives at once)
           if (kb == nk - 1) ptx::mma_commit(&c.tmem_full);
-          PZ_TT(2, tcount);
+          if (mblk == 0) PZ_TT(2, tcount);
         }
         ++tcount;
         __syncwarp();
