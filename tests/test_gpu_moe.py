@@ -203,3 +203,32 @@ def test_residual_stack_matches_chained_oracle(pz):
     ulp = np.abs(ref) * 2.0 ** -8
     assert np.all(np.abs(got - ref) <= 2e-2 + n_layers * ulp), np.max(np.abs(got - ref) - n_layers * ulp)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 5e-3
+
+
+def _random_cases(n, tc, seed):
+    """Seeded random layer shapes: GEMV path (d, d_ff multiples of 64, any T) or tcgen05 path
+    (d % 256, d_ff % 128, T > 64)."""
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        E = int(rng.choice([2, 4, 6, 10, 24, 64]))
+        k = int(rng.integers(1, min(8, E) + 1))
+        if tc:
+            d, f = 256 * int(rng.integers(1, 3)), 128 * int(rng.integers(1, 4))
+            T = int(rng.choice([65, 200, 513]))
+        else:
+            d, f = 64 * int(rng.integers(1, 9)), 64 * int(rng.integers(1, 11))
+            T = int(rng.choice([1, 2, 33, 64]))
+        cases.append((synth.MoEConfig(f"rnd{'tc' if tc else 'gv'}{i}", 60 + i + (20 if tc else 0), d, f, E, k,
+                                      bool(rng.integers(0, 2))), T))
+    return cases
+
+
+@pytest.mark.parametrize("cfg,T", _random_cases(10, False, 11) + _random_cases(6, True, 12),
+                         ids=lambda x: x.name if hasattr(x, "name") else str(x))
+def test_forward_random_shapes(pz, cfg, T):
+    """Random shapes / expert counts / top-k / renormalisation through the path AUTO picks
+    (decode GEMV for T <= 64, tcgen05 otherwise): stream-K splits, ragged row blocks, empty and
+    single-position pairs, multi-pass buckets."""
+    got, ref = _run(pz, cfg, T, pz.PATH_AUTO)
+    assert_close(got, ref, f"{cfg.name} d={cfg.d_model} f={cfg.d_ff} E={cfg.n_experts} k={cfg.top_k} T={T}")
