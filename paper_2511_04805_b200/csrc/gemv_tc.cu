@@ -399,8 +399,10 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     }
     bool signalled = sig_item < 0;
     auto signal = [&]() {
-      __threadfence();  // cumulative: orders the decoders' partial stores (acquired via pdone)
-      atomicAdd(&counters[sig_item], 1);
+      // release at gpu scope, cumulative over the decoders' partial stores (acquired via
+      // pdone); a reduction, not an atomic with a return value: the thread does not wait for
+      // the round trip (it must keep the X ring fed)
+      asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(&counters[sig_item]), "r"(1) : "memory");
       signalled = true;
     };
     for (;;) {
