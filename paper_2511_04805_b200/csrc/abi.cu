@@ -32,10 +32,11 @@ int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16
 bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
                       uint16_t*, float*, int32_t*, cudaStream_t);
-int gemv_tc_max_ctas();
+size_t gemv_tc_part_floats(bool prefill);
+int64_t gemv_tc_counters(int n_rb, int n_pairs, int64_t n_assign);
 bool gemv_supported(int d, int f);
 int launch_gemv_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*,
-                           const int32_t*, const int32_t*, int, int64_t, int, float*, int32_t*, int32_t*,
+                           const int32_t*, const int32_t*, int, int64_t, bool, float*, int32_t*, int32_t*,
                            uint16_t*, float*, cudaStream_t);
 
 namespace {
@@ -135,7 +136,7 @@ int check_layer(const puzzle_moe_layer* L) {
 struct Plan {
   int64_t T = 0, n_assign = 0;
   int k = 0, max_active = 0;
-  int slot_tok = 0;  // GEMV path: assignments of one pair, bound for the stream-K partial slots
+  bool tmem_prefill = false;  // TC path through the decode-into-TMEM kernel's prefill configuration
   int path = PUZZLE_PATH_GEMV;  // resolved (never AUTO)
 };
 
@@ -148,6 +149,16 @@ struct Layout {
       x_perm, route_scratch, total;
 };
 
+// Token-heavy batches: the tcgen05 grouped GEMM (gemm_tc.cu) by default; PUZZLE_PREFILL_IMPL=tmem
+// selects the decode-into-TMEM kernels' prefill configuration (A/B measurements).
+bool prefill_via_tmem() {
+  static const bool v = [] {
+    const char* e = getenv("PUZZLE_PREFILL_IMPL");
+    return e && std::string(e) == "tmem";
+  }();
+  return v;
+}
+
 Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   Plan p;
   p.T = T;
@@ -157,7 +168,7 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   if (path == PUZZLE_PATH_AUTO)
     path = (T > kGemvMaxTokens && tc_supported(L->d_model, L->d_ff)) ? PUZZLE_PATH_TC : PUZZLE_PATH_GEMV;
   p.path = path;
-  if (path == PUZZLE_PATH_GEMV) p.slot_tok = (int)std::min<int64_t>(p.n_assign, 2 * T);  // <= 2 experts per token
+  if (path == PUZZLE_PATH_TC) p.tmem_prefill = prefill_via_tmem();
   return p;
 }
 
@@ -177,12 +188,16 @@ Layout make_layout(const puzzle_moe_layer* L, const Plan& p) {
   o.assign_of = take(na * 4);
   o.active = take(P * 4);
   o.n_active = take(4);
-  o.cnt13 = take(P * (f / 64) * 4);
-  o.cnt2 = take(P * (d / 64) * 4);
+  // work-item counters of the decode-into-TMEM kernels (also the tile claim counters of the
+  // tcgen05 grouped GEMM); zeroed by the routing kernels every call
+  o.cnt13 = take((size_t)gemv_tc_counters((int)(f / 64), (int)P, (int64_t)na) * 4);
+  o.cnt2 = take((size_t)gemv_tc_counters((int)((d + 127) / 128), (int)P, (int64_t)na) * 4);
   o.h = take(na * f * 2);
   o.y = take(na * d * 4);
-  // stream-K partial slots of the decode kernels: 2 per CTA x slot_tok x 128 fp32
-  o.part = take(p.path == PUZZLE_PATH_GEMV ? (size_t)2 * gemv_tc_max_ctas() * p.slot_tok * 128 * 4 : 0);
+  // stream-K partial slots: 2 per CTA x 2 positions x tokens of a pass x 128 fp32
+  o.part = take(p.path == PUZZLE_PATH_GEMV ? gemv_tc_part_floats(false) * 4
+                : p.tmem_prefill         ? gemv_tc_part_floats(true) * 4
+                                         : 0);
   o.x_perm = take(na * d * 2);
   o.route_scratch = take((size_t)std::max<int64_t>(2 * 2 * (int64_t)P, p.T <= kGemvMaxTokens
                                                                           ? route_dec_scratch_ints(p.T, p.k, (int)P)
@@ -323,11 +338,15 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
     if (rc) return rc;
     rows = at<uint16_t>(ws, lay.x_perm);
   }
+  if (plan.path == PUZZLE_PATH_TC && plan.tmem_prefill)
+    return launch_gemv_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
+                                  n_active, plan.max_active, plan.n_assign, true, at<float>(ws, lay.part),
+                                  at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);
   if (plan.path == PUZZLE_PATH_TC)
     return launch_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, at<int32_t>(ws, lay.cnt13), s);  // cnt13: zeroed per call
   return launch_gemv_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
-                                n_active, plan.max_active, plan.n_assign, plan.slot_tok, at<float>(ws, lay.part),
+                                n_active, plan.max_active, plan.n_assign, false, at<float>(ws, lay.part),
                                 at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);
 }
 

@@ -36,8 +36,6 @@
 
 namespace pz {
 
-int gemv_tc_max_ctas();
-
 namespace {
 
 constexpr int kDecWarps = 8;
@@ -47,26 +45,34 @@ constexpr int kThreads = 128 + 32 * kDecWarps;
 constexpr int kBK = 64;                          // K per stage (one 128-byte swizzle row)
 constexpr int kRows = 128;                       // weight rows per tile (UMMA M)
 constexpr int kWBytes = kRows * kBK * 2;         // 16 KB packed words per stage
-constexpr int kNX = 32;                          // tokens per position per pass (UMMA N <= 32)
-constexpr int kXBox = 32;                        // token rows per activation TMA box (= kNX)
-constexpr int kXPos = kNX * kBK * 2;             // 4 KB per position
-constexpr int kXBytes = 2 * kXPos;               // X stage: both positions
 #ifndef PZ_TC_DEFER  // decoders drain a pass's accumulators after two stages of the next pass
 #define PZ_TC_DEFER 0
 #endif
-#ifndef PZ_TC_WST  // W ring depth (tuning knob)
+#ifndef PZ_TC_WST  // W ring depth of the decode configuration (tuning knob)
 #define PZ_TC_WST 4
 #endif
-#ifndef PZ_TC_XST  // X ring depth (tuning knob)
+#ifndef PZ_TC_XST  // X ring depth of the decode configuration (tuning knob)
 #define PZ_TC_XST 5
 #endif
-constexpr int kWStages = PZ_TC_WST;
-constexpr int kXStages = PZ_TC_XST;
-constexpr int kAStages = 3;  // TMEM A buffers
+constexpr int kAStages = 3;  // TMEM A buffers (64 columns each: 64 k of both positions)
 constexpr int kSq = 8;       // stage queue W producer -> X producer
 constexpr int kMinStages = 8;  // stream-K: minimum stages per CTA
-constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kAccCol = 64 * kAStages;      // 192
+constexpr uint32_t kAccCol = 64 * kAStages;      // 192: accumulators of position p at 192 + NX p
+
+// Two configurations of the same kernel:
+//   decode  (NX = 32, 2 CTAs per SM, 256 TMEM columns): batches of 1-64 tokens;
+//   prefill (NX = 128, 1 CTA per SM, 512 TMEM columns): up to 128 tokens per position per pass,
+//            every pass a work item of its own (tokens on the N side, N <= 128).
+template <int NX, int CTAS>
+struct Cfg {
+  static constexpr int kNX = NX;                          // tokens per position per pass (UMMA N <= NX)
+  static constexpr int kXPos = NX * kBK * 2;              // one position's activation rows per stage
+  static constexpr int kXBytes = 2 * kXPos;               // X stage: both positions
+  static constexpr int kWStages = NX == 32 ? PZ_TC_WST : 4;
+  static constexpr int kXStages = NX == 32 ? PZ_TC_XST : 4;
+  static constexpr uint32_t kTmemCols = CTAS == 2 ? 256 : 512;
+  static_assert(kAccCol + 2 * NX <= kTmemCols, "TMEM: A ring + accumulators");
+};
 
 #ifdef PZ_TRACE  // pipeline timeline of one CTA (tuning builds only; scripts/trace_gemv.py)
 __device__ unsigned long long g_trace[8][4096];
@@ -87,24 +93,30 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PZ_TRD(ev, idx)
 #endif
 
+template <int WST, int XST>
 struct alignas(16) Ctl {
-  int4 whdr[kWStages];  // {item, pass base, kb, 0}; item -1 = no more work
-  int4 xhdr[kXStages];
+  int4 whdr[WST];  // stage headers (see Pass); item -1 = no more work
+  int4 xhdr[XST];
   int4 sq[kSq];         // W producer -> X producer: {k column, row0 | active0 << 28, row1 | ...}
   int4 sqh[kSq];        //   ... and the stage headers
-  uint64_t wfull[kWStages], wempty[kWStages], xfull[kXStages], xempty[kXStages], a_full[kAStages],
-      a_empty[kAStages];
+  uint64_t wfull[WST], wempty[WST], xfull[XST], xempty[XST], a_full[kAStages], a_empty[kAStages];
   uint64_t sqfull[kSq], sqempty[kSq];
   uint64_t pdone;  // decoders -> X producer: partials of this CTA's first (signalling) piece stored
   uint64_t acc_full, acc_empty;
   uint32_t tmem_base;
   int s_last;
-  int32_t s_off[kMaxExperts + 1];     // bucket_off[0 .. 2P]
-  int32_t s_active[kMaxExperts / 2];  // active_pairs[0 .. n_active)
+  int32_t s_off[kMaxExperts + 1];       // bucket_off[0 .. 2P]
+  int32_t s_active[kMaxExperts / 2];    // active_pairs[0 .. n_active)
+  int32_t s_item[kMaxExperts / 2 + 1];  // first work item of each active pair (prefix sum)
 };
 
-constexpr size_t kSmem = 1024 + (size_t)kWStages * kWBytes + (size_t)kXStages * kXBytes + sizeof(Ctl);
-static_assert(2 * (kSmem + 1024) <= 228 * 1024, "two CTAs per SM");
+template <class C>
+constexpr size_t smem_bytes() {
+  return 1024 + (size_t)C::kWStages * kWBytes + (size_t)C::kXStages * C::kXBytes +
+         sizeof(Ctl<C::kWStages, C::kXStages>);
+}
+static_assert(2 * (smem_bytes<Cfg<32, 2>>() + 1024) <= 228 * 1024, "decode: two CTAs per SM");
+static_assert(smem_bytes<Cfg<128, 1>>() + 1024 <= 228 * 1024, "prefill: one CTA per SM");
 
 struct PairTokens {
   int off0, cnt0, off1, cnt1;
@@ -182,25 +194,45 @@ __device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
   return v;
 }
 
-// Stage header {item, pass base, kb, kb0 << 16 | kb1}: the stage is k-block kb of the piece
-// [kb0, kb1) of work item `item`, for the tokens [base, base + kNX) of each position.
+// Work items: for every active pair z, its row blocks x its token passes (npass(z) = passes of
+// NX tokens over the larger of its two buckets), pass-minor so that consecutive items share
+// their packed weight rows (L2). Stage header {item, base, kb, kb0 << 16 | kb1}: k-block kb of
+// the piece [kb0, kb1) of `item`, which covers tokens [base, base + NX) of each position.
 struct Pass {
   int item, base, kb0, kb1, rb, p;
   PairTokens pt;
-  int n0, n1;  // tokens of position 0 / 1 in this pass (0 .. kNX)
+  int n0, n1;  // tokens of position 0 / 1 in this pass (0 .. NX)
 };
 
-__device__ __forceinline__ Pass make_pass(const Ctl& c, int4 h, int n_rb) {
+__device__ __forceinline__ int npass_of(const PairTokens& pt, int nx) {
+  return max(1, (max(pt.cnt0, pt.cnt1) + nx - 1) / nx);
+}
+
+// item -> (active pair z, row block, pass): binary search over the per-pair item prefix
+template <int WST, int XST>
+__device__ __forceinline__ void locate(const Ctl<WST, XST>& c, int n_active, int item, int nx, int& p,
+                                      PairTokens& pt, int& rb, int& base) {
+  int lo = 0, hi = n_active - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (c.s_item[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  p = c.s_active[lo];
+  pt = load_pair(c.s_off, p);
+  const int np = npass_of(pt, nx), rem = item - c.s_item[lo];
+  rb = rem / np;
+  base = (rem % np) * nx;
+}
+
+template <int WST, int XST>
+__device__ __forceinline__ Pass make_pass(const Ctl<WST, XST>& c, int4 h, int n_active, int nx) {
   Pass s;
   s.item = h.x;
-  s.base = h.y;
   s.kb0 = h.w >> 16;
   s.kb1 = h.w & 0xFFFF;
-  s.rb = h.x % n_rb;
-  s.p = c.s_active[h.x / n_rb];
-  s.pt = load_pair(c.s_off, s.p);
-  s.n0 = min(max(s.pt.cnt0 - s.base, 0), kNX);
-  s.n1 = min(max(s.pt.cnt1 - s.base, 0), kNX);
+  locate(c, n_active, h.x, nx, s.p, s.pt, s.rb, s.base);
+  s.n0 = min(max(s.pt.cnt0 - s.base, 0), nx);
+  s.n1 = min(max(s.pt.cnt1 - s.base, 0), nx);
   return s;
 }
 
@@ -208,8 +240,9 @@ __device__ __forceinline__ Pass make_pass(const Ctl& c, int4 h, int n_rb) {
 // pos 0, bit 1 = pos 1): decode this thread's 32 packed words per stage (16 registers, k =
 // 32 kh .. 32 kh + 31 of its row) and store the bf16 rows into the TMEM A buffer: register r
 // of chunk i -> column 16 kh + 4 i + r (k pair 32 kh + 8 i + 2 r).
-template <int MODE, class Epi>
-__device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t lane_tmem, const uint32_t (&w_off)[4],
+template <int MODE, int WST, int XST, class Epi>
+__device__ __forceinline__ void decode_pass(Ctl<WST, XST>& c, uint32_t smem_w, uint32_t lane_tmem,
+                                            const uint32_t (&w_off)[4],
                                             int kh, int n_stages, Ring& w, Ring& a, const Muls& mu, int& tcount,
                                             bool kW13, int ep_at, Epi&& epi) {
   const int lane = threadIdx.x & 31;
@@ -237,7 +270,7 @@ __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t la
       }
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&c.wempty[w.i]);  // packed words consumed: the slot may refill
-    w.next<kWStages>();
+    w.next<WST>();
     ptx::mbar_wait(&c.a_empty[a.i], a.ph ^ 1);  // the MMAs that read A buffer a.i have completed
     PZ_TRD(3, tcount);
     ptx::tc_fence_after();
@@ -256,19 +289,24 @@ __device__ __forceinline__ void decode_pass(Ctl& c, uint32_t smem_w, uint32_t la
 }
 
 // part: 2 slots per CTA ([g][0] = its first piece, [g][1] = its last piece), each
-// slot_tok x 128 fp32 (token of the pair x tile row; w13 rows 0-63 = g, 64-127 = u).
-template <bool kW13>
+// [2 positions][NX tokens of the pass][128 tile rows] fp32 (w13 rows 0-63 = g, 64-127 = u);
+// counters: one per work item, zero on entry.
+template <bool kW13, int NX, int CTAS>
 __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM sub-partition
     const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
     const int32_t* __restrict__ bucket_off, const int32_t* __restrict__ active_pairs,
-    const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb, int slot_tok,
+    const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb,
     float* __restrict__ part, int32_t* __restrict__ counters, uint16_t* __restrict__ h_out,
     float* __restrict__ y_out, uint32_t mul_one, int n_bucket_pairs) {
+  using C = Cfg<NX, CTAS>;
+  constexpr int kWStages = C::kWStages, kXStages = C::kXStages, kXBytes = C::kXBytes, kXPos = C::kXPos;
+  constexpr int kSlot = 2 * NX * kRows;  // floats per partial slot
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_w = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;  // == smem, shared window
   const uint32_t smem_x = smem_w + kWStages * kWBytes;
-  Ctl& c = *reinterpret_cast<Ctl*>(smem + (size_t)kWStages * kWBytes + (size_t)kXStages * kXBytes);
+  auto& c = *reinterpret_cast<Ctl<kWStages, kXStages>*>(smem + (size_t)kWStages * kWBytes +
+                                                         (size_t)kXStages * kXBytes);
   const uint32_t whdr_s = ptx::smem_u32(&c.whdr[0]), xhdr_s = ptx::smem_u32(&c.xhdr[0]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -298,7 +336,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
 #ifdef PZ_TRACE
   if (threadIdx.x == 0) g_cta[kW13][blockIdx.x][0] = gtimer();
 #endif
-  if (warp == 1) ptx::tmem_alloc<kTmemCols>(&c.tmem_base);
+  if (warp == 1) ptx::tmem_alloc<C::kTmemCols>(&c.tmem_base);
   pdl_wait();     // route / gather / previous projection complete and visible
 #ifdef PZ_TRACE
   if (threadIdx.x == 0) {
@@ -312,13 +350,22 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   const int n_active = *n_active_ptr;
   for (int i = threadIdx.x; i < n_active; i += blockDim.x) c.s_active[i] = active_pairs[i];
   for (int i = threadIdx.x; i <= 2 * n_bucket_pairs; i += blockDim.x) c.s_off[i] = bucket_off[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {  // work items per active pair: row blocks x token passes
+    int run = 0;
+    for (int z = 0; z < n_active; ++z) {
+      c.s_item[z] = run;
+      run += n_rb * npass_of(load_pair(c.s_off, c.s_active[z]), NX);
+    }
+    c.s_item[n_active] = run;
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = c.tmem_base;
   const int nk = K / kBK;
   StreamK sk;
-  sk.S = n_active * n_rb * nk;
+  sk.S = c.s_item[n_active] * nk;
   sk.G = max(1, min((int)gridDim.x, sk.S / kMinStages));  // >= kMinStages stages per CTA
   const int g = blockIdx.x;
   const int s_begin = g < sk.G ? sk.begin(g) : 0, s_end = g < sk.G ? sk.begin(g + 1) : 0;
@@ -335,11 +382,11 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     for (int s0 = s_begin; s0 < s_end;) {
       const int item = s0 / nk, kb0 = s0 % nk, kb1 = min(nk, kb0 + (s_end - s0));
       s0 += kb1 - kb0;
-      const int rb = item % n_rb, p = c.s_active[item / n_rb];
-      const PairTokens pt = load_pair(c.s_off, p);
-      const int maxcnt = max(pt.cnt0, pt.cnt1);
+      int p, rb, base;
+      PairTokens pt;
+      locate(c, n_active, item, NX, p, pt, rb, base);
       const int wrow = kW13 ? p * 2 * f + rb * (kRows / 2) : p * d + rb * kRows;
-      for (int base = 0; base < maxcnt; base += kNX) {
+      {
         // X-side parameters: one activation box per active position (flag in bit 28)
         const int r0 = (pt.off0 + base) | ((pt.cnt0 > base) << 28);
         const int r1 = (pt.off1 + base) | ((pt.cnt1 > base) << 28);
@@ -394,8 +441,10 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     // in an earlier CTA's range
     int sig_item = s_begin < s_end && s_begin % nk != 0 ? s_begin / nk : -1;
     if (sig_item >= 0) {  // (an active pair always has rows; an empty one would never signal)
-      const PairTokens pt = load_pair(c.s_off, c.s_active[sig_item / n_rb]);
-      if (pt.cnt0 + pt.cnt1 == 0) sig_item = -1;
+      int p, rb, base;
+      PairTokens pt;
+      locate(c, n_active, sig_item, NX, p, pt, rb, base);
+      if (max(pt.cnt0, pt.cnt1) <= base) sig_item = -1;
     }
     bool signalled = sig_item < 0;
     auto signal = [&]() {
@@ -448,10 +497,10 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       ptx::mbar_wait(&c.xfull[x.i], x.ph);
       const int4 h = lds_int4(xhdr_s + 16u * x.i);
       if (h.x < 0) break;
-      const Pass s = make_pass(c, h, n_rb);
+      const Pass s = make_pass(c, h, n_active, NX);
       const int np = mypos ? s.n1 : s.n0;
       const uint32_t idp = ptx::idesc_bf16_f32(128, (uint32_t)((np + 15) & ~15));
-      const uint32_t acc_col = tmem + kAccCol + 32u * mypos;
+      const uint32_t acc_col = tmem + kAccCol + (uint32_t)NX * mypos;
       ptx::mbar_wait(&c.acc_empty, accph ^ 1);  // the previous pass's epilogue drained TMEM
       ptx::tc_fence_after();
       for (int kb = s.kb0; kb < s.kb1; ++kb) {
@@ -508,14 +557,14 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       const int pos = kh;
       const int np = pos ? s.n1 : s.n0;
       const int offp = (pos ? s.pt.off1 : s.pt.off0) + s.base;  // first assignment of this warp
-      float* slot = part + (size_t)(2 * g + (s.item == first_item ? 0 : 1)) * slot_tok * kRows;
-      const uint32_t acc_t = lane_tmem + kAccCol + 32u * pos;
+      float* slot = part + (size_t)(2 * g + (s.item == first_item ? 0 : 1)) * kSlot;
+      const uint32_t acc_t = lane_tmem + kAccCol + (uint32_t)NX * pos;
       for (int c0 = 0; c0 < np; c0 += 16) {
         uint32_t r[16];
         ptx::tmem_ld_32x32b_x16(acc_t + c0, r);
         ptx::tmem_ld_wait();
         if (!whole) {
-          const int t0 = offp - s.pt.off0 + c0;  // token index within the pair's assignments
+          const int t0 = pos * NX + c0;  // (position, token of the pass)
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             if (c0 + i < np) slot[(size_t)(t0 + i) * kRows + prow] = __uint_as_float(r[i]);
@@ -547,7 +596,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&c.acc_empty);
 
-      if (!whole && s.base + kNX >= max(s.pt.cnt0, s.pt.cnt1)) {  // last pass of a split piece
+      if (!whole) {  // a split piece
         const int g_first = sk.owner(s.item * nk), g_last = sk.owner(s.item * nk + nk - 1);
         if (g != g_first) {
           // a signalling piece: the X producer publishes it (fence + counter)
@@ -566,13 +615,15 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           const int r0 = s.rb * (kW13 ? kRows / 2 : kRows);
           const int cols = kW13 ? kRows / 2 : min(kRows, d - r0);  // outputs of this tile, multiple of 4
           const int q4 = cols / 4;
-          const int n_tot = s.pt.cnt0 + s.pt.cnt1;  // buckets 2p and 2p+1 are adjacent
+          const int n_tot = 2 * NX;  // slot rows: (position, token of the pass)
           for (int i = dtid; i < n_tot * q4; i += kDecWarps * 32) {
             const int t = i / q4, cq = 4 * (i % q4);
+            const int pos = t / NX, tk = t % NX;
+            if (tk >= (pos ? s.n1 : s.n0)) continue;
             float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
             for (int gg = g_first; gg <= g_last; ++gg) {
               const int sl = 2 * gg + (s.item == sk.begin(gg) / nk ? 0 : 1);
-              const float* src = part + ((size_t)sl * slot_tok + t) * kRows + cq;
+              const float* src = part + (size_t)sl * kSlot + (size_t)t * kRows + cq;
               const float4 v4 = __ldcg(reinterpret_cast<const float4*>(src));
               s0.x += v4.x; s0.y += v4.y; s0.z += v4.z; s0.w += v4.w;
               if (kW13) {
@@ -580,7 +631,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
                 s1.x += u.x; s1.y += u.y; s1.z += u.z; s1.w += u.w;
               }
             }
-            const size_t aa = (size_t)(s.pt.off0 + t);
+            const size_t aa = (size_t)((pos ? s.pt.off1 : s.pt.off0) + s.base + tk);
             if (kW13) {
               uint2 o;
               o.x = f32_to_bf16_rne_bits(silu_mul(s0.x, s1.x)) | (f32_to_bf16_rne_bits(silu_mul(s0.y, s1.y)) << 16);
@@ -604,7 +655,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       ptx::mbar_wait(&c.wfull[w.i], w.ph);
       const int4 h = lds_int4(whdr_s + 16u * w.i);
       if (h.x < 0) break;
-      const Pass s = make_pass(c, h, n_rb);
+      const Pass s = make_pass(c, h, n_active, NX);
       const int n_st = s.kb1 - s.kb0;
       // PZ_TC_DEFER: drain the previous pass after two stages of this one (its last MMAs have
       // completed by then; the A ring lets the decoders run ahead meanwhile)
@@ -626,62 +677,81 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   ptx::tc_fence_before();
   named_bar_sync(3, 64 + kDecWarps * 32);
   ptx::tc_fence_after();
-  if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+  if (warp == 1) ptx::tmem_dealloc<C::kTmemCols>(tmem);
 #ifdef PZ_TRACE
   if (threadIdx.x == 32) g_cta[kW13][blockIdx.x][3] = gtimer();
 #endif
 }
 
-template <bool kW13>
+template <bool kW13, int NX, int CTAS>
 int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* bucket_off, const int32_t* active,
-               const int32_t* n_active, int K, int f, int d, int n_rb, int max_active, int slot_tok, float* part,
+               const int32_t* n_active, int K, int f, int d, int n_rb, int max_active, int64_t n_assign, float* part,
                int32_t* counters, uint16_t* h, float* y, int n_pairs, cudaStream_t stream) {
-  auto kern = k_gemv_tc<kW13>;
+  using C = Cfg<NX, CTAS>;
+  auto kern = k_gemv_tc<kW13, NX, CTAS>;
+  constexpr size_t kSmem = smem_bytes<C>();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     attr = true;
   }
   // stream-K grid: every resident CTA slot, but >= kMinStages stages each (the device
-  // recomputes the partition from the actual number of active pairs)
-  const int64_t S = (int64_t)max_active * n_rb * (K / kBK);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gemv_tc_max_ctas(), S / kMinStages));
+  // recomputes the partition from the actual active pairs and passes)
+  const int64_t S = ((int64_t)max_active + n_assign / NX) * n_rb * (K / kBK);  // >= the real stage count
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)CTAS * num_sms(), S / kMinStages));
+  const char* name = NX == 32 ? (kW13 ? "w13_gemv" : "w2_gemv") : (kW13 ? "w13_tc" : "w2_tc");
   {
-    ProfScope _ps(kW13 ? "w13_gemv" : "w2_gemv", stream);
+    ProfScope _ps(name, stream);
     cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kThreads), kSmem, stream, tw, tx, bucket_off, active, n_active,
-                               K, f, d, n_rb, slot_tok, part, counters, h, y, 1u, n_pairs);
-    if (e != cudaSuccess) return cuda_check(e, kW13 ? "w13_gemv launch" : "w2_gemv launch");
+                               K, f, d, n_rb, part, counters, h, y, 1u, n_pairs);
+    if (e != cudaSuccess) return cuda_check(e, name);
   }
-  return cuda_check(cudaGetLastError(), kW13 ? "w13_gemv launch" : "w2_gemv launch");
+  return cuda_check(cudaGetLastError(), name);
 }
 
-}  // namespace
-
-// Resident CTA slots of the decode kernels (2 per SM): bounds the stream-K grid and the
-// partial-slot workspace.
-int gemv_tc_max_ctas() { return 2 * num_sms(); }
-bool gemv_supported(int d, int f) { return d % 64 == 0 && f % 64 == 0 && d <= 65535 * 64 && f <= 65535 * 64; }
-
-// x_rows: [n_assign_cap][d] bf16 in bucket order (TMA source); h: [n_assign_cap][f];
-// y: [n_assign_cap][d]; part: 2 * gemv_tc_max_ctas() * slot_tok * 128 floats, slot_tok >= the
-// assignments of any one pair; counters13 / counters2: >= n_pairs * row blocks, zero.
-int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f,
-                           const uint16_t* x_rows, const int32_t* bucket_off, const int32_t* active_pairs,
-                           const int32_t* n_active, int max_active, int64_t n_assign_cap, int slot_tok, float* part,
-                           int32_t* counters13, int32_t* counters2, uint16_t* h, float* y, cudaStream_t stream) {
+template <int NX, int CTAS>
+int launch_both(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f, const uint16_t* x_rows,
+                const int32_t* bucket_off, const int32_t* active_pairs, const int32_t* n_active, int max_active,
+                int64_t n_assign_cap, float* part, int32_t* counters13, int32_t* counters2, uint16_t* h, float* y,
+                cudaStream_t stream) {
   if (max_active == 0 || n_assign_cap == 0) return PUZZLE_OK;
   CUtensorMap tw13, tx13, tw2, tx2;
   int rc;
   if ((rc = make_tmap_2d(&tw13, w13, (int64_t)n_pairs * 2 * f, d, kRows / 2, kBK))) return rc;
-  if ((rc = make_tmap_2d(&tx13, x_rows, n_assign_cap, d, kXBox, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx13, x_rows, n_assign_cap, d, NX, kBK))) return rc;
   if ((rc = make_tmap_2d(&tw2, w2, (int64_t)n_pairs * d, f, kRows, kBK))) return rc;
-  if ((rc = make_tmap_2d(&tx2, h, n_assign_cap, f, kXBox, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx2, h, n_assign_cap, f, NX, kBK))) return rc;
   const int rb13 = f / (kRows / 2), rb2 = (d + kRows - 1) / kRows;
-  if ((rc = launch_one<true>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, max_active, slot_tok,
-                             part, counters13, h, y, n_pairs, stream)))
+  if ((rc = launch_one<true, NX, CTAS>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, max_active,
+                                       n_assign_cap, part, counters13, h, y, n_pairs, stream)))
     return rc;
-  return launch_one<false>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, max_active, slot_tok, part,
-                           counters2, h, y, n_pairs, stream);
+  return launch_one<false, NX, CTAS>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, max_active,
+                                     n_assign_cap, part, counters2, h, y, n_pairs, stream);
+}
+
+}  // namespace
+
+// Partial-slot floats of the two configurations (2 slots per CTA x 2 positions x NX x 128).
+size_t gemv_tc_part_floats(bool prefill) {
+  return prefill ? (size_t)2 * num_sms() * 2 * 128 * kRows : (size_t)2 * 2 * num_sms() * 2 * 32 * kRows;
+}
+// Work-item counters per projection: row blocks x (pairs + passes).
+int64_t gemv_tc_counters(int n_rb, int n_pairs, int64_t n_assign) { return (int64_t)n_rb * (n_pairs + n_assign / 32 + 1); }
+bool gemv_supported(int d, int f) { return d % 64 == 0 && f % 64 == 0 && d <= 65535 * 64 && f <= 65535 * 64; }
+
+// x_rows: [n_assign_cap][d] bf16 in bucket order (TMA source); h: [n_assign_cap][f];
+// y: [n_assign_cap][d]; part: gemv_tc_part_floats(prefill) floats; counters13 / counters2:
+// gemv_tc_counters(row blocks, ...) ints, zero. prefill = the 128-token, one-CTA-per-SM
+// configuration (token-heavy batches), otherwise the decode configuration.
+int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f,
+                           const uint16_t* x_rows, const int32_t* bucket_off, const int32_t* active_pairs,
+                           const int32_t* n_active, int max_active, int64_t n_assign_cap, bool prefill, float* part,
+                           int32_t* counters13, int32_t* counters2, uint16_t* h, float* y, cudaStream_t stream) {
+  if (prefill)
+    return launch_both<128, 1>(w13, w2, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
+                               n_assign_cap, part, counters13, counters2, h, y, stream);
+  return launch_both<32, 2>(w13, w2, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
+                            n_assign_cap, part, counters13, counters2, h, y, stream);
 }
 
 #ifdef PZ_TRACE
