@@ -121,26 +121,34 @@ __device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
 }
 
 // Algorithm 1 in place on one packed B stage (shared-space address `b_tile`): elementwise, so
-// the TMA's swizzled layout is preserved. Shifts/adds on the FMA pipe (register multipliers).
+// the TMA's swizzled layout is preserved. Per 32-bit register (2 words):
+//   mag = (w & 0x0FFF0FFF) + 0x57805780   |W^| x 2^63 (exponent e' + 112 + 63, no lane carry)
+//   W^  = bf16x2(mag) x bf16x2(w' & 0xA000A000), w' = w (pos 0) or w << 1 (pos 1)
+// the sign and mask bits of the position form +-2^-63 or +-0, so one exact bf16x2 multiply
+// applies sign, mask and rescale on the FMA pipe (gemv_tc.cu uses the same form).
+__device__ __forceinline__ uint32_t bf16x2_mul_tc(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
 template <int POS>
-__device__ __forceinline__ uint32_t dec_word(uint32_t w, uint32_t one, uint32_t two, uint32_t four, uint32_t eight) {
-  const uint32_t b0 = imad(w & 0x8FFF8FFFu, one, 0x38003800u);
-  if (POS == 0) return b0 & lane_msb_mask(imul(w, four));
-  return lop3_select_sign(imul(w, two), b0) & lane_msb_mask(imul(w, eight));
+__device__ __forceinline__ uint32_t dec_word(uint32_t w, uint32_t one, uint32_t two) {
+  const uint32_t mag = imad(w & 0x0FFF0FFFu, one, 0x57805780u);
+  return bf16x2_mul_tc(mag, (POS == 0 ? w : imul(w, two)) & 0xA000A000u);
 }
 template <int POS>
 __device__ __forceinline__ void decode_tile(uint32_t b_tile, int tid, uint32_t one) {
-  const uint32_t two = one * 2u, four = one * 4u, eight = one * 8u;
+  const uint32_t two = one * 2u;
   constexpr int kPer = kBBytes / 16 / (kDecodeWarps * 32);  // uint4 per thread per stage
   uint4 v[kPer];
 #pragma unroll
   for (int j = 0; j < kPer; ++j) v[j] = lds128(b_tile + (uint32_t)(tid + j * kDecodeWarps * 32) * 16u);
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
-    v[j].x = dec_word<POS>(v[j].x, one, two, four, eight);
-    v[j].y = dec_word<POS>(v[j].y, one, two, four, eight);
-    v[j].z = dec_word<POS>(v[j].z, one, two, four, eight);
-    v[j].w = dec_word<POS>(v[j].w, one, two, four, eight);
+    v[j].x = dec_word<POS>(v[j].x, one, two);
+    v[j].y = dec_word<POS>(v[j].y, one, two);
+    v[j].z = dec_word<POS>(v[j].z, one, two);
+    v[j].w = dec_word<POS>(v[j].w, one, two);
   }
 #pragma unroll
   for (int j = 0; j < kPer; ++j) sts128(b_tile + (uint32_t)(tid + j * kDecodeWarps * 32) * 16u, v[j]);
