@@ -104,12 +104,8 @@ __device__ __forceinline__ uint32_t decode2(uint32_t w) {
   return decode2<POS>(w, decode_base(w));
 }
 
-// Both positions of one 32-bit register of packed words, arranged so that the SWAR work
-// splits between the ALU pipe (LOP3 / PRMT: 6 ops) and the FMA pipe (IMAD: 4 ops):
-//   b0 = (w & 0x8FFF8FFF) + 0x38003800   sign S_i (bit 15) rides along: no carry leaves a lane
-//   v0 = b0 & msb_mask(w << 2)            mask M_i (bit 13) -> bit 15
-//   b1 = select(0x80008000: w << 1, else b0)   sign S_j (bit 14) -> bit 15
-//   v1 = b1 & msb_mask(w << 3)            mask M_j (bit 12) -> bit 15
+// Integer multiply / multiply-add through inline PTX with a register operand (a value ptxas
+// cannot see), so shifts and adds of the SWAR decode issue as IMAD on the FMA pipe.
 __device__ __forceinline__ uint32_t imul(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -120,18 +116,6 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
   return r;
 }
-__device__ __forceinline__ uint32_t decode_b0(uint32_t w) { return imad(w & 0x8FFF8FFFu, 1u, 0x38003800u); }
-__device__ __forceinline__ uint32_t decode_v0(uint32_t w, uint32_t b0) { return b0 & lane_msb_mask(imul(w, 4u)); }
-__device__ __forceinline__ uint32_t lop3_select_sign(uint32_t from_sign, uint32_t rest) {
-  // (from_sign & 0x80008000) | (rest & 0x7FFF7FFF) in one LOP3 (LUT 0xE2 = B ? A : C)
-  uint32_t r;
-  asm("lop3.b32 %0, %1, 0x80008000, %2, 0xE2;" : "=r"(r) : "r"(from_sign), "r"(rest));
-  return r;
-}
-__device__ __forceinline__ uint32_t decode_v1(uint32_t w, uint32_t b0) {
-  const uint32_t b1 = lop3_select_sign(imul(w, 2u), b0);
-  return b1 & lane_msb_mask(imul(w, 8u));
-}
 
 // ---- memory helpers ----
 __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
@@ -141,28 +125,7 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
                : "l"(p));
   return r;
 }
-__device__ __forceinline__ uint4 ldg_v4(const void* p) {
-  uint4 r;
-  asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
 
-// ---- legacy tensor-core MMA (decode-shape GEMV path) ----
-// D[16x8] += A[16x16] * B[16x8], bf16 inputs, fp32 accumulate.
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                               uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-// silu(g) * u with the SFU exponential and an approximate division (both ~2 ulp of fp32, far
-// below the bf16 rounding of h that follows): the IEEE expf + division cost ~30 instructions
-// and dominated the prefill epilogue. g -> -inf: exp -> inf, the quotient -> 0 (silu's limit).
 __device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
 __device__ __forceinline__ uint16_t f32_to_bf16_bits_rn(float x) {
