@@ -1,0 +1,9 @@
+#!/bin/bash
+# decode A/B: default build vs build/variants/* on the five decode configs (graph replay)
+cd $GRAFT_REPO_ROOT
+for cb in "mixtral 64" "mixtral 1" "qwen15 64" "qwen15 1" "deepseek 64"; do set -- $cb
+  timeout 200 python bench.py --config $1 --batch $2 --steps 100 --warmup 5 --no-extra --no-cpu > gpurun_out/da_default_$1_$2.log 2>&1
+  for d in build/variants/*/; do [ -d "$d" ] || continue; n=$(basename $d); case $n in trace*|tctrace) continue;; esac
+    PUZZLE_LIB=$d/libpuzzlemoe.so timeout 200 python bench.py --config $1 --batch $2 --steps 100 --warmup 5 --no-extra --no-cpu > gpurun_out/da_${n}_$1_$2.log 2>&1
+  done
+done
