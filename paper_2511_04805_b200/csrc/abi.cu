@@ -32,6 +32,8 @@ int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16
 bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
                       uint16_t*, float*, int32_t*, cudaStream_t);
+int launch_tc2_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
+                       uint16_t*, float*, cudaStream_t);
 size_t gemv_tc_part_floats(bool prefill);
 int64_t gemv_tc_counters(int n_rb, int n_pairs, int64_t n_assign);
 bool gemv_supported(int d, int f);
@@ -150,14 +152,17 @@ struct Layout {
 };
 
 // Token-heavy batches: the tcgen05 grouped GEMM (gemm_tc.cu) by default; PUZZLE_PREFILL_IMPL=tmem
-// selects the decode-into-TMEM kernels' prefill configuration (A/B measurements).
-bool prefill_via_tmem() {
-  static const bool v = [] {
+// selects the decode-into-TMEM kernels' prefill configuration, =pair the CTA-pair
+// (cta_group::2) grouped GEMM (gemm_tc2.cu) -- A/B measurements.
+const char* prefill_impl() {
+  static const char* v = [] {
     const char* e = getenv("PUZZLE_PREFILL_IMPL");
-    return e && std::string(e) == "tmem";
+    return e ? e : "";
   }();
   return v;
 }
+bool prefill_via_tmem() { return std::string(prefill_impl()) == "tmem"; }
+bool prefill_via_pair() { return std::string(prefill_impl()) == "pair"; }
 
 Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   Plan p;
@@ -342,6 +347,9 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
     return launch_gemv_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
                                   n_active, plan.max_active, plan.n_assign, true, at<float>(ws, lay.part),
                                   at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);
+  if (plan.path == PUZZLE_PATH_TC && prefill_via_pair())
+    return launch_tc2_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
+                              at<uint16_t>(ws, lay.h), y, s);
   if (plan.path == PUZZLE_PATH_TC)
     return launch_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, at<int32_t>(ws, lay.cnt13), s);  // cnt13: zeroed per call
