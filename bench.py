@@ -131,19 +131,32 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- workload
-def build_layer_gpu(pz, cfg, seed: int, device):
+def build_layer_gpu(pz, cfg, seed: int, device, ratio: float = 0.5):
     """Synthetic experts drawn on the GPU (generator G1 statistics) and merged + packed by
-    puzzle_merge_experts_pack (Eq. 1-7 + pack, tau = 0.4)."""
+    puzzle_merge_experts_pack (Eq. 1-7 + pack, tau = 0.4). ratio 0.5: every pair merged;
+    ratio 0.25 (reading R20): the first E/4 pairs merged, the other experts kept as
+    dense bf16 slots (E/4 + E/2 = 3E/4 slots)."""
     import torch
-    _, slot = synth.pairing(cfg, seed)
+    pairs, slot = synth.pairing(cfg, seed)
     w = synth.packed_statistical_torch(cfg, device, seed)
     stats = pz.new_stats(device)
+    n_merged = cfg.n_pairs if ratio == 0.5 else cfg.n_experts // 4
     packed = {}
     for name, (w_i, w_j, n_i, n_j) in w.items():
-        packed[name] = pz.merge_experts_pack(w_i, w_j, n_i, n_j, 0.4, stats=stats)
+        merged = pz.merge_experts_pack(w_i[:n_merged].contiguous(), w_j[:n_merged].contiguous(),
+                                       n_i[:n_merged].contiguous(), n_j[:n_merged].contiguous(), 0.4, stats=stats)
+        if n_merged < cfg.n_pairs:  # dense slots: expert i then expert j of each unmerged pair
+            rest = torch.stack([w_i[n_merged:], w_j[n_merged:]], dim=1).flatten(0, 1).view(torch.int16)
+            merged = torch.cat([merged, rest])
+        packed[name] = merged
     del w
+    dense = None
+    if n_merged < cfg.n_pairs:
+        for p, (a, b) in enumerate(pairs[n_merged:]):
+            slot[a], slot[b] = 2 * (n_merged + 2 * p), 2 * (n_merged + 2 * p + 1)
+        dense = torch.tensor([0] * n_merged + [1] * (2 * (cfg.n_pairs - n_merged)), dtype=torch.uint8, device=device)
     w13 = torch.stack([packed["w1"], packed["w3"]], dim=1).contiguous()
-    layer = pz.PackedMoELayer(w13, packed["w2"].contiguous(), torch.from_numpy(slot).to(device))
+    layer = pz.PackedMoELayer(w13, packed["w2"].contiguous(), torch.from_numpy(slot).to(device), dense)
     torch.cuda.synchronize(device)
     return layer, stats.cpu().tolist()
 
@@ -568,12 +581,13 @@ def sweep(pz, args, device, pk):
     path (tensor-bound, TFLOP/s of the dense-equivalent 2*3*d*f*T*k)."""
     import torch
     res = []
-    for name, T in (("mixtral", 1), ("mixtral", 16), ("qwen15", 1), ("qwen15", 16), ("qwen15", 64),
-                    ("deepseek", 1), ("deepseek", 16), ("deepseek", 64),
-                    ("mixtral", 4096), ("qwen15", 4096), ("deepseek", 4096)):
+    for name, T, ratio in (("mixtral", 1, 0.5), ("mixtral", 16, 0.5), ("qwen15", 1, 0.5), ("qwen15", 16, 0.5),
+                           ("qwen15", 64, 0.5), ("deepseek", 1, 0.5), ("deepseek", 16, 0.5), ("deepseek", 64, 0.5),
+                           ("mixtral", 4096, 0.5), ("qwen15", 4096, 0.5), ("deepseek", 4096, 0.5),
+                           ("mixtral", 64, 0.25), ("deepseek", 64, 0.25), ("mixtral", 4096, 0.25)):
         cfg = synth.CONFIGS[name]
         try:
-            layer, _ = build_layer_gpu(pz, cfg, synth.seeds(cfg)["weights"], device)
+            layer, _ = build_layer_gpu(pz, cfg, synth.seeds(cfg)["weights"], device, ratio)
             hidden, logits = make_inputs(cfg, T, synth.seeds(cfg)["activations"], device)
             out = torch.empty_like(hidden)
             ws = layer.workspace(T, cfg.top_k)
@@ -601,6 +615,9 @@ def sweep(pz, args, device, pk):
             gbs = (ab["w13"] + ab["w2"]) / (ms / 1e3) / 1e9
             row = {"config": name, "batch": T, "tokens_per_s": T / (ms / 1e3), "ms_per_step": ms,
                    "touched_pairs": nt, "kernel_avg_ms": kern}
+            if ratio != 0.5:
+                row.update({"compression": "25% (merged pairs + dense bf16 slots, R20)",
+                            "slots": layer.n_pairs, "packed_gb": layer.packed_bytes / 1e9})
             if T <= 64:
                 row.update({"weight_gbs": gbs, "frac_hbm": gbs / pk["hbm_gbs"]})
             else:
@@ -613,7 +630,7 @@ def sweep(pz, args, device, pk):
             del layer, flush_buf
             torch.cuda.empty_cache()
         except Exception as e:  # pragma: no cover
-            res.append({"config": name, "batch": T, "error": repr(e)})
+            res.append({"config": name, "batch": T, "ratio": ratio, "error": repr(e)})
     return res
 
 

@@ -115,13 +115,21 @@ int puzzle_merge_experts_pack(const uint16_t* w_i, const uint16_t* w_j, const fl
                               puzzle_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
- * One MoE layer whose experts are PuzzleMoE-merged pairs (50% compression).
+ * One MoE layer whose experts are PuzzleMoE-merged pairs (50% compression), or --
+ * the 25% ratio, experts cut to 75% of the original count -- some merged pairs plus
+ * unmerged experts kept exactly (reading R20).
  * Weight orientation (out x in) row-major as in HF Mixtral/Qwen (reading R11):
  *   w13  u16 [n_pairs][2][d_ff][d_model]  packed gate (w1) rows, then up (w3) rows
  *   w2   u16 [n_pairs][d_model][d_ff]     packed down projection
- *   expert_slot  i32 [n_experts] (device) = 2*pair + pos  -- the pairing plan
- * Requirements: n_experts == 2*n_pairs, 2 <= n_experts <= 512; d_model and d_ff multiples
- * of 64; w13/w2 16-byte aligned.
+ *   expert_slot  i32 [n_experts] (device) = 2*pair + pos  -- the pairing plan;
+ *                distinct slots for distinct experts (not checked: device memory)
+ *   pair_dense   u8 [n_pairs] (device) or NULL (= all slots merged pairs). pair_dense[q] != 0:
+ *                slot q holds ONE unmerged expert as plain bf16 bits in the same w13/w2
+ *                shape, read without Algorithm 1; only 2*q + 0 may appear in expert_slot
+ *                (routing an expert to 2*q + 1 of such a slot gives undefined outputs).
+ * Requirements: 1 <= n_experts <= 2*n_pairs <= 512; d_model and d_ff multiples of 64;
+ * w13/w2 16-byte aligned. The experimental CTA-pair prefill (PUZZLE_PREFILL_IMPL=pair)
+ * rejects pair_dense with PUZZLE_ERR_UNSUPPORTED.
  * ------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_experts;
@@ -131,6 +139,7 @@ typedef struct {
   const uint16_t* w13;
   const uint16_t* w2;
   const int32_t* expert_slot;
+  const uint8_t* pair_dense;
 } puzzle_moe_layer;
 
 /* Kernel path for puzzle_moe_forward_ex. AUTO picks by token count. */

@@ -50,8 +50,8 @@ def _load():
             lib.oracle_pack.argtypes = [P, P, P, P, P, I64, P, P]
             lib.oracle_unpack.argtypes = [P, I, I64, P]
             lib.oracle_route.argtypes = [P, I64, I, I, I, P, P]
-            lib.oracle_moe_forward.argtypes = [P, P, P, I, I, I, P, P, I64, I, I, I, P, P]
-            lib.oracle_expert_ffn.argtypes = [P, P, I, I, I, I, P, I64, P]
+            lib.oracle_moe_forward.argtypes = [P, P, P, P, I, I, I, P, P, I64, I, I, I, P, P]
+            lib.oracle_expert_ffn.argtypes = [P, P, I, I, I, I, I, P, I64, P]
             lib.oracle_expert_ffn.restype = I
             lib.oracle_num_threads.restype = I
             lib.oracle_set_num_threads.argtypes = [I]
@@ -162,12 +162,13 @@ def route(logits, k: int, renormalize: bool) -> tuple[np.ndarray, np.ndarray]:
 
 
 def moe_forward(w13, w2, expert_slot, hidden_bits, logits, k: int, renormalize: bool,
-                residual_bits=None) -> np.ndarray:
+                residual_bits=None, pair_dense=None) -> np.ndarray:
     """f64 [T, d] = residual + sum_j gate_j * FFN_{e_j}(x) over packed pairs.
 
     w13: uint16 [P, 2, f, d]; w2: uint16 [P, d, f]; expert_slot: int32 [E]
-    (2*pair+pos); hidden_bits / residual_bits: uint16 bf16 bits [T, d];
-    logits: f32 [T, E]."""
+    (2*pair+pos, E <= 2P, distinct); hidden_bits / residual_bits: uint16 bf16 bits
+    [T, d]; logits: f32 [T, E]; pair_dense: None or uint8 [P], 1 = the slot holds one
+    unmerged expert's plain bf16 weights at position 0 (25% ratio, reading R20)."""
     w13 = _c(w13, np.uint16)
     w2 = _c(w2, np.uint16)
     P, two, f, d = w13.shape
@@ -179,22 +180,24 @@ def moe_forward(w13, w2, expert_slot, hidden_bits, logits, k: int, renormalize: 
     E = lg.shape[1]
     assert hb.shape == (T, d) and lg.shape == (T, E) and slot.shape == (E,)
     res = None if residual_bits is None else _c(residual_bits, np.uint16)
+    dense = None if pair_dense is None else _c(pair_dense, np.uint8).reshape(-1)
+    assert dense is None or dense.shape == (P,)
     out = np.empty((T, d), np.float64)
-    rc = _load().oracle_moe_forward(_ptr(w13), _ptr(w2), _ptr(slot), P, d, f, _ptr(hb), _ptr(lg),
+    rc = _load().oracle_moe_forward(_ptr(w13), _ptr(w2), _ptr(slot), _ptr(dense), P, d, f, _ptr(hb), _ptr(lg),
                                     T, E, k, int(bool(renormalize)), _ptr(res), _ptr(out))
     if rc != 0:
         raise ValueError(f"oracle_moe_forward failed rc={rc}")
     return out
 
 
-def expert_ffn(w13, w2, pair: int, pos: int, x_bits) -> np.ndarray:
+def expert_ffn(w13, w2, pair: int, pos: int, x_bits, dense: bool = False) -> np.ndarray:
     """f64 [n, d] = W2_pos (silu(W1_pos x) * (W3_pos x)) for rows already routed to expert
-    (pair, pos); no gate, no residual."""
+    (pair, pos); no gate, no residual. dense: the slot holds plain bf16 weights (R20)."""
     w13 = _c(w13, np.uint16)
     w2 = _c(w2, np.uint16)
     P, two, f, d = w13.shape
     xb = _c(x_bits, np.uint16).reshape(-1, d)
     y = np.empty((xb.shape[0], d), np.float64)
-    if _load().oracle_expert_ffn(_ptr(w13), _ptr(w2), int(pair), int(pos), d, f, _ptr(xb), xb.shape[0], _ptr(y)) != 0:
+    if _load().oracle_expert_ffn(_ptr(w13), _ptr(w2), int(pair), int(pos), int(bool(dense)), d, f, _ptr(xb), xb.shape[0], _ptr(y)) != 0:
         raise ValueError("bad expert position")
     return y

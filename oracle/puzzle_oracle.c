@@ -21,7 +21,8 @@
  *   oracle_unpack       pinned (exhaustive 2^16 x 2 vs byte-literal Alg. 1)
  *   oracle_route        pinned (torch.topk / torch.softmax library routines)
  *   oracle_moe_forward  pinned (self-merge == dense torch f64 FFN, top-1 gate
- *                               == 1, token-permutation equivariance)
+ *                               == 1, token-permutation equivariance; dense
+ *                               slots == torch f64 FFN of the bf16 weights)
  */
 #include <math.h>
 #include <stdint.h>
@@ -226,16 +227,28 @@ int oracle_route(const float* logits, int64_t T, int E, int k, int renormalize, 
 /*   expert_slot[e] = 2*pair + pos (the pairing plan)              */
 /*   hidden: bf16 bits [T][d]; logits: f32 [T][E]; residual: bf16 bits or 0   */
 /*   out: f64 [T][d] = residual + sum_j gate_j * W2_e (silu(W1_e x) * W3_e x) */
+/*   pair_dense: NULL, or u8 [P]: slot q holds ONE unmerged expert as plain   */
+/*   bf16 bits in the same [2][f][d] / [d][f] shape, position 0 only (the 25% */
+/*   compression ratio: experts cut to 75%, the rest kept unchanged;   */
+/*   reading R20). E <= 2P; the slots of distinct experts must be distinct.   */
 /* All products and sums in f64 on the exact bf16 operand values; h is NOT   */
 /* rounded to bf16 (reading R16). One token per OpenMP iteration.            */
 /* ------------------------------------------------------------------------ */
+static double slot_weight(uint16_t w, int pos, int dense) {
+  return bf16_to_double(dense ? w : decode_word(w, pos));
+}
+
 int oracle_moe_forward(const uint16_t* w13, const uint16_t* w2, const int32_t* expert_slot,
-                       int n_pairs, int d, int f, const uint16_t* hidden, const float* logits,
-                       int64_t T, int E, int k, int renormalize, const uint16_t* residual,
-                       double* out) {
-  if (E < 1 || E > 1024 || k < 1 || k > E || d < 1 || f < 1) return 1;
-  for (int e = 0; e < E; ++e)
+                       const uint8_t* pair_dense, int n_pairs, int d, int f, const uint16_t* hidden,
+                       const float* logits, int64_t T, int E, int k, int renormalize,
+                       const uint16_t* residual, double* out) {
+  if (E < 1 || E > 1024 || E > 2 * n_pairs || k < 1 || k > E || d < 1 || f < 1) return 1;
+  for (int e = 0; e < E; ++e) {
     if (expert_slot[e] < 0 || expert_slot[e] >= 2 * n_pairs) return 1;
+    if (pair_dense && pair_dense[expert_slot[e] / 2] && expert_slot[e] % 2 != 0) return 1;
+    for (int e2 = 0; e2 < e; ++e2)
+      if (expert_slot[e2] == expert_slot[e]) return 1;
+  }
   int err = 0;
 #pragma omp parallel
   {
@@ -258,20 +271,21 @@ int oracle_moe_forward(const uint16_t* w13, const uint16_t* w2, const int32_t* e
       for (int j = 0; j < k; ++j) {
         int slot = expert_slot[sel[j]];
         int pair = slot / 2, pos = slot % 2;
+        int dense = pair_dense ? pair_dense[pair] != 0 : 0;
         const uint16_t* W1 = w13 + ((size_t)pair * 2 + 0) * (size_t)f * d; /* gate */
         const uint16_t* W3 = w13 + ((size_t)pair * 2 + 1) * (size_t)f * d; /* up   */
         const uint16_t* W2 = w2 + (size_t)pair * (size_t)d * f;
         for (int r = 0; r < f; ++r) {
           double g = 0.0, u = 0.0;
           for (int c = 0; c < d; ++c) {
-            g += bf16_to_double(decode_word(W1[(size_t)r * d + c], pos)) * x[c];
-            u += bf16_to_double(decode_word(W3[(size_t)r * d + c], pos)) * x[c];
+            g += slot_weight(W1[(size_t)r * d + c], pos, dense) * x[c];
+            u += slot_weight(W3[(size_t)r * d + c], pos, dense) * x[c];
           }
           h[r] = g / (1.0 + exp(-g)) * u; /* silu(g) * u */
         }
         for (int r = 0; r < d; ++r) {
           double acc = 0.0;
-          for (int c = 0; c < f; ++c) acc += bf16_to_double(decode_word(W2[(size_t)r * f + c], pos)) * h[c];
+          for (int c = 0; c < f; ++c) acc += slot_weight(W2[(size_t)r * f + c], pos, dense) * h[c];
           y[r] = acc;
         }
         for (int r = 0; r < d; ++r) o[r] += gate[j] * y[r];
@@ -289,9 +303,10 @@ int oracle_moe_forward(const uint16_t* w13, const uint16_t* w2, const int32_t* e
 /*      y[n] = W2_pos (silu(W1_pos x[n]) * (W3_pos x[n])), f64, no gate.     */
 /*      (The EP tests' CPU stand-in for the expert kernels.)                  */
 /* ------------------------------------------------------------------------ */
-int oracle_expert_ffn(const uint16_t* w13, const uint16_t* w2, int pair, int pos, int d, int f,
-                      const uint16_t* x_rows, int64_t n, double* y) {
+int oracle_expert_ffn(const uint16_t* w13, const uint16_t* w2, int pair, int pos, int dense, int d,
+                      int f, const uint16_t* x_rows, int64_t n, double* y) {
   if (pos != 0 && pos != 1) return 1;
+  if (dense && pos != 0) return 1;
   const uint16_t* W1 = w13 + ((size_t)pair * 2 + 0) * (size_t)f * d;
   const uint16_t* W3 = w13 + ((size_t)pair * 2 + 1) * (size_t)f * d;
   const uint16_t* W2 = w2 + (size_t)pair * (size_t)d * f;
@@ -303,14 +318,14 @@ int oracle_expert_ffn(const uint16_t* w13, const uint16_t* w2, int pair, int pos
       double g = 0.0, u = 0.0;
       for (int c = 0; c < d; ++c) {
         double xc = bf16_to_double(x[c]);
-        g += bf16_to_double(decode_word(W1[(size_t)r * d + c], pos)) * xc;
-        u += bf16_to_double(decode_word(W3[(size_t)r * d + c], pos)) * xc;
+        g += slot_weight(W1[(size_t)r * d + c], pos, dense) * xc;
+        u += slot_weight(W3[(size_t)r * d + c], pos, dense) * xc;
       }
       h[r] = g / (1.0 + exp(-g)) * u;
     }
     for (int r = 0; r < d; ++r) {
       double acc = 0.0;
-      for (int c = 0; c < f; ++c) acc += bf16_to_double(decode_word(W2[(size_t)r * f + c], pos)) * h[c];
+      for (int c = 0; c < f; ++c) acc += slot_weight(W2[(size_t)r * f + c], pos, dense) * h[c];
       y[t * d + r] = acc;
     }
     free(h);

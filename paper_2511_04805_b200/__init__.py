@@ -49,7 +49,7 @@ class MoELayerDesc(ctypes.Structure):
     """puzzle_moe_layer."""
     _fields_ = [("n_experts", ctypes.c_int32), ("n_pairs", ctypes.c_int32), ("d_model", ctypes.c_int32),
                 ("d_ff", ctypes.c_int32), ("w13", ctypes.c_void_p), ("w2", ctypes.c_void_p),
-                ("expert_slot", ctypes.c_void_p)]
+                ("expert_slot", ctypes.c_void_p), ("pair_dense", ctypes.c_void_p)]
 
 
 _lib = None
@@ -167,16 +167,21 @@ def new_stats(device="cuda") -> torch.Tensor:
 class PackedMoELayer:
     """Device tensors of one packed MoE layer plus its C descriptor.
 
-    w13: packed [P, 2, d_ff, d_model]; w2: packed [P, d_model, d_ff]; expert_slot: int32 [E]."""
+    w13: packed [P, 2, d_ff, d_model]; w2: packed [P, d_model, d_ff]; expert_slot: int32 [E],
+    E <= 2P; pair_dense: None or uint8 [P] (1 = the slot holds one unmerged expert's bf16
+    weights, position 0 only: the 25% ratio, reading R20)."""
 
-    def __init__(self, w13: torch.Tensor, w2: torch.Tensor, expert_slot: torch.Tensor):
+    def __init__(self, w13: torch.Tensor, w2: torch.Tensor, expert_slot: torch.Tensor, pair_dense=None):
         P, two, f, d = w13.shape
         assert two == 2 and tuple(w2.shape) == (P, d, f), (w13.shape, w2.shape)
-        assert expert_slot.dtype == torch.int32 and expert_slot.numel() == 2 * P
+        assert expert_slot.dtype == torch.int32 and 1 <= expert_slot.numel() <= 2 * P
+        assert pair_dense is None or (pair_dense.dtype == torch.uint8 and pair_dense.numel() == P)
         self.w13, self.w2, self.expert_slot = _u16(w13).contiguous(), _u16(w2).contiguous(), expert_slot.contiguous()
-        self.n_pairs, self.n_experts, self.d_model, self.d_ff = P, 2 * P, d, f
+        self.pair_dense = None if pair_dense is None else pair_dense.contiguous()
+        self.n_pairs, self.n_experts, self.d_model, self.d_ff = P, expert_slot.numel(), d, f
         self.desc = MoELayerDesc(self.n_experts, P, d, f, self.w13.data_ptr(), self.w2.data_ptr(),
-                                 self.expert_slot.data_ptr())
+                                 self.expert_slot.data_ptr(),
+                                 None if self.pair_dense is None else self.pair_dense.data_ptr())
         self._ws = None
 
     @property
@@ -229,11 +234,11 @@ class RoutingLayer:
     device tensor standing in for the weight pointers, which routing never dereferences."""
 
     def __init__(self, n_pairs: int, d_model: int, d_ff: int, expert_slot: torch.Tensor, anchor: torch.Tensor):
-        assert expert_slot.dtype == torch.int32 and expert_slot.numel() == 2 * n_pairs
+        assert expert_slot.dtype == torch.int32 and 1 <= expert_slot.numel() <= 2 * n_pairs
         self.expert_slot, self.anchor = expert_slot.contiguous(), anchor
         self.n_pairs = n_pairs
-        self.desc = MoELayerDesc(2 * n_pairs, n_pairs, d_model, d_ff, anchor.data_ptr(), anchor.data_ptr(),
-                                 self.expert_slot.data_ptr())
+        self.desc = MoELayerDesc(expert_slot.numel(), n_pairs, d_model, d_ff, anchor.data_ptr(), anchor.data_ptr(),
+                                 self.expert_slot.data_ptr(), None)
 
     def route(self, router_logits, top_k: int, renormalize: bool, stream=None):
         return _route(self.desc, self.n_pairs, router_logits, top_k, renormalize, stream)

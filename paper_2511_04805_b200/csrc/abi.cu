@@ -30,14 +30,15 @@ int launch_combine(const float*, const int32_t*, const float*, int64_t, int, int
                    uint16_t*, cudaStream_t);
 int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16_t*, cudaStream_t);
 bool tc_supported(int d, int f);
-int launch_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
-                      uint16_t*, float*, int32_t*, cudaStream_t);
+int launch_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
+                      const int32_t*, int64_t, uint16_t*, float*, int32_t*, cudaStream_t);
 int launch_tc2_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
                        uint16_t*, float*, cudaStream_t);
 size_t gemv_tc_part_floats(bool prefill);
 int64_t gemv_tc_counters(int n_rb, int n_pairs, int64_t n_assign);
 bool gemv_supported(int d, int f);
-int launch_gemv_tc_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*,
+int launch_gemv_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
+                           const int32_t*,
                            const int32_t*, const int32_t*, int, int64_t, bool, float*, int32_t*, int32_t*,
                            uint16_t*, float*, cudaStream_t);
 
@@ -125,9 +126,9 @@ int check_layer(const puzzle_moe_layer* L) {
   if (!L) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "layer descriptor is NULL");
   if (!L->w13 || !L->w2 || !L->expert_slot)
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "layer weights / expert_slot NULL");
-  if (L->n_pairs < 1 || L->n_experts != 2 * L->n_pairs)
-    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "n_experts must equal 2*n_pairs >= 2 (50% merge)");
-  if (L->n_experts > kMaxExperts) return fail(PUZZLE_ERR_UNSUPPORTED, "n_experts > 512");
+  if (L->n_pairs < 1 || L->n_experts < 1 || L->n_experts > 2 * L->n_pairs)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "need 1 <= n_experts <= 2*n_pairs");
+  if (2 * L->n_pairs > kMaxExperts) return fail(PUZZLE_ERR_UNSUPPORTED, "2*n_pairs > 512");
   if (L->d_model < 64 || L->d_ff < 64 || L->d_model % 64 || L->d_ff % 64)
     return fail(PUZZLE_ERR_UNSUPPORTED, "d_model and d_ff must be positive multiples of 64");
   if (!al16(L->w13) || !al16(L->w2)) return fail(PUZZLE_ERR_UNSUPPORTED, "weights must be 16-byte aligned");
@@ -344,16 +345,18 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
     rows = at<uint16_t>(ws, lay.x_perm);
   }
   if (plan.path == PUZZLE_PATH_TC && plan.tmem_prefill)
-    return launch_gemv_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
+    return launch_gemv_tc_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
                                   n_active, plan.max_active, plan.n_assign, true, at<float>(ws, lay.part),
                                   at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);
-  if (plan.path == PUZZLE_PATH_TC && prefill_via_pair())
+  if (plan.path == PUZZLE_PATH_TC && prefill_via_pair()) {
+    if (L->pair_dense) return fail(PUZZLE_ERR_UNSUPPORTED, "experimental CTA-pair prefill: no dense slots");
     return launch_tc2_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                               at<uint16_t>(ws, lay.h), y, s);
+  }
   if (plan.path == PUZZLE_PATH_TC)
-    return launch_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
+    return launch_tc_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, at<int32_t>(ws, lay.cnt13), s);  // cnt13: zeroed per call
-  return launch_gemv_tc_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
+  return launch_gemv_tc_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
                                 n_active, plan.max_active, plan.n_assign, false, at<float>(ws, lay.part),
                                 at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);
 }

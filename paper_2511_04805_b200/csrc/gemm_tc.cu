@@ -80,6 +80,7 @@ struct alignas(8) SmemCtl {
   int32_t bucket_off[kMaxBuckets + 1];
   int32_t mtiles[kMaxBuckets];          // M tiles of each bucket
   int32_t pair_off[kMaxBuckets / 2 + 1];  // first tile of each pair (pair-major tile order)
+  uint8_t dense[kMaxBuckets / 2];         // slot holds plain bf16 weights: no decode (R20)
 };
 
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + sizeof(SmemCtl);
@@ -162,7 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
     uint16_t* __restrict__ h_out,  // w13: [n_assign][f] bf16
     float* __restrict__ y_out,     // w2:  [n_assign][d] f32
     int32_t* __restrict__ work_ctr,  // zero on entry: tiles are claimed with an atomic
-    uint32_t mul_one) {            // = 1, opaque to ptxas (keeps decode shifts on the FMA pipe)
+    uint32_t mul_one,              // = 1, opaque to ptxas (keeps decode shifts on the FMA pipe)
+    const uint8_t* __restrict__ pair_dense) {  // NULL or [n_buckets / 2]
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   SmemCtl& c = *reinterpret_cast<SmemCtl*>(smem + (size_t)kStages * kStageBytes);
@@ -176,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
 #endif
   pdl_trigger();
   for (int i = threadIdx.x; i <= n_buckets; i += blockDim.x) c.bucket_off[i] = bucket_off[i];
+  for (int i = threadIdx.x; i < n_buckets / 2; i += blockDim.x) c.dense[i] = pair_dense ? pair_dense[i] : 0;
   __syncthreads();
   if (threadIdx.x == 0) {
     c.n_buckets = n_buckets;
@@ -363,10 +366,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       }
       const TileInfo t = tile_info(c, tile, n_blocks);
       const int pos = t.bucket & 1;
+      const bool dense = c.dense[t.bucket >> 1] != 0;  // the TMA-loaded words are the bf16 weights
       for (int kb = 0; kb < nk; ++kb) {
         ptx::mbar_wait(&c.full[stage], phase);
         const uint32_t sb = smem_base + (uint32_t)stage * kStageBytes + kABytes;
-        if (pos == 0) decode_tile<0>(sb, tid, mul_one); else decode_tile<1>(sb, tid, mul_one);
+        if (dense) {
+        } else if (pos == 0) {
+          decode_tile<0>(sb, tid, mul_one);
+        } else {
+          decode_tile<1>(sb, tid, mul_one);
+        }
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&c.dec[stage]);
@@ -404,9 +413,10 @@ bool tc_supported(int d, int f) { return d % BN == 0 && f % (BN / 2) == 0 && d %
 
 // x_rows: [n_rows_cap][d] bf16 grouped by bucket; h: [n_rows_cap][f]; y: [n_rows_cap][d]
 // work_ctrs: 2 ints, zero on entry (tile claim counters of the w13 and the w2 launch).
-int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f, const uint16_t* x_rows,
-                      const int32_t* bucket_off, int64_t n_rows_cap, uint16_t* h, float* y, int32_t* work_ctrs,
-                      cudaStream_t stream) {
+// pair_dense: NULL or [n_pairs] device flags (slot holds one unmerged expert's bf16 weights).
+int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_dense, int n_pairs, int d,
+                      int f, const uint16_t* x_rows, const int32_t* bucket_off, int64_t n_rows_cap, uint16_t* h,
+                      float* y, int32_t* work_ctrs, cudaStream_t stream) {
   if (!tc_supported(d, f)) return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d % 256 == 0 and d_ff % 128 == 0");
   if (n_rows_cap == 0) return PUZZLE_OK;
   static std::once_flag attr_once;
@@ -424,14 +434,16 @@ int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int 
   {
     ProfScope _ps("w13_tc", stream);
     cudaError_t e = launch_pdl(k_tc_experts<true>, dim3(grid), dim3(kThreads), kSmemBytes, stream, ta13, tb13,
-                               bucket_off, 2 * n_pairs, d, f, d, f / (BN / 2), h, (float*)nullptr, work_ctrs, 1u);
+                               bucket_off, 2 * n_pairs, d, f, d, f / (BN / 2), h, (float*)nullptr, work_ctrs, 1u,
+                               pair_dense);
     if (e != cudaSuccess) return cuda_check(e, "w13_tc launch");
   }
   if ((rc = cuda_check(cudaGetLastError(), "w13_tc launch"))) return rc;
   {
     ProfScope _ps("w2_tc", stream);
     cudaError_t e = launch_pdl(k_tc_experts<false>, dim3(grid), dim3(kThreads), kSmemBytes, stream, ta2, tb2,
-                               bucket_off, 2 * n_pairs, f, f, d, d / BN, (uint16_t*)nullptr, y, work_ctrs + 1, 1u);
+                               bucket_off, 2 * n_pairs, f, f, d, d / BN, (uint16_t*)nullptr, y, work_ctrs + 1, 1u,
+                               pair_dense);
     if (e != cudaSuccess) return cuda_check(e, "w2_tc launch");
   }
   return cuda_check(cudaGetLastError(), "w2_tc launch");

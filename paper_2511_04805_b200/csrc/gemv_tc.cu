@@ -237,7 +237,7 @@ __device__ __forceinline__ Pass make_pass(const Ctl<WST, XST>& c, int4 h, int n_
 }
 
 // One pass of the decoders over the piece's stages for the active position(s) (MODE bit 0 =
-// pos 0, bit 1 = pos 1): decode this thread's 32 packed words per stage (16 registers, k =
+// pos 0, bit 1 = pos 1, bit 2 = pos 0 of a dense slot: the words are the bf16 weights): decode this thread's 32 packed words per stage (16 registers, k =
 // 32 kh .. 32 kh + 31 of its row) and store the bf16 rows into the TMEM A buffer: register r
 // of chunk i -> column 16 kh + 4 i + r (k pair 32 kh + 8 i + 2 r).
 template <int MODE, int WST, int XST, class Epi>
@@ -265,6 +265,7 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST>& c, uint32_t smem_w, u
         const uint32_t mag = imad(x & 0x0FFF0FFFu, mu.one, 0x57805780u);
         // sign S_i (bit 15) + mask M_i (bit 13) = +-2^-63 or +-0 as bf16: one exact product
         if (MODE & 1) d0[4 * i + j] = bf16x2_mul(mag, x & 0xA000A000u);
+        if (MODE & 4) d0[4 * i + j] = x;
         // S_j (bit 14) and M_j (bit 12) shifted to bits 15 / 13
         if (MODE & 2) d1[4 * i + j] = bf16x2_mul(mag, imul(x, mu.two) & 0xA000A000u);
       }
@@ -275,7 +276,7 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST>& c, uint32_t smem_w, u
     PZ_TRD(3, tcount);
     ptx::tc_fence_after();
     const uint32_t t0 = lane_tmem + 64u * a.i + 16u * kh;
-    if (MODE & 1) ptx::tmem_st_32x32b_x16(t0, d0);
+    if (MODE & 5) ptx::tmem_st_32x32b_x16(t0, d0);
     if (MODE & 2) ptx::tmem_st_32x32b_x16(t0 + 32u, d1);
     ptx::tmem_st_wait();
     ptx::tc_fence_before();
@@ -297,7 +298,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     const int32_t* __restrict__ bucket_off, const int32_t* __restrict__ active_pairs,
     const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb,
     float* __restrict__ part, int32_t* __restrict__ counters, uint16_t* __restrict__ h_out,
-    float* __restrict__ y_out, uint32_t mul_one, int n_bucket_pairs) {
+    float* __restrict__ y_out, uint32_t mul_one, int n_bucket_pairs, const uint8_t* __restrict__ pair_dense) {
   using C = Cfg<NX, CTAS>;
   constexpr int kWStages = C::kWStages, kXStages = C::kXStages, kXBytes = C::kXBytes, kXPos = C::kXPos;
   constexpr int kSlot = 2 * NX * kRows;  // floats per partial slot
@@ -660,7 +661,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       // PZ_TC_DEFER: drain the previous pass after two stages of this one (its last MMAs have
       // completed by then; the A ring lets the decoders run ahead meanwhile)
       const int ep_at = PZ_TC_DEFER ? min(1, n_st - 1) : -1;
-      if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      // a dense slot (R20) is only ever routed at position 0
+      if (pair_dense != nullptr && pair_dense[s.p]) decode_pass<4>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      else if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
       else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
       else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
       if (PZ_TC_DEFER) {
@@ -686,7 +689,8 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
 template <bool kW13, int NX, int CTAS>
 int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* bucket_off, const int32_t* active,
                const int32_t* n_active, int K, int f, int d, int n_rb, int max_active, int64_t n_assign, float* part,
-               int32_t* counters, uint16_t* h, float* y, int n_pairs, cudaStream_t stream) {
+               int32_t* counters, uint16_t* h, float* y, int n_pairs, const uint8_t* pair_dense,
+               cudaStream_t stream) {
   using C = Cfg<NX, CTAS>;
   auto kern = k_gemv_tc<kW13, NX, CTAS>;
   constexpr size_t kSmem = smem_bytes<C>();
@@ -703,14 +707,14 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
   {
     ProfScope _ps(name, stream);
     cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kThreads), kSmem, stream, tw, tx, bucket_off, active, n_active,
-                               K, f, d, n_rb, part, counters, h, y, 1u, n_pairs);
+                               K, f, d, n_rb, part, counters, h, y, 1u, n_pairs, pair_dense);
     if (e != cudaSuccess) return cuda_check(e, name);
   }
   return cuda_check(cudaGetLastError(), name);
 }
 
 template <int NX, int CTAS>
-int launch_both(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f, const uint16_t* x_rows,
+int launch_both(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_dense, int n_pairs, int d, int f, const uint16_t* x_rows,
                 const int32_t* bucket_off, const int32_t* active_pairs, const int32_t* n_active, int max_active,
                 int64_t n_assign_cap, float* part, int32_t* counters13, int32_t* counters2, uint16_t* h, float* y,
                 cudaStream_t stream) {
@@ -723,10 +727,10 @@ int launch_both(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int
   if ((rc = make_tmap_2d(&tx2, h, n_assign_cap, f, NX, kBK))) return rc;
   const int rb13 = f / (kRows / 2), rb2 = (d + kRows - 1) / kRows;
   if ((rc = launch_one<true, NX, CTAS>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, max_active,
-                                       n_assign_cap, part, counters13, h, y, n_pairs, stream)))
+                                       n_assign_cap, part, counters13, h, y, n_pairs, pair_dense, stream)))
     return rc;
   return launch_one<false, NX, CTAS>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, max_active,
-                                     n_assign_cap, part, counters2, h, y, n_pairs, stream);
+                                     n_assign_cap, part, counters2, h, y, n_pairs, pair_dense, stream);
 }
 
 }  // namespace
@@ -742,15 +746,16 @@ bool gemv_supported(int d, int f) { return d % 64 == 0 && f % 64 == 0 && d <= 65
 // x_rows: [n_assign_cap][d] bf16 in bucket order (TMA source); h: [n_assign_cap][f];
 // y: [n_assign_cap][d]; part: gemv_tc_part_floats(prefill) floats; counters13 / counters2:
 // gemv_tc_counters(row blocks, ...) ints, zero. prefill = the 128-token, one-CTA-per-SM
-// configuration (token-heavy batches), otherwise the decode configuration.
-int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, int n_pairs, int d, int f,
+// configuration (token-heavy batches), otherwise the decode configuration. pair_dense: NULL or
+// [n_pairs] device flags (slot holds one unmerged expert's bf16 weights, position 0 only).
+int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_dense, int n_pairs, int d, int f,
                            const uint16_t* x_rows, const int32_t* bucket_off, const int32_t* active_pairs,
                            const int32_t* n_active, int max_active, int64_t n_assign_cap, bool prefill, float* part,
                            int32_t* counters13, int32_t* counters2, uint16_t* h, float* y, cudaStream_t stream) {
   if (prefill)
-    return launch_both<128, 1>(w13, w2, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
+    return launch_both<128, 1>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
                                n_assign_cap, part, counters13, counters2, h, y, stream);
-  return launch_both<32, 2>(w13, w2, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
+  return launch_both<32, 2>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
                             n_assign_cap, part, counters13, counters2, h, y, stream);
 }
 

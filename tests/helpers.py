@@ -54,3 +54,39 @@ def assert_close(gpu_out: np.ndarray, ref: np.ndarray, what: str = ""):
     m = compare(gpu_out, ref)
     assert m["max_abs"] <= MAX_ABS and m["rel_l2"] <= REL_L2, f"{what}: {m}"
     return m
+
+
+@functools.lru_cache(maxsize=8)
+def oracle_mixed_layer(cfg: synth.MoEConfig, n_merged: int, seed: int | None = None, tau: float = 0.4):
+    """The 25%-ratio layout (reading R20): the generator's first `n_merged` pairs merged +
+    packed by the ORACLE, every other expert kept as plain bf16 bits in a dense slot of its
+    own; slots in a seeded random order. Returns w13 [P',2,f,d], w2 [P',d,f] (uint16),
+    expert_slot [E] and pair_dense [P'] with P' = E - n_merged."""
+    pairs, _ = synth.pairing(cfg, seed)
+    d, f = cfg.d_model, cfg.d_ff
+    n_slots = cfg.n_experts - n_merged
+    order = np.random.default_rng(1234 + n_merged).permutation(n_slots)
+    w13 = np.empty((n_slots, 2, f, d), np.uint16)
+    w2 = np.empty((n_slots, d, f), np.uint16)
+    slot = np.empty(cfg.n_experts, np.int32)
+    dense = np.zeros(n_slots, np.uint8)
+    nxt = 0
+    for p, (a, b) in enumerate(pairs):
+        per = {}
+        for slot_name in synth.SLOTS:
+            w_i, w_j, n_i, n_j = synth.expert_pair_slot(cfg, p, slot_name, seed)
+            if p < n_merged:
+                per[slot_name] = (oracle.pack_artifacts(oracle.merge(w_i, w_j, n_i, n_j, tau))[0],)
+            else:
+                per[slot_name] = (synth.to_bf16_bits(w_i), synth.to_bf16_bits(w_j))
+        if p < n_merged:
+            q = int(order[nxt]); nxt += 1
+            w13[q, 0], w13[q, 1], w2[q] = per["w1"][0], per["w3"][0], per["w2"][0]
+            slot[a], slot[b] = 2 * q, 2 * q + 1
+        else:
+            for j, e in enumerate((a, b)):
+                q = int(order[nxt]); nxt += 1
+                w13[q, 0], w13[q, 1], w2[q] = per["w1"][j], per["w3"][j], per["w2"][j]
+                slot[e] = 2 * q
+                dense[q] = 1
+    return w13, w2, slot, dense

@@ -60,8 +60,11 @@ def test_argument_errors_are_synchronous(lib):
     assert lib.puzzle_merge_pack(None, None, None, None, None, -1, None, None, None) == 1
     assert lib.puzzle_merge_experts_pack(None, None, None, None, 1, 1, 8, ctypes.c_float(1.5), None, None, None) == 1
     import paper_2511_04805_b200 as pz
-    desc = pz.MoELayerDesc(7, 4, 4096, 14336, 4096, 4096, 4096)     # E != 2P
+    desc = pz.MoELayerDesc(9, 4, 4096, 14336, 4096, 4096, 4096)     # E > 2P
     assert lib.puzzle_moe_forward(ctypes.byref(desc), None, None, 1, 2, 1, None, None, None, 0, None) == 1
+    # E < 2P (the 25% ratio: merged pairs + dense slots, R20) is a valid layer: sizes only
+    desc = pz.MoELayerDesc(8, 6, 4096, 14336, 4096, 4096, 4096, 4096)
+    assert lib.puzzle_moe_workspace_size(ctypes.byref(desc), 64, 2) > 0
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device path")

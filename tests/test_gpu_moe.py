@@ -232,3 +232,36 @@ def test_forward_random_shapes(pz, cfg, T):
     single-position pairs, multi-pass buckets."""
     got, ref = _run(pz, cfg, T, pz.PATH_AUTO)
     assert_close(got, ref, f"{cfg.name} d={cfg.d_model} f={cfg.d_ff} E={cfg.n_experts} k={cfg.top_k} T={T}")
+
+
+# ---- the 25% compression ratio: merged pairs + unmerged dense bf16 slots (reading R20) ----
+MIXED = [
+    (synth.MoEConfig("mix25_small", 12, 256, 512, 8, 2, True), 2),     # Mixtral-like: 2 pairs + 4 dense
+    (synth.MoEConfig("mix25_fine", 13, 256, 384, 16, 4, False), 4),    # 4 pairs + 8 dense
+    (synth.MoEConfig("mix25_alldense", 14, 256, 256, 6, 2, True), 0),  # every expert dense
+]
+
+
+def _run_mixed(pz, cfg, n_merged, T, path, seed_shift=0):
+    from helpers import oracle_mixed_layer
+    w13, w2, slot, dense = oracle_mixed_layer(cfg, n_merged)
+    layer = pz.PackedMoELayer(torch.from_numpy(w13.view(np.int16)).cuda(), torch.from_numpy(w2.view(np.int16)).cuda(),
+                              torch.from_numpy(slot).cuda(), torch.from_numpy(dense).cuda())
+    hb = synth.hidden_bits(cfg, T, seed=synth.seeds(cfg)["activations"] + seed_shift)
+    lg = synth.router_logits(cfg, T, seed=synth.seeds(cfg)["logits"] + seed_shift)
+    rb = synth.hidden_bits(cfg, T, seed=synth.seeds(cfg)["activations"] + 1000 + seed_shift)
+    out = layer.forward(torch.from_numpy(hb.view(np.int16)).cuda().view(torch.bfloat16), torch.from_numpy(lg).cuda(),
+                        cfg.top_k, cfg.renormalize,
+                        residual=torch.from_numpy(rb.view(np.int16)).cuda().view(torch.bfloat16), path=path)
+    torch.cuda.synchronize()
+    ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, rb, pair_dense=dense)
+    return out.float().cpu().numpy(), ref
+
+
+@pytest.mark.parametrize("case", MIXED, ids=lambda c: c[0].name)
+@pytest.mark.parametrize("T", [1, 7, 64, 200])
+@pytest.mark.parametrize("path", ["gemv", "tc"])
+def test_forward_mixed_dense_slots(pz, case, T, path):
+    cfg, n_merged = case
+    got, ref = _run_mixed(pz, cfg, n_merged, T, pz.PATH_GEMV if path == "gemv" else pz.PATH_TC)
+    assert_close(got, ref, f"{cfg.name} merged={n_merged} T={T} {path}")

@@ -155,3 +155,77 @@ def test_expert_ffn_matches_forward_and_dense():
         logits[:, pos] = 1.0  # expert `pos` is at position pos with expert_slot = [0, 1]
         out = oracle.moe_forward(w13, w2, np.array([0, 1], np.int32), hb, logits, 1, True)
         np.testing.assert_allclose(out, y, rtol=1e-12, atol=1e-13)
+
+
+def _mixed_layer(cfg, rng, n_merged, n_dense):
+    """25% ratio layout (reading R20): n_merged packed pairs, then n_dense slots that each
+    hold one unmerged expert's plain bf16 weights at position 0. Returns w13, w2,
+    expert_slot, pair_dense and the dense experts' float weights."""
+    d, f = cfg.d_model, cfg.d_ff
+    w13, w2, dense_src = [], [], []
+    for _ in range(n_merged):
+        a, b, _ = _merged_pair(cfg, rng)
+        w13.append(a[0])
+        w2.append(b[0])
+    for _ in range(n_dense):
+        w1 = synth.to_bf16_values(rng.standard_normal((f, d)).astype(np.float32) / np.sqrt(d))
+        w3 = synth.to_bf16_values(rng.standard_normal((f, d)).astype(np.float32) / np.sqrt(d))
+        wd = synth.to_bf16_values(rng.standard_normal((d, f)).astype(np.float32) / np.sqrt(f))
+        w13.append(np.stack([synth.to_bf16_bits(w1), synth.to_bf16_bits(w3)]))
+        w2.append(synth.to_bf16_bits(wd))
+        dense_src.append((w1, w3, wd))
+    P = n_merged + n_dense
+    slot = np.array([2 * p + q for p in range(n_merged) for q in (0, 1)] +
+                    [2 * (n_merged + i) for i in range(n_dense)], np.int32)
+    pair_dense = np.array([0] * n_merged + [1] * n_dense, np.uint8)
+    return np.stack(w13), np.stack(w2), slot, pair_dense, dense_src
+
+
+def test_dense_slots_equal_plain_bf16_ffn():
+    """R20: a dense slot computes the FFN of its bf16 weights as stored (no Algorithm-1
+    decode, no exponent clamp), pinned by torch f64 matmuls on the float weights; the
+    merged pair next to it is unchanged (Eq. 8 reconstruction)."""
+    cfg = synth.MoEConfig("t25", 0, 32, 64, 4, 2, True)
+    rng = np.random.default_rng(31)
+    w13, w2, slot, dense, dsrc = _mixed_layer(cfg, rng, 1, 2)
+    # tiny magnitudes below 2^-15 would be clamped by a packed slot but not by a dense one
+    w13[1, 0, 0, :4] = synth.to_bf16_bits(np.array([1e-6, -3e-7, 2e-8, 0.0], np.float32))
+    dsrc[0] = (oracle.bf16_bits_to_f32(w13[1, 0]), dsrc[0][1], dsrc[0][2])
+    T = 12
+    hb = synth.hidden_bits(cfg, T, seed=32)
+    x = oracle.bf16_bits_to_f32(hb)
+    logits = synth.router_logits(cfg, T, seed=33)
+    out = oracle.moe_forward(w13, w2, slot, hb, logits, 2, True, pair_dense=dense)
+    idx, gate = oracle.route(logits, 2, True)
+    want = np.zeros((T, cfg.d_model))
+    for t in range(T):
+        for j in range(2):
+            e = int(idx[t, j])
+            if e >= 2:
+                w1, w3, wd = dsrc[e - 2]
+            else:
+                w1, w3, wd = (oracle.bf16_bits_to_f32(oracle.unpack(w, e)) for w in (w13[0, 0], w13[0, 1], w2[0]))
+            want[t] += gate[t, j] * _dense_ffn_f64(x[t:t + 1], w1, w3, wd).numpy()[0]
+    np.testing.assert_allclose(out, want, rtol=1e-12, atol=1e-13)
+    assert set(idx.reshape(-1).tolist()) >= {0, 1, 2, 3}  # every slot kind exercised
+    for e in (2, 3):
+        y = oracle.expert_ffn(w13, w2, int(slot[e]) // 2, 0, hb, dense=True)
+        np.testing.assert_allclose(y, _dense_ffn_f64(x, *dsrc[e - 2]).numpy(), rtol=1e-12, atol=1e-13)
+
+
+def test_dense_slot_layout_errors():
+    cfg = synth.MoEConfig("t25", 0, 32, 64, 4, 2, True)
+    rng = np.random.default_rng(34)
+    w13, w2, slot, dense, _ = _mixed_layer(cfg, rng, 1, 2)
+    hb = synth.hidden_bits(cfg, 3, seed=35)
+    logits = synth.router_logits(cfg, 3, seed=36)
+    bad = slot.copy()
+    bad[3] = 5  # position 1 of a dense slot
+    with pytest.raises(ValueError):
+        oracle.moe_forward(w13, w2, bad, hb, logits, 2, True, pair_dense=dense)
+    bad = slot.copy()
+    bad[3] = bad[2]  # two experts in one slot
+    with pytest.raises(ValueError):
+        oracle.moe_forward(w13, w2, bad, hb, logits, 2, True, pair_dense=dense)
+    with pytest.raises(ValueError):
+        oracle.expert_ffn(w13, w2, 1, 1, hb, dense=True)
