@@ -53,6 +53,8 @@ def _load():
             lib.oracle_moe_forward.argtypes = [P, P, P, P, I, I, I, P, P, I64, I, I, I, P, P]
             lib.oracle_expert_ffn.argtypes = [P, P, I, I, I, I, I, P, I64, P]
             lib.oracle_expert_ffn.restype = I
+            lib.oracle_calib_sumsq.argtypes = [P, P, P, I, I, I, P, P, I64, I, I, I, P, P]
+            lib.oracle_calib_sumsq.restype = I
             lib.oracle_num_threads.restype = I
             lib.oracle_set_num_threads.argtypes = [I]
             for name in ("oracle_bf16_round", "oracle_merge", "oracle_pack", "oracle_unpack",
@@ -201,3 +203,25 @@ def expert_ffn(w13, w2, pair: int, pos: int, x_bits, dense: bool = False) -> np.
     if _load().oracle_expert_ffn(_ptr(w13), _ptr(w2), int(pair), int(pos), int(bool(dense)), d, f, _ptr(xb), xb.shape[0], _ptr(y)) != 0:
         raise ValueError("bad expert position")
     return y
+
+
+def calib_sumsq(w13, expert_slot, hidden_bits, logits, k: int, renormalize: bool, pair_dense=None,
+                want_h: bool = True) -> tuple[np.ndarray, np.ndarray | None]:
+    """NEXT-4, Eq. 4 statistics: per slot b, f64 sums of squares per input
+    column of the activations routed to it -- x for W1/W3 ([2P, d]) and the SwiGLU
+    intermediate h for W2 ([2P, f]); ||X||_2 = sqrt of these."""
+    w13 = _c(w13, np.uint16)
+    P, two, f, d = w13.shape
+    slot = _c(expert_slot, np.int32)
+    hb = _c(hidden_bits, np.uint16)
+    lg = _c(logits, np.float32)
+    T, E = lg.shape
+    assert hb.shape == (T, d) and slot.shape == (E,)
+    dense = None if pair_dense is None else _c(pair_dense, np.uint8).reshape(-1)
+    sx = np.empty((2 * P, d), np.float64)
+    sh = np.empty((2 * P, f), np.float64) if want_h else None
+    rc = _load().oracle_calib_sumsq(_ptr(w13), _ptr(slot), _ptr(dense), P, d, f, _ptr(hb), _ptr(lg), T, E, k,
+                                    int(bool(renormalize)), _ptr(sx), _ptr(sh))
+    if rc != 0:
+        raise ValueError(f"oracle_calib_sumsq failed rc={rc}")
+    return sx, sh

@@ -23,6 +23,8 @@
  *   oracle_moe_forward  pinned (self-merge == dense torch f64 FFN, top-1 gate
  *                               == 1, token-permutation equivariance; dense
  *                               slots == torch f64 FFN of the bf16 weights)
+ *   oracle_calib_sumsq  pinned (numpy column norms of the routed rows, torch
+ *                               f64 SwiGLU intermediate, duplicate-token scaling)
  */
 #include <math.h>
 #include <stdint.h>
@@ -296,6 +298,56 @@ int oracle_moe_forward(const uint16_t* w13, const uint16_t* w2, const int32_t* e
     free(y);
   }
   return err;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O6. Calibration statistics for Eq. 4 (NEXT-4): ||X||_2 per input column   */
+/*     over "a sample of input activations to a certain expert",      */
+/*     from "a single forward pass"; per column, unnormalised (R12).  */
+/*     Returned as sums of squares per slot b = expert_slot[e] (the norms are */
+/*     their square roots):                                                   */
+/*       sumsq_x[b][c] = sum over (t, j) routed to b of x_t[c]^2  (W1/W3 in)  */
+/*       sumsq_h[b][r] = sum over (t, j) routed to b of h_t[r]^2  (W2 input), */
+/*       h = silu(W1 x) * (W3 x) of the slot's expert, f64, not rounded (R16).*/
+/*     Serial, f64. Either output may be NULL.                                */
+/* ------------------------------------------------------------------------ */
+int oracle_calib_sumsq(const uint16_t* w13, const int32_t* expert_slot, const uint8_t* pair_dense,
+                       int n_pairs, int d, int f, const uint16_t* hidden, const float* logits,
+                       int64_t T, int E, int k, int renormalize, double* sumsq_x, double* sumsq_h) {
+  if (E < 1 || E > 1024 || E > 2 * n_pairs || k < 1 || k > E || d < 1 || f < 1) return 1;
+  for (int e = 0; e < E; ++e)
+    if (expert_slot[e] < 0 || expert_slot[e] >= 2 * n_pairs) return 1;
+  if (sumsq_x) memset(sumsq_x, 0, sizeof(double) * (size_t)2 * n_pairs * d);
+  if (sumsq_h) memset(sumsq_h, 0, sizeof(double) * (size_t)2 * n_pairs * f);
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  if (!x) return 2;
+  for (int64_t t = 0; t < T; ++t) {
+    int32_t sel[1024];
+    double gate[1024];
+    route_token(logits + t * E, E, k, renormalize, sel, gate);
+    for (int c = 0; c < d; ++c) x[c] = bf16_to_double(hidden[t * d + c]);
+    for (int j = 0; j < k; ++j) {
+      int slot = expert_slot[sel[j]];
+      int pair = slot / 2, pos = slot % 2;
+      int dense = pair_dense ? pair_dense[pair] != 0 : 0;
+      if (sumsq_x)
+        for (int c = 0; c < d; ++c) sumsq_x[(size_t)slot * d + c] += x[c] * x[c];
+      if (!sumsq_h) continue;
+      const uint16_t* W1 = w13 + ((size_t)pair * 2 + 0) * (size_t)f * d;
+      const uint16_t* W3 = w13 + ((size_t)pair * 2 + 1) * (size_t)f * d;
+      for (int r = 0; r < f; ++r) {
+        double g = 0.0, u = 0.0;
+        for (int c = 0; c < d; ++c) {
+          g += slot_weight(W1[(size_t)r * d + c], pos, dense) * x[c];
+          u += slot_weight(W3[(size_t)r * d + c], pos, dense) * x[c];
+        }
+        double h = g / (1.0 + exp(-g)) * u;
+        sumsq_h[(size_t)slot * f + r] += h * h;
+      }
+    }
+  }
+  free(x);
+  return 0;
 }
 
 /* ------------------------------------------------------------------------ */
