@@ -135,12 +135,13 @@ def build_layer_gpu(pz, cfg, seed: int, device, ratio: float = 0.5):
     """Synthetic experts drawn on the GPU (generator G1 statistics) and merged + packed by
     puzzle_merge_experts_pack (Eq. 1-7 + pack, tau = 0.4). ratio 0.5: every pair merged;
     ratio 0.25 (reading R20): the first E/4 pairs merged, the other experts kept as
-    dense bf16 slots (E/4 + E/2 = 3E/4 slots)."""
+    dense bf16 slots (E/4 + E/2 = 3E/4 slots); ratio 1.0: the unmerged model, every expert a
+    dense slot."""
     import torch
     pairs, slot = synth.pairing(cfg, seed)
     w = synth.packed_statistical_torch(cfg, device, seed)
     stats = pz.new_stats(device)
-    n_merged = cfg.n_pairs if ratio == 0.5 else cfg.n_experts // 4
+    n_merged = cfg.n_pairs if ratio == 0.5 else cfg.n_experts // 4 if ratio == 0.25 else 0  # 1.0: unmerged
     packed = {}
     for name, (w_i, w_j, n_i, n_j) in w.items():
         merged = pz.merge_experts_pack(w_i[:n_merged].contiguous(), w_j[:n_merged].contiguous(),
@@ -472,34 +473,102 @@ def run_ours(args):
                 "step_share": kern[dom]["total_ms"] / max(sum(v["total_ms"] for v in kern.values()), 1e-9)}
     step_gbs = (ab["w13"] + ab["w2"]) / (ms / 1e3) / 1e9
 
-    # e2e through the public API with host buffers (pinned), copies inside the timed region
-    h_host = hidden.cpu().pin_memory()
-    l_host = logits.cpu().pin_memory()
-    o_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-    h_dev = torch.empty_like(hidden)
-    l_dev = torch.empty_like(logits)
+    # e2e through the public API with host buffers (pinned), copies inside the timed region.
+    # Single GPU: a serving-style pipeline -- step i's inputs are copied in on a copy stream
+    # while step i-1 computes, and its output is copied out on another while step i+1
+    # computes (two buffer sets; every step still moves its own inputs and output across
+    # PCIe inside the timed region). EP: sequential (host-side split sizes).
+    h_host = [hidden.cpu().pin_memory() for _ in range(2)]
+    l_host = [logits.cpu().pin_memory() for _ in range(2)]
+    o_host = [torch.empty(out.shape, dtype=out.dtype).pin_memory() for _ in range(2)]
+    h_dev = [torch.empty_like(hidden) for _ in range(2)]
+    l_dev = [torch.empty_like(logits) for _ in range(2)]
+    o_dev = [torch.empty_like(out) for _ in range(2)]
+    comp = torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "comp", "out")}
+    e2e_graphs = [None, None]
+    if ep is None and graph is not None:
+        for b in range(2):
+            layer.forward(h_dev[b], l_dev[b], cfg.top_k, cfg.renormalize, out=o_dev[b], workspace=ws)
+            torch.cuda.synchronize()
+            e2e_graphs[b] = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(e2e_graphs[b]):
+                layer.forward(h_dev[b], l_dev[b], cfg.top_k, cfg.renormalize, out=o_dev[b], workspace=ws)
+    it = [0]
 
     def e2e_step():
-        h_dev.copy_(h_host, non_blocking=True)
-        l_dev.copy_(l_host, non_blocking=True)
+        b = it[0] & 1
+        it[0] += 1
         if ep is not None:
-            o_host.copy_(ep.forward(h_dev, l_dev, cfg.top_k, cfg.renormalize), non_blocking=True)
+            h_dev[0].copy_(h_host[0], non_blocking=True)
+            l_dev[0].copy_(l_host[0], non_blocking=True)
+            o_host[0].copy_(ep.forward(h_dev[0], l_dev[0], cfg.top_k, cfg.renormalize), non_blocking=True)
+            return
+        s_in.wait_event(ev["comp"][b])  # buffer set b's previous forward has read its inputs
+        with torch.cuda.stream(s_in):
+            h_dev[b].copy_(h_host[b], non_blocking=True)
+            l_dev[b].copy_(l_host[b], non_blocking=True)
+            ev["in"][b].record(s_in)
+        comp.wait_event(ev["in"][b])
+        comp.wait_event(ev["out"][b])  # o_dev[b] has been copied out
+        if e2e_graphs[b] is not None:
+            e2e_graphs[b].replay()
         else:
-            layer.forward(h_dev, l_dev, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
-            o_host.copy_(out, non_blocking=True)
+            layer.forward(h_dev[b], l_dev[b], cfg.top_k, cfg.renormalize, out=o_dev[b], workspace=ws)
+        ev["comp"][b].record(comp)
+        s_out.wait_event(ev["comp"][b])
+        with torch.cuda.stream(s_out):
+            o_host[b].copy_(o_dev[b], non_blocking=True)
+            ev["out"][b].record(s_out)
 
+    def e2e_drain():
+        for b in range(2):
+            comp.wait_event(ev["out"][b])
+
+    for b in range(2):  # initial state: every event recorded once
+        for k in ev:
+            ev[k][b].record(comp)
     for _ in range(W):
         e2e_step()
+    e2e_drain()
     torch.cuda.synchronize()
-    e2e_ms = timed_steps(e2e_step, K, flush) / K
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if flush is None:
+        e0.record(comp)
+        s_in.wait_event(e0)  # the first copy-in starts after e0
+        for _ in range(K):
+            e2e_step()
+        e2e_drain()  # the last outputs are on the host
+        e1.record(comp)
+        e1.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / K
+    else:  # small layers: L2 flushed between steps, each step timed alone (no overlap)
+        tot = 0.0
+        for _ in range(K):
+            flush()
+            e0.record(comp)
+            s_in.wait_event(e0)
+            e2e_step()
+            e2e_drain()
+            e1.record(comp)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        e2e_ms = tot / K
+    o_ok = bool(torch.equal(o_host[0].view(torch.int16), out.cpu().view(torch.int16))) if ep is None else None
     if world > 1:
         t = torch.tensor([e2e_ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     log("e2e", e2e_ms)
     e2e = {"value": T * world / (e2e_ms / 1e3), "unit": "tokens/s",
-           "h2d_bytes_per_step": h_host.numel() * 2 + l_host.numel() * 4, "d2h_bytes_per_step": o_host.numel() * 2,
-           "ms_per_step": e2e_ms, "api": "PackedMoELayer.forward -> puzzle_moe_forward_ex (host pinned buffers)"}
+           "h2d_bytes_per_step": h_host[0].numel() * 2 + l_host[0].numel() * 4,
+           "d2h_bytes_per_step": o_host[0].numel() * 2, "ms_per_step": e2e_ms,
+           "api": "PackedMoELayer.forward -> puzzle_moe_forward_ex (host pinned buffers)",
+           "pipelined": ep is None and flush is None,
+           "note": "copy-in of step i+1 and copy-out of step i-1 overlap step i's forward (two buffer sets, "
+                   "separate copy streams)" if ep is None and flush is None else "sequential copies",
+           "output_matches_device_run": o_ok}
 
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -526,6 +595,10 @@ def run_ours(args):
                 line["aux"]["unpacked_bf16_baseline"] = {"error": repr(e)}
             line["aux"]["packer"] = packer_rates(pz, layer, device)
             line["aux"]["sweep"] = sweep(pz, args, device, pk)
+            try:
+                line["aux"]["calib"] = calib_run(pz, args, device, pk)
+            except Exception as e:  # pragma: no cover
+                line["aux"]["calib"] = {"error": repr(e)}
             try:
                 del layer
                 torch.cuda.empty_cache()
@@ -632,6 +705,41 @@ def sweep(pz, args, device, pk):
         except Exception as e:  # pragma: no cover
             res.append({"config": name, "batch": T, "ratio": ratio, "error": repr(e)})
     return res
+
+
+def calib_run(pz, args, device, pk, T: int = 4096):
+    """NEXT-4: one calibration batch (T tokens) through the UNMERGED Mixtral layer (8 dense bf16
+    slots) with puzzle_moe_forward_calib: the forward plus the Eq. 4 column statistics of x and
+    h per expert. The statistics kernel is HBM-bound: it reads the bucket-ordered x and h rows
+    once (n_assign * (d + f) * 2 B per step, over its two launches)."""
+    import torch
+    cfg = synth.CONFIGS["mixtral"]
+    layer, _ = build_layer_gpu(pz, cfg, synth.seeds(cfg)["weights"], device, ratio=1.0)
+    hidden, logits = make_inputs(cfg, T, synth.seeds(cfg)["activations"], device)
+    sx = torch.zeros((2 * layer.n_pairs, cfg.d_model), dtype=torch.float64, device=device)
+    sh = torch.zeros((2 * layer.n_pairs, cfg.d_ff), dtype=torch.float64, device=device)
+    step = lambda: layer.forward_calib(hidden, logits, cfg.top_k, cfg.renormalize, sx, sh)
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    K = 10
+    flush_buf = torch.empty(2 * l2_bytes(device), dtype=torch.uint8, device=device)
+    ms = timed_steps(step, K, lambda: flush_buf.zero_()) / K
+    with pz.profile_window() as prof:
+        timed_steps(step, K, lambda: flush_buf.zero_())
+    n_launch, total = prof.kernels.get("calib_colsumsq", (0, 0.0))
+    kern = {k: round(t / n, 5) for k, (n, t) in prof.kernels.items()}
+    n_assign = T * cfg.top_k
+    stat_bytes = n_assign * (cfg.d_model + cfg.d_ff) * 2
+    stat_ms = total / K if n_launch else 0.0  # both launches (x rows, h rows) of one step
+    gbs = stat_bytes / (stat_ms / 1e3) / 1e9 if stat_ms else None
+    out = {"config": "mixtral unmerged (8 dense slots)", "batch": T, "ms_per_step": ms,
+           "tokens_per_s": T / (ms / 1e3), "kernel_avg_ms": kern, "stat_bytes_per_step": stat_bytes,
+           "stat_gbs": gbs, "stat_frac_hbm": gbs / pk["hbm_gbs"] if gbs else None,
+           "norms_finite": bool(torch.isfinite(sx).all().item() and torch.isfinite(sh).all().item())}
+    del layer, flush_buf
+    torch.cuda.empty_cache()
+    return out
 
 
 def stack_runs(pz, args, device, pk):

@@ -222,6 +222,44 @@ int puzzle_gather_rows(const uint16_t* src, const int32_t* index, int64_t n_rows
                        uint16_t* dst, puzzle_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
+ * NEXT-4: calibration statistics for Eq. 4 (reading R12). The Wanda saliency
+ * A = |W| (.) ||X||_2 needs, per expert, the L2 norm of every input column over "a sample of
+ * input activations to a certain expert", gathered in "a single forward pass"
+ * (P:142). Both calls produce f64 SUMS OF SQUARES, ACCUMULATED into the caller's buffers
+ * (zero them first; several calibration batches add up); the norms are their square roots.
+ * Summation is deterministic (no atomics): the same inputs give the same bits every run.
+ *
+ * puzzle_group_colsumsq -- sumsq[g][c] += sum over rows r in [group_off[g], group_off[g+1])
+ *   of rows[r][c]^2.
+ *   rows       bf16 [group_off[n_groups]][cols] (device, 16-byte aligned), cols % 8 == 0
+ *   group_off  i32  [n_groups + 1] (device) non-decreasing row offsets, group_off[0] >= 0
+ *   sumsq      f64  [n_groups][cols] (device, 16-byte aligned), accumulated
+ *   workspace  >= puzzle_group_colsumsq_workspace_size(n_groups, cols) bytes (device)
+ *   Errors: INVALID_ARGUMENT (NULL, negative sizes), UNSUPPORTED (alignment, cols % 8),
+ *   WORKSPACE. n_groups == 0 or cols == 0 is a no-op.
+ *
+ * puzzle_moe_forward_calib -- puzzle_moe_forward_ex (same arguments and output) that also
+ *   accumulates, per bucket b = expert_slot[e] (= 2*pair + pos):
+ *     sumsq_x  f64 [2*n_pairs][d_model]  squares of the x rows routed to b (W1 / W3 input)
+ *     sumsq_h  f64 [2*n_pairs][d_ff]     squares of the bf16 SwiGLU rows silu(W1 x)*(W3 x)
+ *                                        of b's assignments (W2 input; h is rounded to bf16
+ *                                        as in the forward, reading R16)
+ *   Either may be NULL (not both); 16-byte aligned. To calibrate an UNMERGED model, describe
+ *   it as a layer of dense slots (pair_dense = 1, expert_slot[e] = 2e, n_pairs = n_experts):
+ *   bucket 2e then holds expert e's statistics.
+ *   workspace  >= puzzle_moe_calib_workspace_size(L, T, top_k) bytes.
+ * ------------------------------------------------------------------------------------- */
+size_t puzzle_group_colsumsq_workspace_size(int n_groups, int64_t cols);
+int puzzle_group_colsumsq(const uint16_t* rows, const int32_t* group_off, int n_groups, int64_t cols,
+                          double* sumsq, void* workspace, size_t workspace_bytes, puzzle_stream_t stream);
+size_t puzzle_moe_calib_workspace_size(const puzzle_moe_layer* L, int64_t max_tokens, int top_k);
+int puzzle_moe_forward_calib(const puzzle_moe_layer* L, const uint16_t* hidden,
+                             const float* router_logits, int64_t T, int top_k, int renormalize,
+                             const uint16_t* residual, uint16_t* out, double* sumsq_x,
+                             double* sumsq_h, void* workspace, size_t workspace_bytes, int path,
+                             puzzle_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
  * Measurement plumbing (not part of the method). While a profiling window is open, every
  * kernel the library launches is bracketed by CUDA events recorded on the SAME stream the
  * kernel is launched on. puzzle_profile_end() synchronises those events and writes one

@@ -225,3 +225,15 @@ def calib_sumsq(w13, expert_slot, hidden_bits, logits, k: int, renormalize: bool
     if rc != 0:
         raise ValueError(f"oracle_calib_sumsq failed rc={rc}")
     return sx, sh
+
+
+def group_colsumsq(rows_bits, group_off) -> np.ndarray:
+    """NEXT-4 building block, the plain definition: f64 [G, cols] with row g = the column sums
+    of squares of the bf16 rows [group_off[g], group_off[g+1])."""
+    x = bf16_bits_to_f32(_c(rows_bits, np.uint16)).astype(np.float64)
+    off = np.asarray(group_off, np.int64)
+    out = np.zeros((off.size - 1, x.shape[1]), np.float64)
+    for g in range(off.size - 1):
+        for r in range(off[g], off[g + 1]):
+            out[g] += x[r] * x[r]
+    return out

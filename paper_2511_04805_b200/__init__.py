@@ -30,7 +30,8 @@ EXPORTED_SYMBOLS = (
     "puzzle_unpack", "puzzle_merge_experts_pack", "puzzle_moe_workspace_size", "puzzle_moe_forward",
     "puzzle_moe_forward_ex", "puzzle_moe_route", "puzzle_moe_experts_workspace_size",
     "puzzle_moe_experts", "puzzle_moe_combine", "puzzle_gather_rows", "puzzle_profile_begin",
-    "puzzle_profile_end", "puzzle_moe_route_workspace_size",
+    "puzzle_profile_end", "puzzle_moe_route_workspace_size", "puzzle_group_colsumsq_workspace_size",
+    "puzzle_group_colsumsq", "puzzle_moe_calib_workspace_size", "puzzle_moe_forward_calib",
 )
 
 
@@ -83,6 +84,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_moe_experts": ([P, P, P, I64, P, P, SZ, I, P], I),
             "puzzle_moe_combine": ([P, P, P, I64, I, I, P, P, P], I),
             "puzzle_gather_rows": ([P, P, I64, I64, P, P], I),
+            "puzzle_group_colsumsq_workspace_size": ([I, I64], SZ),
+            "puzzle_group_colsumsq": ([P, P, I, I64, P, P, SZ, P], I),
+            "puzzle_moe_calib_workspace_size": ([P, I64, I], SZ),
+            "puzzle_moe_forward_calib": ([P, P, P, I64, I, I, P, P, P, P, P, SZ, I, P], I),
             "puzzle_profile_begin": ([], I),
             "puzzle_profile_end": ([ctypes.c_char_p, SZ], I),
         }
@@ -211,6 +216,24 @@ class PackedMoELayer:
 
     __call__ = forward
 
+    def forward_calib(self, hidden, router_logits, top_k: int, renormalize: bool, sumsq_x=None, sumsq_h=None,
+                      residual=None, out=None, path: int = PATH_AUTO, stream=None) -> torch.Tensor:
+        """puzzle_moe_forward_calib (NEXT-4): the forward, plus f64 per-bucket column sums of
+        squares of x ([2P, d_model]) and of the SwiGLU rows ([2P, d_ff]) ACCUMULATED into
+        sumsq_x / sumsq_h (either may be None)."""
+        T = hidden.shape[0]
+        assert hidden.dtype == torch.bfloat16 and router_logits.dtype == torch.float32
+        for t, cols in ((sumsq_x, self.d_model), (sumsq_h, self.d_ff)):
+            assert t is None or (t.dtype == torch.float64 and tuple(t.shape) == (2 * self.n_pairs, cols))
+        out = torch.empty_like(hidden) if out is None else out
+        need = int(load_library().puzzle_moe_calib_workspace_size(ctypes.byref(self.desc), T, int(top_k)))
+        ws = torch.empty(max(need, 256), dtype=torch.uint8, device=hidden.device)
+        _check(load_library().puzzle_moe_forward_calib(
+            ctypes.byref(self.desc), _p(hidden), _p(router_logits), T, int(top_k), int(bool(renormalize)),
+            _p(residual), _p(out), _p(sumsq_x), _p(sumsq_h), _p(ws), ws.numel(), int(path), _stream(stream)),
+            "puzzle_moe_forward_calib")
+        return out
+
     def route(self, router_logits, top_k: int, renormalize: bool, stream=None):
         """puzzle_moe_route -> (topk_idx, topk_gate, bucket_off, assign_token, assign_of)."""
         return _route(self.desc, self.n_pairs, router_logits, top_k, renormalize, stream)
@@ -295,3 +318,17 @@ class profile_window:
             name, n, ms = line.split()
             self.kernels[name] = (int(n), float(ms))
         return False
+
+
+def group_colsumsq(rows, group_off, sumsq, stream=None) -> torch.Tensor:
+    """puzzle_group_colsumsq (NEXT-4): sumsq[g] += column sums of squares of bf16 rows
+    [group_off[g], group_off[g+1]); sumsq f64 [G, cols] (accumulated, returned)."""
+    rows = _u16(rows)
+    G = group_off.numel() - 1
+    cols = rows.shape[-1]
+    assert group_off.dtype == torch.int32 and sumsq.dtype == torch.float64 and tuple(sumsq.shape) == (G, cols)
+    need = int(load_library().puzzle_group_colsumsq_workspace_size(G, cols))
+    ws = torch.empty(max(need, 256), dtype=torch.uint8, device=rows.device)
+    _check(load_library().puzzle_group_colsumsq(_p(rows), _p(group_off), G, cols, _p(sumsq), _p(ws), ws.numel(),
+                                                _stream(stream)), "puzzle_group_colsumsq")
+    return sumsq

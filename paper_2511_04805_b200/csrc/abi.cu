@@ -37,6 +37,8 @@ int launch_tc2_experts(const uint16_t*, const uint16_t*, int, int, int, const ui
 size_t gemv_tc_part_floats(bool prefill);
 int64_t gemv_tc_counters(int n_rb, int n_pairs, int64_t n_assign);
 bool gemv_supported(int d, int f);
+size_t calib_workspace_bytes(int n_groups, int64_t cols);
+int launch_group_colsumsq(const uint16_t*, const int32_t*, int, int64_t, double*, double*, cudaStream_t);
 int launch_gemv_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
                            const int32_t*,
                            const int32_t*, const int32_t*, int, int64_t, bool, float*, int32_t*, int32_t*,
@@ -361,9 +363,17 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
                                 at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);
 }
 
-int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits,
-                          int64_t T, int k, int renorm, const uint16_t* residual, uint16_t* out,
-                          void* ws, size_t ws_bytes, int path, puzzle_stream_t stream) {
+static size_t calib_bytes(const puzzle_moe_layer* L) {
+  return align_up(std::max(calib_workspace_bytes(2 * L->n_pairs, L->d_model),
+                           calib_workspace_bytes(2 * L->n_pairs, L->d_ff)));
+}
+
+// The forward; with sumsq_x / sumsq_h (NEXT-4) it also accumulates the per-bucket column sums of
+// squares of the bucket-ordered x rows and SwiGLU rows, using `calib` bytes after the layout.
+static int forward_impl(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits,
+                        int64_t T, int k, int renorm, const uint16_t* residual, uint16_t* out,
+                        void* ws, size_t ws_bytes, int path, puzzle_stream_t stream, double* sumsq_x,
+                        double* sumsq_h) {
   if (int rc = check_layer(L)) return rc;
   if (T < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "T < 0");
   if (k < 1 || k > L->n_experts) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "top_k outside [1, n_experts]");
@@ -378,8 +388,10 @@ int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, con
     return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d_model % 256 == 0 and d_ff % 128 == 0");
   const Plan plan = make_plan(L, T, k, path);
   const Layout lay = make_layout(L, plan);
-  if (!ws || ws_bytes < lay.total)
-    return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_moe_workspace_size(L, T, top_k)");
+  const bool calib = sumsq_x || sumsq_h;
+  if (!ws || ws_bytes < lay.total + (calib ? calib_bytes(L) : 0))
+    return fail(PUZZLE_ERR_WORKSPACE, calib ? "workspace smaller than puzzle_moe_calib_workspace_size(L, T, top_k)"
+                                            : "workspace smaller than puzzle_moe_workspace_size(L, T, top_k)");
   cudaStream_t s = (cudaStream_t)stream;
   bool rows_written = false;
   int rc;
@@ -406,8 +418,54 @@ int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, con
                    rows_written ? nullptr : at<int32_t>(ws, lay.assign_token), at<int32_t>(ws, lay.bucket_off),
                    at<int32_t>(ws, lay.active), at<int32_t>(ws, lay.n_active), at<float>(ws, lay.y), s);
   if (rc) return rc;
+  // x_perm and h now hold the bucket-ordered x rows and SwiGLU rows of every assignment
+  if (sumsq_x && (rc = launch_group_colsumsq(at<uint16_t>(ws, lay.x_perm), at<int32_t>(ws, lay.bucket_off),
+                                             2 * L->n_pairs, L->d_model, sumsq_x, at<double>(ws, lay.total), s)))
+    return rc;
+  if (sumsq_h && (rc = launch_group_colsumsq(at<uint16_t>(ws, lay.h), at<int32_t>(ws, lay.bucket_off),
+                                             2 * L->n_pairs, L->d_ff, sumsq_h, at<double>(ws, lay.total), s)))
+    return rc;
   return launch_combine(at<float>(ws, lay.y), at<int32_t>(ws, lay.assign_of), at<float>(ws, lay.topk_gate),
                         T, k, L->d_model, residual, out, s);
+}
+
+int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits,
+                          int64_t T, int k, int renorm, const uint16_t* residual, uint16_t* out,
+                          void* ws, size_t ws_bytes, int path, puzzle_stream_t stream) {
+  return forward_impl(L, hidden, logits, T, k, renorm, residual, out, ws, ws_bytes, path, stream, nullptr, nullptr);
+}
+
+size_t puzzle_moe_calib_workspace_size(const puzzle_moe_layer* L, int64_t max_tokens, int top_k) {
+  const size_t base = puzzle_moe_workspace_size(L, max_tokens, top_k);
+  return base ? base + calib_bytes(L) : 0;
+}
+
+int puzzle_moe_forward_calib(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits,
+                             int64_t T, int k, int renorm, const uint16_t* residual, uint16_t* out,
+                             double* sumsq_x, double* sumsq_h, void* ws, size_t ws_bytes, int path,
+                             puzzle_stream_t stream) {
+  if (!sumsq_x && !sumsq_h) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "sumsq_x and sumsq_h both NULL");
+  if ((sumsq_x && (reinterpret_cast<uintptr_t>(sumsq_x) & 15u)) || (sumsq_h && (reinterpret_cast<uintptr_t>(sumsq_h) & 15u)))
+    return fail(PUZZLE_ERR_UNSUPPORTED, "sumsq outputs must be 16-byte aligned");
+  return forward_impl(L, hidden, logits, T, k, renorm, residual, out, ws, ws_bytes, path, stream, sumsq_x, sumsq_h);
+}
+
+size_t puzzle_group_colsumsq_workspace_size(int n_groups, int64_t cols) {
+  if (n_groups < 0 || cols < 0) return 0;
+  return calib_workspace_bytes(n_groups, cols);
+}
+
+int puzzle_group_colsumsq(const uint16_t* rows, const int32_t* group_off, int n_groups, int64_t cols,
+                          double* sumsq, void* ws, size_t ws_bytes, puzzle_stream_t stream) {
+  if (n_groups < 0 || cols < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "negative sizes");
+  if (n_groups == 0 || cols == 0) return PUZZLE_OK;
+  if (!rows || !group_off || !sumsq) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (cols % 8 || !al16(rows) || (reinterpret_cast<uintptr_t>(sumsq) & 15u))
+    return fail(PUZZLE_ERR_UNSUPPORTED, "cols % 8 == 0 and 16-byte aligned rows / sums required");
+  if (int rc = check_device()) return rc;
+  if (!ws || ws_bytes < calib_workspace_bytes(n_groups, cols) || (reinterpret_cast<uintptr_t>(ws) & 15u))
+    return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_group_colsumsq_workspace_size");
+  return launch_group_colsumsq(rows, group_off, n_groups, cols, sumsq, static_cast<double*>(ws), (cudaStream_t)stream);
 }
 
 int puzzle_moe_forward(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits, int64_t T,

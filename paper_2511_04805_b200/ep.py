@@ -73,6 +73,14 @@ def shard_packed(w13: torch.Tensor, w2: torch.Tensor, part: Partition, rank: int
     return w13_l, w2_l
 
 
+def shard_dense(pair_dense: torch.Tensor | None, part: Partition, rank: int):
+    """This rank's slice of the dense-slot flags (25% ratio, reading R20); None stays None."""
+    if pair_dense is None:
+        return None
+    p0, p1 = part.pairs_of(rank)
+    return pair_dense[p0:p1].contiguous()
+
+
 class CudaOps:
     """Device ops of the EP data path: libpuzzlemoe kernels."""
 

@@ -16,7 +16,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from helpers import oracle_packed_layer
+from helpers import oracle_mixed_layer, oracle_packed_layer
 
 
 class OracleOps:
@@ -40,13 +40,14 @@ class OracleOps:
         return src[index.long()]
 
     def experts(self, local_layer, x_rows, bucket_off):
-        w13, w2 = local_layer
+        w13, w2, dense = local_layer
         off = bucket_off.numpy()
         bits = x_rows.contiguous().view(torch.int16).numpy().view(np.uint16)
         y = np.zeros((x_rows.shape[0], w13.shape[3]), np.float32)
         for b in range(len(off) - 1):
             if off[b + 1] > off[b]:
-                y[off[b]:off[b + 1]] = oracle.expert_ffn(w13, w2, b // 2, b % 2, bits[off[b]:off[b + 1]])
+                y[off[b]:off[b + 1]] = oracle.expert_ffn(w13, w2, b // 2, b % 2, bits[off[b]:off[b + 1]],
+                                                         dense=dense is not None and bool(dense[b // 2]))
         return torch.from_numpy(y)
 
     def combine(self, y, assign_of, gate, residual):
@@ -57,18 +58,25 @@ class OracleOps:
         return out
 
 
-def _worker(rank, world, port, cfg_fields, T, outdir):
+def _worker(rank, world, port, cfg_fields, T, outdir, n_merged=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_packed
+        from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_dense, shard_packed
         cfg = synth.MoEConfig(*cfg_fields)
-        w13, w2, slot, _ = oracle_packed_layer(cfg)
-        part = Partition(cfg.n_pairs, world)
+        if n_merged is None:
+            w13, w2, slot, _ = oracle_packed_layer(cfg)
+            dense = None
+        else:  # 25% ratio: merged pairs + dense slots (R20)
+            w13, w2, slot, dense = oracle_mixed_layer(cfg, n_merged)
+        n_slots = w13.shape[0]
+        part = Partition(n_slots, world)
         w13_l, w2_l = shard_packed(torch.from_numpy(w13.view(np.int16)), torch.from_numpy(w2.view(np.int16)), part, rank)
-        local = (w13_l.numpy().view(np.uint16), w2_l.numpy().view(np.uint16))
-        layer = ExpertParallelMoE(part, rank, {"expert_slot": slot, "n_pairs": cfg.n_pairs}, local, cfg.d_model,
+        dense_l = shard_dense(None if dense is None else torch.from_numpy(dense), part, rank)
+        local = (w13_l.numpy().view(np.uint16), w2_l.numpy().view(np.uint16),
+                 None if dense_l is None else dense_l.numpy())
+        layer = ExpertParallelMoE(part, rank, {"expert_slot": slot, "n_pairs": n_slots}, local, cfg.d_model,
                                   ops=OracleOps())
         hb = synth.hidden_bits(cfg, T, seed=100 + rank)
         lg = synth.router_logits(cfg, T, seed=200 + rank)
@@ -76,7 +84,7 @@ def _worker(rank, world, port, cfg_fields, T, outdir):
         hidden = torch.from_numpy(hb.view(np.int16)).view(torch.bfloat16)
         resid = torch.from_numpy(oracle.bf16_bits_to_f32(rb))
         out = layer.forward(hidden, torch.from_numpy(lg), cfg.top_k, cfg.renormalize, residual=resid)
-        ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, rb)
+        ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, rb, pair_dense=dense)
         np.save(os.path.join(outdir, f"out{rank}.npy"), out.numpy())
         np.save(os.path.join(outdir, f"ref{rank}.npy"), ref)
     finally:
@@ -96,8 +104,20 @@ def _free_port():
     (("ep1k2", 23, 64, 128, 2, 2, True), 4),    # both experts of the one pair, d_ff split
 ])
 def test_ep_world2_matches_oracle(cfg_fields, T):
+    _run_world2(cfg_fields, T, None)
+
+
+@pytest.mark.parametrize("cfg_fields,T,n_merged", [
+    (("ep25", 24, 64, 128, 8, 2, True), 9, 2),   # 2 merged pairs + 4 dense slots over 2 ranks
+    (("ep25s", 25, 64, 128, 2, 1, True), 6, 0),  # 2 dense slots, one per rank
+])
+def test_ep_world2_dense_slots_match_oracle(cfg_fields, T, n_merged):
+    _run_world2(cfg_fields, T, n_merged)
+
+
+def _run_world2(cfg_fields, T, n_merged):
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(2, _free_port(), cfg_fields, T, d), nprocs=2, join=True)
+        mp.spawn(_worker, args=(2, _free_port(), cfg_fields, T, d, n_merged), nprocs=2, join=True)
         for r in range(2):
             out = np.load(os.path.join(d, f"out{r}.npy"))
             ref = np.load(os.path.join(d, f"ref{r}.npy"))

@@ -65,3 +65,9 @@ def test_matches_routed_rows_and_torch_swiglu():
         xt = torch.from_numpy(x[rows])
         h = torch.nn.functional.silu(xt @ torch.from_numpy(w1).double().T) * (xt @ torch.from_numpy(w3).double().T)
         np.testing.assert_allclose(sh[b], (h ** 2).sum(0).numpy(), rtol=1e-11, atol=1e-300)
+
+
+def test_group_colsumsq_worked_case():
+    rows = synth.to_bf16_bits(np.array([[1.0, 2.0], [3.0, -1.0], [0.5, 0.0], [-2.0, 4.0]], np.float32))
+    out = oracle.group_colsumsq(rows, [0, 2, 2, 4])  # groups: rows 0-1, empty, rows 2-3
+    assert out.tolist() == [[10.0, 5.0], [0.0, 0.0], [4.25, 16.0]]
