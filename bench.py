@@ -371,7 +371,7 @@ def run_ours(args):
     T, K, W = args.batch, args.steps, args.warmup
     seed = synth.seeds(cfg)["weights"]
     log("building layer", cfg.name)
-    layer, pack_stats = build_layer_gpu(pz, cfg, seed, device)
+    layer, pack_stats = build_layer_gpu(pz, cfg, seed, device, args.ratio)
     log("layer built", layer.packed_bytes)
     hidden, logits = make_inputs(cfg, T, seed + 100 * rank + 2, device)
     out = torch.empty_like(hidden)
@@ -380,11 +380,12 @@ def run_ours(args):
     ep = None
     if world > 1:
         # expert parallelism: this rank keeps only its pairs (or d_ff slice) of the layer
-        from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_packed
-        part = Partition(cfg.n_pairs, world)
+        from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_dense, shard_packed
+        part = Partition(layer.n_pairs, world)
         w13_l, w2_l = shard_packed(layer.w13, layer.w2, part, rank)
-        local = pz.PackedMoELayer(w13_l, w2_l, torch.arange(2 * w13_l.shape[0], dtype=torch.int32, device=device))
-        routing = pz.RoutingLayer(cfg.n_pairs, cfg.d_model, cfg.d_ff, layer.expert_slot, w13_l)
+        local = pz.PackedMoELayer(w13_l, w2_l, torch.arange(2 * w13_l.shape[0], dtype=torch.int32, device=device),
+                                  shard_dense(layer.pair_dense, part, rank))
+        routing = pz.RoutingLayer(layer.n_pairs, cfg.d_model, cfg.d_ff, layer.expert_slot, w13_l)
         ep = ExpertParallelMoE(part, rank, routing, local, cfg.d_model)
 
     def step():
@@ -574,6 +575,7 @@ def run_ours(args):
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded N(0,1/in) experts merged+packed on GPU, tau=0.4; N(0,1) hidden and logits)",
             "config": {"workload": f"{cfg.name} single MoE layer decode, batch {T} per GPU"
+                                   + (" (25% ratio: merged pairs + dense bf16 slots)" if args.ratio == 0.25 else "")
                                    + (" (BASELINE.json configs[1])" if cfg.name == "mixtral" else ""),
                        "d_model": cfg.d_model, "d_ff": cfg.d_ff, "n_experts": cfg.n_experts,
                        "n_pairs": cfg.n_pairs, "top_k": cfg.top_k, "batch_per_gpu": T,
@@ -807,6 +809,9 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(synth.CONFIGS), default="mixtral")
     ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--ratio", type=float, choices=[0.5, 0.25], default=0.5,
+                    help="compression ratio of the timed layer: 0.5 (all pairs merged, the headline) or "
+                         "0.25 (merged pairs + dense bf16 slots, R20)")
     ap.add_argument("--no-extra", action="store_true", help="skip the unpacked baseline / sweep / packer lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")

@@ -17,7 +17,13 @@ namespace {
 
 constexpr int kColsPerCta = 512;  // 64 column threads x 8 bf16
 constexpr int kRowLanes = 4;
-constexpr int kUnroll = 8;
+#ifndef PZ_CALIB_UNROLL
+#define PZ_CALIB_UNROLL 8
+#endif
+#ifndef PZ_CALIB_MINB  // resident CTAs per SM the register allocation must allow
+#define PZ_CALIB_MINB 3
+#endif
+constexpr int kUnroll = PZ_CALIB_UNROLL;
 constexpr int kCalibThreads = 64 * kRowLanes;
 #ifndef PZ_CALIB_CTAS  // target CTAs per SM of the grid
 #define PZ_CALIB_CTAS 3
@@ -37,7 +43,7 @@ __device__ __forceinline__ int split_of(int64_t base, int64_t n, int S, int64_t 
 // reduced (4 row lanes, fixed order) and written to part[split][group]. Every thread sums its
 // kUnroll rows in f32 (the square of a bf16 value is exact in f32; 8 terms lose <= 2^-21
 // relative) and adds that to its f64 accumulators.
-__global__ void __launch_bounds__(kCalibThreads) k_group_colsumsq_part(const uint16_t* __restrict__ rows,
+__global__ void __launch_bounds__(kCalibThreads, PZ_CALIB_MINB) k_group_colsumsq_part(const uint16_t* __restrict__ rows,
                                                                        const int32_t* __restrict__ group_off,
                                                                        int n_groups, int64_t cols, int splits,
                                                                        double* __restrict__ part) {

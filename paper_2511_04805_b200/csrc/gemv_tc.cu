@@ -48,6 +48,9 @@ constexpr int kWBytes = kRows * kBK * 2;         // 16 KB packed words per stage
 #ifndef PZ_TC_DEFER  // decoders drain a pass's accumulators after two stages of the next pass
 #define PZ_TC_DEFER 0
 #endif
+#ifndef PZ_TC_ORMAG  // 1: |W^| * 2^48 with one LOP3 (exponent offset ORed in), accumulators x 2^15
+#define PZ_TC_ORMAG 1
+#endif
 #ifndef PZ_TC_WST  // W ring depth of the decode configuration (tuning knob)
 #define PZ_TC_WST 4
 #endif
@@ -261,11 +264,17 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST>& c, uint32_t smem_w, u
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t x = comp(v[i], j);
+#if PZ_TC_ORMAG
+        // |W^| * 2^48: exponent field e' + 160 = e' | 0xA0 (e' < 32: no carry), ONE LOP3; the
+        // 2^-63 of the sign/mask factor leaves W^ * 2^-15, undone (exactly) in the epilogue
+        const uint32_t mag = (x & 0x0FFF0FFFu) | 0x50005000u;
+#else
         // |W^| * 2^63: exponent field e' + 112 + 63 (never carries out of a lane)
         const uint32_t mag = imad(x & 0x0FFF0FFFu, mu.one, 0x57805780u);
+#endif
         // sign S_i (bit 15) + mask M_i (bit 13) = +-2^-63 or +-0 as bf16: one exact product
         if (MODE & 1) d0[4 * i + j] = bf16x2_mul(mag, x & 0xA000A000u);
-        if (MODE & 4) d0[4 * i + j] = x;
+        if (MODE & 4) d0[4 * i + j] = PZ_TC_ORMAG ? bf16x2_mul(x, 0x38003800u) : x;  // x 2^-15 (exact)
         // S_j (bit 14) and M_j (bit 12) shifted to bits 15 / 13
         if (MODE & 2) d1[4 * i + j] = bf16x2_mul(mag, imul(x, mu.two) & 0xA000A000u);
       }
@@ -560,10 +569,14 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       const int offp = (pos ? s.pt.off1 : s.pt.off0) + s.base;  // first assignment of this warp
       float* slot = part + (size_t)(2 * g + (s.item == first_item ? 0 : 1)) * kSlot;
       const uint32_t acc_t = lane_tmem + kAccCol + (uint32_t)NX * pos;
+      // the A operand is W^ * 2^-15 (PZ_TC_ORMAG; dense slots scaled to match): scale back, exact
+      constexpr float acc_scale = PZ_TC_ORMAG ? 32768.0f : 1.0f;
       for (int c0 = 0; c0 < np; c0 += 16) {
         uint32_t r[16];
         ptx::tmem_ld_32x32b_x16(acc_t + c0, r);
         ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * acc_scale);
         if (!whole) {
           const int t0 = pos * NX + c0;  // (position, token of the pass)
 #pragma unroll

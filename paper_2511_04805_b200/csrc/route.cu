@@ -227,8 +227,10 @@ __global__ void __launch_bounds__(64) k_route_scan(const int32_t* __restrict__ g
 }
 
 // Each CTA reserves slot ranges for its chunk of assignments (one atomic per bucket), then its
-// warps copy the assignments' token rows to their slots (fused gather into bucket order).
-constexpr int kScatterChunk = kBigThreads;
+// warps copy the assignments' token rows to their slots (fused gather into bucket order). 32
+// assignments per CTA: the copy (the bulk of the bytes) is spread over >= 2 CTAs per SM at
+// prefill sizes, 4 rows per warp with 4 x 16 B loads in flight per lane.
+constexpr int kScatterChunk = 32;
 __global__ void __launch_bounds__(kBigThreads) k_route_scatter(
     const int32_t* __restrict__ topk_idx, int64_t n_assign, int k, const int32_t* __restrict__ expert_slot,
     int n_buckets, int32_t* __restrict__ cursor, int32_t* __restrict__ assign_token,
@@ -260,11 +262,21 @@ __global__ void __launch_bounds__(kBigThreads) k_route_scatter(
   __syncthreads();
   if (x_perm == nullptr) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n16 = d / 8;  // 16-byte chunks per row
   for (int j = warp; j < n; j += kBigThreads / 32) {
     const int64_t t = (i0 + j) / k;
     const uint4* src = reinterpret_cast<const uint4*>(hidden + t * d);
     uint4* dst = reinterpret_cast<uint4*>(x_perm + (int64_t)s_slotof[j] * d);
-    for (int c = lane; c < d / 8; c += 32) dst[c] = src[c];
+    int c = lane;
+    for (; c + 96 < n16; c += 128) {
+      const uint4 v0 = ldg_nc_v4(src + c), v1 = ldg_nc_v4(src + c + 32), v2 = ldg_nc_v4(src + c + 64),
+                  v3 = ldg_nc_v4(src + c + 96);
+      dst[c] = v0;
+      dst[c + 32] = v1;
+      dst[c + 64] = v2;
+      dst[c + 96] = v3;
+    }
+    for (; c < n16; c += 32) dst[c] = src[c];
   }
 }
 
