@@ -132,24 +132,32 @@ __device__ __forceinline__ uint32_t bf16x2_mul_tc(uint32_t a, uint32_t b) {
   asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
   return r;
 }
+#ifndef PZ_TC_ORMAG  // 1: |W^| x 2^48 by ORing the exponent offset (one LOP3), tiles hold W^ x 2^-15,
+#define PZ_TC_ORMAG 1  //    the epilogue scales packed tiles' accumulators by 2^15 (exact)
+#endif
 template <int POS>
-__device__ __forceinline__ uint32_t dec_word(uint32_t w, uint32_t one, uint32_t two) {
+__device__ __forceinline__ uint32_t dec_word(uint32_t w, uint32_t one, uint32_t two, uint32_t orc) {
+#if PZ_TC_ORMAG
+  const uint32_t mag = (w & 0x0FFF0FFFu) | orc;  // exponent e' + 160 = e' | 0xA0 (e' < 32)
+#else
+  (void)orc;
   const uint32_t mag = imad(w & 0x0FFF0FFFu, one, 0x57805780u);
+#endif
   return bf16x2_mul_tc(mag, (POS == 0 ? w : imul(w, two)) & 0xA000A000u);
 }
 template <int POS>
 __device__ __forceinline__ void decode_tile(uint32_t b_tile, int tid, uint32_t one) {
-  const uint32_t two = one * 2u;
+  const uint32_t two = one * 2u, orc = one * 0x50005000u;  // orc: a register operand for the LOP3
   constexpr int kPer = kBBytes / 16 / (kDecodeWarps * 32);  // uint4 per thread per stage
   uint4 v[kPer];
 #pragma unroll
   for (int j = 0; j < kPer; ++j) v[j] = lds128(b_tile + (uint32_t)(tid + j * kDecodeWarps * 32) * 16u);
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
-    v[j].x = dec_word<POS>(v[j].x, one, two);
-    v[j].y = dec_word<POS>(v[j].y, one, two);
-    v[j].z = dec_word<POS>(v[j].z, one, two);
-    v[j].w = dec_word<POS>(v[j].w, one, two);
+    v[j].x = dec_word<POS>(v[j].x, one, two, orc);
+    v[j].y = dec_word<POS>(v[j].y, one, two, orc);
+    v[j].z = dec_word<POS>(v[j].z, one, two, orc);
+    v[j].w = dec_word<POS>(v[j].w, one, two, orc);
   }
 #pragma unroll
   for (int j = 0; j < kPer; ++j) sts128(b_tile + (uint32_t)(tid + j * kDecodeWarps * 32) * 16u, v[j]);
@@ -308,6 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
       if (threadIdx.x == 64) PZ_TT(3, tiles_done);
       ptx::mbar_wait(&c.tmem_full, acc_phase);
       ptx::tc_fence_after();
+      // packed tiles were decoded as W^ x 2^-15 (PZ_TC_ORMAG): exact rescale; dense slots as stored
+      const float sc = (PZ_TC_ORMAG && !c.dense[e.bucket >> 1]) ? 32768.0f : 1.0f;
       for (int half = 0; half < 2; ++half) {
         const int m = half * 128 + q * 32 + lane;  // token row within the tile
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + half * 256;
@@ -324,8 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
                 uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                  const float h0 = silu_mul(__uint_as_float(g[2 * i]), __uint_as_float(u[2 * i]));
-                  const float h1 = silu_mul(__uint_as_float(g[2 * i + 1]), __uint_as_float(u[2 * i + 1]));
+                  const float h0 = silu_mul(__uint_as_float(g[2 * i]) * sc, __uint_as_float(u[2 * i]) * sc);
+                  const float h1 = silu_mul(__uint_as_float(g[2 * i + 1]) * sc, __uint_as_float(u[2 * i + 1]) * sc);
                   pk[i] = f32_to_bf16_rne_bits(h0) | (f32_to_bf16_rne_bits(h1) << 16);
                 }
                 uint4* dst = reinterpret_cast<uint4*>(h_out + a * f + e.n_block * (BN / 2) + j);
@@ -340,6 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_experts(
               ptx::tmem_ld_wait();
               if (ok) {
                 uint4* dst = reinterpret_cast<uint4*>(y_out + a * d + e.n_block * BN + j);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
               }

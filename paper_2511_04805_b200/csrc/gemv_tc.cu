@@ -156,6 +156,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 
 struct Muls {
   uint32_t one, two, four, eight;
+  uint32_t orc;  // 0x50005000 in a register: LOP3 takes one immediate, the mask is the other
 };
 
 __device__ __forceinline__ uint32_t comp(const uint4& v, int j) { return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w; }
@@ -267,7 +268,7 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST>& c, uint32_t smem_w, u
 #if PZ_TC_ORMAG
         // |W^| * 2^48: exponent field e' + 160 = e' | 0xA0 (e' < 32: no carry), ONE LOP3; the
         // 2^-63 of the sign/mask factor leaves W^ * 2^-15, undone (exactly) in the epilogue
-        const uint32_t mag = (x & 0x0FFF0FFFu) | 0x50005000u;
+        const uint32_t mag = (x & 0x0FFF0FFFu) | mu.orc;
 #else
         // |W^| * 2^63: exponent field e' + 112 + 63 (never carries out of a lane)
         const uint32_t mag = imad(x & 0x0FFF0FFFu, mu.one, 0x57805780u);
@@ -550,7 +551,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     // partial-slot row of this thread: w13 g rows 0-63 / u rows 64-127 by feature, w2 the tile row
     const int prow = kW13 ? (lane < 16 ? 16 * q + lane : 64 + 16 * q + lane - 16) : row;
     const uint32_t lane_tmem = tmem + ((uint32_t)(32 * q) << 16);
-    const Muls mu{mul_one, mul_one * 2u, mul_one * 4u, mul_one * 8u};
+    const Muls mu{mul_one, mul_one * 2u, mul_one * 4u, mul_one * 8u, mul_one * 0x50005000u};
     uint32_t w_off[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) w_off[i] = swz(srow, 4 * kh + i);
