@@ -211,7 +211,8 @@ int puzzle_moe_experts(const puzzle_moe_layer* L, const uint16_t* x_rows,
                        puzzle_stream_t stream);
 
 /* puzzle_moe_combine -- (a6): out[t] = residual[t] + sum_{j<k} topk_gate[t,j] * y_rows[assign_of[t,j]]
- *   summed in fp32 in slot order j, rounded once to bf16. residual may be NULL. */
+ *   summed in fp32 in slot order j, rounded once to bf16. residual may be NULL.
+ *   Errors: INVALID_ARGUMENT (T < 0, k < 1, d % 4, NULL). */
 int puzzle_moe_combine(const float* y_rows, const int32_t* assign_of, const float* topk_gate,
                        int64_t T, int top_k, int d_model, const uint16_t* residual,
                        uint16_t* out, puzzle_stream_t stream);

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_route_small(
 
 // ------------------------------------------------------------ large batches: three grids
 constexpr int kBigThreads = 256;
-constexpr int kTokensPerWarp = 4;
+constexpr int kTokensPerWarp = 1;  // T = 4096: 512 CTAs (the rank selection is latency-bound per warp)
 
 // top-k per token + per-CTA histogram folded into the global bucket counts
 template <int PER>
