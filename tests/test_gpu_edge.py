@@ -112,3 +112,31 @@ def test_router_512_experts(pz, T):
     np.testing.assert_allclose(gate.cpu().numpy(), want_gate, rtol=2e-6, atol=1e-8)
     counts = np.bincount(synth.pairing(cfg)[1][want_idx.reshape(-1)], minlength=2 * P)
     assert np.array_equal(np.diff(off.cpu().numpy()), counts)
+
+
+@pytest.mark.parametrize("name,T", [("mixtral", 64), ("mixtral", 4096), ("qwen15", 64)])
+def test_graph_replay_matches_eager_full_size(pz, name, T):
+    """bench.py times CUDA-graph replays of the whole forward at the BASELINE sizes: a replay
+    must reproduce the eager call (bit for bit on the deterministic decode path), and sampled
+    rows must match the oracle (oracle-packed weights, seeded inputs)."""
+    cfg = synth.CONFIGS[name]
+    layer, w13, w2, slot = _layer(pz, cfg)
+    hb = synth.hidden_bits(cfg, T, seed=460)
+    lg = synth.router_logits(cfg, T, seed=461)
+    hidden, logits = _dev_bits(hb), torch.from_numpy(lg).cuda()
+    ws = layer.workspace(T, cfg.top_k)
+    eager = layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, workspace=ws).clone()
+    out = torch.empty_like(hidden)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    if T <= 64:
+        assert torch.equal(out.view(torch.int16), eager.view(torch.int16))
+    else:  # prefill: the in-bucket order (R18) may move a row between tiles; same math
+        assert (out.float() - eager.float()).abs().max().item() <= 2e-2
+    rows = np.sort(np.random.default_rng(5).choice(T, 4, replace=False))
+    ref = oracle.moe_forward(w13, w2, slot, hb[rows], lg[rows], cfg.top_k, cfg.renormalize)
+    assert_close(out.float().cpu().numpy()[rows], ref, f"graph {name} T={T}")
