@@ -378,11 +378,15 @@ __global__ void __launch_bounds__(kDecThreads) k_route_dec_scatter(
 }
 
 // out[t] = residual[t] + sum_j gate[t,j] * y[assign_of[t,j]], fp32 in slot order, one bf16 rounding.
+// K > 0: top-k known at compile time (the common 1 / 2 / 4 / 6 / 8), so the k row loads are
+// issued back to back; K = 0: any k.
+template <int K>
 __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y,
                                                  const int32_t* __restrict__ assign_of,
-                                                 const float* __restrict__ gate, int k, int d,
+                                                 const float* __restrict__ gate, int k_rt, int d,
                                                  const uint16_t* __restrict__ residual,
                                                  uint16_t* __restrict__ out) {
+  const int k = K > 0 ? K : k_rt;
   const int64_t t = blockIdx.y;
   const int c4 = blockIdx.x * blockDim.x + threadIdx.x;  // index of a 4-column group
   pdl_wait();
@@ -395,6 +399,7 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y,
     acc = make_float4(bf16_bits_to_f32(r.x & 0xFFFFu), bf16_bits_to_f32(r.x >> 16),
                       bf16_bits_to_f32(r.y & 0xFFFFu), bf16_bits_to_f32(r.y >> 16));
   }
+#pragma unroll
   for (int j = 0; j < k; ++j) {
     const float g = gate[t * k + j];
     const float4 v = *reinterpret_cast<const float4*>(y + (int64_t)assign_of[t * k + j] * d + c4 * 4);
@@ -578,7 +583,9 @@ int launch_combine(const float* y, const int32_t* assign_of, const float* gate, 
   dim3 grid((unsigned)((d / 4 + threads - 1) / threads), (unsigned)T);
   {
     ProfScope _ps("combine", stream);
-    cudaError_t e = launch_pdl(k_combine, grid, dim3(threads), 0, stream, y, assign_of, gate, k, d, residual, out);
+    auto kern = k == 1 ? k_combine<1> : k == 2 ? k_combine<2> : k == 4 ? k_combine<4> : k == 6 ? k_combine<6>
+              : k == 8 ? k_combine<8> : k_combine<0>;
+    cudaError_t e = launch_pdl(kern, grid, dim3(threads), 0, stream, y, assign_of, gate, k, d, residual, out);
     if (e != cudaSuccess) return cuda_check(e, "combine launch");
   }
   return cuda_check(cudaGetLastError(), "combine launch");
