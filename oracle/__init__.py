@@ -54,6 +54,10 @@ def _load():
             lib.oracle_expert_ffn.argtypes = [P, P, I, I, I, I, I, P, I64, P]
             lib.oracle_expert_ffn.restype = I
             lib.oracle_calib_sumsq.argtypes = [P, P, P, I, I, I, P, P, I64, I, I, I, P, P]
+            lib.oracle_quant_pack.argtypes = [P, P, P, P, P, I64, I64, P, P]
+            lib.oracle_quant_pack.restype = I
+            lib.oracle_quant_unpack.argtypes = [P, P, I, I64, I64, P]
+            lib.oracle_quant_unpack.restype = I
             lib.oracle_calib_sumsq.restype = I
             lib.oracle_num_threads.restype = I
             lib.oracle_set_num_threads.argtypes = [I]
@@ -236,4 +240,29 @@ def group_colsumsq(rows_bits, group_off) -> np.ndarray:
     for g in range(off.size - 1):
         for r in range(off[g], off[g + 1]):
             out[g] += x[r] * x[r]
+    return out
+
+
+def quant_pack(w_merged, m0, m1, s0, s1) -> tuple[np.ndarray, np.ndarray]:
+    """NEXT-3 (Appendix A.3; readings R21-R23): merged magnitudes [rows, cols]
+    (cols % 128 == 0) + bit-planes -> codes u8 [rows, cols] (S_i S_j M_i M_j 0 q2 q1 q0) and
+    f32 scales [rows, cols / 128] (max / 7 per group of 128, 1 for an all-zero group)."""
+    w = _c(w_merged, np.float32)
+    rows, cols = w.shape
+    planes = [_c(p, np.uint8) for p in (m0, m1, s0, s1)]
+    codes = np.empty((rows, cols), np.uint8)
+    scales = np.empty((rows, cols // 128), np.float32)
+    if _load().oracle_quant_pack(_ptr(w), *[_ptr(p) for p in planes], rows, cols, _ptr(codes), _ptr(scales)) != 0:
+        raise ValueError("quant_pack: cols must be a multiple of 128")
+    return codes, scales
+
+
+def quant_unpack(codes, scales, pos: int) -> np.ndarray:
+    """Dequantised bf16 bits of expert `pos`: (-1)^S * M * bf16_rne(code * scale)."""
+    codes = _c(codes, np.uint8)
+    scales = _c(scales, np.float32)
+    rows, cols = codes.shape
+    out = np.empty((rows, cols), np.uint16)
+    if _load().oracle_quant_unpack(_ptr(codes), _ptr(scales), int(pos), rows, cols, _ptr(out)) != 0:
+        raise ValueError("quant_unpack: bad position or shape")
     return out

@@ -23,6 +23,9 @@
  *   oracle_moe_forward  pinned (self-merge == dense torch f64 FFN, top-1 gate
  *                               == 1, token-permutation equivariance; dense
  *                               slots == torch f64 FFN of the bf16 weights)
+ *   oracle_quant_pack / oracle_quant_unpack  pinned (SPEC worked example
+ *                               S:478, all-zero group, round-trip bound, masks
+ *                               exactly zero, byte layout)
  *   oracle_calib_sumsq  pinned (numpy column norms of the routed rows, torch
  *                               f64 SwiGLU intermediate, duplicate-token scaling)
  */
@@ -175,6 +178,63 @@ static uint16_t decode_word(uint16_t W, int expert_pos) {
 int oracle_unpack(const uint16_t* packed, int pos, int64_t n, uint16_t* out) {
   if (pos != 0 && pos != 1) return 1;
   for (int64_t x = 0; x < n; ++x) out[x] = decode_word(packed[x], pos);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O4q. Quantised PuzzleMoE (NEXT-3; Appendix A.3): "the resultant */
+/*      floating-point weights are subjected to uniform quantization with a   */
+/*      group size of 128 ... symmetric group quantization ... no zero point;  */
+/*      the final quantized values are stored alongside their corresponding   */
+/*      sign and mask bits". Readings (R21-R23):                     */
+/*   groups: 128 consecutive elements of a row (cols % 128 == 0);              */
+/*   scale = max(group) / 7 in IEEE f32, or 1 if max == 0; code =     */
+/*   rint(7 w / max) in f64 (= round(w / scale) in exact arithmetic, halves to  */
+/*   even), clamped to [0, 7] (3-bit unsigned levels: W_merged >= 0);          */
+/*   one byte per merged element: bit7 S_i | bit6 S_j | bit5 M_i | bit4 M_j |   */
+/*   bit3 0 | bits2-0 code;                                                    */
+/*   dequantised weight of position pos = (-1)^S_pos * M_pos * bf16_rne(f32(  */
+/*   code * scale)) (the bf16 operand of the expert matmul).                   */
+/* ------------------------------------------------------------------------ */
+int oracle_quant_pack(const float* w_merged, const uint8_t* m0, const uint8_t* m1, const uint8_t* s0,
+                      const uint8_t* s1, int64_t rows, int64_t cols, uint8_t* codes, float* scales) {
+  if (cols % 128 != 0 || rows < 0) return 1;
+  for (int64_t r = 0; r < rows; ++r) {
+    for (int64_t g = 0; g < cols / 128; ++g) {
+      const int64_t x0 = r * cols + g * 128;
+      float mx = 0.0f;
+      for (int i = 0; i < 128; ++i)
+        if (w_merged[x0 + i] > mx) mx = w_merged[x0 + i];
+      const float scale = mx == 0.0f ? 1.0f : mx / 7.0f;
+      scales[r * (cols / 128) + g] = scale;
+      for (int i = 0; i < 128; ++i) {
+        const int64_t x = x0 + i;
+        /* code = round(w / (max / 7)) evaluated as rint(7 w / max) in f64: 7 w is exact and the
+         * one correctly rounded division keeps exact halves (2 / (4/7) = 3.5 -> 4) */
+        double q = mx == 0.0f ? 0.0 : rint(7.0 * (double)w_merged[x] / (double)mx); /* half to even */
+        if (q < 0.0) q = 0.0;
+        if (q > 7.0) q = 7.0;
+        codes[x] = (uint8_t)(((s0[x] != 0) << 7) | ((s1[x] != 0) << 6) | ((m0[x] != 0) << 5) |
+                             ((m1[x] != 0) << 4) | (int)q);
+      }
+    }
+  }
+  return 0;
+}
+
+int oracle_quant_unpack(const uint8_t* codes, const float* scales, int pos, int64_t rows, int64_t cols,
+                        uint16_t* out) {
+  if (pos != 0 && pos != 1) return 1;
+  if (cols % 128 != 0 || rows < 0) return 1;
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t c = 0; c < cols; ++c) {
+      const uint8_t b = codes[r * cols + c];
+      const int sign = (b >> (7 - pos)) & 1;
+      const int mask = (b >> (5 - pos)) & 1;
+      const float v = (float)(b & 7) * scales[r * (cols / 128) + c / 128];
+      const uint16_t h = bf16_rne(v);
+      out[r * cols + c] = mask ? (uint16_t)(h | (sign << 15)) : 0;
+    }
   return 0;
 }
 
