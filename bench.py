@@ -650,8 +650,19 @@ def packer_rates(pz, layer, device):
     pz.merge_pack(w, *planes, out=po)
     torch.cuda.synchronize()
     ms2 = timed_steps(lambda: pz.merge_pack(w, *planes, out=po), 5) / 5
+    # NEXT-3 quantised packer pair on the same 2^28 elements as [2^15, 2^13] matrices
+    w2d, pl2d = w.view(1 << 15, 1 << 13), [p.view(1 << 15, 1 << 13) for p in planes]
+    codes, scales = pz.quant_pack(w2d, *pl2d)
+    deq = pz.quant_unpack(codes, scales, 0)
+    torch.cuda.synchronize()
+    ms3 = timed_steps(lambda: pz.quant_pack(w2d, *pl2d), 5) / 5
+    ms4 = timed_steps(lambda: pz.quant_unpack(codes, scales, 0), 5) / 5
+    del deq
     return {"unpack_gbs": unpack_gbs, "unpack_elems": n, "pack_gbs": m * 10 / (ms2 / 1e3) / 1e9, "pack_elems": m,
-            "note": "algorithmic bytes: unpack 4 B/elem, pack 10 B/elem"}
+            "quant_pack_gbs": m * (9 + 4 / 128) / (ms3 / 1e3) / 1e9,
+            "quant_unpack_gbs": m * (3 + 4 / 128) / (ms4 / 1e3) / 1e9,
+            "note": "algorithmic bytes: unpack 4 B/elem, pack 10 B/elem, quant pack 9 B/elem (+ scales), "
+                    "quant unpack 3 B/elem (+ scales); quant timings include the output allocation"}
 
 
 def sweep(pz, args, device, pk):

@@ -115,6 +115,30 @@ int puzzle_merge_experts_pack(const uint16_t* w_i, const uint16_t* w_j, const fl
                               puzzle_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
+ * NEXT-3: the quantised PuzzleMoE format (Appendix A.3: "uniform quantization with
+ * a group size of 128 ... symmetric group quantization ... stored alongside their
+ * corresponding sign and mask bits"; readings R21-R23).
+ *
+ * puzzle_quant_pack -- merged magnitudes + bit-planes -> 3-bit codes with flags + scales.
+ *   w_merged    f32 [rows][cols]  W_merged of Eq. 7 (>= 0, finite), cols % 128 == 0
+ *   m0, m1, s0, s1  u8 [rows][cols]  M_i, M_j, S_i, S_j (nonzero = 1)
+ *   codes_out   u8  [rows][cols]  bit7 S_i | bit6 S_j | bit5 M_i | bit4 M_j | 0 | 3-bit code
+ *   scales_out  f32 [rows][cols/128]  max(group)/7 of each group of 128 consecutive elements of
+ *                                     a row (1 for an all-zero group)
+ *   code = round(w / scale) evaluated as rint(7 w / max) in f64 (halves to even), in [0, 7].
+ *   Bit-identical to the oracle. Pointers 16-byte aligned (device). Errors: INVALID_ARGUMENT
+ *   (NULL, negative sizes), UNSUPPORTED (cols % 128, alignment).
+ *
+ * puzzle_quant_unpack -- the dequantised bf16 weights of expert `pos` (0 = i, 1 = j):
+ *   (-1)^S_pos * M_pos * bf16_rne(f32(code * scale)); masked entries are +0.
+ * ------------------------------------------------------------------------------------- */
+int puzzle_quant_pack(const float* w_merged, const uint8_t* m0, const uint8_t* m1, const uint8_t* s0,
+                      const uint8_t* s1, int64_t rows, int64_t cols, uint8_t* codes_out,
+                      float* scales_out, puzzle_stream_t stream);
+int puzzle_quant_unpack(const uint8_t* codes, const float* scales, int pos, int64_t rows,
+                        int64_t cols, uint16_t* bf16_out, puzzle_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
  * One MoE layer whose experts are PuzzleMoE-merged pairs (50% compression), or --
  * the 25% ratio, experts cut to 75% of the original count -- some merged pairs plus
  * unmerged experts kept exactly (reading R20).

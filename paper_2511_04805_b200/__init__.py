@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "puzzle_moe_experts", "puzzle_moe_combine", "puzzle_gather_rows", "puzzle_profile_begin",
     "puzzle_profile_end", "puzzle_moe_route_workspace_size", "puzzle_group_colsumsq_workspace_size",
     "puzzle_group_colsumsq", "puzzle_moe_calib_workspace_size", "puzzle_moe_forward_calib",
+    "puzzle_quant_pack", "puzzle_quant_unpack",
 )
 
 
@@ -88,6 +89,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_group_colsumsq": ([P, P, I, I64, P, P, SZ, P], I),
             "puzzle_moe_calib_workspace_size": ([P, I64, I], SZ),
             "puzzle_moe_forward_calib": ([P, P, P, I64, I, I, P, P, P, P, P, SZ, I, P], I),
+            "puzzle_quant_pack": ([P, P, P, P, P, I64, I64, P, P, P], I),
+            "puzzle_quant_unpack": ([P, P, I, I64, I64, P, P], I),
             "puzzle_profile_begin": ([], I),
             "puzzle_profile_end": ([ctypes.c_char_p, SZ], I),
         }
@@ -332,3 +335,27 @@ def group_colsumsq(rows, group_off, sumsq, stream=None) -> torch.Tensor:
     _check(load_library().puzzle_group_colsumsq(_p(rows), _p(group_off), G, cols, _p(sumsq), _p(ws), ws.numel(),
                                                 _stream(stream)), "puzzle_group_colsumsq")
     return sumsq
+
+
+def quant_pack(w_merged, m0, m1, s0, s1, stream=None):
+    """puzzle_quant_pack (NEXT-3): f32 [rows, cols] magnitudes + uint8 bit-planes -> (uint8
+    codes [rows, cols], f32 scales [rows, cols / 128])."""
+    assert w_merged.dtype == torch.float32 and w_merged.dim() == 2
+    rows, cols = w_merged.shape
+    for t in (m0, m1, s0, s1):
+        assert t.dtype == torch.uint8 and t.shape == w_merged.shape
+    codes = torch.empty((rows, cols), dtype=torch.uint8, device=w_merged.device)
+    scales = torch.empty((rows, max(cols // 128, 0)), dtype=torch.float32, device=w_merged.device)
+    _check(load_library().puzzle_quant_pack(_p(w_merged), _p(m0), _p(m1), _p(s0), _p(s1), rows, cols, _p(codes),
+                                            _p(scales), _stream(stream)), "puzzle_quant_pack")
+    return codes, scales
+
+
+def quant_unpack(codes, scales, pos: int, stream=None) -> torch.Tensor:
+    """puzzle_quant_unpack: dequantised bf16 [rows, cols] of expert ``pos``."""
+    assert codes.dtype == torch.uint8 and codes.dim() == 2 and scales.dtype == torch.float32
+    rows, cols = codes.shape
+    out = torch.empty((rows, cols), dtype=torch.bfloat16, device=codes.device)
+    _check(load_library().puzzle_quant_unpack(_p(codes), _p(scales), int(pos), rows, cols, _p(out), _stream(stream)),
+           "puzzle_quant_unpack")
+    return out

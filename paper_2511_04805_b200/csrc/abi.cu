@@ -15,6 +15,9 @@ namespace pz {
 int launch_merge_pack(const float*, const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*,
                       int64_t, uint16_t*, puzzle_pack_stats*, cudaStream_t);
 int launch_unpack(const uint16_t*, int, int64_t, uint16_t*, cudaStream_t);
+int launch_quant_pack(const float*, const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int64_t, int64_t,
+                      uint8_t*, float*, cudaStream_t);
+int launch_quant_unpack(const uint8_t*, const float*, int, int64_t, int64_t, uint16_t*, cudaStream_t);
 int launch_merge_experts_pack(const uint16_t*, const uint16_t*, const float*, const float*, int64_t,
                               int64_t, int64_t, float, uint16_t*, puzzle_pack_stats*, cudaStream_t);
 int launch_route(const float*, int64_t, int, int, int, const int32_t*, int, int32_t*, float*, int32_t*,
@@ -309,6 +312,32 @@ int puzzle_unpack(const uint16_t* packed, int pos, int64_t n, uint16_t* out, puz
   if (!packed || !out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (int rc = check_device()) return rc;
   return launch_unpack(packed, pos, n, out, (cudaStream_t)stream);
+}
+
+int puzzle_quant_pack(const float* w_merged, const uint8_t* m0, const uint8_t* m1, const uint8_t* s0,
+                      const uint8_t* s1, int64_t rows, int64_t cols, uint8_t* codes_out, float* scales_out,
+                      puzzle_stream_t stream) {
+  if (rows < 0 || cols < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "negative sizes");
+  if (cols % 128) return fail(PUZZLE_ERR_UNSUPPORTED, "cols must be a multiple of 128 (quantisation groups)");
+  if (rows == 0 || cols == 0) return PUZZLE_OK;
+  if (!w_merged || !m0 || !m1 || !s0 || !s1 || !codes_out || !scales_out)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!al16(w_merged) || !al16(m0) || !al16(m1) || !al16(s0) || !al16(s1) || !al16(codes_out))
+    return fail(PUZZLE_ERR_UNSUPPORTED, "arrays must be 16-byte aligned");
+  if (int rc = check_device()) return rc;
+  return launch_quant_pack(w_merged, m0, m1, s0, s1, rows, cols, codes_out, scales_out, (cudaStream_t)stream);
+}
+
+int puzzle_quant_unpack(const uint8_t* codes, const float* scales, int pos, int64_t rows, int64_t cols,
+                        uint16_t* bf16_out, puzzle_stream_t stream) {
+  if (pos != 0 && pos != 1) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "pos must be 0 or 1");
+  if (rows < 0 || cols < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "negative sizes");
+  if (cols % 128) return fail(PUZZLE_ERR_UNSUPPORTED, "cols must be a multiple of 128 (quantisation groups)");
+  if (rows == 0 || cols == 0) return PUZZLE_OK;
+  if (!codes || !scales || !bf16_out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!al16(codes) || !al16(bf16_out)) return fail(PUZZLE_ERR_UNSUPPORTED, "arrays must be 16-byte aligned");
+  if (int rc = check_device()) return rc;
+  return launch_quant_unpack(codes, scales, pos, rows, cols, bf16_out, (cudaStream_t)stream);
 }
 
 int puzzle_merge_experts_pack(const uint16_t* wi, const uint16_t* wj, const float* ni, const float* nj,
