@@ -79,3 +79,22 @@ def test_binding_rejects_cpu_tensors(lib):
     import paper_2511_04805_b200 as pz
     with pytest.raises(ValueError):
         pz.unpack(torch.zeros(8, dtype=torch.int16), 0)
+
+
+def test_next_row_argument_errors_are_synchronous(lib):
+    """NEXT-3 / NEXT-4 entry points reject bad arguments before touching a device."""
+    assert lib.puzzle_quant_pack(None, None, None, None, None, 2, 100, None, None, None) == 3   # cols % 128
+    assert lib.puzzle_quant_pack(None, None, None, None, None, 2, 128, None, None, None) == 1   # NULL
+    assert lib.puzzle_quant_pack(None, None, None, None, None, 0, 128, None, None, None) == 0   # empty: no-op
+    assert lib.puzzle_quant_unpack(None, None, 2, 1, 128, None, None) == 1                     # pos
+    assert lib.puzzle_quant_unpack(None, None, 0, -1, 128, None, None) == 1                    # negative
+    assert lib.puzzle_group_colsumsq(None, None, 2, 12, None, None, 0, None) == 1              # NULL
+    assert lib.puzzle_group_colsumsq(None, None, 0, 16, None, None, 0, None) == 0              # no groups
+    assert lib.puzzle_group_colsumsq_workspace_size(-1, 8) == 0
+    import paper_2511_04805_b200 as pz
+    desc = pz.MoELayerDesc(8, 4, 4096, 14336, 4096, 4096, 4096)
+    assert lib.puzzle_moe_calib_workspace_size(ctypes.byref(desc), 64, 2) > lib.puzzle_moe_workspace_size(
+        ctypes.byref(desc), 64, 2)
+    # both statistics outputs NULL
+    assert lib.puzzle_moe_forward_calib(ctypes.byref(desc), None, None, 1, 2, 1, None, None, None, None, None, 0, 0,
+                                        None) == 1
