@@ -169,7 +169,7 @@ typedef struct {
 /* Kernel path for puzzle_moe_forward_ex. AUTO picks by token count. */
 typedef enum {
   PUZZLE_PATH_AUTO = 0,
-  PUZZLE_PATH_GEMV = 1,   /* decode shape: register-decode + mma.sync, weights read once per pair */
+  PUZZLE_PATH_GEMV = 1,   /* decode shape: decode into TMEM + tcgen05.mma (weights on M), weights read once per pair */
   PUZZLE_PATH_TC = 2      /* prefill shape: grouped tcgen05/TMEM GEMM, tiles decoded in shared memory */
 } puzzle_path;
 

@@ -4,7 +4,7 @@
 // packed words are streamed from HBM ONCE and decoded for position 0 and/or 1.
 //
 // Warp-specialised, persistent CTAs (2 per SM, 256 TMEM columns each):
-//   warp 0     W producer: one lane claims work items with an atomic (dynamic scheduler)
+//   warp 0     W producer: one lane walks the CTA's stream-K range of stages (see StreamK)
 //              and issues the TMA loads of each 64-wide K stage of the PACKED 128-row weight
 //              tile (2 boxes) into a 4-deep W ring, released by the decoders as soon as they
 //              hold the words in registers; every stage is queued for
