@@ -32,7 +32,8 @@ EXPORTED_SYMBOLS = (
     "puzzle_moe_experts", "puzzle_moe_combine", "puzzle_gather_rows", "puzzle_profile_begin",
     "puzzle_profile_end", "puzzle_moe_route_workspace_size", "puzzle_group_colsumsq_workspace_size",
     "puzzle_group_colsumsq", "puzzle_moe_calib_workspace_size", "puzzle_moe_forward_calib",
-    "puzzle_quant_pack", "puzzle_quant_unpack",
+    "puzzle_quant_pack", "puzzle_quant_unpack", "puzzle_ep_dispatch", "puzzle_ep_recv_plan",
+    "puzzle_ep_home_index",
 )
 
 
@@ -91,6 +92,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_moe_forward_calib": ([P, P, P, I64, I, I, P, P, P, P, P, SZ, I, P], I),
             "puzzle_quant_pack": ([P, P, P, P, P, I64, I64, P, P, P], I),
             "puzzle_quant_unpack": ([P, P, I, I64, I64, P, P], I),
+            "puzzle_ep_dispatch": ([P, P, P, I, P, I, I64, I64, I, I, P, P, P], I),
+            "puzzle_ep_recv_plan": ([P, I, I, I, I64, P, P, P, P], I),
+            "puzzle_ep_home_index": ([P, P, P, I, P, I, I64, I64, I, P, P, P], I),
             "puzzle_profile_begin": ([], I),
             "puzzle_profile_end": ([ctypes.c_char_p, SZ], I),
         }
@@ -302,6 +306,53 @@ def gather_rows(src, index, out=None, stream=None) -> torch.Tensor:
     _check(load_library().puzzle_gather_rows(_p(src), _p(index), n, src.shape[1], _p(out), _stream(stream)),
            "puzzle_gather_rows")
     return out
+
+
+def _dest_pairs(dest_pairs):
+    """[world][2] host int32 array -> ctypes pointer (kept alive by the returned array)."""
+    import numpy as np
+    a = np.ascontiguousarray(np.asarray(dest_pairs, dtype=np.int32).reshape(-1, 2))
+    return a, a.ctypes.data_as(ctypes.c_void_p), a.shape[0]
+
+
+def ep_dispatch(hidden, assign_token, bucket_off, n_pairs: int, dest_pairs, cap: int, lb_max: int,
+                send_rows=None, send_counts=None, stream=None):
+    """puzzle_ep_dispatch -> (send_rows [world*cap][d] bf16, send_counts [world*lb_max] i32)."""
+    arr, dp, world = _dest_pairs(dest_pairs)
+    d = hidden.shape[1]
+    if send_rows is None:
+        send_rows = torch.empty((world * cap, d), dtype=hidden.dtype, device=hidden.device)
+    if send_counts is None:
+        send_counts = torch.empty(world * lb_max, dtype=torch.int32, device=hidden.device)
+    _check(load_library().puzzle_ep_dispatch(_p(hidden), _p(assign_token), _p(bucket_off), int(n_pairs), dp, world,
+                                             assign_token.numel(), int(cap), int(lb_max), d, _p(send_rows),
+                                             _p(send_counts), _stream(stream)), "puzzle_ep_dispatch")
+    return send_rows, send_counts
+
+
+def ep_recv_plan(recv_counts, world: int, lb_max: int, n_local_buckets: int, cap: int, stream=None):
+    """puzzle_ep_recv_plan -> (local_off [lb+1], gather_idx [world*cap], return_idx [world*cap])."""
+    dev = recv_counts.device
+    local_off = torch.empty(n_local_buckets + 1, dtype=torch.int32, device=dev)
+    gidx = torch.empty(world * cap, dtype=torch.int32, device=dev)
+    ridx = torch.empty(world * cap, dtype=torch.int32, device=dev)
+    _check(load_library().puzzle_ep_recv_plan(_p(recv_counts), int(world), int(lb_max), int(n_local_buckets), int(cap),
+                                              _p(local_off), _p(gidx), _p(ridx), _stream(stream)),
+           "puzzle_ep_recv_plan")
+    return local_off, gidx, ridx
+
+
+def ep_home_index(assign_of, topk_gate, bucket_off, n_pairs: int, dest_pairs, slices: int, cap: int, stream=None):
+    """puzzle_ep_home_index -> (aof_s [T*k*S] i32, gate_s [T][k*S] f32)."""
+    arr, dp, world = _dest_pairs(dest_pairs)
+    T, k = topk_gate.shape
+    dev = topk_gate.device
+    aof_s = torch.empty(T * k * slices, dtype=torch.int32, device=dev)
+    gate_s = torch.empty((T, k * slices), dtype=torch.float32, device=dev)
+    _check(load_library().puzzle_ep_home_index(_p(assign_of), _p(topk_gate), _p(bucket_off), int(n_pairs), dp, world,
+                                               int(cap), T, k, _p(aof_s), _p(gate_s), _stream(stream)),
+           "puzzle_ep_home_index")
+    return aof_s, gate_s
 
 
 class profile_window:

@@ -1,0 +1,246 @@
+// Fixed-capacity expert-parallel dispatch plan (BASELINE.json config 5: "expert-
+// parallel with NCCL all-to-all at 2/4/8 B200"; P:31, P:375 for the merged-pair unit).
+//
+// The variable-split dispatch (ep.py ExpertParallelMoE.forward) learns the split sizes on the
+// host -- one device->host copy per layer. These kernels make the split sizes STATIC: every
+// rank reserves `cap` rows per destination (cap >= T*top_k, the worst case of all of its
+// assignments landing on one owner), so the all-to-alls have equal splits known before the
+// step, and the index work that the host did (regroup by local bucket, inverse permutation,
+// the home rank's combine indices) runs here. A whole EP layer is then a device-only chain
+// (route -> dispatch -> a2a -> recv plan -> gather -> experts -> gather -> a2a -> combine)
+// that a CUDA graph can capture.
+//
+// Partition (EpRanks): rank q owns the global pairs [lo[q], hi[q]) -- whole pairs, or the one
+// pair of which it holds a d_ff slice; every pair has the same number S of owners.
+// Local bucket of rank q: 2 * (pair - lo[q]) + pos (bucket b = 2 * pair + pos globally).
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace pz {
+
+constexpr int kEpMaxRanks = 64;
+struct EpRanks {
+  int32_t lo[kEpMaxRanks], hi[kEpMaxRanks];
+  int world;
+};
+
+namespace {
+
+// send_rows[q][i] = hidden[assign_token[off[2 lo_q] + i]] for i < n_q (warp per row, 16-B
+// copies); CTA 0 also writes send_counts[q][b] (0 past q's local buckets).
+__global__ void __launch_bounds__(256) k_ep_dispatch(const uint16_t* __restrict__ hidden,
+                                                     const int32_t* __restrict__ assign_token,
+                                                     const int32_t* __restrict__ off, EpRanks R, int64_t cap,
+                                                     int lb_max, int64_t cols, uint16_t* __restrict__ send_rows,
+                                                     int32_t* __restrict__ send_counts) {
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < R.world * lb_max; i += blockDim.x) {
+      const int q = i / lb_max, b = i - q * lb_max;
+      const int nb = 2 * (R.hi[q] - R.lo[q]);
+      const int g = 2 * R.lo[q] + b;
+      send_counts[i] = b < nb ? off[g + 1] - off[g] : 0;
+    }
+  }
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= (int64_t)R.world * cap) return;
+  const int q = (int)(r / cap);
+  const int64_t i = r - (int64_t)q * cap;
+  const int32_t lo = off[2 * R.lo[q]], n = off[2 * R.hi[q]] - lo;
+  if (i >= n) return;
+  const int lane = threadIdx.x & 31;
+  const uint4* sp = reinterpret_cast<const uint4*>(hidden + (int64_t)assign_token[lo + i] * cols);
+  uint4* dp = reinterpret_cast<uint4*>(send_rows + r * cols);
+  for (int64_t c = lane; c < cols / 8; c += 32) dp[c] = sp[c];
+}
+
+// Owner side. recv_counts[s][b] (s = source rank, b < lb local buckets, row stride lb_max).
+// Local order = (bucket, source, arrival): local row of recv row (s, w) with w in source s's
+// bucket b = loff[b] + sum_{s'<s} rc[s'][b] + (w - sum_{b'<b} rc[s][b']).
+// Every CTA recomputes the (small) prefix tables in shared memory, then handles 1024 rows.
+__global__ void __launch_bounds__(1024) k_ep_recv_plan(const int32_t* __restrict__ rc_g, int world, int lb_max, int lb,
+                                                       int64_t cap, int32_t* __restrict__ local_off,
+                                                       int32_t* __restrict__ gather_idx,
+                                                       int32_t* __restrict__ return_idx) {
+  extern __shared__ int32_t sm[];
+  int32_t* rc = sm;                                 // [world][lb]
+  int32_t* pre_s = rc + world * lb;                 // [world][lb + 1]: exclusive over b, total last
+  int32_t* pre_b = pre_s + world * (lb + 1);        // [world][lb]: exclusive over s
+  int32_t* loff = pre_b + world * lb;               // [lb + 1]
+  __shared__ int32_t warp_sum[32];
+  pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  for (int i = tid; i < world * lb; i += blockDim.x) {
+    const int s = i / lb;
+    rc[i] = rc_g[(int64_t)s * lb_max + (i - s * lb)];
+  }
+  __syncthreads();
+  for (int s = tid; s < world; s += blockDim.x) {
+    int32_t run = 0;
+    for (int b = 0; b < lb; ++b) {
+      pre_s[s * (lb + 1) + b] = run;
+      run += rc[s * lb + b];
+    }
+    pre_s[s * (lb + 1) + lb] = run;
+  }
+  // bucket totals (thread b) and their exclusive scan (block scan; lb <= 1024 checked on the host)
+  int32_t tot = 0;
+  if (tid < lb) {
+    for (int s = 0; s < world; ++s) {
+      pre_b[s * lb + tid] = tot;
+      tot += rc[s * lb + tid];
+    }
+  }
+  const int lane = tid & 31, w = tid >> 5;
+  int32_t inc = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) warp_sum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    int32_t v = lane < nw ? warp_sum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane < nw) warp_sum[lane] = v;  // inclusive warp-prefix totals
+  }
+  __syncthreads();
+  const int32_t excl = inc - tot + (w > 0 ? warp_sum[w - 1] : 0);
+  if (tid < lb) loff[tid] = excl;
+  if (tid == lb - 1) loff[lb] = excl + tot;
+  if (lb == 0 && tid == 0) loff[0] = 0;
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int b = tid; b <= lb; b += blockDim.x) local_off[b] = loff[b];
+  const int32_t n_local = loff[lb];
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + tid;
+  if (r >= (int64_t)world * cap) return;
+  if (r >= n_local) gather_idx[r] = 0;  // padding rows of the experts input: any valid row
+  const int s = (int)(r / cap);
+  const int32_t wi = (int32_t)(r - (int64_t)s * cap);
+  const int32_t* ps = pre_s + s * (lb + 1);
+  if (wi >= ps[lb]) {
+    return_idx[r] = 0;  // an unused slot of source s's region
+    return;
+  }
+  int a = 0, z = lb;  // last b with ps[b] <= wi (non-empty bucket holding wi)
+  while (z - a > 1) {
+    const int m = (a + z) >> 1;
+    if (ps[m] <= wi) a = m; else z = m;
+  }
+  const int32_t l = loff[a] + pre_b[s * lb + a] + (wi - ps[a]);
+  return_idx[r] = l;
+  gather_idx[l] = (int32_t)r;
+}
+
+// Home side: assignment (t, j) = a in global bucket g (pair p = g / 2); its s-th owner q_s
+// (ascending) returned the row q_s * cap + (a - off[2 lo[q_s]]).
+__global__ void __launch_bounds__(256) k_ep_home_index(const int32_t* __restrict__ assign_of,
+                                                       const float* __restrict__ gate, const int32_t* __restrict__ off,
+                                                       int n_buckets, EpRanks R, int slices, int64_t cap, int64_t n,
+                                                       int32_t* __restrict__ aof_s, float* __restrict__ gate_s) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t a = assign_of[i];
+  int lo = 0, hi = n_buckets;  // last g with off[g] <= a
+  while (hi - lo > 1) {
+    const int m = (lo + hi) >> 1;
+    if (off[m] <= a) lo = m; else hi = m;
+  }
+  const int p = lo >> 1;
+  const float g = gate[i];
+  int s = 0;
+  for (int q = 0; q < R.world && s < slices; ++q) {
+    if (R.lo[q] <= p && p < R.hi[q]) {
+      aof_s[i * slices + s] = (int32_t)(q * cap + (a - off[2 * R.lo[q]]));
+      gate_s[i * slices + s] = g;
+      ++s;
+    }
+  }
+}
+
+int fill_ranks(const int32_t* dest_pairs, int world, int n_pairs, EpRanks* R, int* slices) {
+  if (world < 1 || world > kEpMaxRanks) return fail(PUZZLE_ERR_UNSUPPORTED, "world must be in [1, 64]");
+  R->world = world;
+  for (int q = 0; q < world; ++q) {
+    R->lo[q] = dest_pairs[2 * q];
+    R->hi[q] = dest_pairs[2 * q + 1];
+    if (R->lo[q] < 0 || R->hi[q] < R->lo[q] || R->hi[q] > n_pairs)
+      return fail(PUZZLE_ERR_INVALID_ARGUMENT, "dest_pairs: [lo, hi) must lie in [0, n_pairs]");
+  }
+  if (slices) {  // every pair needs the same number of owners
+    int S = -1;
+    for (int p = 0; p < n_pairs; ++p) {
+      int c = 0;
+      for (int q = 0; q < world; ++q) c += R->lo[q] <= p && p < R->hi[q];
+      if (S < 0) S = c;
+      if (c != S || c == 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "dest_pairs: every pair needs the same nonzero owner count");
+    }
+    *slices = S;
+  }
+  return PUZZLE_OK;
+}
+
+}  // namespace
+
+int launch_ep_dispatch(const uint16_t* hidden, const int32_t* assign_token, const int32_t* bucket_off,
+                       const int32_t* dest_pairs, int world, int n_pairs, int64_t cap, int lb_max, int d,
+                       uint16_t* send_rows, int32_t* send_counts, cudaStream_t s) {
+  if ((int64_t)world * cap > INT32_MAX) return fail(PUZZLE_ERR_UNSUPPORTED, "world * cap must fit in int32");
+  EpRanks R;
+  if (int rc = fill_ranks(dest_pairs, world, n_pairs, &R, nullptr)) return rc;
+  for (int q = 0; q < world; ++q)
+    if (2 * (R.hi[q] - R.lo[q]) > lb_max) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "lb_max < a rank's local buckets");
+  const int64_t rows = (int64_t)world * cap;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, (rows + 7) / 8);
+  ProfScope _ps("ep_dispatch", s);
+  cudaError_t e = launch_pdl(k_ep_dispatch, dim3(grid), dim3(256), 0, s, hidden, assign_token, bucket_off, R, cap,
+                             lb_max, (int64_t)d, send_rows, send_counts);
+  if (e != cudaSuccess) return cuda_check(e, "ep_dispatch launch");
+  return cuda_check(cudaGetLastError(), "ep_dispatch launch");
+}
+
+size_t ep_recv_plan_smem(int world, int lb) {
+  return (size_t)(world * lb * 3 + world + lb + 1) * sizeof(int32_t);
+}
+
+int launch_ep_recv_plan(const int32_t* recv_counts, int world, int lb_max, int lb, int64_t cap, int32_t* local_off,
+                        int32_t* gather_idx, int32_t* return_idx, cudaStream_t s) {
+  const size_t smem = ep_recv_plan_smem(world, lb);
+  const int64_t rows = (int64_t)world * cap;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, (rows + 1023) / 1024);
+  ProfScope _ps("ep_recv_plan", s);
+  cudaError_t e = launch_pdl(k_ep_recv_plan, dim3(grid), dim3(1024), smem, s, recv_counts, world, lb_max, lb, cap,
+                             local_off, gather_idx, return_idx);
+  if (e != cudaSuccess) return cuda_check(e, "ep_recv_plan launch");
+  return cuda_check(cudaGetLastError(), "ep_recv_plan launch");
+}
+
+int launch_ep_home_index(const int32_t* assign_of, const float* gate, const int32_t* bucket_off, int n_pairs,
+                         const int32_t* dest_pairs, int world, int64_t cap, int64_t n, int32_t* aof_s,
+                         float* gate_s, int* slices_out, cudaStream_t s) {
+  EpRanks R;
+  int S = 0;
+  if (int rc = fill_ranks(dest_pairs, world, n_pairs, &R, &S)) return rc;
+  if (slices_out) *slices_out = S;
+  if (n == 0) return PUZZLE_OK;
+  ProfScope _ps("ep_home_index", s);
+  cudaError_t e = launch_pdl(k_ep_home_index, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, assign_of, gate,
+                             bucket_off, 2 * n_pairs + 1, R, S, cap, n, aof_s, gate_s);
+  if (e != cudaSuccess) return cuda_check(e, "ep_home_index launch");
+  return cuda_check(cudaGetLastError(), "ep_home_index launch");
+}
+
+}  // namespace pz

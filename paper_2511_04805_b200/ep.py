@@ -17,6 +17,12 @@ Per layer (every rank holds T_local tokens of its own):
   5. outputs un-permuted and sent home (all_to_all), combine (a6) with the home gates.
 Every data-path step runs in libpuzzlemoe kernels (route, gather, experts, combine); torch
 supplies the collectives and the host-side split sizes (one D2H copy of the bucket counts).
+
+forward_fixed is the same layer with FIXED-CAPACITY dispatch: every rank reserves cap =
+cap_tokens*top_k rows per destination, so both all-to-alls have equal splits known up front and
+the index work of steps 3-5 runs in device kernels (puzzle_ep_dispatch / puzzle_ep_recv_plan /
+puzzle_ep_home_index): no device->host copy, so a decode layer can be captured in a CUDA graph.
+It moves world*cap rows per collective instead of the routed count (the price of static splits).
 """
 from __future__ import annotations
 
@@ -96,11 +102,20 @@ class CudaOps:
             return self.pz.gather_rows(src.view(torch.int16), index).view(torch.float32)
         return self.pz.gather_rows(src, index)
 
-    def experts(self, local_layer, x_rows, bucket_off):
-        return local_layer.experts(x_rows, bucket_off)
+    def experts(self, local_layer, x_rows, bucket_off, path=None):
+        return local_layer.experts(x_rows, bucket_off, path=self.pz.PATH_AUTO if path is None else path)
 
     def combine(self, y, assign_of, gate, residual):
         return self.pz.moe_combine(y, assign_of, gate, residual=residual)
+
+    def ep_dispatch(self, hidden, assign_token, bucket_off, n_pairs, dest_pairs, cap, lb_max):
+        return self.pz.ep_dispatch(hidden, assign_token, bucket_off, n_pairs, dest_pairs, cap, lb_max)
+
+    def ep_recv_plan(self, recv_counts, world, lb_max, n_local_buckets, cap):
+        return self.pz.ep_recv_plan(recv_counts, world, lb_max, n_local_buckets, cap)
+
+    def ep_home_index(self, assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, cap):
+        return self.pz.ep_home_index(assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, cap)
 
 
 class ExpertParallelMoE:
@@ -118,6 +133,9 @@ class ExpertParallelMoE:
         # local bucket b_local = 2 * (pair - p0) + pos
         self.p0, self.p1 = part.pairs_of(rank)
         self.n_local_buckets = 2 * (self.p1 - self.p0)
+        # fixed-capacity dispatch tables (host): [world][2] pair ranges, count-table row stride
+        self.dest_pairs = np.array([part.pairs_of(q) for q in range(part.world)], dtype=np.int32)
+        self.lb_max = int(2 * max(b - a for a, b in self.dest_pairs))
 
     def _a2a(self, out, inp, out_splits, in_splits):
         dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
@@ -191,3 +209,38 @@ class ExpertParallelMoE:
         aof_s = pos_of[aof].reshape(T, top_k * S).astype(np.int32)
         gate_s = gate.reshape(T, top_k, 1).expand(T, top_k, S).reshape(T, top_k * S).contiguous()
         return ops.combine(y_back, torch.from_numpy(aof_s).to(dev).reshape(-1), gate_s, residual)
+
+    def _a2a_equal(self, out, inp):
+        dist.all_to_all_single(out, inp, group=self.group)
+
+    def forward_fixed(self, hidden, logits, top_k: int, renormalize: bool, residual=None,
+                      cap_tokens: int | None = None, path=None):
+        """The layer with fixed-capacity dispatch: device-only, no host synchronisation.
+
+        cap_tokens (default: this rank's T) bounds every rank's token count and must be the same
+        on all ranks; each rank sends world * cap_tokens * top_k rows per all-to-all. path is
+        passed to the local experts call (e.g. PATH_GEMV for decode-shape batches, whose owner
+        receives up to world * cap rows)."""
+        ops, part, G = self.ops, self.part, self.world
+        T = hidden.shape[0]
+        cap = (T if cap_tokens is None else int(cap_tokens)) * top_k
+        if cap < T * top_k:
+            raise ValueError("cap_tokens must be >= the number of tokens on this rank")
+        topk_idx, gate, bucket_off, assign_token, assign_of = ops.route(self.route_layer, logits, top_k, renormalize)
+        # 1. every destination's rows (its pairs' buckets) into its fixed region + the bucket counts
+        send_rows, send_counts = ops.ep_dispatch(hidden, assign_token, bucket_off, part.n_pairs, self.dest_pairs, cap,
+                                                 self.lb_max)
+        recv_counts = torch.empty_like(send_counts)
+        self._a2a_equal(recv_counts, send_counts)
+        x_recv = torch.empty_like(send_rows)
+        self._a2a_equal(x_recv, send_rows)
+        # 2. regroup into (local bucket, source) order, local experts, back into the arrival slots
+        local_off, gidx, ridx = ops.ep_recv_plan(recv_counts, G, self.lb_max, self.n_local_buckets, cap)
+        x_local = ops.gather_rows(x_recv, gidx)
+        y_local = ops.experts(self.local_layer, x_local, local_off, path=path)
+        y_recv = ops.gather_rows(y_local, ridx)
+        # 3. outputs home (region q = owner q's results for the rows sent to it) and combine
+        y_back = torch.empty_like(y_recv)
+        self._a2a_equal(y_back, y_recv)
+        aof_s, gate_s = ops.ep_home_index(assign_of, gate, bucket_off, part.n_pairs, self.dest_pairs, part.slices, cap)
+        return ops.combine(y_back, aof_s, gate_s, residual)

@@ -90,3 +90,53 @@ def oracle_mixed_layer(cfg: synth.MoEConfig, n_merged: int, seed: int | None = N
                 slot[e] = 2 * q
                 dense[q] = 1
     return w13, w2, slot, dense
+
+
+# ---- fixed-capacity EP index tables, restated from include/puzzlemoe.h (puzzle_ep_*) ----
+# Plain numpy statements of what the three index kernels must produce; the GPU tests compare
+# the kernels with these, the gloo tests use them as the CPU stand-in of the device ops.
+
+def ep_dispatch_ref(hidden, assign_token, off, dest_pairs, cap, lb_max):
+    """send_rows [G*cap][d] (unwritten rows zero here), send_counts [G*lb_max]."""
+    G = len(dest_pairs)
+    rows = np.zeros((G * cap,) + hidden.shape[1:], hidden.dtype)
+    counts = np.zeros((G, lb_max), np.int32)
+    for q, (lo, hi) in enumerate(dest_pairs):
+        a, b = off[2 * lo], off[2 * hi]
+        rows[q * cap:q * cap + (b - a)] = hidden[assign_token[a:b]]
+        counts[q, :2 * (hi - lo)] = np.diff(off[2 * lo:2 * hi + 1])
+    return rows, counts.reshape(-1)
+
+
+def ep_recv_plan_ref(recv_counts, world, lb_max, lb, cap):
+    """(local_off [lb+1], gather_idx [G*cap], return_idx [G*cap]); local order (bucket, source)."""
+    rc = np.asarray(recv_counts).reshape(world, lb_max)[:, :lb].astype(np.int64)
+    local_off = np.concatenate([[0], np.cumsum(rc.sum(0))]).astype(np.int32)
+    gidx = np.zeros(world * cap, np.int32)
+    ridx = np.zeros(world * cap, np.int32)
+    l = 0
+    for b in range(lb):
+        for s in range(world):
+            w0 = rc[s, :b].sum()
+            for w in range(rc[s, b]):
+                gidx[l] = s * cap + w0 + w
+                ridx[s * cap + w0 + w] = l
+                l += 1
+    return local_off, gidx, ridx
+
+
+def ep_home_index_ref(assign_of, gate, off, dest_pairs, slices, cap):
+    """(aof_s [T*k*S], gate_s [T][k*S])."""
+    T, k = gate.shape
+    aof = np.asarray(assign_of).reshape(-1)
+    aof_s = np.zeros(T * k * slices, np.int32)
+    gate_s = np.zeros((T * k, slices), np.float32)
+    for i, a in enumerate(aof):
+        g = int(np.searchsorted(off, a, side="right")) - 1
+        p = g // 2
+        owners = [q for q, (lo, hi) in enumerate(dest_pairs) if lo <= p < hi]
+        assert len(owners) == slices
+        for s, q in enumerate(owners):
+            aof_s[i * slices + s] = q * cap + (a - off[2 * dest_pairs[q][0]])
+            gate_s[i, s] = gate.reshape(-1)[i]
+    return aof_s, gate_s.reshape(T, k * slices)

@@ -16,7 +16,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from helpers import oracle_mixed_layer, oracle_packed_layer
+from helpers import (ep_dispatch_ref, ep_home_index_ref, ep_recv_plan_ref, oracle_mixed_layer,
+                     oracle_packed_layer)
 
 
 class OracleOps:
@@ -39,7 +40,7 @@ class OracleOps:
     def gather_rows(self, src, index):
         return src[index.long()]
 
-    def experts(self, local_layer, x_rows, bucket_off):
+    def experts(self, local_layer, x_rows, bucket_off, path=None):
         w13, w2, dense = local_layer
         off = bucket_off.numpy()
         bits = x_rows.contiguous().view(torch.int16).numpy().view(np.uint16)
@@ -49,6 +50,19 @@ class OracleOps:
                 y[off[b]:off[b + 1]] = oracle.expert_ffn(w13, w2, b // 2, b % 2, bits[off[b]:off[b + 1]],
                                                          dense=dense is not None and bool(dense[b // 2]))
         return torch.from_numpy(y)
+
+    def ep_dispatch(self, hidden, assign_token, bucket_off, n_pairs, dest_pairs, cap, lb_max):
+        bits = hidden.contiguous().view(torch.int16).numpy()
+        rows, counts = ep_dispatch_ref(bits, assign_token.numpy(), bucket_off.numpy(), dest_pairs, cap, lb_max)
+        return torch.from_numpy(rows).view(hidden.dtype), torch.from_numpy(counts)
+
+    def ep_recv_plan(self, recv_counts, world, lb_max, n_local_buckets, cap):
+        return tuple(torch.from_numpy(a) for a in ep_recv_plan_ref(recv_counts.numpy(), world, lb_max,
+                                                                    n_local_buckets, cap))
+
+    def ep_home_index(self, assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, cap):
+        return tuple(torch.from_numpy(a) for a in ep_home_index_ref(assign_of.numpy(), gate.numpy(),
+                                                                     bucket_off.numpy(), dest_pairs, slices, cap))
 
     def combine(self, y, assign_of, gate, residual):
         T, k = gate.shape
@@ -86,6 +100,10 @@ def _worker(rank, world, port, cfg_fields, T, outdir, n_merged=None):
         out = layer.forward(hidden, torch.from_numpy(lg), cfg.top_k, cfg.renormalize, residual=resid)
         ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, rb, pair_dense=dense)
         np.save(os.path.join(outdir, f"out{rank}.npy"), out.numpy())
+        # fixed-capacity dispatch (device-side index tables; one spare token of capacity)
+        outf = layer.forward_fixed(hidden, torch.from_numpy(lg), cfg.top_k, cfg.renormalize, residual=resid,
+                                   cap_tokens=T + 1)
+        np.save(os.path.join(outdir, f"outf{rank}.npy"), outf.numpy())
         np.save(os.path.join(outdir, f"ref{rank}.npy"), ref)
     finally:
         dist.destroy_process_group()
@@ -122,6 +140,8 @@ def _run_world2(cfg_fields, T, n_merged):
             out = np.load(os.path.join(d, f"out{r}.npy"))
             ref = np.load(os.path.join(d, f"ref{r}.npy"))
             np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-5)
+            outf = np.load(os.path.join(d, f"outf{r}.npy"))
+            np.testing.assert_allclose(outf, ref, rtol=1e-5, atol=1e-5)
 
 
 def test_partition_layout():

@@ -53,3 +53,154 @@ def test_ep_world1_matches_forward_and_oracle(nccl_group, cfg):
     ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize)
     assert_close(out.float().cpu().numpy(), ref, "ep vs oracle")
     assert (out.float() - ref_fwd.float()).abs().max().item() <= 2e-2
+
+
+# ---- fixed-capacity dispatch: the three index kernels against their header definitions ----
+
+def _partitions():
+    from paper_2511_04805_b200.ep import Partition
+    for P, G in [(4, 1), (4, 3), (30, 8), (32, 4), (4, 8), (2, 4), (1, 2)]:
+        part = Partition(P, G)
+        yield P, G, part.slices, np.array([part.pairs_of(q) for q in range(G)], np.int32)
+
+
+def _random_routing(rng, P, T, k):
+    """bucket_off / assign_token / assign_of / gate of a random top-k routing (bucket-major)."""
+    E = 2 * P
+    idx = np.stack([rng.choice(E, size=min(k, E), replace=False) for _ in range(T)]) if T else np.zeros((0, k), np.int64)
+    b = idx.reshape(-1)
+    order = np.argsort(b, kind="stable")
+    off = np.concatenate([[0], np.cumsum(np.bincount(b, minlength=E))]).astype(np.int32)
+    tok = (order // k).astype(np.int32)
+    aof = np.empty(T * k, np.int32)
+    aof[order] = np.arange(T * k, dtype=np.int32)
+    gate = rng.random((T, k)).astype(np.float32)
+    return off, tok, aof, gate
+
+
+@pytest.mark.parametrize("T,k,spare", [(1, 1, 0), (13, 2, 3), (64, 2, 0), (37, 6, 1), (0, 2, 2)])
+def test_ep_dispatch_and_home_index_match_definition(T, k, spare):
+    import paper_2511_04805_b200 as pz
+    from helpers import ep_dispatch_ref, ep_home_index_ref
+    rng = np.random.default_rng(1000 + T * 7 + k)
+    d = 64
+    for P, G, S, dest in _partitions():
+        if k > 2 * P:
+            continue
+        off, tok, aof, gate = _random_routing(rng, P, T, k)
+        cap = (T + spare) * k
+        lb_max = int(2 * max(b - a for a, b in dest))
+        hidden = rng.integers(-2**15, 2**15, size=(max(T, 1), d), dtype=np.int16)
+        h_d = torch.from_numpy(hidden).cuda()
+        tok_d, off_d = torch.from_numpy(tok).cuda(), torch.from_numpy(off).cuda()
+        rows = torch.zeros((G * cap, d), dtype=torch.int16, device="cuda")
+        rows, counts = pz.ep_dispatch(h_d, tok_d, off_d, P, dest, cap, lb_max, send_rows=rows)
+        r_ref, c_ref = ep_dispatch_ref(hidden, tok, off, dest, cap, lb_max)
+        assert np.array_equal(rows.cpu().numpy(), r_ref), (P, G)
+        assert np.array_equal(counts.cpu().numpy(), c_ref), (P, G)
+        aof_s, gate_s = pz.ep_home_index(torch.from_numpy(aof).cuda(), torch.from_numpy(gate).cuda(), off_d, P, dest,
+                                         S, cap)
+        a_ref, g_ref = ep_home_index_ref(aof, gate, off, dest, S, cap)
+        assert np.array_equal(aof_s.cpu().numpy(), a_ref), (P, G)
+        assert np.array_equal(gate_s.cpu().numpy(), g_ref), (P, G)
+
+
+@pytest.mark.parametrize("G,lb,lb_max,cap", [(1, 8, 8, 128), (2, 4, 6, 10), (8, 2, 2, 384), (4, 60, 64, 2048),
+                                            (3, 5, 5, 0), (8, 16, 16, 64)])
+def test_ep_recv_plan_matches_definition(G, lb, lb_max, cap):
+    import paper_2511_04805_b200 as pz
+    from helpers import ep_recv_plan_ref
+    rng = np.random.default_rng(G * 100 + lb)
+    rc = np.zeros((G, lb_max), np.int32)
+    for s in range(G):  # each source sends at most cap rows, some buckets empty
+        n = int(rng.integers(0, cap + 1)) if cap else 0
+        if lb and n:
+            cut = np.sort(rng.integers(0, n + 1, size=lb - 1))
+            rc[s, :lb] = np.diff(np.concatenate([[0], cut, [n]]))
+    lo, gi, ri = pz.ep_recv_plan(torch.from_numpy(rc.reshape(-1)).cuda(), G, lb_max, lb, cap)
+    lo_r, gi_r, ri_r = ep_recv_plan_ref(rc.reshape(-1), G, lb_max, lb, cap)
+    assert np.array_equal(lo.cpu().numpy(), lo_r)
+    assert np.array_equal(gi.cpu().numpy(), gi_r)
+    assert np.array_equal(ri.cpu().numpy(), ri_r)
+
+
+def test_ep_fixed_argument_errors():
+    import paper_2511_04805_b200 as pz
+    h = torch.zeros((4, 64), dtype=torch.int16, device="cuda")
+    tok = torch.zeros(8, dtype=torch.int32, device="cuda")
+    off = torch.zeros(9, dtype=torch.int32, device="cuda")
+    with pytest.raises(pz.PuzzleError):  # cap < T*k
+        pz.ep_dispatch(h, tok, off, 4, [[0, 4]], 7, 8)
+    with pytest.raises(pz.PuzzleError):  # pair range outside [0, n_pairs]
+        pz.ep_dispatch(h, tok, off, 4, [[0, 5]], 8, 10)
+    with pytest.raises(pz.PuzzleError):  # lb_max below a rank's local buckets
+        pz.ep_dispatch(h, tok, off, 4, [[0, 2], [2, 4]], 8, 3)
+    with pytest.raises(pz.PuzzleError):  # pair 3 has no owner
+        pz.ep_home_index(tok, torch.zeros((4, 2), device="cuda"), off, 4, [[0, 3]], 1, 8)
+    with pytest.raises(pz.PuzzleError):  # n_local_buckets > lb_max
+        pz.ep_recv_plan(torch.zeros(4, dtype=torch.int32, device="cuda"), 1, 4, 5, 8)
+
+
+def _ep_world1(cfg):
+    import paper_2511_04805_b200 as pz
+    from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_packed
+    w13, w2, slot, _ = oracle_packed_layer(cfg)
+    w13_d = torch.from_numpy(w13.view(np.int16)).cuda()
+    w2_d = torch.from_numpy(w2.view(np.int16)).cuda()
+    slot_d = torch.from_numpy(slot).cuda()
+    part = Partition(cfg.n_pairs, 1)
+    w13_l, w2_l = shard_packed(w13_d, w2_d, part, 0)
+    local = pz.PackedMoELayer(w13_l, w2_l, torch.arange(2 * w13_l.shape[0], dtype=torch.int32, device="cuda"))
+    route = pz.RoutingLayer(cfg.n_pairs, cfg.d_model, cfg.d_ff, slot_d, w13_l)
+    return ExpertParallelMoE(part, 0, route, local, cfg.d_model), (w13, w2, slot)
+
+
+@pytest.mark.parametrize("cfg", [synth.MoEConfig("ep_small", 30, 256, 512, 8, 2, True),
+                                 synth.MoEConfig("ep_fine", 31, 128, 256, 16, 4, False)], ids=lambda c: c.name)
+@pytest.mark.parametrize("T,path", [(37, 0), (64, 1), (5, 1), (200, 0)])
+def test_ep_fixed_world1_matches_oracle(nccl_group, cfg, T, path):
+    ep, (w13, w2, slot) = _ep_world1(cfg)
+    hb = synth.hidden_bits(cfg, T, seed=7)
+    lg = synth.router_logits(cfg, T, seed=8)
+    rb = synth.hidden_bits(cfg, T, seed=9)
+    h = torch.from_numpy(hb.view(np.int16)).cuda().view(torch.bfloat16)
+    r = torch.from_numpy(rb.view(np.int16)).cuda().view(torch.bfloat16)
+    out = ep.forward_fixed(h, torch.from_numpy(lg).cuda(), cfg.top_k, cfg.renormalize, residual=r,
+                           cap_tokens=T + 3, path=path)
+    torch.cuda.synchronize()
+    ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, rb)
+    assert_close(out.float().cpu().numpy(), ref, "fixed-capacity ep vs oracle")
+
+
+def test_ep_fixed_graph_capture(nccl_group):
+    """The fixed-capacity layer has no host sync: it captures into a CUDA graph (NCCL inside)
+    and a replay on new inputs equals the oracle."""
+    import paper_2511_04805_b200 as pz
+    cfg = synth.MoEConfig("ep_graph", 32, 256, 512, 8, 2, True)
+    ep, (w13, w2, slot) = _ep_world1(cfg)
+    T = 16
+    h = torch.empty((T, cfg.d_model), dtype=torch.bfloat16, device="cuda")
+    lg = torch.empty((T, cfg.n_experts), dtype=torch.float32, device="cuda")
+
+    def load(seed):
+        hb = synth.hidden_bits(cfg, T, seed=seed)
+        lb = synth.router_logits(cfg, T, seed=seed + 1)
+        h.copy_(torch.from_numpy(hb.view(np.int16)).view(torch.bfloat16))
+        lg.copy_(torch.from_numpy(lb))
+        return hb, lb
+
+    load(40)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up outside capture (workspaces, NCCL communicator)
+        ep.forward_fixed(h, lg, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = ep.forward_fixed(h, lg, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV)
+    hb, lb = load(50)
+    g.replay()
+    torch.cuda.synchronize()
+    ref = oracle.moe_forward(w13, w2, slot, hb, lb, cfg.top_k, cfg.renormalize)
+    assert_close(out.float().cpu().numpy(), ref, "graph-replayed fixed-capacity ep vs oracle")
