@@ -13,9 +13,11 @@ batch 64 on one B200. Weights are synthetic (seeded N(0, 1/in) experts merged + 
 the GPU by puzzle_merge_experts_pack); the packed layer (1.41 GB) is >10x the 126 MB L2,
 so no L2 flush is needed for the headline (smaller secondary configs flush L2 per step).
 
-Rank 0 prints ONE JSON line. Under torchrun (N > 1) every rank runs an independent
-replica on its own batch (weak scaling; expert parallelism is tracked in DESIGN.md) and
-the time is the max over ranks.
+Rank 0 prints ONE JSON line. Under torchrun (N > 1) the layer runs expert-parallel: every
+rank holds its share of the merged pairs and its own batch of tokens (weak scaling), tokens go
+to the pair owners and back with NCCL all-to-all -- fixed-capacity dispatch (device-only,
+CUDA-graph captured) for decode batches, variable splits for prefill -- and the time is the
+max over ranks.
 
 --impl reference times the CPU oracle (oracle/, plain C) on the host cores on a bounded
 sample of the same workload (the tier's reference arm).
@@ -340,7 +342,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name} single MoE layer decode, batch {args.batch} (sampled {n} tokens/step)",
+            "config": {"workload": f"{cfg.name} single MoE layer {'decode' if args.batch <= 64 else 'prefill'}, batch {args.batch} (sampled {n} tokens/step)",
                        "d_model": d, "d_ff": f, "n_experts": cfg.n_experts, "top_k": cfg.top_k},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -359,11 +361,23 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1:
+    # --ep1: the expert-parallel code path through a 1-rank NCCL group (tests the EP step on a
+    # one-GPU box; not a multi-GPU measurement)
+    dist_on = world > 1 or args.ep1
+    if dist_on:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if "MASTER_PORT" not in os.environ:
+                import socket
+                with socket.socket() as sk:
+                    sk.bind(("127.0.0.1", 0))
+                    os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=device)
     if rank == 0 and not os.path.exists(pz.LIB_PATH):
         pzbuild.build()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     pz.load_library()
     pk = peaks()
@@ -378,7 +392,7 @@ def run_ours(args):
     ws = layer.workspace(T, cfg.top_k)
     stream = torch.cuda.current_stream()
     ep = None
-    if world > 1:
+    if dist_on:
         # expert parallelism: this rank keeps only its pairs (or d_ff slice) of the layer
         from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_dense, shard_packed
         part = Partition(layer.n_pairs, world)
@@ -388,9 +402,16 @@ def run_ours(args):
         routing = pz.RoutingLayer(layer.n_pairs, cfg.d_model, cfg.d_ff, layer.expert_slot, w13_l)
         ep = ExpertParallelMoE(part, rank, routing, local, cfg.d_model)
 
+    ep_fixed = ep is not None and T <= 64  # decode: static splits, no host sync, graph-capturable
+
+    def ep_forward(h, lg):
+        if ep_fixed:
+            return ep.forward_fixed(h, lg, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV)
+        return ep.forward(h, lg, cfg.top_k, cfg.renormalize)
+
     def step():
         if ep is not None:
-            ep.forward(hidden, logits, cfg.top_k, cfg.renormalize)
+            ep_forward(hidden, logits)
         else:
             layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
 
@@ -407,7 +428,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     log("warmup done")
     graph = None
-    if not args.no_graph and ep is None:  # EP needs host-side split sizes: eager
+    if not args.no_graph and (ep is None or ep_fixed):  # variable-split EP needs host split sizes: eager
         # the whole forward (route .. combine) replayed as one CUDA graph: no host launch gaps
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
@@ -418,7 +439,7 @@ def run_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.1)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -428,7 +449,7 @@ def run_ours(args):
         with pz.profile_window() as prof:
             total_ms = timed_steps(step, K, flush)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     t1 = time.perf_counter()
     if graph is not None:
@@ -440,7 +461,7 @@ def run_ours(args):
     clocks.stop()
     ms = total_ms / K
     log("timed", ms, prof.kernels)
-    if world > 1:
+    if dist_on:
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -508,7 +529,7 @@ def run_ours(args):
         if ep is not None:
             h_dev[0].copy_(h_host[0], non_blocking=True)
             l_dev[0].copy_(l_host[0], non_blocking=True)
-            o_host[0].copy_(ep.forward(h_dev[0], l_dev[0], cfg.top_k, cfg.renormalize), non_blocking=True)
+            o_host[0].copy_(ep_forward(h_dev[0], l_dev[0]), non_blocking=True)
             return
         s_in.wait_event(ev["comp"][b])  # buffer set b's previous forward has read its inputs
         with torch.cuda.stream(s_in):
@@ -561,7 +582,7 @@ def run_ours(args):
             tot += e0.elapsed_time(e1)
         e2e_ms = tot / K
     o_ok = bool(torch.equal(o_host[0].view(torch.int16), out.cpu().view(torch.int16))) if ep is None else None
-    if world > 1:
+    if dist_on:
         t = torch.tensor([e2e_ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
@@ -569,7 +590,8 @@ def run_ours(args):
     e2e = {"value": T * world / (e2e_ms / 1e3), "unit": "tokens/s",
            "h2d_bytes_per_step": h_host[0].numel() * 2 + l_host[0].numel() * 4,
            "d2h_bytes_per_step": o_host[0].numel() * 2, "ms_per_step": e2e_ms,
-           "api": "PackedMoELayer.forward -> puzzle_moe_forward_ex (host pinned buffers)",
+           "api": ("ExpertParallelMoE." + ("forward_fixed" if ep_fixed else "forward") if ep is not None
+                   else "PackedMoELayer.forward -> puzzle_moe_forward_ex") + " (host pinned buffers)",
            "pipelined": ep is None and flush is None,
            "note": "copy-in of step i+1 and copy-out of step i-1 overlap step i's forward (two buffer sets, "
                    "separate copy streams)" if ep is None and flush is None else "sequential copies",
@@ -578,13 +600,15 @@ def run_ours(args):
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded N(0,1/in) experts merged+packed on GPU, tau=0.4; N(0,1) hidden and logits)",
-            "config": {"workload": f"{cfg.name} single MoE layer decode, batch {T} per GPU"
+            "config": {"workload": f"{cfg.name} single MoE layer {'decode' if T <= 64 else 'prefill'}, batch {T} per GPU"
                                    + (" (25% ratio: merged pairs + dense bf16 slots)" if args.ratio == 0.25 else "")
-                                   + (" (BASELINE.json configs[1])" if cfg.name == "mixtral" else ""),
+                                   + (" (BASELINE.json configs[1])" if cfg.name == "mixtral" and T <= 64 else (" (BASELINE.json configs[2])" if cfg.name == "mixtral" else "")),
                        "d_model": cfg.d_model, "d_ff": cfg.d_ff, "n_experts": cfg.n_experts,
                        "n_pairs": cfg.n_pairs, "top_k": cfg.top_k, "batch_per_gpu": T,
                        "parallelism": f"ep{world} (pairs sharded, NCCL all-to-all dispatch/combine, "
-                                      f"{T} tokens per rank)" if world > 1 else "single",
+                                      f"{T} tokens per rank, "
+                                      + ("fixed-capacity dispatch)" if ep_fixed else "variable-split dispatch)")
+                                      if dist_on else "single",
                        "l2": "inputs larger than L2 (packed layer %.2f GB)" % (layer.packed_bytes / 1e9) if big
                        else "L2 flushed between timed steps",
                        "launch": "CUDA graph replay of the whole forward" if graph is not None else "eager"},
@@ -617,7 +641,7 @@ def run_ours(args):
             except Exception as e:  # pragma: no cover
                 line["cpu_baseline"] = {"error": repr(e)}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
     return 0
@@ -829,6 +853,7 @@ def main(argv=None):
                          "0.25 (merged pairs + dense bf16 slots, R20)")
     ap.add_argument("--no-extra", action="store_true", help="skip the unpacked baseline / sweep / packer lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    ap.add_argument("--ep1", action="store_true", help="run the expert-parallel path in a 1-rank NCCL group")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     args = ap.parse_args(argv)
     if args.impl == "reference":
