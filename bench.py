@@ -614,10 +614,14 @@ def run_ours(args):
                        "launch": "CUDA graph replay of the whole forward" if graph is not None else "eager"},
             "roofline": roof, "step_weight_gbs": step_gbs, "gpu_launches": gpu_launches,
             "kernels": kern, "e2e": e2e}
+    if dist_on and ((world > 1 and not args.no_extra) or args.stack_ep):
+        stack_ep = stack_runs_ep(pz, args, device, part, rank, world)
+        line.setdefault("aux", {})["stack32_ep"] = stack_ep
     if rank == 0:
         line["clocks"] = clocks.summary(t0, t1)
-        line["aux"] = {"pack_stats": dict(zip(["rounded_up", "saturated", "nonfinite", "negative"], pack_stats)),
-                       "touched_pairs": n_touched}
+        line["aux"] = dict(line.get("aux", {}),
+                           pack_stats=dict(zip(["rounded_up", "saturated", "nonfinite", "negative"], pack_stats)),
+                           touched_pairs=n_touched)
         if not args.no_extra:
             try:
                 line["aux"]["unpacked_bf16_baseline"] = unpacked_baseline(pz, layer, cfg, hidden, logits, min(K, 50), W)
@@ -840,6 +844,73 @@ def stack_runs(pz, args, device, pk):
     return res
 
 
+def stack_runs_ep(pz, args, device, part, rank, world):
+    """BASELINE.json configs[4] as named: the 32-layer Mixtral-8x7B MoE stack at 50%
+    compression, EXPERT-PARALLEL -- every rank holds its share of each layer's merged pairs and
+    its own tokens (weak scaling), x_{l+1} = x_l + MoE_l(x_l). Batch-64 decode runs the
+    fixed-capacity dispatch (device-only) replayed as one CUDA graph of all 32 layers; the
+    8192-token prefill runs the variable-split dispatch eagerly. Time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2511_04805_b200.ep import ExpertParallelMoE, shard_dense, shard_packed
+    cfg = synth.CONFIGS["mixtral"]
+    n_layers = 32
+    eps = []
+    for l in range(n_layers):
+        layer, _ = build_layer_gpu(pz, cfg, 90000 + l, device)
+        w13_l, w2_l = shard_packed(layer.w13, layer.w2, part, rank)
+        local = pz.PackedMoELayer(w13_l, w2_l, torch.arange(2 * w13_l.shape[0], dtype=torch.int32, device=device),
+                                  shard_dense(layer.pair_dense, part, rank))
+        routing = pz.RoutingLayer(layer.n_pairs, cfg.d_model, cfg.d_ff, layer.expert_slot.clone(), w13_l)
+        eps.append(ExpertParallelMoE(part, rank, routing, local, cfg.d_model))
+        del layer
+    torch.cuda.empty_cache()
+    res = []
+    for T in (64, 8192):
+        g = torch.Generator(device=device)
+        g.manual_seed(777 + T + 1000 * rank)
+        x0 = torch.randn((T, cfg.d_model), generator=g, device=device).to(torch.bfloat16)
+        logits = [torch.randn((T, cfg.n_experts), generator=g, device=device) for _ in range(n_layers)]
+        fixed = T <= 64
+
+        def step():
+            x = x0
+            for l, ep in enumerate(eps):
+                if fixed:
+                    x = ep.forward_fixed(x, logits[l], cfg.top_k, cfg.renormalize, residual=x, path=pz.PATH_GEMV)
+                else:
+                    x = ep.forward(x, logits[l], cfg.top_k, cfg.renormalize, residual=x)
+            return x
+
+        step()
+        torch.cuda.synchronize()
+        run = step
+        if fixed and not args.no_graph:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                step()
+            run = gr.replay
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        dist.barrier()
+        K = 20 if fixed else 5
+        ms = timed_steps(run, K) / K
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        row = {"config": f"mixtral_stack32_ep{world}", "batch_per_rank": T, "ms_per_step": ms,
+               "tokens_per_s": T * world / (ms / 1e3), "layers": n_layers,
+               "dispatch": ("fixed-capacity, one CUDA graph of 32 layers" if fixed and not args.no_graph
+                            else "fixed-capacity, eager" if fixed else "variable-split, eager")}
+        if not fixed:
+            row["tflops_per_rank"] = 2 * 3 * cfg.d_model * cfg.d_ff * T * cfg.top_k * n_layers / (ms / 1e3) / 1e12
+        res.append(row)
+    del eps
+    torch.cuda.empty_cache()
+    return res
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -854,6 +925,7 @@ def main(argv=None):
     ap.add_argument("--no-extra", action="store_true", help="skip the unpacked baseline / sweep / packer lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--ep1", action="store_true", help="run the expert-parallel path in a 1-rank NCCL group")
+    ap.add_argument("--stack-ep", action="store_true", help="with --ep1: also the expert-parallel 32-layer stack")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     args = ap.parse_args(argv)
     if args.impl == "reference":
