@@ -57,6 +57,22 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Copy one row of n16 16-byte words with a warp: 8 loads in flight per lane before the stores
+// (a row is latency-bound: one load->store round trip per 512 B otherwise).
+__device__ __forceinline__ void warp_copy_row(const uint4* __restrict__ sp, uint4* __restrict__ dp, int64_t n16,
+                                              int lane) {
+  constexpr int U = 8;
+  for (int64_t c0 = lane; c0 < n16; c0 += 32 * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c0 + u * 32 < n16) v[u] = sp[c0 + u * 32];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c0 + u * 32 < n16) dp[c0 + u * 32] = v[u];
+  }
+}
+
 // ---- packed word layout (Algorithm 1) ----
 // bit15 S_i | bit14 S_j | bit13 M_i | bit12 M_j | bits 11..7 e' = e-112 | bits 6..0 mantissa
 

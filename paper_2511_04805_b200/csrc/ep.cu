@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) k_ep_dispatch(const uint16_t* __restrict_
   const int lane = threadIdx.x & 31;
   const uint4* sp = reinterpret_cast<const uint4*>(hidden + (int64_t)assign_token[lo + i] * cols);
   uint4* dp = reinterpret_cast<uint4*>(send_rows + r * cols);
-  for (int64_t c = lane; c < cols / 8; c += 32) dp[c] = sp[c];
+  warp_copy_row(sp, dp, cols / 8, lane);
 }
 
 // Owner side. recv_counts[s][b] (s = source rank, b < lb local buckets, row stride lb_max).

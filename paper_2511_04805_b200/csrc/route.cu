@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(256) k_gather_rows(const uint16_t* __restrict_
   const int64_t s = index[i];
   const uint4* sp = reinterpret_cast<const uint4*>(src + s * cols);
   uint4* dp = reinterpret_cast<uint4*>(dst + i * cols);
-  for (int64_t c = lane; c < cols / 8; c += 32) dp[c] = sp[c];
+  warp_copy_row(sp, dp, cols / 8, lane);
   __syncwarp();
   if (lane == 0) PZ_RT(1, true);
 }
