@@ -92,9 +92,10 @@ def _worker(rank, world, port, cfg_fields, T, outdir, n_merged=None):
                  None if dense_l is None else dense_l.numpy())
         layer = ExpertParallelMoE(part, rank, {"expert_slot": slot, "n_pairs": n_slots}, local, cfg.d_model,
                                   ops=OracleOps())
-        hb = synth.hidden_bits(cfg, T, seed=100 + rank)
-        lg = synth.router_logits(cfg, T, seed=200 + rank)
-        rb = synth.hidden_bits(cfg, T, seed=300 + rank)
+        Tr = T - rank  # ragged: the ranks hold different token counts (fixed path: cap_tokens = T + 1)
+        hb = synth.hidden_bits(cfg, Tr, seed=100 + rank)
+        lg = synth.router_logits(cfg, Tr, seed=200 + rank)
+        rb = synth.hidden_bits(cfg, Tr, seed=300 + rank)
         hidden = torch.from_numpy(hb.view(np.int16)).view(torch.bfloat16)
         resid = torch.from_numpy(oracle.bf16_bits_to_f32(rb))
         out = layer.forward(hidden, torch.from_numpy(lg), cfg.top_k, cfg.renormalize, residual=resid)

@@ -10,7 +10,7 @@ import torch.distributed as dist
 
 import oracle
 import synth
-from helpers import assert_close, oracle_packed_layer
+from helpers import assert_close, oracle_mixed_layer, oracle_packed_layer
 
 pytestmark = pytest.mark.gpu
 
@@ -141,25 +141,31 @@ def test_ep_fixed_argument_errors():
         pz.ep_recv_plan(torch.zeros(4, dtype=torch.int32, device="cuda"), 1, 4, 5, 8)
 
 
-def _ep_world1(cfg):
+def _ep_world1(cfg, n_merged=None):
     import paper_2511_04805_b200 as pz
-    from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_packed
-    w13, w2, slot, _ = oracle_packed_layer(cfg)
+    from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_dense, shard_packed
+    if n_merged is None:
+        w13, w2, slot, _ = oracle_packed_layer(cfg)
+        dense = None
+    else:  # 25% ratio: merged pairs + dense bf16 slots (R20)
+        w13, w2, slot, dense = oracle_mixed_layer(cfg, n_merged)
     w13_d = torch.from_numpy(w13.view(np.int16)).cuda()
     w2_d = torch.from_numpy(w2.view(np.int16)).cuda()
     slot_d = torch.from_numpy(slot).cuda()
-    part = Partition(cfg.n_pairs, 1)
+    n_slots = w13.shape[0]
+    part = Partition(n_slots, 1)
     w13_l, w2_l = shard_packed(w13_d, w2_d, part, 0)
-    local = pz.PackedMoELayer(w13_l, w2_l, torch.arange(2 * w13_l.shape[0], dtype=torch.int32, device="cuda"))
-    route = pz.RoutingLayer(cfg.n_pairs, cfg.d_model, cfg.d_ff, slot_d, w13_l)
-    return ExpertParallelMoE(part, 0, route, local, cfg.d_model), (w13, w2, slot)
+    dense_l = shard_dense(None if dense is None else torch.from_numpy(dense.astype(np.uint8)).cuda(), part, 0)
+    local = pz.PackedMoELayer(w13_l, w2_l, torch.arange(2 * w13_l.shape[0], dtype=torch.int32, device="cuda"), dense_l)
+    route = pz.RoutingLayer(n_slots, cfg.d_model, cfg.d_ff, slot_d, w13_l)
+    return ExpertParallelMoE(part, 0, route, local, cfg.d_model), (w13, w2, slot, dense)
 
 
 @pytest.mark.parametrize("cfg", [synth.MoEConfig("ep_small", 30, 256, 512, 8, 2, True),
                                  synth.MoEConfig("ep_fine", 31, 128, 256, 16, 4, False)], ids=lambda c: c.name)
 @pytest.mark.parametrize("T,path", [(37, 0), (64, 1), (5, 1), (200, 0)])
 def test_ep_fixed_world1_matches_oracle(nccl_group, cfg, T, path):
-    ep, (w13, w2, slot) = _ep_world1(cfg)
+    ep, (w13, w2, slot, _) = _ep_world1(cfg)
     hb = synth.hidden_bits(cfg, T, seed=7)
     lg = synth.router_logits(cfg, T, seed=8)
     rb = synth.hidden_bits(cfg, T, seed=9)
@@ -172,12 +178,26 @@ def test_ep_fixed_world1_matches_oracle(nccl_group, cfg, T, path):
     assert_close(out.float().cpu().numpy(), ref, "fixed-capacity ep vs oracle")
 
 
+@pytest.mark.parametrize("T,path", [(64, 1), (150, 0)])
+def test_ep_fixed_world1_dense_slots_match_oracle(nccl_group, T, path):
+    """25% ratio (merged pairs + dense bf16 slots) through the fixed-capacity dispatch."""
+    cfg = synth.MoEConfig("ep25_gpu", 33, 256, 512, 8, 2, True)
+    ep, (w13, w2, slot, dense) = _ep_world1(cfg, n_merged=2)
+    hb = synth.hidden_bits(cfg, T, seed=11)
+    lg = synth.router_logits(cfg, T, seed=12)
+    h = torch.from_numpy(hb.view(np.int16)).cuda().view(torch.bfloat16)
+    out = ep.forward_fixed(h, torch.from_numpy(lg).cuda(), cfg.top_k, cfg.renormalize, path=path)
+    torch.cuda.synchronize()
+    ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, pair_dense=dense)
+    assert_close(out.float().cpu().numpy(), ref, "fixed-capacity ep (dense slots) vs oracle")
+
+
 def test_ep_fixed_graph_capture(nccl_group):
     """The fixed-capacity layer has no host sync: it captures into a CUDA graph (NCCL inside)
     and a replay on new inputs equals the oracle."""
     import paper_2511_04805_b200 as pz
     cfg = synth.MoEConfig("ep_graph", 32, 256, 512, 8, 2, True)
-    ep, (w13, w2, slot) = _ep_world1(cfg)
+    ep, (w13, w2, slot, _) = _ep_world1(cfg)
     T = 16
     h = torch.empty((T, cfg.d_model), dtype=torch.bfloat16, device="cuda")
     lg = torch.empty((T, cfg.n_experts), dtype=torch.float32, device="cuda")
