@@ -374,7 +374,9 @@ def run_ours(args):
                     os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=device)
+        import datetime
+        # generous timeout: the non-zero ranks wait in barriers while rank 0 prints its line
+        dist.init_process_group("nccl", device_id=device, timeout=datetime.timedelta(minutes=30))
     if rank == 0 and not os.path.exists(pz.LIB_PATH):
         pzbuild.build()
     if dist_on:
@@ -622,7 +624,7 @@ def run_ours(args):
         line["aux"] = dict(line.get("aux", {}),
                            pack_stats=dict(zip(["rounded_up", "saturated", "nonfinite", "negative"], pack_stats)),
                            touched_pairs=n_touched)
-        if not args.no_extra:
+        if not args.no_extra and not dist_on:  # single-GPU extras (the N = 1 run carries them)
             try:
                 line["aux"]["unpacked_bf16_baseline"] = unpacked_baseline(pz, layer, cfg, hidden, logits, min(K, 50), W)
             except Exception as e:  # pragma: no cover
