@@ -277,7 +277,8 @@ def unpacked_baseline(pz, layer, cfg, hidden, logits, K: int, W: int):
             "how": "puzzle_unpack once -> dense bf16 experts; per step torch topk/softmax + per-expert cuBLAS bf16 matmuls"}
 
 
-def cpu_oracle_timing(cfg, T_batch: int, budget_s: float = 12.0, max_calls: int | None = None):
+def cpu_oracle_timing(cfg, T_batch: int, budget_s: float = 12.0, max_calls: int | None = None,
+                      one_core: bool = False):
     """Time the oracle (as it stands) on host cores on a bounded sample of the workload:
     `n` tokens of the same config with random packed words (timing is data-independent)."""
     import oracle
@@ -298,10 +299,20 @@ def cpu_oracle_timing(cfg, T_batch: int, budget_s: float = 12.0, max_calls: int 
         calls += 1
         if t_total >= budget_s or (max_calls and calls >= max_calls):
             break
-    return {"value": calls * n / t_total, "unit": "tokens/s", "cores": threads, "kind": "oracle",
-            "sample": f"{calls} oracle calls x {n} tokens of {cfg.name} (d={d}, d_ff={f}, E={cfg.n_experts}, "
-                      f"top-{cfg.top_k}) on random packed words; f64 accumulation, OpenMP over tokens",
-            "seconds": t_total}
+    res = {"value": calls * n / t_total, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+           "sample": f"{calls} oracle calls x {n} tokens of {cfg.name} (d={d}, d_ff={f}, E={cfg.n_experts}, "
+                     f"top-{cfg.top_k}) on random packed words; f64 accumulation, OpenMP over tokens",
+           "seconds": t_total}
+    if one_core and threads > 1:  # also a 1-core number (one token, one call)
+        oracle.set_num_threads(1)
+        try:
+            t0 = time.perf_counter()
+            oracle.moe_forward(w13, w2, slot, hb[:1], lg[:1], cfg.top_k, cfg.renormalize)
+            res["one_core"] = {"value": 1 / (time.perf_counter() - t0), "unit": "tokens/s", "cores": 1,
+                               "sample": "1 oracle call x 1 token"}
+        finally:
+            oracle.set_num_threads(threads)
+    return res
 
 
 # --------------------------------------------------------------------------- arms
@@ -459,6 +470,21 @@ def run_ours(args):
         # the launching stream (graph replays carry no per-kernel events)
         with pz.profile_window() as prof:
             timed_steps(step, K, flush)
+    # per-step distribution (separate pass, one event pair per step; the headline stays the
+    # back-to-back average above)
+    run1 = graph.replay if graph is not None else step
+    ev_pairs = []
+    for _ in range(min(K, 100)):
+        if flush is not None:
+            flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        run1()
+        b.record()
+        ev_pairs.append((a, b))
+    torch.cuda.synchronize()
+    per_step = sorted(a.elapsed_time(b) for a, b in ev_pairs)
+    pct = {q: per_step[min(len(per_step) - 1, int(round(q / 100 * (len(per_step) - 1))))] for q in (10, 50, 90)}
     time.sleep(0.05)
     clocks.stop()
     ms = total_ms / K
@@ -615,6 +641,8 @@ def run_ours(args):
                        else "L2 flushed between timed steps",
                        "launch": "CUDA graph replay of the whole forward" if graph is not None else "eager"},
             "roofline": roof, "step_weight_gbs": step_gbs, "gpu_launches": gpu_launches,
+            "step_ms_percentiles": {"p10": pct[10], "p50": pct[50], "p90": pct[90], "steps": len(per_step),
+                                    "note": "one event pair per step, separate pass (rank-local)"},
             "kernels": kern, "e2e": e2e}
     if dist_on and ((world > 1 and not args.no_extra) or args.stack_ep):
         stack_ep = stack_runs_ep(pz, args, device, part, rank, world)
@@ -643,7 +671,7 @@ def run_ours(args):
                 line["aux"]["stack32"] = {"error": repr(e)}
         if world == 1 and not args.no_cpu:
             try:
-                line["cpu_baseline"] = cpu_oracle_timing(cfg, T)
+                line["cpu_baseline"] = cpu_oracle_timing(cfg, T, one_core=True)
             except Exception as e:  # pragma: no cover
                 line["cpu_baseline"] = {"error": repr(e)}
         print(json.dumps(line), flush=True)
