@@ -214,8 +214,9 @@ int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden,
  *   assign_token i32 [T*top_k]    token of assignment a (assignments grouped by bucket)
  *   assign_of    i32 [T*top_k]    assignment index of (t, j)
  *   The order of assignments inside one bucket is unspecified (results do not depend on it).
- *   workspace: device scratch of >= puzzle_moe_route_workspace_size(L) bytes (used when
- *   T*top_k > 4096; batches up to that size route inside one CTA).
+ *   workspace: device scratch of >= puzzle_moe_route_workspace_size(L) bytes (decode batches,
+ *   T <= 64, route with a top-k grid + a scatter grid and keep per-CTA histograms there; batches
+ *   with T*top_k > 4096 keep global counts there; the sizes in between route inside one CTA).
  * ------------------------------------------------------------------------------------- */
 size_t puzzle_moe_route_workspace_size(const puzzle_moe_layer* L);
 int puzzle_moe_route(const puzzle_moe_layer* L, const float* router_logits, int64_t T,

@@ -512,7 +512,10 @@ int puzzle_moe_forward(const puzzle_moe_layer* L, const uint16_t* hidden, const 
 
 size_t puzzle_moe_route_workspace_size(const puzzle_moe_layer* L) {
   if (check_layer(L)) return 0;
-  return (size_t)2 * 2 * L->n_pairs * sizeof(int32_t);
+  // large batches: global counts + cursors; decode batches: the two-grid routing's histograms
+  const int64_t ints = std::max<int64_t>(2 * 2 * (int64_t)L->n_pairs,
+                                         route_dec_scratch_ints(kGemvMaxTokens, std::min(16, L->n_experts), L->n_pairs));
+  return (size_t)ints * sizeof(int32_t);
 }
 
 int puzzle_moe_route(const puzzle_moe_layer* L, const float* logits, int64_t T, int k, int renorm,
@@ -527,6 +530,10 @@ int puzzle_moe_route(const puzzle_moe_layer* L, const float* logits, int64_t T, 
   if (T == 0) return PUZZLE_OK;
   if (workspace_bytes < puzzle_moe_route_workspace_size(L) || (!workspace && workspace_bytes))
     return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_moe_route_workspace_size(L)");
+  if (T <= kGemvMaxTokens)  // decode batches: the forward's two-grid routing (top-k grid + scatter grid)
+    return launch_route_dec(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs, topk_idx, topk_gate,
+                            bucket_off, assign_token, assign_of, nullptr, nullptr, nullptr, 0,
+                            static_cast<int32_t*>(workspace), nullptr, L->d_model, nullptr, (cudaStream_t)stream);
   return launch_route(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs, topk_idx, topk_gate,
                       bucket_off, assign_token, assign_of, nullptr, nullptr, nullptr, 0,
                       static_cast<int32_t*>(workspace), nullptr, L->d_model, nullptr, nullptr, (cudaStream_t)stream);

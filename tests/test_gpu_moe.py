@@ -70,7 +70,7 @@ def test_skewed_routing_all_tokens_one_pair(pz):
     assert_close(got, ref, "skew")
 
 
-@pytest.mark.parametrize("T", [300, 1000])  # 1000 x 6 > 4096: the multi-CTA routing path
+@pytest.mark.parametrize("T", [7, 37, 64, 300, 1000])  # <= 64: two-grid decode routing; 1000 x 6 > 4096: multi-CTA
 def test_route_outputs(pz, T):
     cfg = synth.MoEConfig("route", 9, 64, 64, 64, 6, False)
     layer, (w13, w2, slot) = _layer(pz, cfg)
