@@ -251,47 +251,54 @@ int puzzle_gather_rows(const uint16_t* src, const int32_t* index, int64_t n_rows
  * Fixed-capacity expert-parallel dispatch (BASELINE.json config 5, "expert-
  * parallel with NCCL all-to-all"; the unit of placement is the merged PAIR, so
  * both experts of a pair stay on one GPU and each packed tile is still read once).
- * Every rank reserves `cap` rows per destination rank in its send buffer (cap >= T*top_k: the
- * worst case, all of its assignments on one owner), so both all-to-alls of a layer have EQUAL,
- * host-known splits and the index work runs on the device: the layer needs no device->host
- * copy and can be captured in a CUDA graph. All ranks must use the same cap.
+ * Every rank reserves R = cap + 1 rows per destination rank in its send buffer (cap >= T*top_k:
+ * the worst case, all of its assignments on one owner; the extra HEADER row carries the
+ * destination's bucket counts), so each all-to-all of a layer has EQUAL, host-known splits, rows
+ * and counts travel together, and the index work runs on the device: the layer needs no
+ * device->host copy and can be captured in a CUDA graph. All ranks must use the same cap.
  *
  * dest_pairs  HOST int32 [world][2]: rank q owns global pairs [dest_pairs[2q], dest_pairs[2q+1])
  *             (whole pairs; or, when pairs are split along d_ff, the one pair q holds a slice
  *             of). Every pair must have the same nonzero number S of owners.
- * Local bucket of rank q: 2*(pair - dest_pairs[2q]) + pos. lb_max >= every rank's local
- * bucket count (the row stride of the count tables). Errors: INVALID_ARGUMENT for bad sizes,
- * NULL pointers or a malformed dest_pairs; UNSUPPORTED for world > 64, world*cap >= 2^31.
+ * Local bucket of rank q: 2*(pair - dest_pairs[2q]) + pos. lb_max >= every rank's local bucket
+ * count, and 4*lb_max <= 2*d_model (the counts fit in one header row). Errors: INVALID_ARGUMENT
+ * for bad sizes, NULL pointers or a malformed dest_pairs; UNSUPPORTED for world > 64,
+ * world*(cap+1) >= 2^31, a header row too small for lb_max counts.
  *
  * puzzle_ep_dispatch -- sender side, after puzzle_moe_route on this rank's T tokens
  *   (n_assign = T*top_k, bucket_off / assign_token as route wrote them):
- *   send_rows   bf16 [world][cap][d_model]: send_rows[q][i] = hidden[assign_token[bucket_off[
- *               2 lo_q] + i]] for i < n_q = bucket_off[2 hi_q] - bucket_off[2 lo_q] (q's rows, in
- *               bucket order); rows i >= n_q are not written (never read downstream).
- *   send_counts i32  [world][lb_max]: per-local-bucket counts of q's buckets, 0-padded.
+ *   send_rows  bf16 [world][cap+1][d_model], region q:
+ *              row i < n_q = bucket_off[2 hi_q] - bucket_off[2 lo_q]: hidden[assign_token[
+ *              bucket_off[2 lo_q] + i]] (q's rows, in bucket order); rows n_q..cap-1 are not
+ *              written (never read downstream);
+ *              row cap (header): int32 [lb_max] in its first 4*lb_max bytes = the counts of
+ *              q's local buckets, 0-padded.
  */
 int puzzle_ep_dispatch(const uint16_t* hidden, const int32_t* assign_token, const int32_t* bucket_off, int n_pairs,
                        const int32_t* dest_pairs, int world, int64_t n_assign, int64_t cap, int lb_max,
-                       int d_model, uint16_t* send_rows, int32_t* send_counts, puzzle_stream_t stream);
+                       int d_model, uint16_t* send_rows, puzzle_stream_t stream);
 
-/* puzzle_ep_recv_plan -- owner side, from recv_counts i32 [world][lb_max] (row s = what source
- *   rank s sent: counts of this rank's n_local_buckets buckets). Received rows sit at
- *   s*cap + w. The local order is (bucket, source, arrival):
+/* puzzle_ep_recv_plan -- owner side, on recv_rows bf16 [world][cap+1][d_model] (region s = what
+ *   source rank s sent: its rows for this rank, then the header with the counts of this rank's
+ *   n_local_buckets buckets). Received row w of region s sits at s*(cap+1) + w. The local order
+ *   is (bucket, source, arrival):
  *   local_off  i32 [n_local_buckets + 1]  bucket offsets of the regrouped rows (the bucket_off
  *              argument of puzzle_moe_experts on this rank's shard)
- *   gather_idx i32 [world*cap]  local row l <- received row gather_idx[l]; l >= local_off[last]
+ *   gather_idx i32 [world*cap]      local row l <- received row gather_idx[l]; l >= local_off[last]
  *              -> 0 (padding: puzzle_gather_rows of all world*cap rows stays in bounds)
- *   return_idx i32 [world*cap]  received slot r <- local row return_idx[r] (0 for unused slots)
+ *   return_idx i32 [world*(cap+1)]  received slot r <- local row return_idx[r] (0 for unused
+ *              slots and header rows): gathering the experts' outputs with it gives the return
+ *              buffer in the same region layout.
  *   Limits: n_local_buckets <= 1024, (3*world*n_local_buckets + world + n_local_buckets + 1)*4
  *   bytes <= 48 KB (UNSUPPORTED otherwise). */
-int puzzle_ep_recv_plan(const int32_t* recv_counts, int world, int lb_max, int n_local_buckets, int64_t cap,
+int puzzle_ep_recv_plan(const uint16_t* recv_rows, int world, int n_local_buckets, int64_t cap, int d_model,
                         int32_t* local_off, int32_t* gather_idx, int32_t* return_idx, puzzle_stream_t stream);
 
-/* puzzle_ep_home_index -- home side, after the return all-to-all (y rows [world][cap], region q
- *   = what owner q computed for this rank's rows, in the order puzzle_ep_dispatch sent them).
+/* puzzle_ep_home_index -- home side, after the return all-to-all (y rows [world][cap+1], region
+ *   q = what owner q computed for this rank's rows, in the order puzzle_ep_dispatch sent them).
  *   For assignment (t, j) = a = assign_of[t*top_k + j] in global bucket g (pair p = g/2) and the
  *   s-th owner q_s of p (ascending rank, s < S):
- *   aof_s  i32 [T][top_k*S]: aof_s[t][j*S + s] = q_s*cap + (a - bucket_off[2 lo_{q_s}])
+ *   aof_s  i32 [T][top_k*S]: aof_s[t][j*S + s] = q_s*(cap+1) + (a - bucket_off[2 lo_{q_s}])
  *   gate_s f32 [T][top_k*S]: gate_s[t][j*S + s] = topk_gate[t][j]
  *   so puzzle_moe_combine(y, aof_s, gate_s, T, top_k*S, ...) sums the S d_ff-slice partials of
  *   every (t, j) with its gate (S = 1: the plain combine of (a6)). */

@@ -92,8 +92,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_moe_forward_calib": ([P, P, P, I64, I, I, P, P, P, P, P, SZ, I, P], I),
             "puzzle_quant_pack": ([P, P, P, P, P, I64, I64, P, P, P], I),
             "puzzle_quant_unpack": ([P, P, I, I64, I64, P, P], I),
-            "puzzle_ep_dispatch": ([P, P, P, I, P, I, I64, I64, I, I, P, P, P], I),
-            "puzzle_ep_recv_plan": ([P, I, I, I, I64, P, P, P, P], I),
+            "puzzle_ep_dispatch": ([P, P, P, I, P, I, I64, I64, I, I, P, P], I),
+            "puzzle_ep_recv_plan": ([P, I, I, I64, I, P, P, P, P], I),
             "puzzle_ep_home_index": ([P, P, P, I, P, I, I64, I64, I, P, P, P], I),
             "puzzle_profile_begin": ([], I),
             "puzzle_profile_end": ([ctypes.c_char_p, SZ], I),
@@ -316,28 +316,33 @@ def _dest_pairs(dest_pairs):
 
 
 def ep_dispatch(hidden, assign_token, bucket_off, n_pairs: int, dest_pairs, cap: int, lb_max: int,
-                send_rows=None, send_counts=None, stream=None):
-    """puzzle_ep_dispatch -> (send_rows [world*cap][d] bf16, send_counts [world*lb_max] i32)."""
+                send_rows=None, stream=None):
+    """puzzle_ep_dispatch -> send_rows [world*(cap+1)][d] (per destination: cap row slots, then the
+    header row whose first 4*lb_max bytes are the int32 bucket counts)."""
     arr, dp, world = _dest_pairs(dest_pairs)
     d = hidden.shape[1]
     if send_rows is None:
-        send_rows = torch.empty((world * cap, d), dtype=hidden.dtype, device=hidden.device)
-    if send_counts is None:
-        send_counts = torch.empty(world * lb_max, dtype=torch.int32, device=hidden.device)
+        send_rows = torch.empty((world * (cap + 1), d), dtype=hidden.dtype, device=hidden.device)
     _check(load_library().puzzle_ep_dispatch(_p(hidden), _p(assign_token), _p(bucket_off), int(n_pairs), dp, world,
                                              assign_token.numel(), int(cap), int(lb_max), d, _p(send_rows),
-                                             _p(send_counts), _stream(stream)), "puzzle_ep_dispatch")
-    return send_rows, send_counts
+                                             _stream(stream)), "puzzle_ep_dispatch")
+    return send_rows
 
 
-def ep_recv_plan(recv_counts, world: int, lb_max: int, n_local_buckets: int, cap: int, stream=None):
-    """puzzle_ep_recv_plan -> (local_off [lb+1], gather_idx [world*cap], return_idx [world*cap])."""
-    dev = recv_counts.device
+def ep_header_counts(rows, world: int, cap: int, lb: int):
+    """The int32 bucket counts carried by the header rows of a [world*(cap+1)][d] region buffer
+    (a view for inspection / tests)."""
+    return rows.view(world, cap + 1, -1)[:, cap].contiguous().view(torch.int32)[:, :lb]
+
+
+def ep_recv_plan(recv_rows, world: int, n_local_buckets: int, cap: int, stream=None):
+    """puzzle_ep_recv_plan -> (local_off [lb+1], gather_idx [world*cap], return_idx [world*(cap+1)])."""
+    dev = recv_rows.device
     local_off = torch.empty(n_local_buckets + 1, dtype=torch.int32, device=dev)
-    gidx = torch.empty(world * cap, dtype=torch.int32, device=dev)
-    ridx = torch.empty(world * cap, dtype=torch.int32, device=dev)
-    _check(load_library().puzzle_ep_recv_plan(_p(recv_counts), int(world), int(lb_max), int(n_local_buckets), int(cap),
-                                              _p(local_off), _p(gidx), _p(ridx), _stream(stream)),
+    gidx = torch.empty(max(world * cap, 1), dtype=torch.int32, device=dev)[:world * cap]
+    ridx = torch.empty(world * (cap + 1), dtype=torch.int32, device=dev)
+    _check(load_library().puzzle_ep_recv_plan(_p(recv_rows), int(world), int(n_local_buckets), int(cap),
+                                              recv_rows.shape[1], _p(local_off), _p(gidx), _p(ridx), _stream(stream)),
            "puzzle_ep_recv_plan")
     return local_off, gidx, ridx
 

@@ -33,9 +33,9 @@ int launch_combine(const float*, const int32_t*, const float*, int64_t, int, int
                    uint16_t*, cudaStream_t);
 int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16_t*, cudaStream_t);
 int launch_ep_dispatch(const uint16_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int64_t, int, int,
-                       uint16_t*, int32_t*, cudaStream_t);
+                       uint16_t*, cudaStream_t);
 size_t ep_recv_plan_smem(int world, int lb);
-int launch_ep_recv_plan(const int32_t*, int, int, int, int64_t, int32_t*, int32_t*, int32_t*, cudaStream_t);
+int launch_ep_recv_plan(const uint16_t*, int, int, int64_t, int, int32_t*, int32_t*, int32_t*, cudaStream_t);
 int launch_ep_home_index(const int32_t*, const float*, const int32_t*, int, const int32_t*, int, int64_t, int64_t,
                          int32_t*, float*, int*, cudaStream_t);
 bool tc_supported(int d, int f);
@@ -587,29 +587,31 @@ int puzzle_gather_rows(const uint16_t* src, const int32_t* index, int64_t n_rows
 
 int puzzle_ep_dispatch(const uint16_t* hidden, const int32_t* assign_token, const int32_t* bucket_off, int n_pairs,
                        const int32_t* dest_pairs, int world, int64_t n_assign, int64_t cap, int lb_max,
-                       int d_model, uint16_t* send_rows, int32_t* send_counts, puzzle_stream_t stream) {
+                       int d_model, uint16_t* send_rows, puzzle_stream_t stream) {
   if (n_pairs < 1 || n_assign < 0 || cap < n_assign || lb_max < 0 || d_model < 8)
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes (need n_pairs >= 1, 0 <= n_assign <= cap)");
-  if (!dest_pairs || !send_counts || !bucket_off || (n_assign > 0 && (!hidden || !assign_token)) ||
-      (cap > 0 && !send_rows))
+  if (!dest_pairs || !bucket_off || !send_rows || (n_assign > 0 && (!hidden || !assign_token)))
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (d_model % 8 || !al16(hidden) || !al16(send_rows)) return fail(PUZZLE_ERR_UNSUPPORTED, "d_model % 8 / alignment");
   if (int rc = check_device()) return rc;
   return launch_ep_dispatch(hidden, assign_token, bucket_off, dest_pairs, world, n_pairs, cap, lb_max, d_model,
-                            send_rows, send_counts, (cudaStream_t)stream);
+                            send_rows, (cudaStream_t)stream);
 }
 
-int puzzle_ep_recv_plan(const int32_t* recv_counts, int world, int lb_max, int n_local_buckets, int64_t cap,
+int puzzle_ep_recv_plan(const uint16_t* recv_rows, int world, int n_local_buckets, int64_t cap, int d_model,
                         int32_t* local_off, int32_t* gather_idx, int32_t* return_idx, puzzle_stream_t stream) {
-  if (world < 1 || world > 64 || n_local_buckets < 0 || n_local_buckets > lb_max || cap < 0)
-    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes (1 <= world <= 64, 0 <= n_local_buckets <= lb_max, cap >= 0)");
+  if (world < 1 || world > 64 || n_local_buckets < 0 || cap < 0 || d_model < 8 || d_model % 8)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes (1 <= world <= 64, n_local_buckets >= 0, cap >= 0, d_model % 8 == 0)");
+  if (4 * (int64_t)n_local_buckets > 2 * (int64_t)d_model)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "header row holds 2 * d_model / 4 counts: n_local_buckets too large");
   if (n_local_buckets > 1024 || pz::ep_recv_plan_smem(world, n_local_buckets) > 48 * 1024 ||
-      (int64_t)world * cap > INT32_MAX)
-    return fail(PUZZLE_ERR_UNSUPPORTED, "n_local_buckets <= 1024, world * n_local_buckets <= ~4000, world * cap < 2^31");
-  if (!recv_counts || !local_off || (cap > 0 && (!gather_idx || !return_idx)))
+      (int64_t)world * (cap + 1) > INT32_MAX)
+    return fail(PUZZLE_ERR_UNSUPPORTED, "n_local_buckets <= 1024, world * n_local_buckets <= ~4000, world * (cap + 1) < 2^31");
+  if (!recv_rows || !local_off || !return_idx || (cap > 0 && !gather_idx))
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!al16(recv_rows)) return fail(PUZZLE_ERR_UNSUPPORTED, "recv_rows must be 16-byte aligned");
   if (int rc = check_device()) return rc;
-  return launch_ep_recv_plan(recv_counts, world, lb_max, n_local_buckets, cap, local_off, gather_idx, return_idx,
+  return launch_ep_recv_plan(recv_rows, world, n_local_buckets, cap, d_model, local_off, gather_idx, return_idx,
                              (cudaStream_t)stream);
 }
 
@@ -620,7 +622,7 @@ int puzzle_ep_home_index(const int32_t* assign_of, const float* topk_gate, const
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes (need n_pairs >= 1, T >= 0, top_k >= 1, cap >= T * top_k)");
   if (!dest_pairs || (T > 0 && (!assign_of || !topk_gate || !bucket_off || !aof_s || !gate_s)))
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
-  if ((int64_t)world * cap > INT32_MAX) return fail(PUZZLE_ERR_UNSUPPORTED, "world * cap must fit in int32");
+  if ((int64_t)world * (cap + 1) > INT32_MAX) return fail(PUZZLE_ERR_UNSUPPORTED, "world * (cap + 1) must fit in int32");
   if (T > 0)
     if (int rc = check_device()) return rc;
   return launch_ep_home_index(assign_of, topk_gate, bucket_off, n_pairs, dest_pairs, world, cap, T * top_k, aof_s,

@@ -10,6 +10,9 @@
 // (route -> dispatch -> a2a -> recv plan -> gather -> experts -> gather -> a2a -> combine)
 // that a CUDA graph can capture.
 //
+// Region layout: every destination q gets R = cap + 1 rows of the send buffer: rows 0..n_q-1
+// carry the token rows, row cap (the HEADER) carries q's per-local-bucket counts as int32 in its
+// first 4*lb_max bytes -- so one all-to-all moves rows and counts together (no count exchange).
 // Partition (EpRanks): rank q owns the global pairs [lo[q], hi[q]) -- whole pairs, or the one
 // pair of which it holds a d_ff slice; every pair has the same number S of owners.
 // Local bucket of rank q: 2 * (pair - lo[q]) + pos (bucket b = 2 * pair + pos globally).
@@ -28,24 +31,24 @@ struct EpRanks {
 
 namespace {
 
-// send_rows[q][i] = hidden[assign_token[off[2 lo_q] + i]] for i < n_q (warp per row, 16-B
-// copies); CTA 0 also writes send_counts[q][b] (0 past q's local buckets).
+// send_rows[q*R + i] = hidden[assign_token[off[2 lo_q] + i]] for i < n_q (warp per row, 8 loads
+// in flight per lane); the header row q*R + cap gets q's bucket counts (0 past q's buckets).
 __global__ void __launch_bounds__(256) k_ep_dispatch(const uint16_t* __restrict__ hidden,
                                                      const int32_t* __restrict__ assign_token,
                                                      const int32_t* __restrict__ off, EpRanks R, int64_t cap,
-                                                     int lb_max, int64_t cols, uint16_t* __restrict__ send_rows,
-                                                     int32_t* __restrict__ send_counts) {
+                                                     int lb_max, int64_t cols, uint16_t* __restrict__ send_rows) {
   pdl_wait();
   pdl_trigger();
+  const int64_t reg = cap + 1;
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < R.world * lb_max; i += blockDim.x) {
       const int q = i / lb_max, b = i - q * lb_max;
       const int nb = 2 * (R.hi[q] - R.lo[q]);
       const int g = 2 * R.lo[q] + b;
-      send_counts[i] = b < nb ? off[g + 1] - off[g] : 0;
+      reinterpret_cast<int32_t*>(send_rows + ((int64_t)q * reg + cap) * cols)[b] = b < nb ? off[g + 1] - off[g] : 0;
     }
   }
-  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // data row (q, i), i < cap
   if (r >= (int64_t)R.world * cap) return;
   const int q = (int)(r / cap);
   const int64_t i = r - (int64_t)q * cap;
@@ -53,16 +56,17 @@ __global__ void __launch_bounds__(256) k_ep_dispatch(const uint16_t* __restrict_
   if (i >= n) return;
   const int lane = threadIdx.x & 31;
   const uint4* sp = reinterpret_cast<const uint4*>(hidden + (int64_t)assign_token[lo + i] * cols);
-  uint4* dp = reinterpret_cast<uint4*>(send_rows + r * cols);
+  uint4* dp = reinterpret_cast<uint4*>(send_rows + ((int64_t)q * reg + i) * cols);
   warp_copy_row(sp, dp, cols / 8, lane);
 }
 
-// Owner side. recv_counts[s][b] (s = source rank, b < lb local buckets, row stride lb_max).
-// Local order = (bucket, source, arrival): local row of recv row (s, w) with w in source s's
-// bucket b = loff[b] + sum_{s'<s} rc[s'][b] + (w - sum_{b'<b} rc[s][b']).
+// Owner side. Received region s (R = cap + 1 rows from source rank s): rows w < total_s, then
+// the header row cap with rc[s][b] (b < lb local buckets, int32). Local order = (bucket, source,
+// arrival): local row of received row (s, w) with w in source s's bucket b =
+// loff[b] + sum_{s'<s} rc[s'][b] + (w - sum_{b'<b} rc[s][b']).
 // Every CTA recomputes the (small) prefix tables in shared memory, then handles 1024 rows.
-__global__ void __launch_bounds__(1024) k_ep_recv_plan(const int32_t* __restrict__ rc_g, int world, int lb_max, int lb,
-                                                       int64_t cap, int32_t* __restrict__ local_off,
+__global__ void __launch_bounds__(1024) k_ep_recv_plan(const uint16_t* __restrict__ recv_rows, int world, int lb,
+                                                       int64_t cap, int64_t cols, int32_t* __restrict__ local_off,
                                                        int32_t* __restrict__ gather_idx,
                                                        int32_t* __restrict__ return_idx) {
   extern __shared__ int32_t sm[];
@@ -73,10 +77,11 @@ __global__ void __launch_bounds__(1024) k_ep_recv_plan(const int32_t* __restrict
   __shared__ int32_t warp_sum[32];
   pdl_wait();
   pdl_trigger();
+  const int64_t reg = cap + 1;
   const int tid = threadIdx.x;
   for (int i = tid; i < world * lb; i += blockDim.x) {
     const int s = i / lb;
-    rc[i] = rc_g[(int64_t)s * lb_max + (i - s * lb)];
+    rc[i] = reinterpret_cast<const int32_t*>(recv_rows + ((int64_t)s * reg + cap) * cols)[i - s * lb];
   }
   __syncthreads();
   for (int s = tid; s < world; s += blockDim.x) {
@@ -124,13 +129,13 @@ __global__ void __launch_bounds__(1024) k_ep_recv_plan(const int32_t* __restrict
     for (int b = tid; b <= lb; b += blockDim.x) local_off[b] = loff[b];
   const int32_t n_local = loff[lb];
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + tid;
-  if (r >= (int64_t)world * cap) return;
-  if (r >= n_local) gather_idx[r] = 0;  // padding rows of the experts input: any valid row
-  const int s = (int)(r / cap);
-  const int32_t wi = (int32_t)(r - (int64_t)s * cap);
+  if (r >= n_local && r < (int64_t)world * cap) gather_idx[r] = 0;  // padding rows of the experts input
+  if (r >= (int64_t)world * reg) return;
+  const int s = (int)(r / reg);
+  const int32_t wi = (int32_t)(r - (int64_t)s * reg);
   const int32_t* ps = pre_s + s * (lb + 1);
   if (wi >= ps[lb]) {
-    return_idx[r] = 0;  // an unused slot of source s's region
+    return_idx[r] = 0;  // an unused slot or the header row of source s's region
     return;
   }
   int a = 0, z = lb;  // last b with ps[b] <= wi (non-empty bucket holding wi)
@@ -144,7 +149,7 @@ __global__ void __launch_bounds__(1024) k_ep_recv_plan(const int32_t* __restrict
 }
 
 // Home side: assignment (t, j) = a in global bucket g (pair p = g / 2); its s-th owner q_s
-// (ascending) returned the row q_s * cap + (a - off[2 lo[q_s]]).
+// (ascending) returned the row q_s * (cap + 1) + (a - off[2 lo[q_s]]).
 __global__ void __launch_bounds__(256) k_ep_home_index(const int32_t* __restrict__ assign_of,
                                                        const float* __restrict__ gate, const int32_t* __restrict__ off,
                                                        int n_buckets, EpRanks R, int slices, int64_t cap, int64_t n,
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(256) k_ep_home_index(const int32_t* __restrict
   int s = 0;
   for (int q = 0; q < R.world && s < slices; ++q) {
     if (R.lo[q] <= p && p < R.hi[q]) {
-      aof_s[i * slices + s] = (int32_t)(q * cap + (a - off[2 * R.lo[q]]));
+      aof_s[i * slices + s] = (int32_t)(q * (cap + 1) + (a - off[2 * R.lo[q]]));
       gate_s[i * slices + s] = g;
       ++s;
     }
@@ -197,8 +202,9 @@ int fill_ranks(const int32_t* dest_pairs, int world, int n_pairs, EpRanks* R, in
 
 int launch_ep_dispatch(const uint16_t* hidden, const int32_t* assign_token, const int32_t* bucket_off,
                        const int32_t* dest_pairs, int world, int n_pairs, int64_t cap, int lb_max, int d,
-                       uint16_t* send_rows, int32_t* send_counts, cudaStream_t s) {
-  if ((int64_t)world * cap > INT32_MAX) return fail(PUZZLE_ERR_UNSUPPORTED, "world * cap must fit in int32");
+                       uint16_t* send_rows, cudaStream_t s) {
+  if ((int64_t)world * (cap + 1) > INT32_MAX) return fail(PUZZLE_ERR_UNSUPPORTED, "world * (cap + 1) must fit in int32");
+  if (4 * (int64_t)lb_max > 2 * (int64_t)d) return fail(PUZZLE_ERR_UNSUPPORTED, "header row: 4 * lb_max must be <= 2 * d_model");
   EpRanks R;
   if (int rc = fill_ranks(dest_pairs, world, n_pairs, &R, nullptr)) return rc;
   for (int q = 0; q < world; ++q)
@@ -207,7 +213,7 @@ int launch_ep_dispatch(const uint16_t* hidden, const int32_t* assign_token, cons
   const unsigned grid = (unsigned)std::max<int64_t>(1, (rows + 7) / 8);
   ProfScope _ps("ep_dispatch", s);
   cudaError_t e = launch_pdl(k_ep_dispatch, dim3(grid), dim3(256), 0, s, hidden, assign_token, bucket_off, R, cap,
-                             lb_max, (int64_t)d, send_rows, send_counts);
+                             lb_max, (int64_t)d, send_rows);
   if (e != cudaSuccess) return cuda_check(e, "ep_dispatch launch");
   return cuda_check(cudaGetLastError(), "ep_dispatch launch");
 }
@@ -216,13 +222,13 @@ size_t ep_recv_plan_smem(int world, int lb) {
   return (size_t)(world * lb * 3 + world + lb + 1) * sizeof(int32_t);
 }
 
-int launch_ep_recv_plan(const int32_t* recv_counts, int world, int lb_max, int lb, int64_t cap, int32_t* local_off,
+int launch_ep_recv_plan(const uint16_t* recv_rows, int world, int lb, int64_t cap, int d, int32_t* local_off,
                         int32_t* gather_idx, int32_t* return_idx, cudaStream_t s) {
   const size_t smem = ep_recv_plan_smem(world, lb);
-  const int64_t rows = (int64_t)world * cap;
+  const int64_t rows = (int64_t)world * (cap + 1);
   const unsigned grid = (unsigned)std::max<int64_t>(1, (rows + 1023) / 1024);
   ProfScope _ps("ep_recv_plan", s);
-  cudaError_t e = launch_pdl(k_ep_recv_plan, dim3(grid), dim3(1024), smem, s, recv_counts, world, lb_max, lb, cap,
+  cudaError_t e = launch_pdl(k_ep_recv_plan, dim3(grid), dim3(1024), smem, s, recv_rows, world, lb, cap, (int64_t)d,
                              local_off, gather_idx, return_idx);
   if (e != cudaSuccess) return cuda_check(e, "ep_recv_plan launch");
   return cuda_check(cudaGetLastError(), "ep_recv_plan launch");

@@ -22,7 +22,8 @@ forward_fixed is the same layer with FIXED-CAPACITY dispatch: every rank reserve
 cap_tokens*top_k rows per destination, so both all-to-alls have equal splits known up front and
 the index work of steps 3-5 runs in device kernels (puzzle_ep_dispatch / puzzle_ep_recv_plan /
 puzzle_ep_home_index): no device->host copy, so a decode layer can be captured in a CUDA graph.
-It moves world*cap rows per collective instead of the routed count (the price of static splits).
+It moves world*(cap+1) rows per collective instead of the routed count (the price of static
+splits; the extra row per destination carries its bucket counts, so no count exchange).
 """
 from __future__ import annotations
 
@@ -111,8 +112,8 @@ class CudaOps:
     def ep_dispatch(self, hidden, assign_token, bucket_off, n_pairs, dest_pairs, cap, lb_max):
         return self.pz.ep_dispatch(hidden, assign_token, bucket_off, n_pairs, dest_pairs, cap, lb_max)
 
-    def ep_recv_plan(self, recv_counts, world, lb_max, n_local_buckets, cap):
-        return self.pz.ep_recv_plan(recv_counts, world, lb_max, n_local_buckets, cap)
+    def ep_recv_plan(self, recv_rows, world, n_local_buckets, cap):
+        return self.pz.ep_recv_plan(recv_rows, world, n_local_buckets, cap)
 
     def ep_home_index(self, assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, cap):
         return self.pz.ep_home_index(assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, cap)
@@ -218,24 +219,23 @@ class ExpertParallelMoE:
         """The layer with fixed-capacity dispatch: device-only, no host synchronisation.
 
         cap_tokens (default: this rank's T) bounds every rank's token count and must be the same
-        on all ranks; each rank sends world * cap_tokens * top_k rows per all-to-all. path is
+        on all ranks; each rank sends world * (cap_tokens * top_k + 1) rows per all-to-all (the +1:
+        a header row with the destination's bucket counts). path is
         passed to the local experts call (e.g. PATH_GEMV for decode-shape batches, whose owner
         receives up to world * cap rows)."""
         ops, part, G = self.ops, self.part, self.world
         T = hidden.shape[0]
-        cap = (T if cap_tokens is None else int(cap_tokens)) * top_k
+        cap = (T if cap_tokens is None else int(cap_tokens)) * top_k  # row slots per destination (+1 header)
         if cap < T * top_k:
             raise ValueError("cap_tokens must be >= the number of tokens on this rank")
         topk_idx, gate, bucket_off, assign_token, assign_of = ops.route(self.route_layer, logits, top_k, renormalize)
-        # 1. every destination's rows (its pairs' buckets) into its fixed region + the bucket counts
-        send_rows, send_counts = ops.ep_dispatch(hidden, assign_token, bucket_off, part.n_pairs, self.dest_pairs, cap,
-                                                 self.lb_max)
-        recv_counts = torch.empty_like(send_counts)
-        self._a2a_equal(recv_counts, send_counts)
+        # 1. every destination's rows (its pairs' buckets) into its fixed region, its bucket counts
+        #    in the region's header row: ONE all-to-all moves both
+        send_rows = ops.ep_dispatch(hidden, assign_token, bucket_off, part.n_pairs, self.dest_pairs, cap, self.lb_max)
         x_recv = torch.empty_like(send_rows)
         self._a2a_equal(x_recv, send_rows)
         # 2. regroup into (local bucket, source) order, local experts, back into the arrival slots
-        local_off, gidx, ridx = ops.ep_recv_plan(recv_counts, G, self.lb_max, self.n_local_buckets, cap)
+        local_off, gidx, ridx = ops.ep_recv_plan(x_recv, G, self.n_local_buckets, cap)
         x_local = ops.gather_rows(x_recv, gidx)
         y_local = ops.experts(self.local_layer, x_local, local_off, path=path)
         y_recv = ops.gather_rows(y_local, ridx)

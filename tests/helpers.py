@@ -97,30 +97,36 @@ def oracle_mixed_layer(cfg: synth.MoEConfig, n_merged: int, seed: int | None = N
 # the kernels with these, the gloo tests use them as the CPU stand-in of the device ops.
 
 def ep_dispatch_ref(hidden, assign_token, off, dest_pairs, cap, lb_max):
-    """send_rows [G*cap][d] (unwritten rows zero here), send_counts [G*lb_max]."""
+    """send_rows [G*(cap+1)][d] int16: per destination q, its rows then a header row whose first
+    2*lb_max 16-bit words are the int32 counts of q's local buckets (everything unwritten 0)."""
     G = len(dest_pairs)
-    rows = np.zeros((G * cap,) + hidden.shape[1:], hidden.dtype)
-    counts = np.zeros((G, lb_max), np.int32)
+    R = cap + 1
+    rows = np.zeros((G * R, hidden.shape[1]), np.int16)
     for q, (lo, hi) in enumerate(dest_pairs):
         a, b = off[2 * lo], off[2 * hi]
-        rows[q * cap:q * cap + (b - a)] = hidden[assign_token[a:b]]
-        counts[q, :2 * (hi - lo)] = np.diff(off[2 * lo:2 * hi + 1])
-    return rows, counts.reshape(-1)
+        rows[q * R:q * R + (b - a)] = hidden[assign_token[a:b]]
+        counts = np.zeros(lb_max, np.int32)
+        counts[:2 * (hi - lo)] = np.diff(off[2 * lo:2 * hi + 1])
+        rows[q * R + cap, :2 * lb_max] = counts.view(np.int16)
+    return rows
 
 
-def ep_recv_plan_ref(recv_counts, world, lb_max, lb, cap):
-    """(local_off [lb+1], gather_idx [G*cap], return_idx [G*cap]); local order (bucket, source)."""
-    rc = np.asarray(recv_counts).reshape(world, lb_max)[:, :lb].astype(np.int64)
+def ep_recv_plan_ref(recv_rows, world, lb, cap):
+    """(local_off [lb+1], gather_idx [G*cap], return_idx [G*(cap+1)]) from the header counts of
+    an int16 [G*(cap+1)][d] region buffer; local order (bucket, source)."""
+    R = cap + 1
+    rows = np.asarray(recv_rows).reshape(world, R, -1)
+    rc = np.ascontiguousarray(rows[:, cap, :2 * lb]).view(np.int32).astype(np.int64).reshape(world, lb)
     local_off = np.concatenate([[0], np.cumsum(rc.sum(0))]).astype(np.int32)
     gidx = np.zeros(world * cap, np.int32)
-    ridx = np.zeros(world * cap, np.int32)
+    ridx = np.zeros(world * R, np.int32)
     l = 0
     for b in range(lb):
         for s in range(world):
             w0 = rc[s, :b].sum()
             for w in range(rc[s, b]):
-                gidx[l] = s * cap + w0 + w
-                ridx[s * cap + w0 + w] = l
+                gidx[l] = s * R + w0 + w
+                ridx[s * R + w0 + w] = l
                 l += 1
     return local_off, gidx, ridx
 
@@ -137,6 +143,6 @@ def ep_home_index_ref(assign_of, gate, off, dest_pairs, slices, cap):
         owners = [q for q, (lo, hi) in enumerate(dest_pairs) if lo <= p < hi]
         assert len(owners) == slices
         for s, q in enumerate(owners):
-            aof_s[i * slices + s] = q * cap + (a - off[2 * dest_pairs[q][0]])
+            aof_s[i * slices + s] = q * (cap + 1) + (a - off[2 * dest_pairs[q][0]])
             gate_s[i, s] = gate.reshape(-1)[i]
     return aof_s, gate_s.reshape(T, k * slices)

@@ -53,12 +53,12 @@ class OracleOps:
 
     def ep_dispatch(self, hidden, assign_token, bucket_off, n_pairs, dest_pairs, cap, lb_max):
         bits = hidden.contiguous().view(torch.int16).numpy()
-        rows, counts = ep_dispatch_ref(bits, assign_token.numpy(), bucket_off.numpy(), dest_pairs, cap, lb_max)
-        return torch.from_numpy(rows).view(hidden.dtype), torch.from_numpy(counts)
+        rows = ep_dispatch_ref(bits, assign_token.numpy(), bucket_off.numpy(), dest_pairs, cap, lb_max)
+        return torch.from_numpy(rows).view(hidden.dtype)
 
-    def ep_recv_plan(self, recv_counts, world, lb_max, n_local_buckets, cap):
-        return tuple(torch.from_numpy(a) for a in ep_recv_plan_ref(recv_counts.numpy(), world, lb_max,
-                                                                    n_local_buckets, cap))
+    def ep_recv_plan(self, recv_rows, world, n_local_buckets, cap):
+        bits = recv_rows.contiguous().view(torch.int16).numpy()
+        return tuple(torch.from_numpy(a) for a in ep_recv_plan_ref(bits, world, n_local_buckets, cap))
 
     def ep_home_index(self, assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, cap):
         return tuple(torch.from_numpy(a) for a in ep_home_index_ref(assign_of.numpy(), gate.numpy(),

@@ -93,11 +93,10 @@ def test_ep_dispatch_and_home_index_match_definition(T, k, spare):
         hidden = rng.integers(-2**15, 2**15, size=(max(T, 1), d), dtype=np.int16)
         h_d = torch.from_numpy(hidden).cuda()
         tok_d, off_d = torch.from_numpy(tok).cuda(), torch.from_numpy(off).cuda()
-        rows = torch.zeros((G * cap, d), dtype=torch.int16, device="cuda")
-        rows, counts = pz.ep_dispatch(h_d, tok_d, off_d, P, dest, cap, lb_max, send_rows=rows)
-        r_ref, c_ref = ep_dispatch_ref(hidden, tok, off, dest, cap, lb_max)
-        assert np.array_equal(rows.cpu().numpy(), r_ref), (P, G)
-        assert np.array_equal(counts.cpu().numpy(), c_ref), (P, G)
+        rows = torch.zeros((G * (cap + 1), d), dtype=torch.int16, device="cuda")
+        rows = pz.ep_dispatch(h_d, tok_d, off_d, P, dest, cap, lb_max, send_rows=rows)
+        r_ref = ep_dispatch_ref(hidden, tok, off, dest, cap, lb_max)
+        assert np.array_equal(rows.cpu().numpy(), r_ref), (P, G)  # rows and header counts
         aof_s, gate_s = pz.ep_home_index(torch.from_numpy(aof).cuda(), torch.from_numpy(gate).cuda(), off_d, P, dest,
                                          S, cap)
         a_ref, g_ref = ep_home_index_ref(aof, gate, off, dest, S, cap)
@@ -105,20 +104,23 @@ def test_ep_dispatch_and_home_index_match_definition(T, k, spare):
         assert np.array_equal(gate_s.cpu().numpy(), g_ref), (P, G)
 
 
-@pytest.mark.parametrize("G,lb,lb_max,cap", [(1, 8, 8, 128), (2, 4, 6, 10), (8, 2, 2, 384), (4, 60, 64, 2048),
-                                            (3, 5, 5, 0), (8, 16, 16, 64)])
-def test_ep_recv_plan_matches_definition(G, lb, lb_max, cap):
+@pytest.mark.parametrize("G,lb,cap,d", [(1, 8, 128, 64), (2, 4, 10, 64), (8, 2, 384, 64), (4, 60, 2048, 128),
+                                        (3, 5, 0, 64), (8, 16, 64, 64), (2, 1024, 40, 2048)])
+def test_ep_recv_plan_matches_definition(G, lb, cap, d):
     import paper_2511_04805_b200 as pz
     from helpers import ep_recv_plan_ref
     rng = np.random.default_rng(G * 100 + lb)
-    rc = np.zeros((G, lb_max), np.int32)
+    R = cap + 1
+    rows = rng.integers(-2**15, 2**15, size=(G * R, d), dtype=np.int16)  # payload is irrelevant
     for s in range(G):  # each source sends at most cap rows, some buckets empty
         n = int(rng.integers(0, cap + 1)) if cap else 0
+        rc = np.zeros(lb, np.int32)
         if lb and n:
             cut = np.sort(rng.integers(0, n + 1, size=lb - 1))
-            rc[s, :lb] = np.diff(np.concatenate([[0], cut, [n]]))
-    lo, gi, ri = pz.ep_recv_plan(torch.from_numpy(rc.reshape(-1)).cuda(), G, lb_max, lb, cap)
-    lo_r, gi_r, ri_r = ep_recv_plan_ref(rc.reshape(-1), G, lb_max, lb, cap)
+            rc = np.diff(np.concatenate([[0], cut, [n]])).astype(np.int32)
+        rows[s * R + cap, :2 * lb] = rc.view(np.int16)
+    lo, gi, ri = pz.ep_recv_plan(torch.from_numpy(rows).cuda(), G, lb, cap)
+    lo_r, gi_r, ri_r = ep_recv_plan_ref(rows, G, lb, cap)
     assert np.array_equal(lo.cpu().numpy(), lo_r)
     assert np.array_equal(gi.cpu().numpy(), gi_r)
     assert np.array_equal(ri.cpu().numpy(), ri_r)
@@ -137,8 +139,10 @@ def test_ep_fixed_argument_errors():
         pz.ep_dispatch(h, tok, off, 4, [[0, 2], [2, 4]], 8, 3)
     with pytest.raises(pz.PuzzleError):  # pair 3 has no owner
         pz.ep_home_index(tok, torch.zeros((4, 2), device="cuda"), off, 4, [[0, 3]], 1, 8)
-    with pytest.raises(pz.PuzzleError):  # n_local_buckets > lb_max
-        pz.ep_recv_plan(torch.zeros(4, dtype=torch.int32, device="cuda"), 1, 4, 5, 8)
+    with pytest.raises(pz.PuzzleError):  # 4 * lb_max > 2 * d_model: the counts do not fit in a header row
+        pz.ep_dispatch(h, tok, off, 4, [[0, 4]], 8, 33)
+    with pytest.raises(pz.PuzzleError):  # n_local_buckets beyond what a 64-wide header row holds
+        pz.ep_recv_plan(torch.zeros((9, 64), dtype=torch.int16, device="cuda"), 1, 33, 8)
 
 
 def _ep_world1(cfg, n_merged=None):
