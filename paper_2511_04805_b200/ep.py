@@ -223,24 +223,41 @@ class ExpertParallelMoE:
         a header row with the destination's bucket counts). path is
         passed to the local experts call (e.g. PATH_GEMV for decode-shape batches, whose owner
         receives up to world * cap rows)."""
-        ops, part, G = self.ops, self.part, self.world
+        send_rows, state = self.fixed_send(hidden, logits, top_k, renormalize, cap_tokens)
+        x_recv = torch.empty_like(send_rows)
+        self._a2a_equal(x_recv, send_rows)
+        y_recv = self.fixed_serve(x_recv, state["cap"], path)
+        y_back = torch.empty_like(y_recv)
+        self._a2a_equal(y_back, y_recv)
+        return self.fixed_finish(y_back, state, residual)
+
+    # The three local phases of forward_fixed, between which the two all-to-alls run (exposed so
+    # a test can drive several ranks' phases in one process with the exchange done by slicing).
+    def fixed_send(self, hidden, logits, top_k: int, renormalize: bool, cap_tokens: int | None = None):
+        """route + dispatch: (send_rows [world*(cap+1)][d], state for fixed_finish)."""
+        ops, part = self.ops, self.part
         T = hidden.shape[0]
         cap = (T if cap_tokens is None else int(cap_tokens)) * top_k  # row slots per destination (+1 header)
         if cap < T * top_k:
             raise ValueError("cap_tokens must be >= the number of tokens on this rank")
         topk_idx, gate, bucket_off, assign_token, assign_of = ops.route(self.route_layer, logits, top_k, renormalize)
-        # 1. every destination's rows (its pairs' buckets) into its fixed region, its bucket counts
-        #    in the region's header row: ONE all-to-all moves both
+        # every destination's rows (its pairs' buckets) into its fixed region, its bucket counts in
+        # the region's header row: ONE all-to-all moves both
         send_rows = ops.ep_dispatch(hidden, assign_token, bucket_off, part.n_pairs, self.dest_pairs, cap, self.lb_max)
-        x_recv = torch.empty_like(send_rows)
-        self._a2a_equal(x_recv, send_rows)
-        # 2. regroup into (local bucket, source) order, local experts, back into the arrival slots
-        local_off, gidx, ridx = ops.ep_recv_plan(x_recv, G, self.n_local_buckets, cap)
+        return send_rows, {"cap": cap, "gate": gate, "bucket_off": bucket_off, "assign_of": assign_of}
+
+    def fixed_serve(self, x_recv, cap: int, path=None):
+        """owner: regroup the received regions into (local bucket, source) order, run the local
+        experts, put the outputs back into the arrival slots (same region layout)."""
+        ops = self.ops
+        local_off, gidx, ridx = ops.ep_recv_plan(x_recv, self.world, self.n_local_buckets, cap)
         x_local = ops.gather_rows(x_recv, gidx)
         y_local = ops.experts(self.local_layer, x_local, local_off, path=path)
-        y_recv = ops.gather_rows(y_local, ridx)
-        # 3. outputs home (region q = owner q's results for the rows sent to it) and combine
-        y_back = torch.empty_like(y_recv)
-        self._a2a_equal(y_back, y_recv)
-        aof_s, gate_s = ops.ep_home_index(assign_of, gate, bucket_off, part.n_pairs, self.dest_pairs, part.slices, cap)
-        return ops.combine(y_back, aof_s, gate_s, residual)
+        return ops.gather_rows(y_local, ridx)
+
+    def fixed_finish(self, y_back, state, residual=None):
+        """home: region q of y_back = owner q's results for the rows sent to it -> combine."""
+        part = self.part
+        aof_s, gate_s = self.ops.ep_home_index(state["assign_of"], state["gate"], state["bucket_off"], part.n_pairs,
+                                               self.dest_pairs, part.slices, state["cap"])
+        return self.ops.combine(y_back, aof_s, gate_s, residual)

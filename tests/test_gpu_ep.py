@@ -228,3 +228,58 @@ def test_ep_fixed_graph_capture(nccl_group):
     torch.cuda.synchronize()
     ref = oracle.moe_forward(w13, w2, slot, hb, lb, cfg.top_k, cfg.renormalize)
     assert_close(out.float().cpu().numpy(), ref, "graph-replayed fixed-capacity ep vs oracle")
+
+
+@pytest.mark.parametrize("cfg,G,n_merged", [
+    (synth.MoEConfig("sim_small", 34, 256, 512, 8, 2, True), 2, None),    # 4 pairs: 2 per rank
+    (synth.MoEConfig("sim_small", 34, 256, 512, 8, 2, True), 3, None),    # uneven pair blocks
+    (synth.MoEConfig("sim_small", 34, 256, 512, 8, 2, True), 8, None),    # world > pairs: d_ff slices
+    (synth.MoEConfig("sim_fine", 35, 128, 256, 16, 4, False), 4, None),   # fine-grained, top-4
+    (synth.MoEConfig("sim_25", 36, 256, 512, 8, 2, True), 3, 2),          # 25 %: pairs + dense slots
+], ids=lambda v: str(v) if not hasattr(v, "name") else v.name)
+def test_ep_fixed_simulated_world_matches_oracle(cfg, G, n_merged):
+    """G ranks' fixed-capacity EP layers driven in ONE process through the real kernels, phase by
+    phase (send -> exchange by slicing -> serve -> exchange -> finish; no rank waits on another
+    inside a kernel): every rank's output equals the oracle on its own (ragged) tokens."""
+    import paper_2511_04805_b200 as pz
+    from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_dense, shard_packed
+    if n_merged is None:
+        w13, w2, slot, _ = oracle_packed_layer(cfg)
+        dense = None
+    else:
+        w13, w2, slot, dense = oracle_mixed_layer(cfg, n_merged)
+    n_slots = w13.shape[0]
+    w13_d = torch.from_numpy(w13.view(np.int16)).cuda()
+    w2_d = torch.from_numpy(w2.view(np.int16)).cuda()
+    slot_d = torch.from_numpy(slot).cuda()
+    dense_d = None if dense is None else torch.from_numpy(dense.astype(np.uint8)).cuda()
+    part = Partition(n_slots, G)
+    eps = []
+    for r in range(G):
+        w13_l, w2_l = shard_packed(w13_d, w2_d, part, r)
+        local = pz.PackedMoELayer(w13_l, w2_l, torch.arange(2 * w13_l.shape[0], dtype=torch.int32, device="cuda"),
+                                  shard_dense(dense_d, part, r))
+        route = pz.RoutingLayer(n_slots, cfg.d_model, cfg.d_ff, slot_d, w13_l)
+        eps.append(ExpertParallelMoE(part, r, route, local, cfg.d_model))
+    T = 24
+    inputs, sends, states = [], [], []
+    for r in range(G):
+        Tr = T - r  # ragged per-rank batches, one capacity for all
+        hb = synth.hidden_bits(cfg, Tr, seed=500 + r)
+        lg = synth.router_logits(cfg, Tr, seed=600 + r)
+        rb = synth.hidden_bits(cfg, Tr, seed=700 + r)
+        inputs.append((hb, lg, rb))
+        h = torch.from_numpy(hb.view(np.int16)).cuda().view(torch.bfloat16)
+        s, st = eps[r].fixed_send(h, torch.from_numpy(lg).cuda(), cfg.top_k, cfg.renormalize, cap_tokens=T)
+        sends.append(s)
+        states.append(st)
+    R = T * cfg.top_k + 1  # rows per region
+    recv = [torch.cat([sends[s][q * R:(q + 1) * R] for s in range(G)]) for q in range(G)]
+    served = [eps[q].fixed_serve(recv[q], R - 1, path=pz.PATH_GEMV) for q in range(G)]
+    for r in range(G):
+        back = torch.cat([served[q][r * R:(r + 1) * R] for q in range(G)])
+        hb, lg, rb = inputs[r]
+        out = eps[r].fixed_finish(back, states[r], torch.from_numpy(rb.view(np.int16)).cuda().view(torch.bfloat16))
+        torch.cuda.synchronize()
+        ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, rb, pair_dense=dense)
+        assert_close(out.float().cpu().numpy(), ref, f"simulated world {G}, rank {r}")
