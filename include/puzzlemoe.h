@@ -307,6 +307,51 @@ int puzzle_ep_home_index(const int32_t* assign_of, const float* topk_gate, const
                          float* gate_s, puzzle_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
+ * The same fixed-capacity layer over NVLink PEER MEMORY: the dispatch kernel stores each
+ * owner's rows (and header) straight into that owner's receive buffer, and the owner's return
+ * kernel stores the expert outputs straight into each home rank's buffer -- the transfers are
+ * fused into the gather / un-permute kernels (no NCCL on the data path, no staging copies).
+ *
+ * Every rank allocates ONE peer buffer of puzzle_ep_peer_buffer_size(world, cap, d_model) bytes
+ * (symmetric: same size on all ranks, mapped into every peer's address space, e.g. CUDA IPC /
+ * torch symmetric memory; 256-byte aligned; zero-initialised once). Layout:
+ *   recv_x  bf16 [world][cap+1][d_model] at offset 0 (region s: rows + header from source s,
+ *           exactly puzzle_ep_dispatch's region for this rank),
+ *   recv_y  f32  [world][cap+1][d_model] at an offset aligned to 256 B after recv_x (region q:
+ *           the outputs owner q returned for this rank's rows),
+ *   flags   u32  [2][world] (dispatch / return epochs) after recv_y.
+ * peer_bases  HOST u64 [world]: the device address of rank q's peer buffer as mapped on THIS
+ *             rank (peer_bases[rank] = its own buffer).
+ * state       device u32 [4], zero-initialised once, private to the rank and the layer: the step
+ *             counter (epochs) and the kernels' CTA completion counters.
+ * Per layer call (stream-ordered on one stream; graph-capturable):
+ *   puzzle_moe_route -> puzzle_ep_dispatch_peer -> puzzle_ep_wait_dispatch (waits until every
+ *   source's region of this step has landed) -> puzzle_ep_recv_plan(recv_x) -> gather ->
+ *   puzzle_moe_experts -> puzzle_ep_return_peer -> puzzle_ep_home_index_peer (waits for every
+ *   owner's return; advances the step) -> puzzle_moe_combine(recv_y, ...).
+ * Every rank must make the same sequence of calls (the waits are cross-rank: a rank that stops
+ * calling stalls its peers). Errors as for the NCCL form; peer_bases entries must be non-NULL and
+ * 256-byte aligned.
+ * ------------------------------------------------------------------------------------- */
+size_t puzzle_ep_peer_buffer_size(int world, int64_t cap, int d_model);
+int puzzle_ep_dispatch_peer(const uint16_t* hidden, const int32_t* assign_token, const int32_t* bucket_off,
+                            int n_pairs, const int32_t* dest_pairs, int world, int rank, int64_t n_assign,
+                            int64_t cap, int lb_max, int d_model, const unsigned long long* peer_bases,
+                            uint32_t* state, puzzle_stream_t stream);
+int puzzle_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d_model, const uint32_t* state,
+                            puzzle_stream_t stream);
+/* y_local f32 [world*cap][d_model] (the experts' outputs in local order), return_idx from
+ * puzzle_ep_recv_plan: slot (s, w) of home rank s's recv_y region [rank] <- y_local[return_idx]. */
+int puzzle_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int64_t cap,
+                          int d_model, const unsigned long long* peer_bases, uint32_t* state,
+                          puzzle_stream_t stream);
+/* As puzzle_ep_home_index (region stride cap+1), after waiting for every owner's return. */
+int puzzle_ep_home_index_peer(const int32_t* assign_of, const float* topk_gate, const int32_t* bucket_off,
+                              int n_pairs, const int32_t* dest_pairs, int world, int64_t cap, int64_t T, int top_k,
+                              int d_model, const void* my_base, int32_t* aof_s, float* gate_s, uint32_t* state,
+                              puzzle_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
  * NEXT-4: calibration statistics for Eq. 4 (reading R12). The Wanda saliency
  * A = |W| (.) ||X||_2 needs, per expert, the L2 norm of every input column over "a sample of
  * input activations to a certain expert", gathered in "a single forward pass"

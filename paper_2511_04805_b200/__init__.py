@@ -33,7 +33,8 @@ EXPORTED_SYMBOLS = (
     "puzzle_profile_end", "puzzle_moe_route_workspace_size", "puzzle_group_colsumsq_workspace_size",
     "puzzle_group_colsumsq", "puzzle_moe_calib_workspace_size", "puzzle_moe_forward_calib",
     "puzzle_quant_pack", "puzzle_quant_unpack", "puzzle_ep_dispatch", "puzzle_ep_recv_plan",
-    "puzzle_ep_home_index",
+    "puzzle_ep_home_index", "puzzle_ep_peer_buffer_size", "puzzle_ep_dispatch_peer", "puzzle_ep_wait_dispatch",
+    "puzzle_ep_return_peer", "puzzle_ep_home_index_peer",
 )
 
 
@@ -95,6 +96,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_ep_dispatch": ([P, P, P, I, P, I, I64, I64, I, I, P, P], I),
             "puzzle_ep_recv_plan": ([P, I, I, I64, I, P, P, P, P], I),
             "puzzle_ep_home_index": ([P, P, P, I, P, I, I64, I64, I, P, P, P], I),
+            "puzzle_ep_peer_buffer_size": ([I, I64, I], SZ),
+            "puzzle_ep_dispatch_peer": ([P, P, P, I, P, I, I, I64, I64, I, I, P, P, P], I),
+            "puzzle_ep_wait_dispatch": ([P, I, I64, I, P, P], I),
+            "puzzle_ep_return_peer": ([P, P, I, I, I64, I, P, P, P], I),
+            "puzzle_ep_home_index_peer": ([P, P, P, I, P, I, I64, I64, I, I, P, P, P, P, P], I),
             "puzzle_profile_begin": ([], I),
             "puzzle_profile_end": ([ctypes.c_char_p, SZ], I),
         }
@@ -357,6 +363,64 @@ def ep_home_index(assign_of, topk_gate, bucket_off, n_pairs: int, dest_pairs, sl
     _check(load_library().puzzle_ep_home_index(_p(assign_of), _p(topk_gate), _p(bucket_off), int(n_pairs), dp, world,
                                                int(cap), T, k, _p(aof_s), _p(gate_s), _stream(stream)),
            "puzzle_ep_home_index")
+    return aof_s, gate_s
+
+
+class EpPeerBuffer:
+    """This rank's peer buffer (puzzle_ep_peer_buffer_size bytes) + its view of every peer's
+    buffer address + the private step state. `buffer` may come from torch symmetric memory
+    (multi-GPU) or be a plain device tensor (peers in one process, tests)."""
+
+    def __init__(self, buffer: torch.Tensor, peer_ptrs, world: int, cap: int, d_model: int):
+        import numpy as np
+        need = int(load_library().puzzle_ep_peer_buffer_size(world, cap, d_model))
+        if buffer.numel() * buffer.element_size() < need:
+            raise ValueError(f"peer buffer of {buffer.numel()} bytes < {need}")
+        self.buffer, self.world, self.cap, self.d = buffer, world, cap, d_model
+        self.peers = np.ascontiguousarray(np.asarray(peer_ptrs, dtype=np.uint64))
+        assert self.peers.size == world
+        self.state = torch.zeros(4, dtype=torch.int32, device=buffer.device)
+        R = cap + 1
+        self.recv_x = buffer.view(torch.uint8)[:world * R * d_model * 2].view(torch.bfloat16).view(world * R, d_model)
+        off_y = (world * R * d_model * 2 + 255) // 256 * 256
+        self.recv_y = buffer.view(torch.uint8)[off_y:off_y + world * R * d_model * 4].view(torch.float32).view(world * R, d_model)
+
+    @staticmethod
+    def size(world: int, cap: int, d_model: int) -> int:
+        return int(load_library().puzzle_ep_peer_buffer_size(world, cap, d_model))
+
+    def _peers(self):
+        return self.peers.ctypes.data_as(ctypes.c_void_p)
+
+
+def ep_dispatch_peer(hidden, assign_token, bucket_off, n_pairs: int, dest_pairs, rank: int, pb: EpPeerBuffer,
+                     lb_max: int, stream=None):
+    arr, dp, world = _dest_pairs(dest_pairs)
+    _check(load_library().puzzle_ep_dispatch_peer(_p(hidden), _p(assign_token), _p(bucket_off), int(n_pairs), dp, world,
+                                                  int(rank), assign_token.numel(), pb.cap, int(lb_max), pb.d,
+                                                  pb._peers(), _p(pb.state), _stream(stream)), "puzzle_ep_dispatch_peer")
+
+
+def ep_wait_dispatch(pb: EpPeerBuffer, stream=None):
+    _check(load_library().puzzle_ep_wait_dispatch(_p(pb.buffer), pb.world, pb.cap, pb.d, _p(pb.state), _stream(stream)),
+           "puzzle_ep_wait_dispatch")
+
+
+def ep_return_peer(y_local, return_idx, rank: int, pb: EpPeerBuffer, stream=None):
+    _check(load_library().puzzle_ep_return_peer(_p(y_local), _p(return_idx), pb.world, int(rank), pb.cap, pb.d,
+                                                pb._peers(), _p(pb.state), _stream(stream)), "puzzle_ep_return_peer")
+
+
+def ep_home_index_peer(assign_of, topk_gate, bucket_off, n_pairs: int, dest_pairs, slices: int, pb: EpPeerBuffer,
+                       stream=None):
+    arr, dp, world = _dest_pairs(dest_pairs)
+    T, k = topk_gate.shape
+    dev = topk_gate.device
+    aof_s = torch.empty(max(T * k * slices, 1), dtype=torch.int32, device=dev)[:T * k * slices]
+    gate_s = torch.empty((T, k * slices), dtype=torch.float32, device=dev)
+    _check(load_library().puzzle_ep_home_index_peer(_p(assign_of), _p(topk_gate), _p(bucket_off), int(n_pairs), dp,
+                                                    world, pb.cap, T, k, pb.d, _p(pb.buffer), _p(aof_s), _p(gate_s),
+                                                    _p(pb.state), _stream(stream)), "puzzle_ep_home_index_peer")
     return aof_s, gate_s
 
 

@@ -38,6 +38,14 @@ size_t ep_recv_plan_smem(int world, int lb);
 int launch_ep_recv_plan(const uint16_t*, int, int, int64_t, int, int32_t*, int32_t*, int32_t*, cudaStream_t);
 int launch_ep_home_index(const int32_t*, const float*, const int32_t*, int, const int32_t*, int, int64_t, int64_t,
                          int32_t*, float*, int*, cudaStream_t);
+size_t ep_peer_buffer_bytes(int world, int64_t cap, int d);
+int launch_ep_dispatch_peer(const uint16_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int, int64_t, int,
+                            int, const unsigned long long*, uint32_t*, cudaStream_t);
+int launch_ep_wait_dispatch(const void*, int, int64_t, int, const uint32_t*, cudaStream_t);
+int launch_ep_return_peer(const float*, const int32_t*, int, int, int64_t, int, const unsigned long long*, uint32_t*,
+                          cudaStream_t);
+int launch_ep_home_index_peer(const int32_t*, const float*, const int32_t*, int, const int32_t*, int, int64_t, int,
+                              int64_t, const void*, int32_t*, float*, uint32_t*, cudaStream_t);
 bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
                       const int32_t*, int64_t, uint16_t*, float*, int32_t*, cudaStream_t);
@@ -627,6 +635,69 @@ int puzzle_ep_home_index(const int32_t* assign_of, const float* topk_gate, const
     if (int rc = check_device()) return rc;
   return launch_ep_home_index(assign_of, topk_gate, bucket_off, n_pairs, dest_pairs, world, cap, T * top_k, aof_s,
                               gate_s, nullptr, (cudaStream_t)stream);
+}
+
+static int check_peer_common(int world, int rank, int64_t cap, int d_model) {
+  if (world < 1 || world > 64 || rank < 0 || rank >= world || cap < 0 || d_model < 8 || d_model % 8)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes (1 <= world <= 64, 0 <= rank < world, cap >= 0, d_model % 8 == 0)");
+  if ((int64_t)world * (cap + 1) > INT32_MAX) return fail(PUZZLE_ERR_UNSUPPORTED, "world * (cap + 1) must fit in int32");
+  return PUZZLE_OK;
+}
+
+size_t puzzle_ep_peer_buffer_size(int world, int64_t cap, int d_model) {
+  if (check_peer_common(world, 0, cap, d_model)) return 0;
+  return pz::ep_peer_buffer_bytes(world, cap, d_model);
+}
+
+int puzzle_ep_dispatch_peer(const uint16_t* hidden, const int32_t* assign_token, const int32_t* bucket_off,
+                            int n_pairs, const int32_t* dest_pairs, int world, int rank, int64_t n_assign,
+                            int64_t cap, int lb_max, int d_model, const unsigned long long* peer_bases,
+                            uint32_t* state, puzzle_stream_t stream) {
+  if (int rc = check_peer_common(world, rank, cap, d_model)) return rc;
+  if (n_pairs < 1 || n_assign < 0 || cap < n_assign || lb_max < 0)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes (need n_pairs >= 1, 0 <= n_assign <= cap)");
+  if (!dest_pairs || !bucket_off || !peer_bases || !state || (n_assign > 0 && (!hidden || !assign_token)))
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  for (int q = 0; q < world; ++q)
+    if (!peer_bases[q] || (peer_bases[q] & 255)) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "peer_bases: NULL or not 256-byte aligned");
+  if (!al16(hidden)) return fail(PUZZLE_ERR_UNSUPPORTED, "hidden must be 16-byte aligned");
+  if (int rc = check_device()) return rc;
+  return launch_ep_dispatch_peer(hidden, assign_token, bucket_off, dest_pairs, world, rank, n_pairs, cap, lb_max,
+                                 d_model, peer_bases, state, (cudaStream_t)stream);
+}
+
+int puzzle_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d_model, const uint32_t* state,
+                            puzzle_stream_t stream) {
+  if (int rc = check_peer_common(world, 0, cap, d_model)) return rc;
+  if (!my_base || !state) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (int rc = check_device()) return rc;
+  return launch_ep_wait_dispatch(my_base, world, cap, d_model, state, (cudaStream_t)stream);
+}
+
+int puzzle_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int64_t cap,
+                          int d_model, const unsigned long long* peer_bases, uint32_t* state,
+                          puzzle_stream_t stream) {
+  if (int rc = check_peer_common(world, rank, cap, d_model)) return rc;
+  if (!y_local || !return_idx || !peer_bases || !state) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  for (int q = 0; q < world; ++q)
+    if (!peer_bases[q] || (peer_bases[q] & 255)) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "peer_bases: NULL or not 256-byte aligned");
+  if (!al16(y_local)) return fail(PUZZLE_ERR_UNSUPPORTED, "y_local must be 16-byte aligned");
+  if (int rc = check_device()) return rc;
+  return launch_ep_return_peer(y_local, return_idx, world, rank, cap, d_model, peer_bases, state, (cudaStream_t)stream);
+}
+
+int puzzle_ep_home_index_peer(const int32_t* assign_of, const float* topk_gate, const int32_t* bucket_off,
+                              int n_pairs, const int32_t* dest_pairs, int world, int64_t cap, int64_t T, int top_k,
+                              int d_model, const void* my_base, int32_t* aof_s, float* gate_s, uint32_t* state,
+                              puzzle_stream_t stream) {
+  if (int rc = check_peer_common(world, 0, cap, d_model)) return rc;
+  if (n_pairs < 1 || T < 0 || top_k < 1 || cap < T * top_k)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes (need n_pairs >= 1, T >= 0, top_k >= 1, cap >= T * top_k)");
+  if (!dest_pairs || !my_base || !state || !bucket_off || (T > 0 && (!assign_of || !topk_gate || !aof_s || !gate_s)))
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (int rc = check_device()) return rc;
+  return launch_ep_home_index_peer(assign_of, topk_gate, bucket_off, n_pairs, dest_pairs, world, cap, d_model,
+                                   T * top_k, my_base, aof_s, gate_s, state, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -176,6 +176,176 @@ __global__ void __launch_bounds__(256) k_ep_home_index(const int32_t* __restrict
   }
 }
 
+// ---- NVLink peer-memory form: rows stored straight into the owners' receive buffers ----
+// Every rank holds one symmetric buffer (same layout on all ranks, mapped into every peer):
+//   recv_x  bf16 [world][cap+1][d]   region s = what source rank s dispatched to this rank
+//   recv_y  f32  [world][cap+1][d]   region q = what owner q returned for this rank's rows
+//   flags   u32  [2][world]          [0][s] / [1][q]: the epoch of the last region s / q stored
+// and a local state (u32: step, then per-kernel CTA completion counters; zero-initialised).
+// Epochs: every layer call of a rank reads step e; its stores are published with e + 1
+// (release, system scope, by the last CTA of the storing kernel after all CTAs' stores); the
+// consumers wait for e + 1 (acquire); the home-index kernel's last CTA advances step. Flags only
+// grow, so CUDA-graph replays need no reset. Buffer reuse is ordered by the layer's causal chain
+// (a rank dispatches step e + 1 only after its combine of step e, which waited for every owner's
+// return of step e, which each owner stored after reading its step-e receive regions).
+struct EpPeers {
+  unsigned long long base[kEpMaxRanks];
+};
+constexpr int kStStep = 0, kStDispatch = 1, kStReturn = 2, kStHome = 3;
+
+__host__ __device__ inline size_t ep_off_y(int world, int64_t cap, int d) {
+  return ((size_t)world * (cap + 1) * d * 2 + 255) / 256 * 256;
+}
+__host__ __device__ inline size_t ep_off_flags(int world, int64_t cap, int d) {
+  return ep_off_y(world, cap, d) + ((size_t)world * (cap + 1) * d * 4 + 255) / 256 * 256;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// After this CTA's stores: the last CTA of the grid (counter) publishes `epoch` into flag slot
+// `slot` of every peer (or, with self_flag, into this rank's own flags of every source... n/a).
+__device__ __forceinline__ bool ep_last_cta(uint32_t* done) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // this CTA's peer stores before its arrival
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (last) {
+      *done = 0;  // ready for the next call
+      __threadfence_system();
+    }
+  }
+  __syncthreads();
+  return last;
+}
+
+// Dispatch straight into the owners' recv_x regions [rank] (rows + header), then publish.
+__global__ void __launch_bounds__(256) k_ep_dispatch_peer(const uint16_t* __restrict__ hidden,
+                                                          const int32_t* __restrict__ assign_token,
+                                                          const int32_t* __restrict__ off, EpRanks R, EpPeers Pe,
+                                                          int rank, int64_t cap, int lb_max, int64_t cols,
+                                                          uint32_t* __restrict__ state) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t reg = cap + 1;
+  const uint32_t epoch = state[kStStep] + 1;
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < R.world * lb_max; i += blockDim.x) {
+      const int q = i / lb_max, b = i - q * lb_max;
+      const int nb = 2 * (R.hi[q] - R.lo[q]);
+      const int g = 2 * R.lo[q] + b;
+      uint16_t* dst = reinterpret_cast<uint16_t*>(Pe.base[q]) + ((int64_t)rank * reg + cap) * cols;
+      reinterpret_cast<int32_t*>(dst)[b] = b < nb ? off[g + 1] - off[g] : 0;
+    }
+  }
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r < (int64_t)R.world * cap) {
+    const int q = (int)(r / cap);
+    const int64_t i = r - (int64_t)q * cap;
+    const int32_t lo = off[2 * R.lo[q]], n = off[2 * R.hi[q]] - lo;
+    if (i < n) {
+      const uint4* sp = reinterpret_cast<const uint4*>(hidden + (int64_t)assign_token[lo + i] * cols);
+      uint4* dp = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(Pe.base[q]) + ((int64_t)rank * reg + i) * cols);
+      warp_copy_row(sp, dp, cols / 8, threadIdx.x & 31);
+    }
+  }
+  if (ep_last_cta(state + kStDispatch) && threadIdx.x < R.world) {
+    const int q = threadIdx.x;
+    uint32_t* fl = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(Pe.base[q]) + ep_off_flags(R.world, cap, (int)(cols)));
+    st_release_sys(fl + rank, epoch);  // flags[0][rank] of owner q
+  }
+}
+
+// Owner: wait until every source's region of this step has landed (flags[0][s] >= epoch).
+__global__ void k_ep_wait_flags(const uint32_t* __restrict__ flags, int world, const uint32_t* __restrict__ state) {
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t epoch = state[kStStep] + 1;
+  for (int s = threadIdx.x; s < world; s += blockDim.x)
+    while (ld_acquire_sys(flags + s) < epoch) __nanosleep(32);
+  __syncthreads();
+}
+
+// Owner: return the experts' outputs into every home rank's recv_y region [rank], slot by slot
+// (y_local rows through return_idx; unused slots carry a valid but unread row), then publish.
+__global__ void __launch_bounds__(256) k_ep_return_peer(const uint16_t* __restrict__ y_local,
+                                                        const int32_t* __restrict__ return_idx, EpPeers Pe, int world,
+                                                        int rank, int64_t cap, int64_t cols_y, int d,
+                                                        uint32_t* __restrict__ state) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t reg = cap + 1;
+  const uint32_t epoch = state[kStStep] + 1;
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // received slot (s, w)
+  if (r < (int64_t)world * reg) {
+    const int s = (int)(r / reg);
+    const int64_t w = r - (int64_t)s * reg;
+    if (w < cap) {
+      const uint4* sp = reinterpret_cast<const uint4*>(y_local + (int64_t)return_idx[r] * cols_y);
+      uint16_t* ybase = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(Pe.base[s]) + ep_off_y(world, cap, d));
+      uint4* dp = reinterpret_cast<uint4*>(ybase + ((int64_t)rank * reg + w) * cols_y);
+      warp_copy_row(sp, dp, cols_y / 8, threadIdx.x & 31);
+    }
+  }
+  if (ep_last_cta(state + kStReturn) && threadIdx.x < world) {
+    const int q = threadIdx.x;  // home rank q
+    uint32_t* fl = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(Pe.base[q]) + ep_off_flags(world, cap, d));
+    st_release_sys(fl + world + rank, epoch);  // flags[1][rank] of home q
+  }
+}
+
+// Home: wait for every owner's return of this step, then the combine indices (as
+// k_ep_home_index, region stride cap + 1); the last CTA advances the step.
+__global__ void __launch_bounds__(256) k_ep_home_index_peer(const int32_t* __restrict__ assign_of,
+                                                            const float* __restrict__ gate,
+                                                            const int32_t* __restrict__ off, int n_buckets, EpRanks R,
+                                                            int slices, int64_t cap, int64_t n,
+                                                            const uint32_t* __restrict__ flags_y,
+                                                            int32_t* __restrict__ aof_s, float* __restrict__ gate_s,
+                                                            uint32_t* __restrict__ state) {
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t epoch = state[kStStep] + 1;
+  for (int q = threadIdx.x; q < R.world; q += blockDim.x)
+    while (ld_acquire_sys(flags_y + q) < epoch) __nanosleep(32);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int32_t a = assign_of[i];
+    int lo = 0, hi = n_buckets;
+    while (hi - lo > 1) {
+      const int m = (lo + hi) >> 1;
+      if (off[m] <= a) lo = m; else hi = m;
+    }
+    const int p = lo >> 1;
+    const float g = gate[i];
+    int s = 0;
+    for (int q = 0; q < R.world && s < slices; ++q) {
+      if (R.lo[q] <= p && p < R.hi[q]) {
+        aof_s[i * slices + s] = (int32_t)(q * (cap + 1) + (a - off[2 * R.lo[q]]));
+        gate_s[i * slices + s] = g;
+        ++s;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(state + kStHome, 1u) == gridDim.x - 1) {  // every CTA has read the step
+      state[kStHome] = 0;
+      state[kStStep] = epoch;
+      __threadfence();
+    }
+  }
+}
+
 int fill_ranks(const int32_t* dest_pairs, int world, int n_pairs, EpRanks* R, int* slices) {
   if (world < 1 || world > kEpMaxRanks) return fail(PUZZLE_ERR_UNSUPPORTED, "world must be in [1, 64]");
   R->world = world;
@@ -247,6 +417,69 @@ int launch_ep_home_index(const int32_t* assign_of, const float* gate, const int3
                              bucket_off, 2 * n_pairs + 1, R, S, cap, n, aof_s, gate_s);
   if (e != cudaSuccess) return cuda_check(e, "ep_home_index launch");
   return cuda_check(cudaGetLastError(), "ep_home_index launch");
+}
+
+size_t ep_peer_buffer_bytes(int world, int64_t cap, int d) {
+  return ep_off_flags(world, cap, d) + (size_t)2 * world * sizeof(uint32_t);
+}
+
+static void fill_peers(const unsigned long long* bases, int world, EpPeers* Pe) {
+  for (int q = 0; q < world; ++q) Pe->base[q] = bases[q];
+}
+
+int launch_ep_dispatch_peer(const uint16_t* hidden, const int32_t* assign_token, const int32_t* bucket_off,
+                            const int32_t* dest_pairs, int world, int rank, int n_pairs, int64_t cap, int lb_max,
+                            int d, const unsigned long long* peer_bases, uint32_t* state, cudaStream_t s) {
+  if (4 * (int64_t)lb_max > 2 * (int64_t)d) return fail(PUZZLE_ERR_UNSUPPORTED, "header row: 4 * lb_max must be <= 2 * d_model");
+  EpRanks R;
+  if (int rc = fill_ranks(dest_pairs, world, n_pairs, &R, nullptr)) return rc;
+  for (int q = 0; q < world; ++q)
+    if (2 * (R.hi[q] - R.lo[q]) > lb_max) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "lb_max < a rank's local buckets");
+  EpPeers Pe;
+  fill_peers(peer_bases, world, &Pe);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, ((int64_t)world * cap + 7) / 8);
+  ProfScope _ps("ep_dispatch_peer", s);
+  cudaError_t e = launch_pdl(k_ep_dispatch_peer, dim3(grid), dim3(256), 0, s, hidden, assign_token, bucket_off, R, Pe,
+                             rank, cap, lb_max, (int64_t)d, state);
+  if (e != cudaSuccess) return cuda_check(e, "ep_dispatch_peer launch");
+  return cuda_check(cudaGetLastError(), "ep_dispatch_peer launch");
+}
+
+int launch_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d, const uint32_t* state, cudaStream_t s) {
+  const uint32_t* flags = reinterpret_cast<const uint32_t*>(static_cast<const char*>(my_base) + ep_off_flags(world, cap, d));
+  ProfScope _ps("ep_wait", s);
+  cudaError_t e = launch_pdl(k_ep_wait_flags, dim3(1), dim3(64), 0, s, flags, world, state);
+  if (e != cudaSuccess) return cuda_check(e, "ep_wait launch");
+  return cuda_check(cudaGetLastError(), "ep_wait launch");
+}
+
+int launch_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int64_t cap, int d,
+                          const unsigned long long* peer_bases, uint32_t* state, cudaStream_t s) {
+  EpPeers Pe;
+  fill_peers(peer_bases, world, &Pe);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, ((int64_t)world * (cap + 1) + 7) / 8);
+  ProfScope _ps("ep_return_peer", s);
+  cudaError_t e = launch_pdl(k_ep_return_peer, dim3(grid), dim3(256), 0, s,
+                             reinterpret_cast<const uint16_t*>(y_local), return_idx, Pe, world, rank, cap,
+                             (int64_t)2 * d, d, state);
+  if (e != cudaSuccess) return cuda_check(e, "ep_return_peer launch");
+  return cuda_check(cudaGetLastError(), "ep_return_peer launch");
+}
+
+int launch_ep_home_index_peer(const int32_t* assign_of, const float* gate, const int32_t* bucket_off, int n_pairs,
+                              const int32_t* dest_pairs, int world, int64_t cap, int d, int64_t n, const void* my_base,
+                              int32_t* aof_s, float* gate_s, uint32_t* state, cudaStream_t s) {
+  EpRanks R;
+  int S = 0;
+  if (int rc = fill_ranks(dest_pairs, world, n_pairs, &R, &S)) return rc;
+  const uint32_t* flags_y =
+      reinterpret_cast<const uint32_t*>(static_cast<const char*>(my_base) + ep_off_flags(world, cap, d)) + world;
+  ProfScope _ps("ep_home_index_peer", s);
+  cudaError_t e = launch_pdl(k_ep_home_index_peer, dim3((unsigned)std::max<int64_t>(1, (n + 255) / 256)), dim3(256), 0,
+                             s, assign_of, gate, bucket_off, 2 * n_pairs + 1, R, S, cap, n, flags_y, aof_s, gate_s,
+                             state);
+  if (e != cudaSuccess) return cuda_check(e, "ep_home_index_peer launch");
+  return cuda_check(cudaGetLastError(), "ep_home_index_peer launch");
 }
 
 }  // namespace pz

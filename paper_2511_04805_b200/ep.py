@@ -118,6 +118,19 @@ class CudaOps:
     def ep_home_index(self, assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, cap):
         return self.pz.ep_home_index(assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, cap)
 
+    # NVLink peer-memory form (transfers fused into the dispatch / return kernels)
+    def ep_dispatch_peer(self, hidden, assign_token, bucket_off, n_pairs, dest_pairs, rank, pb, lb_max):
+        self.pz.ep_dispatch_peer(hidden, assign_token, bucket_off, n_pairs, dest_pairs, rank, pb, lb_max)
+
+    def ep_wait_dispatch(self, pb):
+        self.pz.ep_wait_dispatch(pb)
+
+    def ep_return_peer(self, y_local, return_idx, rank, pb):
+        self.pz.ep_return_peer(y_local, return_idx, rank, pb)
+
+    def ep_home_index_peer(self, assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, pb):
+        return self.pz.ep_home_index_peer(assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, pb)
+
 
 class ExpertParallelMoE:
     """One MoE layer sharded by merged pairs over `world` ranks of `group`.
@@ -261,3 +274,54 @@ class ExpertParallelMoE:
         aof_s, gate_s = self.ops.ep_home_index(state["assign_of"], state["gate"], state["bucket_off"], part.n_pairs,
                                                self.dest_pairs, part.slices, state["cap"])
         return self.ops.combine(y_back, aof_s, gate_s, residual)
+
+    # ---- the fixed-capacity layer over NVLink peer memory (no NCCL on the data path) ----
+    def attach_peer_buffer(self, pb):
+        """pb: paper_2511_04805_b200.EpPeerBuffer of this rank (see make_peer_buffer)."""
+        self.pb = pb
+
+    def forward_peer(self, hidden, logits, top_k: int, renormalize: bool, residual=None, path=None):
+        """forward_fixed with the transfers fused into the dispatch / return kernels: rows are
+        stored straight into the owners' peer buffers, outputs straight into the home ranks'
+        (cap = the peer buffer's capacity; the same on every rank)."""
+        state = self.peer_send(hidden, logits, top_k, renormalize)
+        self.peer_serve(path)
+        return self.peer_finish(state, residual)
+
+    def peer_send(self, hidden, logits, top_k: int, renormalize: bool):
+        ops, part, pb = self.ops, self.part, self.pb
+        if hidden.shape[0] * top_k > pb.cap:
+            raise ValueError("more assignments than the peer buffer's capacity")
+        topk_idx, gate, bucket_off, assign_token, assign_of = ops.route(self.route_layer, logits, top_k, renormalize)
+        ops.ep_dispatch_peer(hidden, assign_token, bucket_off, part.n_pairs, self.dest_pairs, self.rank, pb, self.lb_max)
+        return {"gate": gate, "bucket_off": bucket_off, "assign_of": assign_of}
+
+    def peer_serve(self, path=None):
+        ops, pb = self.ops, self.pb
+        ops.ep_wait_dispatch(pb)
+        local_off, gidx, ridx = ops.ep_recv_plan(pb.recv_x, self.world, self.n_local_buckets, pb.cap)
+        x_local = ops.gather_rows(pb.recv_x, gidx)
+        y_local = ops.experts(self.local_layer, x_local, local_off, path=path)
+        ops.ep_return_peer(y_local, ridx, self.rank, pb)
+
+    def peer_finish(self, state, residual=None):
+        ops, part, pb = self.ops, self.part, self.pb
+        aof_s, gate_s = ops.ep_home_index_peer(state["assign_of"], state["gate"], state["bucket_off"], part.n_pairs,
+                                               self.dest_pairs, part.slices, pb)
+        return ops.combine(pb.recv_y, aof_s, gate_s, residual)
+
+
+def make_peer_buffer(world: int, cap: int, d_model: int, device, group=None):
+    """This rank's EpPeerBuffer in torch symmetric memory (CUDA peer mappings over NVLink):
+    every rank of `group` calls it with the same (world, cap, d_model)."""
+    import paper_2511_04805_b200 as pz
+    import torch.distributed._symmetric_memory as symm
+    nbytes = pz.EpPeerBuffer.size(world, cap, d_model)
+    group = group if group is not None else dist.group.WORLD
+    name = group.group_name
+    buf = symm.empty(nbytes, dtype=torch.uint8, device=device)
+    hdl = symm.rendezvous(buf, name)
+    buf.zero_()
+    torch.cuda.synchronize(device)
+    dist.barrier(group=group)
+    return pz.EpPeerBuffer(buf, [int(p) for p in hdl.buffer_ptrs], world, cap, d_model)

@@ -283,3 +283,107 @@ def test_ep_fixed_simulated_world_matches_oracle(cfg, G, n_merged):
         torch.cuda.synchronize()
         ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, rb, pair_dense=dense)
         assert_close(out.float().cpu().numpy(), ref, f"simulated world {G}, rank {r}")
+
+
+# ---- the NVLink peer-memory form: transfers fused into the dispatch / return kernels ----
+
+def _sim_world(cfg, G, n_merged=None):
+    import paper_2511_04805_b200 as pz
+    from paper_2511_04805_b200.ep import ExpertParallelMoE, Partition, shard_dense, shard_packed
+    if n_merged is None:
+        w13, w2, slot, _ = oracle_packed_layer(cfg)
+        dense = None
+    else:
+        w13, w2, slot, dense = oracle_mixed_layer(cfg, n_merged)
+    n_slots = w13.shape[0]
+    w13_d = torch.from_numpy(w13.view(np.int16)).cuda()
+    w2_d = torch.from_numpy(w2.view(np.int16)).cuda()
+    slot_d = torch.from_numpy(slot).cuda()
+    dense_d = None if dense is None else torch.from_numpy(dense.astype(np.uint8)).cuda()
+    part = Partition(n_slots, G)
+    eps = []
+    for r in range(G):
+        w13_l, w2_l = shard_packed(w13_d, w2_d, part, r)
+        local = pz.PackedMoELayer(w13_l, w2_l, torch.arange(2 * w13_l.shape[0], dtype=torch.int32, device="cuda"),
+                                  shard_dense(dense_d, part, r))
+        route = pz.RoutingLayer(n_slots, cfg.d_model, cfg.d_ff, slot_d, w13_l)
+        eps.append(ExpertParallelMoE(part, r, route, local, cfg.d_model))
+    return eps, (w13, w2, slot, dense)
+
+
+@pytest.mark.parametrize("cfg,G,n_merged", [
+    (synth.MoEConfig("peer_small", 37, 256, 512, 8, 2, True), 2, None),
+    (synth.MoEConfig("peer_small", 37, 256, 512, 8, 2, True), 8, None),   # d_ff slices
+    (synth.MoEConfig("peer_fine", 38, 128, 256, 16, 4, False), 4, None),
+    (synth.MoEConfig("peer_25", 39, 256, 512, 8, 2, True), 3, 2),
+], ids=lambda v: str(v) if not hasattr(v, "name") else v.name)
+def test_ep_peer_simulated_world_matches_oracle(cfg, G, n_merged):
+    """G ranks' peer buffers in one process (plain device memory standing in for the NVLink
+    mappings), phases run rank after rank -- every wait is already satisfied when it runs, no
+    rank waits on another inside a kernel. Two consecutive steps (the epochs advance)."""
+    import paper_2511_04805_b200 as pz
+    eps, (w13, w2, slot, dense) = _sim_world(cfg, G, n_merged)
+    T = 20
+    cap = T * cfg.top_k
+    nbytes = pz.EpPeerBuffer.size(G, cap, cfg.d_model)
+    bufs = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(G)]
+    ptrs = [b.data_ptr() for b in bufs]
+    for r in range(G):
+        eps[r].attach_peer_buffer(pz.EpPeerBuffer(bufs[r], ptrs, G, cap, cfg.d_model))
+    for step in range(2):
+        inputs, states = [], []
+        for r in range(G):
+            Tr = T - (r + step) % 3  # ragged
+            hb = synth.hidden_bits(cfg, Tr, seed=800 + 10 * step + r)
+            lg = synth.router_logits(cfg, Tr, seed=900 + 10 * step + r)
+            inputs.append((hb, lg))
+            h = torch.from_numpy(hb.view(np.int16)).cuda().view(torch.bfloat16)
+            states.append(eps[r].peer_send(h, torch.from_numpy(lg).cuda(), cfg.top_k, cfg.renormalize))
+        for r in range(G):
+            eps[r].peer_serve(path=pz.PATH_GEMV)
+        for r in range(G):
+            out = eps[r].peer_finish(states[r])
+            torch.cuda.synchronize()
+            hb, lg = inputs[r]
+            ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, pair_dense=dense)
+            assert_close(out.float().cpu().numpy(), ref, f"peer world {G}, step {step}, rank {r}")
+    assert all(int(ep.pb.state[0].item()) == 2 for ep in eps)  # two steps published
+
+
+def test_ep_peer_world1_symmetric_memory_graph(nccl_group):
+    """World 1 through torch symmetric memory (the multi-GPU allocation path) and a CUDA graph:
+    the device-side epochs make replays correct without any reset."""
+    import paper_2511_04805_b200 as pz
+    from paper_2511_04805_b200.ep import make_peer_buffer
+    cfg = synth.MoEConfig("peer_graph", 40, 256, 512, 8, 2, True)
+    ep, (w13, w2, slot, _) = _ep_world1(cfg)
+    T = 16
+    try:
+        pb = make_peer_buffer(1, T * cfg.top_k, cfg.d_model, torch.device("cuda", 0))
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"torch symmetric memory unavailable here: {e!r}")
+    ep.attach_peer_buffer(pb)
+    h = torch.empty((T, cfg.d_model), dtype=torch.bfloat16, device="cuda")
+    lg = torch.empty((T, cfg.n_experts), dtype=torch.float32, device="cuda")
+
+    def load(seed):
+        hb = synth.hidden_bits(cfg, T, seed=seed)
+        lb = synth.router_logits(cfg, T, seed=seed + 1)
+        h.copy_(torch.from_numpy(hb.view(np.int16)).view(torch.bfloat16))
+        lg.copy_(torch.from_numpy(lb))
+        return hb, lb
+
+    hb, lb = load(60)
+    out = ep.forward_peer(h, lg, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV)  # eager
+    torch.cuda.synchronize()
+    assert_close(out.float().cpu().numpy(), oracle.moe_forward(w13, w2, slot, hb, lb, cfg.top_k, cfg.renormalize),
+                 "peer world 1 eager")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = ep.forward_peer(h, lg, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV)
+    for seed in (70, 80):
+        hb, lb = load(seed)
+        g.replay()
+        torch.cuda.synchronize()
+        assert_close(out.float().cpu().numpy(), oracle.moe_forward(w13, w2, slot, hb, lb, cfg.top_k, cfg.renormalize),
+                     f"peer world 1 replay {seed}")
