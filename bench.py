@@ -416,8 +416,21 @@ def run_ours(args):
         ep = ExpertParallelMoE(part, rank, routing, local, cfg.d_model)
 
     ep_fixed = ep is not None and T <= 64  # decode: static splits, no host sync, graph-capturable
+    ep_peer = None
+    if ep_fixed and args.ep_transport == "peer":
+        # rows / outputs stored straight into the owners' / home ranks' symmetric buffers by the
+        # dispatch / return kernels (NVLink peer memory, no NCCL on the data path)
+        from paper_2511_04805_b200.ep import make_peer_buffer
+        try:
+            ep_peer = make_peer_buffer(world, T * cfg.top_k, cfg.d_model, device)
+            ep.attach_peer_buffer(ep_peer)
+        except Exception as e:  # pragma: no cover
+            log("peer buffer unavailable, NCCL transport:", repr(e))
+            ep_peer = None
 
     def ep_forward(h, lg):
+        if ep_peer is not None:
+            return ep.forward_peer(h, lg, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV)
         if ep_fixed:
             return ep.forward_fixed(h, lg, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV)
         return ep.forward(h, lg, cfg.top_k, cfg.renormalize)
@@ -618,7 +631,8 @@ def run_ours(args):
     e2e = {"value": T * world / (e2e_ms / 1e3), "unit": "tokens/s",
            "h2d_bytes_per_step": h_host[0].numel() * 2 + l_host[0].numel() * 4,
            "d2h_bytes_per_step": o_host[0].numel() * 2, "ms_per_step": e2e_ms,
-           "api": ("ExpertParallelMoE." + ("forward_fixed" if ep_fixed else "forward") if ep is not None
+           "api": ("ExpertParallelMoE." + ("forward_peer" if ep_peer is not None else "forward_fixed" if ep_fixed
+                                           else "forward") if ep is not None
                    else "PackedMoELayer.forward -> puzzle_moe_forward_ex") + " (host pinned buffers)",
            "pipelined": ep is None and flush is None,
            "note": "copy-in of step i+1 and copy-out of step i-1 overlap step i's forward (two buffer sets, "
@@ -635,12 +649,15 @@ def run_ours(args):
                        "n_pairs": cfg.n_pairs, "top_k": cfg.top_k, "batch_per_gpu": T,
                        "parallelism": f"ep{world} (pairs sharded, NCCL all-to-all dispatch/combine, "
                                       f"{T} tokens per rank, "
-                                      + ("fixed-capacity dispatch)" if ep_fixed else "variable-split dispatch)")
+                                      + ("fixed-capacity dispatch over NVLink peer memory)" if ep_peer is not None
+                                         else "fixed-capacity dispatch, NCCL)" if ep_fixed
+                                         else "variable-split dispatch, NCCL)")
                                       if dist_on else "single",
                        "l2": "inputs larger than L2 (packed layer %.2f GB)" % (layer.packed_bytes / 1e9) if big
                        else "L2 flushed between timed steps",
                        "launch": "CUDA graph replay of the whole forward" if graph is not None else "eager"},
             "roofline": roof, "step_weight_gbs": step_gbs, "gpu_launches": gpu_launches,
+            **({"ep_peer_wait_timeouts": ep_peer.wait_timeouts()} if ep_peer is not None else {}),
             "step_ms_percentiles": {"p10": pct[10], "p50": pct[50], "p90": pct[90], "steps": len(per_step),
                                     "note": "one event pair per step, separate pass (rank-local)"},
             "kernels": kern, "e2e": e2e}
@@ -895,6 +912,16 @@ def stack_runs_ep(pz, args, device, part, rank, world):
         eps.append(ExpertParallelMoE(part, rank, routing, local, cfg.d_model))
         del layer
     torch.cuda.empty_cache()
+    pb = None
+    if args.ep_transport == "peer":  # one peer buffer serves every layer (calls are sequential)
+        from paper_2511_04805_b200.ep import make_peer_buffer
+        try:
+            pb = make_peer_buffer(world, 64 * cfg.top_k, cfg.d_model, device)
+            for ep in eps:
+                ep.attach_peer_buffer(pb)
+        except Exception as e:  # pragma: no cover
+            log("peer buffer unavailable, NCCL transport:", repr(e))
+            pb = None
     res = []
     for T in (64, 8192):
         g = torch.Generator(device=device)
@@ -906,7 +933,9 @@ def stack_runs_ep(pz, args, device, part, rank, world):
         def step():
             x = x0
             for l, ep in enumerate(eps):
-                if fixed:
+                if fixed and pb is not None:
+                    x = ep.forward_peer(x, logits[l], cfg.top_k, cfg.renormalize, residual=x, path=pz.PATH_GEMV)
+                elif fixed:
                     x = ep.forward_fixed(x, logits[l], cfg.top_k, cfg.renormalize, residual=x, path=pz.PATH_GEMV)
                 else:
                     x = ep.forward(x, logits[l], cfg.top_k, cfg.renormalize, residual=x)
@@ -931,8 +960,11 @@ def stack_runs_ep(pz, args, device, part, rank, world):
         ms = float(t.item())
         row = {"config": f"mixtral_stack32_ep{world}", "batch_per_rank": T, "ms_per_step": ms,
                "tokens_per_s": T * world / (ms / 1e3), "layers": n_layers,
-               "dispatch": ("fixed-capacity, one CUDA graph of 32 layers" if fixed and not args.no_graph
-                            else "fixed-capacity, eager" if fixed else "variable-split, eager")}
+               "dispatch": (("fixed-capacity over NVLink peer memory" if pb is not None else "fixed-capacity, NCCL")
+                            + (", one CUDA graph of 32 layers" if not args.no_graph else ", eager")
+                            if fixed else "variable-split, NCCL, eager")}
+        if fixed and pb is not None:
+            row["peer_wait_timeouts"] = pb.wait_timeouts()
         if not fixed:
             row["tflops_per_rank"] = 2 * 3 * cfg.d_model * cfg.d_ff * T * cfg.top_k * n_layers / (ms / 1e3) / 1e12
         res.append(row)
@@ -955,6 +987,8 @@ def main(argv=None):
     ap.add_argument("--no-extra", action="store_true", help="skip the unpacked baseline / sweep / packer lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--ep1", action="store_true", help="run the expert-parallel path in a 1-rank NCCL group")
+    ap.add_argument("--ep-transport", choices=["peer", "nccl"], default="peer",
+                    help="EP decode transport: kernels storing into peer memory, or NCCL all-to-all")
     ap.add_argument("--stack-ep", action="store_true", help="with --ep1: also the expert-parallel 32-layer stack")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     args = ap.parse_args(argv)

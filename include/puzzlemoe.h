@@ -322,8 +322,10 @@ int puzzle_ep_home_index(const int32_t* assign_of, const float* topk_gate, const
  *   flags   u32  [2][world] (dispatch / return epochs) after recv_y.
  * peer_bases  HOST u64 [world]: the device address of rank q's peer buffer as mapped on THIS
  *             rank (peer_bases[rank] = its own buffer).
- * state       device u32 [4], zero-initialised once, private to the rank and the layer: the step
- *             counter (epochs) and the kernels' CTA completion counters.
+ * state       device u32 [8], zero-initialised once, private to the rank and the layer: [0] the
+ *             step counter (epochs), [1..3] the kernels' CTA completion counters, [4] the number
+ *             of cross-rank waits that gave up after ~10 s (a peer never arrived: the outputs of
+ *             that step are invalid; nonzero means the ranks' call sequences diverged).
  * Per layer call (stream-ordered on one stream; graph-capturable):
  *   puzzle_moe_route -> puzzle_ep_dispatch_peer -> puzzle_ep_wait_dispatch (waits until every
  *   source's region of this step has landed) -> puzzle_ep_recv_plan(recv_x) -> gather ->
@@ -338,7 +340,7 @@ int puzzle_ep_dispatch_peer(const uint16_t* hidden, const int32_t* assign_token,
                             int n_pairs, const int32_t* dest_pairs, int world, int rank, int64_t n_assign,
                             int64_t cap, int lb_max, int d_model, const unsigned long long* peer_bases,
                             uint32_t* state, puzzle_stream_t stream);
-int puzzle_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d_model, const uint32_t* state,
+int puzzle_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d_model, uint32_t* state,
                             puzzle_stream_t stream);
 /* y_local f32 [world*cap][d_model] (the experts' outputs in local order), return_idx from
  * puzzle_ep_recv_plan: slot (s, w) of home rank s's recv_y region [rank] <- y_local[return_idx]. */

@@ -379,11 +379,15 @@ class EpPeerBuffer:
         self.buffer, self.world, self.cap, self.d = buffer, world, cap, d_model
         self.peers = np.ascontiguousarray(np.asarray(peer_ptrs, dtype=np.uint64))
         assert self.peers.size == world
-        self.state = torch.zeros(4, dtype=torch.int32, device=buffer.device)
+        self.state = torch.zeros(8, dtype=torch.int32, device=buffer.device)
         R = cap + 1
         self.recv_x = buffer.view(torch.uint8)[:world * R * d_model * 2].view(torch.bfloat16).view(world * R, d_model)
         off_y = (world * R * d_model * 2 + 255) // 256 * 256
         self.recv_y = buffer.view(torch.uint8)[off_y:off_y + world * R * d_model * 4].view(torch.float32).view(world * R, d_model)
+
+    def wait_timeouts(self) -> int:
+        """Cross-rank waits that gave up (state[4]); nonzero = some step's outputs are invalid."""
+        return int(self.state[4].item())
 
     @staticmethod
     def size(world: int, cap: int, d_model: int) -> int:

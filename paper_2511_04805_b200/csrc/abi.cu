@@ -41,7 +41,7 @@ int launch_ep_home_index(const int32_t*, const float*, const int32_t*, int, cons
 size_t ep_peer_buffer_bytes(int world, int64_t cap, int d);
 int launch_ep_dispatch_peer(const uint16_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int, int64_t, int,
                             int, const unsigned long long*, uint32_t*, cudaStream_t);
-int launch_ep_wait_dispatch(const void*, int, int64_t, int, const uint32_t*, cudaStream_t);
+int launch_ep_wait_dispatch(const void*, int, int64_t, int, uint32_t*, cudaStream_t);
 int launch_ep_return_peer(const float*, const int32_t*, int, int, int64_t, int, const unsigned long long*, uint32_t*,
                           cudaStream_t);
 int launch_ep_home_index_peer(const int32_t*, const float*, const int32_t*, int, const int32_t*, int, int64_t, int,
@@ -666,7 +666,7 @@ int puzzle_ep_dispatch_peer(const uint16_t* hidden, const int32_t* assign_token,
                                  d_model, peer_bases, state, (cudaStream_t)stream);
 }
 
-int puzzle_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d_model, const uint32_t* state,
+int puzzle_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d_model, uint32_t* state,
                             puzzle_stream_t stream) {
   if (int rc = check_peer_common(world, 0, cap, d_model)) return rc;
   if (!my_base || !state) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");

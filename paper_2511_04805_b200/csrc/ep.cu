@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(256) k_ep_home_index(const int32_t* __restrict
 //   recv_x  bf16 [world][cap+1][d]   region s = what source rank s dispatched to this rank
 //   recv_y  f32  [world][cap+1][d]   region q = what owner q returned for this rank's rows
 //   flags   u32  [2][world]          [0][s] / [1][q]: the epoch of the last region s / q stored
-// and a local state (u32: step, then per-kernel CTA completion counters; zero-initialised).
+// and a local state (u32 [8]: step, per-kernel CTA completion counters, wait-timeout count;
+// zero-initialised).
 // Epochs: every layer call of a rank reads step e; its stores are published with e + 1
 // (release, system scope, by the last CTA of the storing kernel after all CTAs' stores); the
 // consumers wait for e + 1 (acquire); the home-index kernel's last CTA advances step. Flags only
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(256) k_ep_home_index(const int32_t* __restrict
 struct EpPeers {
   unsigned long long base[kEpMaxRanks];
 };
-constexpr int kStStep = 0, kStDispatch = 1, kStReturn = 2, kStHome = 3;
+constexpr int kStStep = 0, kStDispatch = 1, kStReturn = 2, kStHome = 3, kStError = 4;
 
 __host__ __device__ inline size_t ep_off_y(int world, int64_t cap, int d) {
   return ((size_t)world * (cap + 1) * d * 2 + 255) / 256 * 256;
@@ -263,13 +264,30 @@ __global__ void __launch_bounds__(256) k_ep_dispatch_peer(const uint16_t* __rest
   }
 }
 
+// Bounded cross-rank wait: a peer that never arrives (a rank that stopped calling, a bug)
+// must not hang the GPU -- after ~10 s the waiter records the failure in state[kStError] (the
+// host reads it with puzzle_ep_peer_status semantics via the state tensor) and proceeds.
+__device__ __forceinline__ void ep_wait_epoch(const uint32_t* flag, uint32_t epoch, uint32_t* state) {
+  if (*reinterpret_cast<volatile uint32_t*>(state + kStError)) return;  // sticky: fail fast once diverged
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (ld_acquire_sys(flag) < epoch) {
+    __nanosleep(64);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10000000000ull) {
+      atomicAdd(state + kStError, 1u);
+      return;
+    }
+  }
+}
+
 // Owner: wait until every source's region of this step has landed (flags[0][s] >= epoch).
-__global__ void k_ep_wait_flags(const uint32_t* __restrict__ flags, int world, const uint32_t* __restrict__ state) {
+__global__ void k_ep_wait_flags(const uint32_t* __restrict__ flags, int world, uint32_t* __restrict__ state) {
   pdl_wait();
   pdl_trigger();
   const uint32_t epoch = state[kStStep] + 1;
-  for (int s = threadIdx.x; s < world; s += blockDim.x)
-    while (ld_acquire_sys(flags + s) < epoch) __nanosleep(32);
+  for (int s = threadIdx.x; s < world; s += blockDim.x) ep_wait_epoch(flags + s, epoch, state);
   __syncthreads();
 }
 
@@ -313,8 +331,7 @@ __global__ void __launch_bounds__(256) k_ep_home_index_peer(const int32_t* __res
   pdl_wait();
   pdl_trigger();
   const uint32_t epoch = state[kStStep] + 1;
-  for (int q = threadIdx.x; q < R.world; q += blockDim.x)
-    while (ld_acquire_sys(flags_y + q) < epoch) __nanosleep(32);
+  for (int q = threadIdx.x; q < R.world; q += blockDim.x) ep_wait_epoch(flags_y + q, epoch, state);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
@@ -445,7 +462,7 @@ int launch_ep_dispatch_peer(const uint16_t* hidden, const int32_t* assign_token,
   return cuda_check(cudaGetLastError(), "ep_dispatch_peer launch");
 }
 
-int launch_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d, const uint32_t* state, cudaStream_t s) {
+int launch_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d, uint32_t* state, cudaStream_t s) {
   const uint32_t* flags = reinterpret_cast<const uint32_t*>(static_cast<const char*>(my_base) + ep_off_flags(world, cap, d));
   ProfScope _ps("ep_wait", s);
   cudaError_t e = launch_pdl(k_ep_wait_flags, dim3(1), dim3(64), 0, s, flags, world, state);

@@ -348,6 +348,7 @@ def test_ep_peer_simulated_world_matches_oracle(cfg, G, n_merged):
             ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, pair_dense=dense)
             assert_close(out.float().cpu().numpy(), ref, f"peer world {G}, step {step}, rank {r}")
     assert all(int(ep.pb.state[0].item()) == 2 for ep in eps)  # two steps published
+    assert all(ep.pb.wait_timeouts() == 0 for ep in eps)
 
 
 def test_ep_peer_world1_symmetric_memory_graph(nccl_group):
@@ -387,3 +388,4 @@ def test_ep_peer_world1_symmetric_memory_graph(nccl_group):
         torch.cuda.synchronize()
         assert_close(out.float().cpu().numpy(), oracle.moe_forward(w13, w2, slot, hb, lb, cfg.top_k, cfg.renormalize),
                      f"peer world 1 replay {seed}")
+    assert pb.wait_timeouts() == 0 and int(pb.state[0].item()) == 3
