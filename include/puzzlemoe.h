@@ -327,8 +327,8 @@ int puzzle_ep_home_index(const int32_t* assign_of, const float* topk_gate, const
  *             of cross-rank waits that gave up after ~10 s (a peer never arrived: the outputs of
  *             that step are invalid; nonzero means the ranks' call sequences diverged).
  * Per layer call (stream-ordered on one stream; graph-capturable):
- *   puzzle_moe_route -> puzzle_ep_dispatch_peer -> puzzle_ep_wait_dispatch (waits until every
- *   source's region of this step has landed) -> puzzle_ep_recv_plan(recv_x) -> gather ->
+ *   puzzle_moe_route -> puzzle_ep_dispatch_peer -> puzzle_ep_recv_plan_peer (waits until every
+ *   source's region of this step has landed, then plans on recv_x) -> gather ->
  *   puzzle_moe_experts -> puzzle_ep_return_peer -> puzzle_ep_home_index_peer (waits for every
  *   owner's return; advances the step) -> puzzle_moe_combine(recv_y, ...).
  * Every rank must make the same sequence of calls (the waits are cross-rank: a rank that stops
@@ -342,6 +342,11 @@ int puzzle_ep_dispatch_peer(const uint16_t* hidden, const int32_t* assign_token,
                             uint32_t* state, puzzle_stream_t stream);
 int puzzle_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d_model, uint32_t* state,
                             puzzle_stream_t stream);
+/* puzzle_ep_wait_dispatch + puzzle_ep_recv_plan(recv_x of my_base) in one kernel (the form the
+ * layer uses: one launch less). */
+int puzzle_ep_recv_plan_peer(const void* my_base, int world, int n_local_buckets, int64_t cap, int d_model,
+                             uint32_t* state, int32_t* local_off, int32_t* gather_idx, int32_t* return_idx,
+                             puzzle_stream_t stream);
 /* y_local f32 [world*cap][d_model] (the experts' outputs in local order), return_idx from
  * puzzle_ep_recv_plan: slot (s, w) of home rank s's recv_y region [rank] <- y_local[return_idx]. */
 int puzzle_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int64_t cap,

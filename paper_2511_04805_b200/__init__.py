@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = (
     "puzzle_group_colsumsq", "puzzle_moe_calib_workspace_size", "puzzle_moe_forward_calib",
     "puzzle_quant_pack", "puzzle_quant_unpack", "puzzle_ep_dispatch", "puzzle_ep_recv_plan",
     "puzzle_ep_home_index", "puzzle_ep_peer_buffer_size", "puzzle_ep_dispatch_peer", "puzzle_ep_wait_dispatch",
-    "puzzle_ep_return_peer", "puzzle_ep_home_index_peer",
+    "puzzle_ep_return_peer", "puzzle_ep_home_index_peer", "puzzle_ep_recv_plan_peer",
 )
 
 
@@ -99,6 +99,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_ep_peer_buffer_size": ([I, I64, I], SZ),
             "puzzle_ep_dispatch_peer": ([P, P, P, I, P, I, I, I64, I64, I, I, P, P, P], I),
             "puzzle_ep_wait_dispatch": ([P, I, I64, I, P, P], I),
+            "puzzle_ep_recv_plan_peer": ([P, I, I, I64, I, P, P, P, P, P], I),
             "puzzle_ep_return_peer": ([P, P, I, I, I64, I, P, P, P], I),
             "puzzle_ep_home_index_peer": ([P, P, P, I, P, I, I64, I64, I, I, P, P, P, P, P], I),
             "puzzle_profile_begin": ([], I),
@@ -408,6 +409,19 @@ def ep_dispatch_peer(hidden, assign_token, bucket_off, n_pairs: int, dest_pairs,
 def ep_wait_dispatch(pb: EpPeerBuffer, stream=None):
     _check(load_library().puzzle_ep_wait_dispatch(_p(pb.buffer), pb.world, pb.cap, pb.d, _p(pb.state), _stream(stream)),
            "puzzle_ep_wait_dispatch")
+
+
+def ep_recv_plan_peer(pb: "EpPeerBuffer", n_local_buckets: int, stream=None):
+    """wait for this step's dispatch into pb, then puzzle_ep_recv_plan on pb.recv_x (one kernel)."""
+    dev = pb.buffer.device
+    world, cap = pb.world, pb.cap
+    local_off = torch.empty(n_local_buckets + 1, dtype=torch.int32, device=dev)
+    gidx = torch.empty(max(world * cap, 1), dtype=torch.int32, device=dev)[:world * cap]
+    ridx = torch.empty(world * (cap + 1), dtype=torch.int32, device=dev)
+    _check(load_library().puzzle_ep_recv_plan_peer(_p(pb.buffer), world, int(n_local_buckets), cap, pb.d,
+                                                   _p(pb.state), _p(local_off), _p(gidx), _p(ridx), _stream(stream)),
+           "puzzle_ep_recv_plan_peer")
+    return local_off, gidx, ridx
 
 
 def ep_return_peer(y_local, return_idx, rank: int, pb: EpPeerBuffer, stream=None):

@@ -35,7 +35,7 @@ int launch_gather_rows(const uint16_t*, const int32_t*, int64_t, int64_t, uint16
 int launch_ep_dispatch(const uint16_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int64_t, int, int,
                        uint16_t*, cudaStream_t);
 size_t ep_recv_plan_smem(int world, int lb);
-int launch_ep_recv_plan(const uint16_t*, int, int, int64_t, int, int32_t*, int32_t*, int32_t*, cudaStream_t);
+int launch_ep_recv_plan(const uint16_t*, int, int, int64_t, int, int32_t*, int32_t*, int32_t*, uint32_t*, cudaStream_t);
 int launch_ep_home_index(const int32_t*, const float*, const int32_t*, int, const int32_t*, int, int64_t, int64_t,
                          int32_t*, float*, int*, cudaStream_t);
 size_t ep_peer_buffer_bytes(int world, int64_t cap, int d);
@@ -606,8 +606,7 @@ int puzzle_ep_dispatch(const uint16_t* hidden, const int32_t* assign_token, cons
                             send_rows, (cudaStream_t)stream);
 }
 
-int puzzle_ep_recv_plan(const uint16_t* recv_rows, int world, int n_local_buckets, int64_t cap, int d_model,
-                        int32_t* local_off, int32_t* gather_idx, int32_t* return_idx, puzzle_stream_t stream) {
+static int check_recv_plan_sizes(int world, int n_local_buckets, int64_t cap, int d_model) {
   if (world < 1 || world > 64 || n_local_buckets < 0 || cap < 0 || d_model < 8 || d_model % 8)
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes (1 <= world <= 64, n_local_buckets >= 0, cap >= 0, d_model % 8 == 0)");
   if (4 * (int64_t)n_local_buckets > 2 * (int64_t)d_model)
@@ -615,12 +614,30 @@ int puzzle_ep_recv_plan(const uint16_t* recv_rows, int world, int n_local_bucket
   if (n_local_buckets > 1024 || pz::ep_recv_plan_smem(world, n_local_buckets) > 48 * 1024 ||
       (int64_t)world * (cap + 1) > INT32_MAX)
     return fail(PUZZLE_ERR_UNSUPPORTED, "n_local_buckets <= 1024, world * n_local_buckets <= ~4000, world * (cap + 1) < 2^31");
+  return PUZZLE_OK;
+}
+
+int puzzle_ep_recv_plan(const uint16_t* recv_rows, int world, int n_local_buckets, int64_t cap, int d_model,
+                        int32_t* local_off, int32_t* gather_idx, int32_t* return_idx, puzzle_stream_t stream) {
+  if (int rc = check_recv_plan_sizes(world, n_local_buckets, cap, d_model)) return rc;
   if (!recv_rows || !local_off || !return_idx || (cap > 0 && !gather_idx))
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (!al16(recv_rows)) return fail(PUZZLE_ERR_UNSUPPORTED, "recv_rows must be 16-byte aligned");
   if (int rc = check_device()) return rc;
   return launch_ep_recv_plan(recv_rows, world, n_local_buckets, cap, d_model, local_off, gather_idx, return_idx,
-                             (cudaStream_t)stream);
+                             nullptr, (cudaStream_t)stream);
+}
+
+int puzzle_ep_recv_plan_peer(const void* my_base, int world, int n_local_buckets, int64_t cap, int d_model,
+                             uint32_t* state, int32_t* local_off, int32_t* gather_idx, int32_t* return_idx,
+                             puzzle_stream_t stream) {
+  if (int rc = check_recv_plan_sizes(world, n_local_buckets, cap, d_model)) return rc;
+  if (!my_base || !state || !local_off || !return_idx || (cap > 0 && !gather_idx))
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (reinterpret_cast<uintptr_t>(my_base) & 255) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "my_base must be 256-byte aligned");
+  if (int rc = check_device()) return rc;
+  return launch_ep_recv_plan(static_cast<const uint16_t*>(my_base), world, n_local_buckets, cap, d_model, local_off,
+                             gather_idx, return_idx, state, (cudaStream_t)stream);
 }
 
 int puzzle_ep_home_index(const int32_t* assign_of, const float* topk_gate, const int32_t* bucket_off, int n_pairs,

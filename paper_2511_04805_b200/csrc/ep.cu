@@ -31,6 +31,33 @@ struct EpRanks {
 
 namespace {
 
+// Peer-memory form state (see below): u32 [8].
+constexpr int kStStep = 0, kStDispatch = 1, kStReturn = 2, kStHome = 3, kStError = 4;
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Bounded cross-rank wait: a peer that never arrives (a rank that stopped calling, a bug)
+// must not hang the GPU -- after ~10 s the waiter records the failure in state[kStError] (the
+// host reads it with puzzle_ep_peer_status semantics via the state tensor) and proceeds.
+__device__ __forceinline__ void ep_wait_epoch(const uint32_t* flag, uint32_t epoch, uint32_t* state) {
+  if (*reinterpret_cast<volatile uint32_t*>(state + kStError)) return;  // sticky: fail fast once diverged
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (ld_acquire_sys(flag) < epoch) {
+    __nanosleep(64);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10000000000ull) {
+      atomicAdd(state + kStError, 1u);
+      return;
+    }
+  }
+}
+
 // send_rows[q*R + i] = hidden[assign_token[off[2 lo_q] + i]] for i < n_q (warp per row, 8 loads
 // in flight per lane); the header row q*R + cap gets q's bucket counts (0 past q's buckets).
 __global__ void __launch_bounds__(256) k_ep_dispatch(const uint16_t* __restrict__ hidden,
@@ -68,7 +95,9 @@ __global__ void __launch_bounds__(256) k_ep_dispatch(const uint16_t* __restrict_
 __global__ void __launch_bounds__(1024) k_ep_recv_plan(const uint16_t* __restrict__ recv_rows, int world, int lb,
                                                        int64_t cap, int64_t cols, int32_t* __restrict__ local_off,
                                                        int32_t* __restrict__ gather_idx,
-                                                       int32_t* __restrict__ return_idx) {
+                                                       int32_t* __restrict__ return_idx,
+                                                       const uint32_t* __restrict__ wait_flags,
+                                                       uint32_t* __restrict__ state) {
   extern __shared__ int32_t sm[];
   int32_t* rc = sm;                                 // [world][lb]
   int32_t* pre_s = rc + world * lb;                 // [world][lb + 1]: exclusive over b, total last
@@ -79,6 +108,11 @@ __global__ void __launch_bounds__(1024) k_ep_recv_plan(const uint16_t* __restric
   pdl_trigger();
   const int64_t reg = cap + 1;
   const int tid = threadIdx.x;
+  if (wait_flags != nullptr) {  // peer-memory form: every source's region of this step has landed
+    const uint32_t epoch = state[kStStep] + 1;
+    for (int s = tid; s < world; s += blockDim.x) ep_wait_epoch(wait_flags + s, epoch, state);
+    __syncthreads();
+  }
   for (int i = tid; i < world * lb; i += blockDim.x) {
     const int s = i / lb;
     rc[i] = reinterpret_cast<const int32_t*>(recv_rows + ((int64_t)s * reg + cap) * cols)[i - s * lb];
@@ -192,7 +226,6 @@ __global__ void __launch_bounds__(256) k_ep_home_index(const int32_t* __restrict
 struct EpPeers {
   unsigned long long base[kEpMaxRanks];
 };
-constexpr int kStStep = 0, kStDispatch = 1, kStReturn = 2, kStHome = 3, kStError = 4;
 
 __host__ __device__ inline size_t ep_off_y(int world, int64_t cap, int d) {
   return ((size_t)world * (cap + 1) * d * 2 + 255) / 256 * 256;
@@ -204,19 +237,16 @@ __host__ __device__ inline size_t ep_off_flags(int world, int64_t cap, int d) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
-// After this CTA's stores: the last CTA of the grid (counter) publishes `epoch` into flag slot
-// `slot` of every peer (or, with self_flag, into this rank's own flags of every source... n/a).
+// After this CTA's stores: true in the last CTA of the grid to arrive (it then publishes).
 __device__ __forceinline__ bool ep_last_cta(uint32_t* done) {
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();  // this CTA's peer stores before its arrival
+    // GPU-scope release of this CTA's stores (the bar.sync above orders the other threads'),
+    // then ONE system-scope fence in the last CTA: causality is transitive across the two
+    // synchronisations (CTA -> last CTA at gpu scope, last CTA -> peer reader at sys scope)
+    __threadfence();
     last = atomicAdd(done, 1u) == gridDim.x - 1;
     if (last) {
       *done = 0;  // ready for the next call
@@ -261,24 +291,6 @@ __global__ void __launch_bounds__(256) k_ep_dispatch_peer(const uint16_t* __rest
     const int q = threadIdx.x;
     uint32_t* fl = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(Pe.base[q]) + ep_off_flags(R.world, cap, (int)(cols)));
     st_release_sys(fl + rank, epoch);  // flags[0][rank] of owner q
-  }
-}
-
-// Bounded cross-rank wait: a peer that never arrives (a rank that stopped calling, a bug)
-// must not hang the GPU -- after ~10 s the waiter records the failure in state[kStError] (the
-// host reads it with puzzle_ep_peer_status semantics via the state tensor) and proceeds.
-__device__ __forceinline__ void ep_wait_epoch(const uint32_t* flag, uint32_t epoch, uint32_t* state) {
-  if (*reinterpret_cast<volatile uint32_t*>(state + kStError)) return;  // sticky: fail fast once diverged
-  uint64_t t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (ld_acquire_sys(flag) < epoch) {
-    __nanosleep(64);
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 10000000000ull) {
-      atomicAdd(state + kStError, 1u);
-      return;
-    }
   }
 }
 
@@ -410,13 +422,17 @@ size_t ep_recv_plan_smem(int world, int lb) {
 }
 
 int launch_ep_recv_plan(const uint16_t* recv_rows, int world, int lb, int64_t cap, int d, int32_t* local_off,
-                        int32_t* gather_idx, int32_t* return_idx, cudaStream_t s) {
+                        int32_t* gather_idx, int32_t* return_idx, uint32_t* state, cudaStream_t s) {
+  // state != NULL: recv_rows is this rank's peer buffer; wait for its dispatch flags first
+  const uint32_t* wait_flags =
+      state ? reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(recv_rows) + ep_off_flags(world, cap, d))
+            : nullptr;
   const size_t smem = ep_recv_plan_smem(world, lb);
   const int64_t rows = (int64_t)world * (cap + 1);
   const unsigned grid = (unsigned)std::max<int64_t>(1, (rows + 1023) / 1024);
   ProfScope _ps("ep_recv_plan", s);
   cudaError_t e = launch_pdl(k_ep_recv_plan, dim3(grid), dim3(1024), smem, s, recv_rows, world, lb, cap, (int64_t)d,
-                             local_off, gather_idx, return_idx);
+                             local_off, gather_idx, return_idx, wait_flags, state);
   if (e != cudaSuccess) return cuda_check(e, "ep_recv_plan launch");
   return cuda_check(cudaGetLastError(), "ep_recv_plan launch");
 }

@@ -125,6 +125,9 @@ class CudaOps:
     def ep_wait_dispatch(self, pb):
         self.pz.ep_wait_dispatch(pb)
 
+    def ep_recv_plan_peer(self, pb, n_local_buckets):
+        return self.pz.ep_recv_plan_peer(pb, n_local_buckets)
+
     def ep_return_peer(self, y_local, return_idx, rank, pb):
         self.pz.ep_return_peer(y_local, return_idx, rank, pb)
 
@@ -298,8 +301,7 @@ class ExpertParallelMoE:
 
     def peer_serve(self, path=None):
         ops, pb = self.ops, self.pb
-        ops.ep_wait_dispatch(pb)
-        local_off, gidx, ridx = ops.ep_recv_plan(pb.recv_x, self.world, self.n_local_buckets, pb.cap)
+        local_off, gidx, ridx = ops.ep_recv_plan_peer(pb, self.n_local_buckets)  # waits for the dispatch
         x_local = ops.gather_rows(pb.recv_x, gidx)
         y_local = ops.experts(self.local_layer, x_local, local_off, path=path)
         ops.ep_return_peer(y_local, ridx, self.rank, pb)
