@@ -214,6 +214,7 @@ int puzzle_moe_forward_ex(const puzzle_moe_layer* L, const uint16_t* hidden,
  *   assign_token i32 [T*top_k]    token of assignment a (assignments grouped by bucket)
  *   assign_of    i32 [T*top_k]    assignment index of (t, j)
  *   The order of assignments inside one bucket is unspecified (results do not depend on it).
+ *   T = 0 writes an all-zero bucket_off (every bucket empty) and nothing else.
  *   workspace: device scratch of >= puzzle_moe_route_workspace_size(L) bytes (decode batches,
  *   T <= 64, route with a top-k grid + a scatter grid and keep per-CTA histograms there; batches
  *   with T*top_k > 4096 keep global counts there; the sizes in between route inside one CTA).

@@ -532,10 +532,12 @@ int puzzle_moe_route(const puzzle_moe_layer* L, const float* logits, int64_t T, 
   if (int rc = check_layer(L)) return rc;
   if (T < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "T < 0");
   if (k < 1 || k > L->n_experts) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "top_k outside [1, n_experts]");
-  if (!logits || !topk_idx || !topk_gate || !bucket_off || !assign_token || !assign_of)
+  if (!bucket_off || (T > 0 && (!logits || !topk_idx || !topk_gate || !assign_token || !assign_of)))
     return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (int rc = check_device()) return rc;
-  if (T == 0) return PUZZLE_OK;
+  if (T == 0)  // no assignments: every bucket empty (consumers such as the EP dispatch read the offsets)
+    return cuda_check(cudaMemsetAsync(bucket_off, 0, (size_t)(2 * L->n_pairs + 1) * sizeof(int32_t),
+                                      (cudaStream_t)stream), "route memset");
   if (workspace_bytes < puzzle_moe_route_workspace_size(L) || (!workspace && workspace_bytes))
     return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_moe_route_workspace_size(L)");
   if (T <= kGemvMaxTokens)  // decode batches: the forward's two-grid routing (top-k grid + scatter grid)

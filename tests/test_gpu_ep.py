@@ -264,7 +264,7 @@ def test_ep_fixed_simulated_world_matches_oracle(cfg, G, n_merged):
     T = 24
     inputs, sends, states = [], [], []
     for r in range(G):
-        Tr = T - r  # ragged per-rank batches, one capacity for all
+        Tr = T - r if r < G - 1 or G < 3 else 0  # ragged per-rank batches (an idle rank at G >= 3), one capacity
         hb = synth.hidden_bits(cfg, Tr, seed=500 + r)
         lg = synth.router_logits(cfg, Tr, seed=600 + r)
         rb = synth.hidden_bits(cfg, Tr, seed=700 + r)
@@ -281,6 +281,9 @@ def test_ep_fixed_simulated_world_matches_oracle(cfg, G, n_merged):
         hb, lg, rb = inputs[r]
         out = eps[r].fixed_finish(back, states[r], torch.from_numpy(rb.view(np.int16)).cuda().view(torch.bfloat16))
         torch.cuda.synchronize()
+        if hb.shape[0] == 0:
+            assert out.shape == (0, cfg.d_model)
+            continue
         ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, rb, pair_dense=dense)
         assert_close(out.float().cpu().numpy(), ref, f"simulated world {G}, rank {r}")
 
@@ -333,7 +336,7 @@ def test_ep_peer_simulated_world_matches_oracle(cfg, G, n_merged):
     for step in range(2):
         inputs, states = [], []
         for r in range(G):
-            Tr = T - (r + step) % 3  # ragged
+            Tr = T - (r + step) % 3 if (r, step) != (G - 1, 1) else 0  # ragged; the last rank idle in step 1
             hb = synth.hidden_bits(cfg, Tr, seed=800 + 10 * step + r)
             lg = synth.router_logits(cfg, Tr, seed=900 + 10 * step + r)
             inputs.append((hb, lg))
@@ -345,6 +348,9 @@ def test_ep_peer_simulated_world_matches_oracle(cfg, G, n_merged):
             out = eps[r].peer_finish(states[r])
             torch.cuda.synchronize()
             hb, lg = inputs[r]
+            if hb.shape[0] == 0:
+                assert out.shape == (0, cfg.d_model)
+                continue
             ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, pair_dense=dense)
             assert_close(out.float().cpu().numpy(), ref, f"peer world {G}, step {step}, rank {r}")
     assert all(int(ep.pb.state[0].item()) == 2 for ep in eps)  # two steps published
