@@ -508,6 +508,17 @@ def run_ours(args):
         ms = float(t.item())
     value = T * world / (ms / 1e3)
 
+    # the peer-memory transport moves the same rows in the same order as the NCCL form, so the
+    # two must agree bit for bit: a runtime self-check of the cross-rank protocol (all ranks)
+    ep_peer_check = None
+    if ep_peer is not None:
+        o_peer = ep.forward_peer(hidden, logits, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV)
+        o_nccl = ep.forward_fixed(hidden, logits, cfg.top_k, cfg.renormalize, path=pz.PATH_GEMV)
+        ok = torch.tensor([1 if torch.equal(o_peer.view(torch.int16), o_nccl.view(torch.int16)) else 0],
+                          device=device, dtype=torch.int32)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        ep_peer_check = bool(ok.item()) and ep_peer.wait_timeouts() == 0
+
     # roofline of the dominant kernel (largest share of the profiled step)
     kern = {k: {"launches": n, "total_ms": t, "avg_ms": t / max(n, 1)} for k, (n, t) in prof.kernels.items()}
     gpu_launches = sum(v["launches"] for v in kern.values())
@@ -657,7 +668,8 @@ def run_ours(args):
                        else "L2 flushed between timed steps",
                        "launch": "CUDA graph replay of the whole forward" if graph is not None else "eager"},
             "roofline": roof, "step_weight_gbs": step_gbs, "gpu_launches": gpu_launches,
-            **({"ep_peer_wait_timeouts": ep_peer.wait_timeouts()} if ep_peer is not None else {}),
+            **({"ep_peer_wait_timeouts": ep_peer.wait_timeouts(), "ep_peer_matches_nccl": ep_peer_check}
+               if ep_peer is not None else {}),
             "step_ms_percentiles": {"p10": pct[10], "p50": pct[50], "p90": pct[90], "steps": len(per_step),
                                     "note": "one event pair per step, separate pass (rank-local)"},
             "kernels": kern, "e2e": e2e}
