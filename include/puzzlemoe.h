@@ -349,9 +349,10 @@ int puzzle_ep_recv_plan_peer(const void* my_base, int world, int n_local_buckets
                              uint32_t* state, int32_t* local_off, int32_t* gather_idx, int32_t* return_idx,
                              puzzle_stream_t stream);
 /* y_local f32 [world*cap][d_model] (the experts' outputs in local order), return_idx from
- * puzzle_ep_recv_plan: slot (s, w) of home rank s's recv_y region [rank] <- y_local[return_idx]. */
-int puzzle_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int64_t cap,
-                          int d_model, const unsigned long long* peer_bases, uint32_t* state,
+ * puzzle_ep_recv_plan: slot (s, w) of home rank s's recv_y region [rank] <- y_local[return_idx],
+ * for the w < (rows source s sent, from the header of this rank's recv_x region s) only. */
+int puzzle_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int n_local_buckets,
+                          int64_t cap, int d_model, const unsigned long long* peer_bases, uint32_t* state,
                           puzzle_stream_t stream);
 /* As puzzle_ep_home_index (region stride cap+1), after waiting for every owner's return. */
 int puzzle_ep_home_index_peer(const int32_t* assign_of, const float* topk_gate, const int32_t* bucket_off,

@@ -100,7 +100,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_ep_dispatch_peer": ([P, P, P, I, P, I, I, I64, I64, I, I, P, P, P], I),
             "puzzle_ep_wait_dispatch": ([P, I, I64, I, P, P], I),
             "puzzle_ep_recv_plan_peer": ([P, I, I, I64, I, P, P, P, P, P], I),
-            "puzzle_ep_return_peer": ([P, P, I, I, I64, I, P, P, P], I),
+            "puzzle_ep_return_peer": ([P, P, I, I, I, I64, I, P, P, P], I),
             "puzzle_ep_home_index_peer": ([P, P, P, I, P, I, I64, I64, I, I, P, P, P, P, P], I),
             "puzzle_profile_begin": ([], I),
             "puzzle_profile_end": ([ctypes.c_char_p, SZ], I),
@@ -424,8 +424,9 @@ def ep_recv_plan_peer(pb: "EpPeerBuffer", n_local_buckets: int, stream=None):
     return local_off, gidx, ridx
 
 
-def ep_return_peer(y_local, return_idx, rank: int, pb: EpPeerBuffer, stream=None):
-    _check(load_library().puzzle_ep_return_peer(_p(y_local), _p(return_idx), pb.world, int(rank), pb.cap, pb.d,
+def ep_return_peer(y_local, return_idx, rank: int, n_local_buckets: int, pb: EpPeerBuffer, stream=None):
+    _check(load_library().puzzle_ep_return_peer(_p(y_local), _p(return_idx), pb.world, int(rank), int(n_local_buckets),
+                                                pb.cap, pb.d,
                                                 pb._peers(), _p(pb.state), _stream(stream)), "puzzle_ep_return_peer")
 
 

@@ -42,8 +42,8 @@ size_t ep_peer_buffer_bytes(int world, int64_t cap, int d);
 int launch_ep_dispatch_peer(const uint16_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int, int64_t, int,
                             int, const unsigned long long*, uint32_t*, cudaStream_t);
 int launch_ep_wait_dispatch(const void*, int, int64_t, int, uint32_t*, cudaStream_t);
-int launch_ep_return_peer(const float*, const int32_t*, int, int, int64_t, int, const unsigned long long*, uint32_t*,
-                          cudaStream_t);
+int launch_ep_return_peer(const float*, const int32_t*, int, int, int, int64_t, int, const unsigned long long*,
+                          uint32_t*, cudaStream_t);
 int launch_ep_home_index_peer(const int32_t*, const float*, const int32_t*, int, const int32_t*, int, int64_t, int,
                               int64_t, const void*, int32_t*, float*, uint32_t*, cudaStream_t);
 bool tc_supported(int d, int f);
@@ -693,16 +693,19 @@ int puzzle_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d_m
   return launch_ep_wait_dispatch(my_base, world, cap, d_model, state, (cudaStream_t)stream);
 }
 
-int puzzle_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int64_t cap,
-                          int d_model, const unsigned long long* peer_bases, uint32_t* state,
+int puzzle_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int n_local_buckets,
+                          int64_t cap, int d_model, const unsigned long long* peer_bases, uint32_t* state,
                           puzzle_stream_t stream) {
   if (int rc = check_peer_common(world, rank, cap, d_model)) return rc;
+  if (n_local_buckets < 0 || 4 * (int64_t)n_local_buckets > 2 * (int64_t)d_model)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "n_local_buckets outside [0, d_model / 2]");
   if (!y_local || !return_idx || !peer_bases || !state) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
   for (int q = 0; q < world; ++q)
     if (!peer_bases[q] || (peer_bases[q] & 255)) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "peer_bases: NULL or not 256-byte aligned");
   if (!al16(y_local)) return fail(PUZZLE_ERR_UNSUPPORTED, "y_local must be 16-byte aligned");
   if (int rc = check_device()) return rc;
-  return launch_ep_return_peer(y_local, return_idx, world, rank, cap, d_model, peer_bases, state, (cudaStream_t)stream);
+  return launch_ep_return_peer(y_local, return_idx, world, rank, n_local_buckets, cap, d_model, peer_bases, state,
+                               (cudaStream_t)stream);
 }
 
 int puzzle_ep_home_index_peer(const int32_t* assign_of, const float* topk_gate, const int32_t* bucket_off,

@@ -304,24 +304,33 @@ __global__ void k_ep_wait_flags(const uint32_t* __restrict__ flags, int world, u
 }
 
 // Owner: return the experts' outputs into every home rank's recv_y region [rank], slot by slot
-// (y_local rows through return_idx; unused slots carry a valid but unread row), then publish.
+// (y_local rows through return_idx; unused slots are not sent), then publish.
 __global__ void __launch_bounds__(256) k_ep_return_peer(const uint16_t* __restrict__ y_local,
                                                         const int32_t* __restrict__ return_idx, EpPeers Pe, int world,
-                                                        int rank, int64_t cap, int64_t cols_y, int d,
+                                                        int rank, int lb, int64_t cap, int64_t cols_y, int d,
                                                         uint32_t* __restrict__ state) {
   pdl_wait();
   pdl_trigger();
   const int64_t reg = cap + 1;
   const uint32_t epoch = state[kStStep] + 1;
+  const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // received slot (s, w)
   if (r < (int64_t)world * reg) {
     const int s = (int)(r / reg);
     const int64_t w = r - (int64_t)s * reg;
-    if (w < cap) {
+    // only the slots source s filled travel back over NVLink: its total from the header row of
+    // region s of this rank's own recv_x
+    const int32_t* hdr = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint16_t*>(Pe.base[rank]) +
+                                                          ((int64_t)s * reg + cap) * (cols_y / 2));
+    int32_t tot = 0;
+    for (int b = lane; b < lb; b += 32) tot += hdr[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (w < tot) {
       const uint4* sp = reinterpret_cast<const uint4*>(y_local + (int64_t)return_idx[r] * cols_y);
       uint16_t* ybase = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(Pe.base[s]) + ep_off_y(world, cap, d));
       uint4* dp = reinterpret_cast<uint4*>(ybase + ((int64_t)rank * reg + w) * cols_y);
-      warp_copy_row(sp, dp, cols_y / 8, threadIdx.x & 31);
+      warp_copy_row(sp, dp, cols_y / 8, lane);
     }
   }
   if (ep_last_cta(state + kStReturn) && threadIdx.x < world) {
@@ -486,14 +495,14 @@ int launch_ep_wait_dispatch(const void* my_base, int world, int64_t cap, int d, 
   return cuda_check(cudaGetLastError(), "ep_wait launch");
 }
 
-int launch_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int64_t cap, int d,
-                          const unsigned long long* peer_bases, uint32_t* state, cudaStream_t s) {
+int launch_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int lb, int64_t cap,
+                          int d, const unsigned long long* peer_bases, uint32_t* state, cudaStream_t s) {
   EpPeers Pe;
   fill_peers(peer_bases, world, &Pe);
   const unsigned grid = (unsigned)std::max<int64_t>(1, ((int64_t)world * (cap + 1) + 7) / 8);
   ProfScope _ps("ep_return_peer", s);
   cudaError_t e = launch_pdl(k_ep_return_peer, dim3(grid), dim3(256), 0, s,
-                             reinterpret_cast<const uint16_t*>(y_local), return_idx, Pe, world, rank, cap,
+                             reinterpret_cast<const uint16_t*>(y_local), return_idx, Pe, world, rank, lb, cap,
                              (int64_t)2 * d, d, state);
   if (e != cudaSuccess) return cuda_check(e, "ep_return_peer launch");
   return cuda_check(cudaGetLastError(), "ep_return_peer launch");

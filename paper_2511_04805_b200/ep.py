@@ -128,8 +128,8 @@ class CudaOps:
     def ep_recv_plan_peer(self, pb, n_local_buckets):
         return self.pz.ep_recv_plan_peer(pb, n_local_buckets)
 
-    def ep_return_peer(self, y_local, return_idx, rank, pb):
-        self.pz.ep_return_peer(y_local, return_idx, rank, pb)
+    def ep_return_peer(self, y_local, return_idx, rank, n_local_buckets, pb):
+        self.pz.ep_return_peer(y_local, return_idx, rank, n_local_buckets, pb)
 
     def ep_home_index_peer(self, assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, pb):
         return self.pz.ep_home_index_peer(assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, pb)
@@ -304,7 +304,7 @@ class ExpertParallelMoE:
         local_off, gidx, ridx = ops.ep_recv_plan_peer(pb, self.n_local_buckets)  # waits for the dispatch
         x_local = ops.gather_rows(pb.recv_x, gidx)
         y_local = ops.experts(self.local_layer, x_local, local_off, path=path)
-        ops.ep_return_peer(y_local, ridx, self.rank, pb)
+        ops.ep_return_peer(y_local, ridx, self.rank, self.n_local_buckets, pb)
 
     def peer_finish(self, state, residual=None):
         ops, part, pb = self.ops, self.part, self.pb
