@@ -330,8 +330,8 @@ int puzzle_ep_home_index(const int32_t* assign_of, const float* topk_gate, const
  * Per layer call (stream-ordered on one stream; graph-capturable):
  *   puzzle_moe_route -> puzzle_ep_dispatch_peer -> puzzle_ep_recv_plan_peer (waits until every
  *   source's region of this step has landed, then plans on recv_x) -> gather ->
- *   puzzle_moe_experts -> puzzle_ep_return_peer -> puzzle_ep_home_index_peer (waits for every
- *   owner's return; advances the step) -> puzzle_moe_combine(recv_y, ...).
+ *   puzzle_moe_experts -> puzzle_ep_return_peer -> puzzle_ep_combine_peer (waits for every
+ *   owner's return, combines from recv_y, advances the step).
  * Every rank must make the same sequence of calls (the waits are cross-rank: a rank that stops
  * calling stalls its peers). Errors as for the NCCL form; peer_bases entries must be non-NULL and
  * 256-byte aligned.
@@ -354,7 +354,17 @@ int puzzle_ep_recv_plan_peer(const void* my_base, int world, int n_local_buckets
 int puzzle_ep_return_peer(const float* y_local, const int32_t* return_idx, int world, int rank, int n_local_buckets,
                           int64_t cap, int d_model, const unsigned long long* peer_bases, uint32_t* state,
                           puzzle_stream_t stream);
-/* As puzzle_ep_home_index (region stride cap+1), after waiting for every owner's return. */
+/* puzzle_ep_combine_peer -- the layer's last step: waits for every owner's return, then
+ * out[t] = residual[t] + sum over slots (j, s) of topk_gate[t][j] * recv_y[row of (t, j, s)] with
+ * the rows of puzzle_ep_home_index, fp32 in slot order, one bf16 rounding (the arithmetic of
+ * puzzle_moe_combine on those tables, bit for bit); advances the step. residual may be NULL;
+ * T <= 65535, top_k * S <= 256. */
+int puzzle_ep_combine_peer(const int32_t* assign_of, const float* topk_gate, const int32_t* bucket_off, int n_pairs,
+                           const int32_t* dest_pairs, int world, int64_t cap, int64_t T, int top_k, int d_model,
+                           const void* my_base, const uint16_t* residual, uint16_t* out, uint32_t* state,
+                           puzzle_stream_t stream);
+/* As puzzle_ep_home_index (region stride cap+1), after waiting for every owner's return; advances
+ * the step (use it with puzzle_moe_combine on recv_y INSTEAD of puzzle_ep_combine_peer). */
 int puzzle_ep_home_index_peer(const int32_t* assign_of, const float* topk_gate, const int32_t* bucket_off,
                               int n_pairs, const int32_t* dest_pairs, int world, int64_t cap, int64_t T, int top_k,
                               int d_model, const void* my_base, int32_t* aof_s, float* gate_s, uint32_t* state,

@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = (
     "puzzle_group_colsumsq", "puzzle_moe_calib_workspace_size", "puzzle_moe_forward_calib",
     "puzzle_quant_pack", "puzzle_quant_unpack", "puzzle_ep_dispatch", "puzzle_ep_recv_plan",
     "puzzle_ep_home_index", "puzzle_ep_peer_buffer_size", "puzzle_ep_dispatch_peer", "puzzle_ep_wait_dispatch",
-    "puzzle_ep_return_peer", "puzzle_ep_home_index_peer", "puzzle_ep_recv_plan_peer",
+    "puzzle_ep_return_peer", "puzzle_ep_home_index_peer", "puzzle_ep_recv_plan_peer", "puzzle_ep_combine_peer",
 )
 
 
@@ -100,6 +100,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_ep_dispatch_peer": ([P, P, P, I, P, I, I, I64, I64, I, I, P, P, P], I),
             "puzzle_ep_wait_dispatch": ([P, I, I64, I, P, P], I),
             "puzzle_ep_recv_plan_peer": ([P, I, I, I64, I, P, P, P, P, P], I),
+            "puzzle_ep_combine_peer": ([P, P, P, I, P, I, I64, I64, I, I, P, P, P, P, P], I),
             "puzzle_ep_return_peer": ([P, P, I, I, I, I64, I, P, P, P], I),
             "puzzle_ep_home_index_peer": ([P, P, P, I, P, I, I64, I64, I, I, P, P, P, P, P], I),
             "puzzle_profile_begin": ([], I),
@@ -428,6 +429,18 @@ def ep_return_peer(y_local, return_idx, rank: int, n_local_buckets: int, pb: EpP
     _check(load_library().puzzle_ep_return_peer(_p(y_local), _p(return_idx), pb.world, int(rank), int(n_local_buckets),
                                                 pb.cap, pb.d,
                                                 pb._peers(), _p(pb.state), _stream(stream)), "puzzle_ep_return_peer")
+
+
+def ep_combine_peer(assign_of, topk_gate, bucket_off, n_pairs: int, dest_pairs, pb: EpPeerBuffer, residual=None,
+                    out=None, stream=None):
+    """puzzle_ep_combine_peer -> out [T][d] bf16 (waits for the returns; advances the step)."""
+    arr, dp, world = _dest_pairs(dest_pairs)
+    T, k = topk_gate.shape
+    out = torch.empty((T, pb.d), dtype=torch.bfloat16, device=topk_gate.device) if out is None else out
+    _check(load_library().puzzle_ep_combine_peer(_p(assign_of), _p(topk_gate), _p(bucket_off), int(n_pairs), dp, world,
+                                                 pb.cap, T, k, pb.d, _p(pb.buffer), _p(residual), _p(out),
+                                                 _p(pb.state), _stream(stream)), "puzzle_ep_combine_peer")
+    return out
 
 
 def ep_home_index_peer(assign_of, topk_gate, bucket_off, n_pairs: int, dest_pairs, slices: int, pb: EpPeerBuffer,

@@ -46,6 +46,8 @@ int launch_ep_return_peer(const float*, const int32_t*, int, int, int, int64_t, 
                           uint32_t*, cudaStream_t);
 int launch_ep_home_index_peer(const int32_t*, const float*, const int32_t*, int, const int32_t*, int, int64_t, int,
                               int64_t, const void*, int32_t*, float*, uint32_t*, cudaStream_t);
+int launch_ep_combine_peer(const int32_t*, const float*, const int32_t*, int, const int32_t*, int, int64_t, int64_t, int,
+                           int, const void*, const uint16_t*, uint16_t*, uint32_t*, cudaStream_t);
 bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
                       const int32_t*, int64_t, uint16_t*, float*, int32_t*, cudaStream_t);
@@ -720,6 +722,21 @@ int puzzle_ep_home_index_peer(const int32_t* assign_of, const float* topk_gate, 
   if (int rc = check_device()) return rc;
   return launch_ep_home_index_peer(assign_of, topk_gate, bucket_off, n_pairs, dest_pairs, world, cap, d_model,
                                    T * top_k, my_base, aof_s, gate_s, state, (cudaStream_t)stream);
+}
+
+int puzzle_ep_combine_peer(const int32_t* assign_of, const float* topk_gate, const int32_t* bucket_off, int n_pairs,
+                           const int32_t* dest_pairs, int world, int64_t cap, int64_t T, int top_k, int d_model,
+                           const void* my_base, const uint16_t* residual, uint16_t* out, uint32_t* state,
+                           puzzle_stream_t stream) {
+  if (int rc = check_peer_common(world, 0, cap, d_model)) return rc;
+  if (n_pairs < 1 || T < 0 || T > 65535 || top_k < 1 || cap < T * top_k || d_model % 4)
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad sizes (need n_pairs >= 1, 0 <= T <= 65535, top_k >= 1, cap >= T * top_k)");
+  if (!dest_pairs || !my_base || !state || !bucket_off || (T > 0 && (!assign_of || !topk_gate || !out)))
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (reinterpret_cast<uintptr_t>(my_base) & 255) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "my_base must be 256-byte aligned");
+  if (int rc = check_device()) return rc;
+  return launch_ep_combine_peer(assign_of, topk_gate, bucket_off, n_pairs, dest_pairs, world, cap, T, top_k, d_model,
+                                my_base, residual, out, state, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -24,6 +24,7 @@
 namespace pz {
 
 constexpr int kEpMaxRanks = 64;
+constexpr int kEpMaxSlots = 256;  // top_k * owners per pair, per token (combine of the peer form)
 struct EpRanks {
   int32_t lo[kEpMaxRanks], hi[kEpMaxRanks];
   int world;
@@ -384,6 +385,81 @@ __global__ void __launch_bounds__(256) k_ep_home_index_peer(const int32_t* __res
   }
 }
 
+// Home: the combine (a6) of the peer form with the home-index step folded in. Every block waits
+// for every owner's return of this step; the first k*S threads resolve the token's slot rows
+// (as k_ep_home_index) into shared memory; then out[t] = residual[t] + sum over slots (j, s) in
+// order of gate[t,j] * y[row], fp32, one bf16 rounding -- the same arithmetic as k_combine on
+// puzzle_ep_home_index's tables. The last block advances the step.
+__global__ void __launch_bounds__(256) k_ep_combine_peer(const float* __restrict__ y,
+                                                         const int32_t* __restrict__ assign_of,
+                                                         const float* __restrict__ gate,
+                                                         const int32_t* __restrict__ off, int n_buckets, EpRanks R,
+                                                         int slices, int k, int64_t T, int64_t cap, int d,
+                                                         const uint16_t* __restrict__ residual,
+                                                         uint16_t* __restrict__ out,
+                                                         const uint32_t* __restrict__ flags_y,
+                                                         uint32_t* __restrict__ state) {
+  __shared__ int32_t s_row[kEpMaxSlots];
+  __shared__ float s_gate[kEpMaxSlots];
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t epoch = state[kStStep] + 1;
+  for (int q = threadIdx.x; q < R.world; q += blockDim.x) ep_wait_epoch(flags_y + q, epoch, state);
+  const int64_t t = blockIdx.y;
+  const int ks = k * slices;
+  if (t < T && threadIdx.x < ks) {
+    const int j = threadIdx.x / slices, want = threadIdx.x - j * slices;
+    const int32_t a = assign_of[t * k + j];
+    int lo = 0, hi = n_buckets;
+    while (hi - lo > 1) {
+      const int m = (lo + hi) >> 1;
+      if (off[m] <= a) lo = m; else hi = m;
+    }
+    const int p = lo >> 1;
+    int sidx = 0;
+    for (int q = 0; q < R.world; ++q) {
+      if (R.lo[q] <= p && p < R.hi[q]) {
+        if (sidx == want) {
+          s_row[threadIdx.x] = (int32_t)(q * (cap + 1) + (a - off[2 * R.lo[q]]));
+          s_gate[threadIdx.x] = gate[t * k + j];
+        }
+        ++sidx;
+      }
+    }
+  }
+  __syncthreads();
+  const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T && c4 * 4 < d) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (residual != nullptr) {
+      const uint2 r = *reinterpret_cast<const uint2*>(residual + t * d + c4 * 4);
+      acc = make_float4(bf16_bits_to_f32(r.x & 0xFFFFu), bf16_bits_to_f32(r.x >> 16),
+                        bf16_bits_to_f32(r.y & 0xFFFFu), bf16_bits_to_f32(r.y >> 16));
+    }
+    for (int i = 0; i < ks; ++i) {
+      const float g = s_gate[i];
+      const float4 v = *reinterpret_cast<const float4*>(y + (int64_t)s_row[i] * d + c4 * 4);
+      acc.x += g * v.x;
+      acc.y += g * v.y;
+      acc.z += g * v.z;
+      acc.w += g * v.w;
+    }
+    uint2 o;
+    o.x = f32_to_bf16_rne_bits(acc.x) | (f32_to_bf16_rne_bits(acc.y) << 16);
+    o.y = f32_to_bf16_rne_bits(acc.z) | (f32_to_bf16_rne_bits(acc.w) << 16);
+    *reinterpret_cast<uint2*>(out + t * d + c4 * 4) = o;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(state + kStHome, 1u) == gridDim.x * gridDim.y - 1) {  // every block has read the step
+      state[kStHome] = 0;
+      state[kStStep] = epoch;
+      __threadfence();
+    }
+  }
+}
+
 int fill_ranks(const int32_t* dest_pairs, int world, int n_pairs, EpRanks* R, int* slices) {
   if (world < 1 || world > kEpMaxRanks) return fail(PUZZLE_ERR_UNSUPPORTED, "world must be in [1, 64]");
   R->world = world;
@@ -522,6 +598,26 @@ int launch_ep_home_index_peer(const int32_t* assign_of, const float* gate, const
                              state);
   if (e != cudaSuccess) return cuda_check(e, "ep_home_index_peer launch");
   return cuda_check(cudaGetLastError(), "ep_home_index_peer launch");
+}
+
+int launch_ep_combine_peer(const int32_t* assign_of, const float* gate, const int32_t* bucket_off, int n_pairs,
+                           const int32_t* dest_pairs, int world, int64_t cap, int64_t T, int k, int d,
+                           const void* my_base, const uint16_t* residual, uint16_t* out, uint32_t* state,
+                           cudaStream_t s) {
+  EpRanks R;
+  int S = 0;
+  if (int rc = fill_ranks(dest_pairs, world, n_pairs, &R, &S)) return rc;
+  if (k * S > kEpMaxSlots) return fail(PUZZLE_ERR_UNSUPPORTED, "top_k * owners per pair > 256");
+  const float* y = reinterpret_cast<const float*>(static_cast<const char*>(my_base) + ep_off_y(world, cap, d));
+  const uint32_t* flags_y =
+      reinterpret_cast<const uint32_t*>(static_cast<const char*>(my_base) + ep_off_flags(world, cap, d)) + world;
+  const int threads = 256;
+  const dim3 grid((unsigned)((d / 4 + threads - 1) / threads), (unsigned)std::max<int64_t>(T, 1));
+  ProfScope _ps("ep_combine_peer", s);
+  cudaError_t e = launch_pdl(k_ep_combine_peer, grid, dim3(threads), 0, s, y, assign_of, gate, bucket_off,
+                             2 * n_pairs + 1, R, S, k, T, cap, d, residual, out, flags_y, state);
+  if (e != cudaSuccess) return cuda_check(e, "ep_combine_peer launch");
+  return cuda_check(cudaGetLastError(), "ep_combine_peer launch");
 }
 
 }  // namespace pz

@@ -134,6 +134,9 @@ class CudaOps:
     def ep_home_index_peer(self, assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, pb):
         return self.pz.ep_home_index_peer(assign_of, gate, bucket_off, n_pairs, dest_pairs, slices, pb)
 
+    def ep_combine_peer(self, assign_of, gate, bucket_off, n_pairs, dest_pairs, pb, residual):
+        return self.pz.ep_combine_peer(assign_of, gate, bucket_off, n_pairs, dest_pairs, pb, residual=residual)
+
 
 class ExpertParallelMoE:
     """One MoE layer sharded by merged pairs over `world` ranks of `group`.
@@ -308,9 +311,9 @@ class ExpertParallelMoE:
 
     def peer_finish(self, state, residual=None):
         ops, part, pb = self.ops, self.part, self.pb
-        aof_s, gate_s = ops.ep_home_index_peer(state["assign_of"], state["gate"], state["bucket_off"], part.n_pairs,
-                                               self.dest_pairs, part.slices, pb)
-        return ops.combine(pb.recv_y, aof_s, gate_s, residual)
+        # waits for every owner's return, combines from recv_y, advances the step (one kernel)
+        return ops.ep_combine_peer(state["assign_of"], state["gate"], state["bucket_off"], part.n_pairs,
+                                   self.dest_pairs, pb, residual)
 
 
 def make_peer_buffer(world: int, cap: int, d_model: int, device, group=None):

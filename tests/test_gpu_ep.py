@@ -345,7 +345,13 @@ def test_ep_peer_simulated_world_matches_oracle(cfg, G, n_merged):
         for r in range(G):
             eps[r].peer_serve(path=pz.PATH_GEMV)
         for r in range(G):
-            out = eps[r].peer_finish(states[r])
+            if (r, step) == (0, 1):  # the two-call form: home-index tables + the plain combine
+                st, ep = states[r], eps[r]
+                aof_s, gate_s = pz.ep_home_index_peer(st["assign_of"], st["gate"], st["bucket_off"], ep.part.n_pairs,
+                                                      ep.dest_pairs, ep.part.slices, ep.pb)
+                out = pz.moe_combine(ep.pb.recv_y, aof_s, gate_s)
+            else:
+                out = eps[r].peer_finish(states[r])
             torch.cuda.synchronize()
             hb, lg = inputs[r]
             if hb.shape[0] == 0:
