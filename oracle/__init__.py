@@ -266,3 +266,16 @@ def quant_unpack(codes, scales, pos: int) -> np.ndarray:
     if _load().oracle_quant_unpack(_ptr(codes), _ptr(scales), int(pos), rows, cols, _ptr(out)) != 0:
         raise ValueError("quant_unpack: bad position or shape")
     return out
+
+
+def quant_gemv(codes, scales, x_i, x_j) -> tuple[np.ndarray, np.ndarray]:
+    """NEXT-3 expert GEMV over the quantised format (Appendix A.3; reading R23:
+    the dequantised Ŵ_pos is the bf16 operand of the expert matmul, as Algorithm 1's output
+    is). The tokens routed to expert i of the pair (x_i, bf16 bits [n_i, cols]) see Ŵ_0, those
+    routed to j (x_j [n_j, cols]) see Ŵ_1: y_i = x_i Ŵ_0^T, y_j = x_j Ŵ_1^T, in f64
+    ([n_i, rows], [n_j, rows])."""
+    def bf16(bits):
+        return (np.asarray(bits, np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    w0 = bf16(quant_unpack(codes, scales, 0))
+    w1 = bf16(quant_unpack(codes, scales, 1))
+    return bf16(x_i) @ w0.T, bf16(x_j) @ w1.T

@@ -86,3 +86,30 @@ def test_quantised_merge_pipeline_error():
     ref = np.where(art["s_i"] == 1, -1.0, 1.0) * art["w_merged"]
     assert np.all(np.abs(deq[kept] - ref[kept]) <= sc[kept] * 0.5 + np.abs(ref[kept]) * 2 ** -8 + 1e-12)
     assert np.all(deq[~kept] == 0)
+
+
+def test_quant_gemv_lossless_case_equals_plain_matmul():
+    """quant_gemv pinned to the plain definition y = x ((-1)^S M w)^T, built from the original
+    magnitudes and bit-planes (not from the codes): with every group's values on the grid
+    k * 2^e (k in 0..7, the group maximum 7 * 2^e) the format is lossless (scale = 2^e exactly,
+    codes = k, bf16(k * 2^e) exact), so the GEMV must equal the signed, masked dense matmul.
+    Non-square shapes and unequal token counts catch a transposed operand or swapped
+    positions; the sign / mask planes of i and j differ, so taking j's bits for i fails."""
+    rng = np.random.default_rng(11)
+    rows, cols, n_i, n_j = 5, 256, 3, 4
+    k = rng.integers(0, 8, (rows, cols)).astype(np.float32)
+    k[:, ::128] = 7.0
+    e = rng.integers(-6, 4, (rows, cols // 128)).astype(np.float32)
+    w = k * np.repeat(np.exp2(e), 128, axis=1)
+    m0, m1, s0, s1 = _planes((rows, cols), rng)
+    codes, scales = oracle.quant_pack(w, m0, m1, s0, s1)
+    xs = [torch.randn(n, cols).to(torch.bfloat16) for n in (n_i, n_j)]
+    xbits = [t.view(torch.int16).numpy().view(np.uint16) for t in xs]
+    y_i, y_j = oracle.quant_gemv(codes, scales, *xbits)
+    wd = w.astype(np.float64)
+    want_i = xs[0].double().numpy() @ (np.where(s0 != 0, -1.0, 1.0) * (m0 != 0) * wd).T
+    want_j = xs[1].double().numpy() @ (np.where(s1 != 0, -1.0, 1.0) * (m1 != 0) * wd).T
+    assert y_i.shape == (n_i, rows) and y_j.shape == (n_j, rows)
+    np.testing.assert_allclose(y_i, want_i, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(y_j, want_j, rtol=0, atol=1e-12)
+    assert not np.allclose(y_i, xs[0].double().numpy() @ (np.where(s1 != 0, -1.0, 1.0) * (m1 != 0) * wd).T)
