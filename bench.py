@@ -745,11 +745,39 @@ def packer_rates(pz, layer, device):
     ms3 = timed_steps(lambda: pz.quant_pack(w2d, *pl2d), 5) / 5
     ms4 = timed_steps(lambda: pz.quant_unpack(codes, scales, 0), 5) / 5
     del deq
-    return {"unpack_gbs": unpack_gbs, "unpack_elems": n, "pack_gbs": m * 10 / (ms2 / 1e3) / 1e9, "pack_elems": m,
+    qg = quant_gemv_rates(pz, w, planes, device)
+    return {"quant_gemv": qg, "unpack_gbs": unpack_gbs, "unpack_elems": n, "pack_gbs": m * 10 / (ms2 / 1e3) / 1e9, "pack_elems": m,
             "quant_pack_gbs": m * (9 + 4 / 128) / (ms3 / 1e3) / 1e9,
             "quant_unpack_gbs": m * (3 + 4 / 128) / (ms4 / 1e3) / 1e9,
             "note": "algorithmic bytes: unpack 4 B/elem, pack 10 B/elem, quant pack 9 B/elem (+ scales), "
                     "quant unpack 3 B/elem (+ scales); quant timings include the output allocation"}
+
+
+def quant_gemv_rates(pz, w, planes, device):
+    """NEXT-3 expert GEMV over the quantised format (puzzle_quant_gemv) on Mixtral w13-shaped
+    merged pairs ([2 d_ff, d] = [28672, 4096] codes), 4 pairs cycled per launch round so the
+    470 MB of codes exceed L2; tokens per expert n_i = n_j in {1, 8, 16}. Algorithmic bytes per
+    pair: codes 1 B/elem + scales 4 B/128 elem + the token rows in and outputs out."""
+    import torch
+    rows, cols = 28672, 4096
+    e = rows * cols
+    pairs = [pz.quant_pack(w[k * e:(k + 1) * e].view(rows, cols), *[p[k * e:(k + 1) * e].view(rows, cols)
+                           for p in planes]) for k in range(2)]
+    pairs = pairs + [(c.clone(), s.clone()) for c, s in pairs]  # 4 distinct buffers (2^28 elements hold 2 pairs)
+    out = []
+    for n in (1, 8, 16):
+        xi = torch.randn(n, cols, device=device).to(torch.bfloat16)
+        xj = torch.randn(n, cols, device=device).to(torch.bfloat16)
+        for c, s in pairs:
+            pz.quant_gemv(c, s, xi, xj)
+        torch.cuda.synchronize()
+        reps = 10
+        ms = timed_steps(lambda: [pz.quant_gemv(c, s, xi, xj) for c, s in pairs], reps) / (reps * len(pairs))
+        nbytes = e * (1 + 4 / 128) + 2 * n * cols * 2 + 2 * n * rows * 4
+        out.append({"tokens_per_expert": n, "us_per_pair": ms * 1e3, "gbs": nbytes / (ms / 1e3) / 1e9,
+                    "bytes_per_pair": nbytes})
+    return {"shape": [rows, cols], "pairs_cycled": len(pairs), "points": out,
+            "note": "CUDA-core GEMV (k_quant_gemv); timings include the output allocation"}
 
 
 def sweep(pz, args, device, pk):

@@ -138,6 +138,21 @@ int puzzle_quant_pack(const float* w_merged, const uint8_t* m0, const uint8_t* m
 int puzzle_quant_unpack(const uint8_t* codes, const float* scales, int pos, int64_t rows,
                         int64_t cols, uint16_t* bf16_out, puzzle_stream_t stream);
 
+/* puzzle_quant_gemv -- the expert GEMV over the quantised format (NEXT-3; R23: Ŵ_pos is the bf16
+ *   operand of the expert matmul, Algorithm 1 / Eq. 8's y = Ŵ x). One merged pair, both experts
+ *   from one read of the code bytes:
+ *   codes   u8  [rows][cols], scales f32 [rows][cols/128]  (puzzle_quant_pack's output)
+ *   x_i     bf16 [n_i][cols]  tokens routed to expert i (position 0); x_j [n_j][cols] to j
+ *   y_i     f32 [n_i][rows]   y_i[t][r] = sum_c Ŵ_0[r][c] x_i[t][c]; y_j likewise with Ŵ_1
+ *   f32 FMA accumulation (each lane sums cols/32 products in order, then a 5-level warp tree).
+ *   Device pointers; codes, x_i, x_j 16-byte aligned; the caller owns every buffer. n_i or n_j
+ *   may be 0 (that side is not touched). Errors: INVALID_ARGUMENT (negative sizes, NULL),
+ *   UNSUPPORTED (cols % 128, alignment).
+ */
+int puzzle_quant_gemv(const uint8_t* codes, const float* scales, int64_t rows, int64_t cols,
+                      const uint16_t* x_i, int64_t n_i, const uint16_t* x_j, int64_t n_j,
+                      float* y_i, float* y_j, puzzle_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * One MoE layer whose experts are PuzzleMoE-merged pairs (50% compression), or --
  * the 25% ratio, experts cut to 75% of the original count -- some merged pairs plus

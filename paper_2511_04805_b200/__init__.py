@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "puzzle_moe_experts", "puzzle_moe_combine", "puzzle_gather_rows", "puzzle_profile_begin",
     "puzzle_profile_end", "puzzle_moe_route_workspace_size", "puzzle_group_colsumsq_workspace_size",
     "puzzle_group_colsumsq", "puzzle_moe_calib_workspace_size", "puzzle_moe_forward_calib",
-    "puzzle_quant_pack", "puzzle_quant_unpack", "puzzle_ep_dispatch", "puzzle_ep_recv_plan",
+    "puzzle_quant_pack", "puzzle_quant_unpack", "puzzle_quant_gemv", "puzzle_ep_dispatch", "puzzle_ep_recv_plan",
     "puzzle_ep_home_index", "puzzle_ep_peer_buffer_size", "puzzle_ep_dispatch_peer", "puzzle_ep_wait_dispatch",
     "puzzle_ep_return_peer", "puzzle_ep_home_index_peer", "puzzle_ep_recv_plan_peer", "puzzle_ep_combine_peer",
 )
@@ -93,6 +93,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_moe_forward_calib": ([P, P, P, I64, I, I, P, P, P, P, P, SZ, I, P], I),
             "puzzle_quant_pack": ([P, P, P, P, P, I64, I64, P, P, P], I),
             "puzzle_quant_unpack": ([P, P, I, I64, I64, P, P], I),
+            "puzzle_quant_gemv": ([P, P, I64, I64, P, I64, P, I64, P, P, P], I),
             "puzzle_ep_dispatch": ([P, P, P, I, P, I, I64, I64, I, I, P, P], I),
             "puzzle_ep_recv_plan": ([P, I, I, I64, I, P, P, P, P], I),
             "puzzle_ep_home_index": ([P, P, P, I, P, I, I64, I64, I, P, P, P], I),
@@ -511,3 +512,17 @@ def quant_unpack(codes, scales, pos: int, stream=None) -> torch.Tensor:
     _check(load_library().puzzle_quant_unpack(_p(codes), _p(scales), int(pos), rows, cols, _p(out), _stream(stream)),
            "puzzle_quant_unpack")
     return out
+
+
+def quant_gemv(codes, scales, x_i, x_j, stream=None):
+    """puzzle_quant_gemv (NEXT-3): both experts of one quantised merged pair on their routed
+    tokens, x_i / x_j bf16 [n, cols] -> (y_i, y_j) f32 [n, rows]."""
+    assert codes.dtype == torch.uint8 and codes.dim() == 2 and scales.dtype == torch.float32
+    rows, cols = codes.shape
+    for x in (x_i, x_j):
+        assert x.dtype == torch.bfloat16 and x.dim() == 2 and x.shape[1] == cols and x.is_contiguous()
+    y_i = torch.empty((x_i.shape[0], rows), dtype=torch.float32, device=codes.device)
+    y_j = torch.empty((x_j.shape[0], rows), dtype=torch.float32, device=codes.device)
+    _check(load_library().puzzle_quant_gemv(_p(codes), _p(scales), rows, cols, _p(x_i), x_i.shape[0], _p(x_j),
+                                            x_j.shape[0], _p(y_i), _p(y_j), _stream(stream)), "puzzle_quant_gemv")
+    return y_i, y_j

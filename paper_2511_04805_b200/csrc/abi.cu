@@ -18,6 +18,8 @@ int launch_unpack(const uint16_t*, int, int64_t, uint16_t*, cudaStream_t);
 int launch_quant_pack(const float*, const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int64_t, int64_t,
                       uint8_t*, float*, cudaStream_t);
 int launch_quant_unpack(const uint8_t*, const float*, int, int64_t, int64_t, uint16_t*, cudaStream_t);
+int launch_quant_gemv(const uint8_t*, const float*, int64_t, int64_t, const uint16_t*, int64_t, const uint16_t*, int64_t,
+                      float*, float*, cudaStream_t);
 int launch_merge_experts_pack(const uint16_t*, const uint16_t*, const float*, const float*, int64_t,
                               int64_t, int64_t, float, uint16_t*, puzzle_pack_stats*, cudaStream_t);
 int launch_route(const float*, int64_t, int, int, int, const int32_t*, int, int32_t*, float*, int32_t*,
@@ -354,6 +356,19 @@ int puzzle_quant_unpack(const uint8_t* codes, const float* scales, int pos, int6
   if (!al16(codes) || !al16(bf16_out)) return fail(PUZZLE_ERR_UNSUPPORTED, "arrays must be 16-byte aligned");
   if (int rc = check_device()) return rc;
   return launch_quant_unpack(codes, scales, pos, rows, cols, bf16_out, (cudaStream_t)stream);
+}
+
+int puzzle_quant_gemv(const uint8_t* codes, const float* scales, int64_t rows, int64_t cols, const uint16_t* x_i,
+                      int64_t n_i, const uint16_t* x_j, int64_t n_j, float* y_i, float* y_j, puzzle_stream_t stream) {
+  if (rows < 0 || cols < 0 || n_i < 0 || n_j < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "negative sizes");
+  if (cols % 128) return fail(PUZZLE_ERR_UNSUPPORTED, "cols must be a multiple of 128 (quantisation groups)");
+  if (rows == 0 || (n_i == 0 && n_j == 0)) return PUZZLE_OK;
+  if (cols > 0 && (!codes || !scales)) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if ((n_i > 0 && (!y_i || (cols > 0 && !x_i))) || (n_j > 0 && (!y_j || (cols > 0 && !x_j))))
+    return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!al16(codes) || !al16(x_i) || !al16(x_j)) return fail(PUZZLE_ERR_UNSUPPORTED, "arrays must be 16-byte aligned");
+  if (int rc = check_device()) return rc;
+  return launch_quant_gemv(codes, scales, rows, cols, x_i, n_i, x_j, n_j, y_i, y_j, (cudaStream_t)stream);
 }
 
 int puzzle_merge_experts_pack(const uint16_t* wi, const uint16_t* wj, const float* ni, const float* nj,

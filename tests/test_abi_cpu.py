@@ -88,6 +88,10 @@ def test_next_row_argument_errors_are_synchronous(lib):
     assert lib.puzzle_quant_pack(None, None, None, None, None, 0, 128, None, None, None) == 0   # empty: no-op
     assert lib.puzzle_quant_unpack(None, None, 2, 1, 128, None, None) == 1                     # pos
     assert lib.puzzle_quant_unpack(None, None, 0, -1, 128, None, None) == 1                    # negative
+    assert lib.puzzle_quant_gemv(None, None, 4, 100, None, 1, None, 0, None, None, None) == 3   # cols % 128
+    assert lib.puzzle_quant_gemv(None, None, 4, 128, None, -1, None, 0, None, None, None) == 1  # negative
+    assert lib.puzzle_quant_gemv(None, None, 4, 128, None, 1, None, 0, None, None, None) == 1   # NULL
+    assert lib.puzzle_quant_gemv(None, None, 4, 128, None, 0, None, 0, None, None, None) == 0   # no tokens: no-op
     assert lib.puzzle_group_colsumsq(None, None, 2, 12, None, None, 0, None) == 1              # NULL
     assert lib.puzzle_group_colsumsq(None, None, 0, 16, None, None, 0, None) == 0              # no groups
     assert lib.puzzle_group_colsumsq_workspace_size(-1, 8) == 0

@@ -54,3 +54,41 @@ def test_quant_argument_errors(pz):
     u = torch.zeros((2, 100), dtype=torch.uint8, device="cuda")
     with pytest.raises(pz.PuzzleError):
         pz.quant_pack(x, u, u, u, u)  # cols % 128 != 0
+
+
+def _bf16_tokens(n, cols, seed):
+    return torch.randn(n, cols, generator=torch.Generator().manual_seed(seed)).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("rows,cols,n_i,n_j", [(1, 128, 1, 0), (3, 128, 0, 2), (37, 384, 5, 9), (256, 1408, 8, 17),
+                                               (1023, 4096, 23, 3), (4096, 14336, 12, 20)])
+def test_quant_gemv_matches_oracle(pz, rows, cols, n_i, n_j):
+    """puzzle_quant_gemv vs oracle.quant_gemv (f64): ragged row pairs (odd rows), token chunks of
+    8 with ragged tails, an empty side, and the Mixtral w2 shape (4096 x 14336) of one merged
+    pair. Tolerance derived from the kernel's summation: each lane sums cols/32 products in order
+    and a 5-level tree follows, so |err| <= (cols/32 + 5) * 2^-24 * sum|w x| (plus one rounding
+    of the sum), here with a factor 2 margin."""
+    w, planes = _case(rows, cols, rows + cols)
+    codes_np, scales_np = oracle.quant_pack(w, *planes)
+    xi, xj = _bf16_tokens(n_i, cols, 1), _bf16_tokens(n_j, cols, 2)
+    bits = [t.view(torch.int16).numpy().view(np.uint16) for t in (xi, xj)]
+    want_i, want_j = oracle.quant_gemv(codes_np, scales_np, *bits)
+    codes, scales = torch.from_numpy(codes_np).cuda(), torch.from_numpy(scales_np).cuda()
+    y_i, y_j = pz.quant_gemv(codes, scales, xi.cuda(), xj.cuda())
+    torch.cuda.synchronize()
+    for pos, (x, got, want) in enumerate(((xi, y_i, want_i), (xj, y_j, want_j))):
+        assert got.shape == (x.shape[0], rows)
+        if x.shape[0] == 0:
+            continue
+        wabs = np.abs(oracle.bf16_bits_to_f32(oracle.quant_unpack(codes_np, scales_np, pos)).astype(np.float64))
+        bound = np.abs(x.double().numpy()) @ wabs.T
+        tol = 2 * ((cols / 32 + 6) * 2.0 ** -24) * bound + 1e-30
+        err = np.abs(got.cpu().double().numpy() - want)
+        assert (err <= tol).all(), (pos, float(err.max()), float((err / np.maximum(bound, 1e-30)).max()))
+
+
+def test_quant_gemv_argument_errors(pz):
+    codes = torch.zeros((4, 100), dtype=torch.uint8, device="cuda")
+    with pytest.raises(pz.PuzzleError):
+        pz.quant_gemv(codes, torch.ones((4, 1), device="cuda"), torch.zeros((1, 100), dtype=torch.bfloat16,
+                      device="cuda"), torch.zeros((0, 100), dtype=torch.bfloat16, device="cuda"))
