@@ -95,7 +95,8 @@ __global__ void __launch_bounds__(kQThreads) k_quant_unpack(const uint4* __restr
 // position's tokens (f32, sequential per lane over its cols / 32 columns); the sums are
 // warp-reduced (5 butterfly levels). CUDA cores, not tcgen05: at decode batch sizes the code
 // bytes (1 per merged element) are the traffic and the per-byte decode is the ALU work.
-constexpr int kGemvTB = 4;
+// tokens per position per work item: 2 for decode-sized inputs (fewer accumulator registers,
+// no spills under the 2-CTA cap), 4 otherwise (fewer re-decodes of the codes per token)
 
 __device__ __forceinline__ uint32_t cvt_bf16x2(float hi, float lo) {
   uint32_t d;
@@ -135,10 +136,10 @@ __device__ __forceinline__ void bf16x8_to_f32(uint4 v, float* f) {
   }
 }
 
-template <int POS>
+template <int POS, int TB>
 __device__ __forceinline__ void fma_tokens(const uint32_t q0[4], const uint32_t q1[4], const uint32_t* m0,
                                            const uint32_t* m1, const uint16_t* __restrict__ x, int64_t cols,
-                                           int64_t c, int nt, float (*acc)[kGemvTB]) {
+                                           int64_t c, int nt, float (*acc)[TB]) {
   float w0[16], w1[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
@@ -146,7 +147,7 @@ __device__ __forceinline__ void fma_tokens(const uint32_t q0[4], const uint32_t 
     w1[e] = signed_w<POS>(q1, m1, e);
   }
 #pragma unroll
-  for (int t = 0; t < kGemvTB; ++t) {
+  for (int t = 0; t < TB; ++t) {
     if (t < nt) {
       const uint4* xp = reinterpret_cast<const uint4*>(x + t * cols + c);
       float xf[16];
@@ -161,10 +162,11 @@ __device__ __forceinline__ void fma_tokens(const uint32_t q0[4], const uint32_t 
   }
 }
 
-__device__ __forceinline__ void store_sums(float (*acc)[kGemvTB], int nt, int lane, float* y, int64_t rows,
+template <int TB>
+__device__ __forceinline__ void store_sums(float (*acc)[TB], int nt, int lane, float* y, int64_t rows,
                                            int64_t r0, bool has1) {
 #pragma unroll
-  for (int t = 0; t < kGemvTB; ++t) {
+  for (int t = 0; t < TB; ++t) {
     if (t < nt) {  // nt is warp-uniform
       float a = acc[0][t], b = acc[1][t];
 #pragma unroll
@@ -180,6 +182,7 @@ __device__ __forceinline__ void store_sums(float (*acc)[kGemvTB], int nt, int la
   }
 }
 
+template <int TB>
 __global__ void __launch_bounds__(kQThreads, 2) k_quant_gemv(const uint8_t* __restrict__ codes,
                                                           const float* __restrict__ scales, int64_t rows,
                                                           int64_t cols, const uint16_t* __restrict__ x_i,
@@ -188,21 +191,21 @@ __global__ void __launch_bounds__(kQThreads, 2) k_quant_gemv(const uint8_t* __re
                                                           float* __restrict__ y_j) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kQThreads / 32);
-  const int64_t nch = ((n_i > n_j ? n_i : n_j) + kGemvTB - 1) / kGemvTB;
+  const int64_t nch = ((n_i > n_j ? n_i : n_j) + TB - 1) / TB;
   const int64_t n_rp = (rows + 1) / 2, gpr = cols / 128;
   for (int64_t item = blockIdx.x * (int64_t)(kQThreads / 32) + (threadIdx.x >> 5); item < n_rp * nch;
        item += warps) {
-    const int64_t rp = item / nch, t0 = (item % nch) * kGemvTB;
-    const int nti = (int)(n_i - t0 <= 0 ? 0 : (n_i - t0 < kGemvTB ? n_i - t0 : kGemvTB));
-    const int ntj = (int)(n_j - t0 <= 0 ? 0 : (n_j - t0 < kGemvTB ? n_j - t0 : kGemvTB));
+    const int64_t rp = item / nch, t0 = (item % nch) * TB;
+    const int nti = (int)(n_i - t0 <= 0 ? 0 : (n_i - t0 < TB ? n_i - t0 : TB));
+    const int ntj = (int)(n_j - t0 <= 0 ? 0 : (n_j - t0 < TB ? n_j - t0 : TB));
     const int64_t r0 = 2 * rp, r1 = r0 + 1 < rows ? r0 + 1 : r0;
     const uint8_t* c0 = codes + r0 * cols;
     const uint8_t* c1 = codes + r1 * cols;
     const uint16_t* xi = x_i + t0 * cols;
     const uint16_t* xj = x_j + t0 * cols;
-    float ai[2][kGemvTB], aj[2][kGemvTB];
+    float ai[2][TB], aj[2][TB];
 #pragma unroll
-    for (int t = 0; t < kGemvTB; ++t) ai[0][t] = ai[1][t] = aj[0][t] = aj[1][t] = 0.0f;
+    for (int t = 0; t < TB; ++t) ai[0][t] = ai[1][t] = aj[0][t] = aj[1][t] = 0.0f;
     int64_t c = lane * 16;
     uint4 b0 = make_uint4(0, 0, 0, 0), b1 = b0;
     float s0 = 0.0f, s1 = 0.0f;
@@ -220,8 +223,8 @@ __global__ void __launch_bounds__(kQThreads, 2) k_quant_gemv(const uint8_t* __re
       uint32_t m0[16], m1[16];
       decode_mag16(q0, cs0, m0);
       decode_mag16(q1, cs1, m1);
-      if (nti > 0) fma_tokens<0>(q0, q1, m0, m1, xi, cols, c, nti, ai);
-      if (ntj > 0) fma_tokens<1>(q0, q1, m0, m1, xj, cols, c, ntj, aj);
+      if (nti > 0) fma_tokens<0, TB>(q0, q1, m0, m1, xi, cols, c, nti, ai);
+      if (ntj > 0) fma_tokens<1, TB>(q0, q1, m0, m1, xj, cols, c, ntj, aj);
     }
     store_sums(ai, nti, lane, y_i + t0 * rows, rows, r0, r0 + 1 < rows);
     store_sums(aj, ntj, lane, y_j + t0 * rows, rows, r0, r0 + 1 < rows);
@@ -268,12 +271,14 @@ int launch_quant_unpack(const uint8_t* codes, const float* scales, int pos, int6
 // x_i / x_j bf16 [n][cols] (16-byte aligned), y_i / y_j f32 [n][rows]
 int launch_quant_gemv(const uint8_t* codes, const float* scales, int64_t rows, int64_t cols, const uint16_t* x_i,
                       int64_t n_i, const uint16_t* x_j, int64_t n_j, float* y_i, float* y_j, cudaStream_t stream) {
-  const int64_t items = (rows + 1) / 2 * ((std::max(n_i, n_j) + kGemvTB - 1) / kGemvTB);
+  const int tb = std::max(n_i, n_j) <= 2 ? 2 : 4;
+  const int64_t items = (rows + 1) / 2 * ((std::max(n_i, n_j) + tb - 1) / tb);
   if (items == 0) return PUZZLE_OK;
   {
     ProfScope _ps("quant_gemv", stream);
-    k_quant_gemv<<<qgrid(items, kQThreads / 32), kQThreads, 0, stream>>>(codes, scales, rows, cols, x_i, n_i, x_j,
-                                                                        n_j, y_i, y_j);
+    auto kern = tb == 2 ? k_quant_gemv<2> : k_quant_gemv<4>;
+    kern<<<qgrid(items, kQThreads / 32), kQThreads, 0, stream>>>(codes, scales, rows, cols, x_i, n_i, x_j, n_j, y_i,
+                                                                 y_j);
   }
   return cuda_check(cudaGetLastError(), "puzzle_quant_gemv launch");
 }
