@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(kQThreads) k_quant_unpack(const uint4* __restr
 // position's tokens (f32, sequential per lane over its cols / 32 columns); the sums are
 // warp-reduced (5 butterfly levels). CUDA cores, not tcgen05: at decode batch sizes the code
 // bytes (1 per merged element) are the traffic and the per-byte decode is the ALU work.
-// tokens per position per work item: 2 for decode-sized inputs (fewer accumulator registers,
-// no spills under the 2-CTA cap), 4 otherwise (fewer re-decodes of the codes per token)
+// tokens per position per work item (TB): 1 or 2 for decode-sized inputs (fewer accumulator
+// registers: TB = 1 fits 3 CTAs per SM), 4 otherwise (fewer re-decodes of the codes per token)
 
 __device__ __forceinline__ uint32_t cvt_bf16x2(float hi, float lo) {
   uint32_t d;
@@ -183,7 +183,7 @@ __device__ __forceinline__ void store_sums(float (*acc)[TB], int nt, int lane, f
 }
 
 template <int TB>
-__global__ void __launch_bounds__(kQThreads, 2) k_quant_gemv(const uint8_t* __restrict__ codes,
+__global__ void __launch_bounds__(kQThreads, TB == 1 ? 3 : 2) k_quant_gemv(const uint8_t* __restrict__ codes,
                                                           const float* __restrict__ scales, int64_t rows,
                                                           int64_t cols, const uint16_t* __restrict__ x_i,
                                                           int64_t n_i, const uint16_t* __restrict__ x_j,
@@ -271,12 +271,13 @@ int launch_quant_unpack(const uint8_t* codes, const float* scales, int pos, int6
 // x_i / x_j bf16 [n][cols] (16-byte aligned), y_i / y_j f32 [n][rows]
 int launch_quant_gemv(const uint8_t* codes, const float* scales, int64_t rows, int64_t cols, const uint16_t* x_i,
                       int64_t n_i, const uint16_t* x_j, int64_t n_j, float* y_i, float* y_j, cudaStream_t stream) {
-  const int tb = std::max(n_i, n_j) <= 2 ? 2 : 4;
+  const int64_t nmax = std::max(n_i, n_j);
+  const int tb = nmax <= 1 ? 1 : nmax <= 2 ? 2 : 4;
   const int64_t items = (rows + 1) / 2 * ((std::max(n_i, n_j) + tb - 1) / tb);
   if (items == 0) return PUZZLE_OK;
   {
     ProfScope _ps("quant_gemv", stream);
-    auto kern = tb == 2 ? k_quant_gemv<2> : k_quant_gemv<4>;
+    auto kern = tb == 1 ? k_quant_gemv<1> : tb == 2 ? k_quant_gemv<2> : k_quant_gemv<4>;
     kern<<<qgrid(items, kQThreads / 32), kQThreads, 0, stream>>>(codes, scales, rows, cols, x_i, n_i, x_j, n_j, y_i,
                                                                  y_j);
   }

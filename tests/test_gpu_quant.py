@@ -60,11 +60,12 @@ def _bf16_tokens(n, cols, seed):
     return torch.randn(n, cols, generator=torch.Generator().manual_seed(seed)).to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("rows,cols,n_i,n_j", [(1, 128, 1, 0), (3, 128, 0, 2), (37, 384, 5, 9), (256, 1408, 8, 17),
+@pytest.mark.parametrize("rows,cols,n_i,n_j", [(1, 128, 1, 0), (3, 128, 0, 2), (1023, 4096, 1, 1), (513, 1408, 2, 1),
+                                               (37, 384, 5, 9), (256, 1408, 8, 17),
                                                (1023, 4096, 23, 3), (4096, 14336, 12, 20)])
 def test_quant_gemv_matches_oracle(pz, rows, cols, n_i, n_j):
     """puzzle_quant_gemv vs oracle.quant_gemv (f64): ragged row pairs (odd rows), token chunks of
-    8 with ragged tails, an empty side, and the Mixtral w2 shape (4096 x 14336) of one merged
+    1 / 2 / 4 tokens per position (all three kernel instances) with ragged tails, an empty side, and the Mixtral w2 shape (4096 x 14336) of one merged
     pair. Tolerance derived from the kernel's summation: each lane sums cols/32 products in order
     and a 5-level tree follows, so |err| <= (cols/32 + 5) * 2^-24 * sum|w x| (plus one rounding
     of the sum), here with a factor 2 margin."""
