@@ -60,7 +60,7 @@ def _bf16_tokens(n, cols, seed):
     return torch.randn(n, cols, generator=torch.Generator().manual_seed(seed)).to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("rows,cols,n_i,n_j", [(1, 128, 1, 0), (3, 128, 0, 2), (1023, 4096, 1, 1), (513, 1408, 2, 1),
+@pytest.mark.parametrize("rows,cols,n_i,n_j", [(1, 128, 1, 0), (3, 128, 0, 2), (1023, 4096, 1, 1), (513, 1408, 2, 1), (65, 512, 3, 7),
                                                (37, 384, 5, 9), (256, 1408, 8, 17),
                                                (1023, 4096, 23, 3), (4096, 14336, 12, 20)])
 def test_quant_gemv_matches_oracle(pz, rows, cols, n_i, n_j):
