@@ -59,6 +59,7 @@ static float bits_f32(uint32_t u) {
 static uint16_t bf16_rne(float x) {
   uint32_t u = f32_bits(x);
   uint32_t lsb = (u >> 16) & 1u;
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return (uint16_t)((u >> 16) | 0x40u); /* NaN stays a quiet NaN (IEEE) */
   return (uint16_t)((u + 0x7FFFu + lsb) >> 16);
 }
 

@@ -53,16 +53,14 @@ int launch_ep_combine_peer(const int32_t*, const float*, const int32_t*, int, co
 bool tc_supported(int d, int f);
 int launch_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
                       const int32_t*, int64_t, uint16_t*, float*, int32_t*, cudaStream_t);
-int launch_tc2_experts(const uint16_t*, const uint16_t*, int, int, int, const uint16_t*, const int32_t*, int64_t,
-                       uint16_t*, float*, cudaStream_t);
-size_t gemv_tc_part_floats(bool prefill);
+size_t gemv_tc_part_floats();
 int64_t gemv_tc_counters(int n_rb, int n_pairs, int64_t n_assign);
 bool gemv_supported(int d, int f);
 size_t calib_workspace_bytes(int n_groups, int64_t cols);
 int launch_group_colsumsq(const uint16_t*, const int32_t*, int, int64_t, double*, double*, cudaStream_t);
 int launch_gemv_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
                            const int32_t*,
-                           const int32_t*, const int32_t*, int, int64_t, bool, float*, int32_t*, int32_t*,
+                           const int32_t*, const int32_t*, int, int64_t, float*, int32_t*, int32_t*,
                            uint16_t*, float*, cudaStream_t);
 
 namespace {
@@ -117,18 +115,23 @@ int cuda_check(cudaError_t e, const char* what) {
   return fail(PUZZLE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  return dev;
+}
+
+// SM count of the current device, cached per device ordinal (thread-safe: a racing first
+// query stores the same value twice).
 int num_sms() {
-  static int cached = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0, n = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
-      cached = n;
-    else
-      cached = 148;  // B200
-  });
-  return cached;
+  static std::atomic<int> cached[64];
+  const int dev = current_device() & 63;
+  int n = cached[dev].load(std::memory_order_relaxed);
+  if (n > 0) return n;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device()) != cudaSuccess || n <= 0)
+    n = 148;  // B200
+  cached[dev].store(n, std::memory_order_relaxed);
+  return n;
 }
 
 namespace {
@@ -162,7 +165,6 @@ int check_layer(const puzzle_moe_layer* L) {
 struct Plan {
   int64_t T = 0, n_assign = 0;
   int k = 0, max_active = 0;
-  bool tmem_prefill = false;  // TC path through the decode-into-TMEM kernel's prefill configuration
   int path = PUZZLE_PATH_GEMV;  // resolved (never AUTO)
 };
 
@@ -175,19 +177,6 @@ struct Layout {
       x_perm, route_scratch, total;
 };
 
-// Token-heavy batches: the tcgen05 grouped GEMM (gemm_tc.cu) by default; PUZZLE_PREFILL_IMPL=tmem
-// selects the decode-into-TMEM kernels' prefill configuration, =pair the CTA-pair
-// (cta_group::2) grouped GEMM (gemm_tc2.cu) -- A/B measurements.
-const char* prefill_impl() {
-  static const char* v = [] {
-    const char* e = getenv("PUZZLE_PREFILL_IMPL");
-    return e ? e : "";
-  }();
-  return v;
-}
-bool prefill_via_tmem() { return std::string(prefill_impl()) == "tmem"; }
-bool prefill_via_pair() { return std::string(prefill_impl()) == "pair"; }
-
 Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   Plan p;
   p.T = T;
@@ -197,7 +186,6 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   if (path == PUZZLE_PATH_AUTO)
     path = (T > kGemvMaxTokens && tc_supported(L->d_model, L->d_ff)) ? PUZZLE_PATH_TC : PUZZLE_PATH_GEMV;
   p.path = path;
-  if (path == PUZZLE_PATH_TC) p.tmem_prefill = prefill_via_tmem();
   return p;
 }
 
@@ -224,9 +212,7 @@ Layout make_layout(const puzzle_moe_layer* L, const Plan& p) {
   o.h = take(na * f * 2);
   o.y = take(na * d * 4);
   // stream-K partial slots: 2 per CTA x 2 positions x tokens of a pass x 128 fp32
-  o.part = take(p.path == PUZZLE_PATH_GEMV ? gemv_tc_part_floats(false) * 4
-                : p.tmem_prefill         ? gemv_tc_part_floats(true) * 4
-                                         : 0);
+  o.part = take(p.path == PUZZLE_PATH_GEMV ? gemv_tc_part_floats() * 4 : 0);
   o.x_perm = take(na * d * 2);
   o.route_scratch = take((size_t)std::max<int64_t>(2 * 2 * (int64_t)P, p.T <= kGemvMaxTokens
                                                                           ? route_dec_scratch_ints(p.T, p.k, (int)P)
@@ -406,20 +392,11 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
     if (rc) return rc;
     rows = at<uint16_t>(ws, lay.x_perm);
   }
-  if (plan.path == PUZZLE_PATH_TC && plan.tmem_prefill)
-    return launch_gemv_tc_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
-                                  n_active, plan.max_active, plan.n_assign, true, at<float>(ws, lay.part),
-                                  at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);
-  if (plan.path == PUZZLE_PATH_TC && prefill_via_pair()) {
-    if (L->pair_dense) return fail(PUZZLE_ERR_UNSUPPORTED, "experimental CTA-pair prefill: no dense slots");
-    return launch_tc2_experts(L->w13, L->w2, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
-                              at<uint16_t>(ws, lay.h), y, s);
-  }
   if (plan.path == PUZZLE_PATH_TC)
     return launch_tc_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, at<int32_t>(ws, lay.cnt13), s);  // cnt13: zeroed per call
   return launch_gemv_tc_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, active,
-                                n_active, plan.max_active, plan.n_assign, false, at<float>(ws, lay.part),
+                                n_active, plan.max_active, plan.n_assign, at<float>(ws, lay.part),
                                 at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2), at<uint16_t>(ws, lay.h), y, s);
 }
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <utility>
 
@@ -23,6 +24,21 @@ int cuda_check(cudaError_t e, const char* what);
 int num_sms();
 
 constexpr int kMaxExperts = 512;
+
+// The current device (attributes and SM counts below are per device: a process may drive
+// several GPUs, one per thread or one after the other).
+int current_device();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): `mask` is the
+// kernel's own set of devices already configured (bit = device ordinal, < 64).
+template <typename K>
+cudaError_t ensure_smem_attr(K* kern, size_t bytes, std::atomic<uint64_t>& mask) {
+  const uint64_t bit = 1ull << (current_device() & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // Per-kernel event bracketing while a puzzle_profile window is open (abi.cu).
 void prof_mark_begin(const char* name, cudaStream_t s);
@@ -77,9 +93,11 @@ __device__ __forceinline__ void warp_copy_row(const uint4* __restrict__ sp, uint
 // bit15 S_i | bit14 S_j | bit13 M_i | bit12 M_j | bits 11..7 e' = e-112 | bits 6..0 mantissa
 
 // f32 -> bf16 round-to-nearest-even in integer arithmetic (reading R3). Integer-only so
-// that FTZ / fast-math settings can never change the result.
+// that FTZ / fast-math settings can never change the result. NaN stays NaN (quiet, sign and
+// top payload bits kept: IEEE / torch's cast), so an overflow inside an expert propagates.
 __device__ __forceinline__ uint32_t f32_to_bf16_rne_bits(float x) {
   uint32_t u = __float_as_uint(x);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return (u >> 16) | 0x40u;
   return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
 }
 

@@ -431,11 +431,9 @@ int launch_tc_experts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pa
                       float* y, int32_t* work_ctrs, cudaStream_t stream) {
   if (!tc_supported(d, f)) return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d % 256 == 0 and d_ff % 128 == 0");
   if (n_rows_cap == 0) return PUZZLE_OK;
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(k_tc_experts<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    cudaFuncSetAttribute(k_tc_experts<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-  });
+  static std::atomic<uint64_t> attr13{0}, attr2{0};
+  if (int rc = cuda_check(ensure_smem_attr(k_tc_experts<true>, kSmemBytes, attr13), "w13_tc smem attribute")) return rc;
+  if (int rc = cuda_check(ensure_smem_attr(k_tc_experts<false>, kSmemBytes, attr2), "w2_tc smem attribute")) return rc;
   CUtensorMap ta13, tb13, ta2, tb2;
   int rc;
   if ((rc = make_tmap_2d(&ta13, x_rows, n_rows_cap, d, BM, BK))) return rc;

@@ -62,10 +62,8 @@ constexpr int kSq = 8;       // stage queue W producer -> X producer
 constexpr int kMinStages = 8;  // stream-K: minimum stages per CTA
 constexpr uint32_t kAccCol = 64 * kAStages;      // 192: accumulators of position p at 192 + NX p
 
-// Two configurations of the same kernel:
-//   decode  (NX = 32, 2 CTAs per SM, 256 TMEM columns): batches of 1-64 tokens;
-//   prefill (NX = 128, 1 CTA per SM, 512 TMEM columns): up to 128 tokens per position per pass,
-//            every pass a work item of its own (tokens on the N side, N <= 128).
+// Configuration: NX = 32 tokens per position per pass, 2 CTAs per SM, 256 TMEM columns
+// (batches of 1-64 tokens; larger batches go to the prefill kernels).
 template <int NX, int CTAS>
 struct Cfg {
   static constexpr int kNX = NX;                          // tokens per position per pass (UMMA N <= NX)
@@ -119,7 +117,6 @@ constexpr size_t smem_bytes() {
          sizeof(Ctl<C::kWStages, C::kXStages>);
 }
 static_assert(2 * (smem_bytes<Cfg<32, 2>>() + 1024) <= 228 * 1024, "decode: two CTAs per SM");
-static_assert(smem_bytes<Cfg<128, 1>>() + 1024 <= 228 * 1024, "prefill: one CTA per SM");
 
 struct PairTokens {
   int off0, cnt0, off1, cnt1;
@@ -708,11 +705,8 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
   using C = Cfg<NX, CTAS>;
   auto kern = k_gemv_tc<kW13, NX, CTAS>;
   constexpr size_t kSmem = smem_bytes<C>();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (int rc = cuda_check(ensure_smem_attr(kern, kSmem, attr), "gemv smem attribute")) return rc;
   // stream-K grid: every resident CTA slot, but >= kMinStages stages each (the device
   // recomputes the partition from the actual active pairs and passes)
   const int64_t S = ((int64_t)max_active + n_assign / NX) * n_rb * (K / kBK);  // >= the real stage count
@@ -749,26 +743,20 @@ int launch_both(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_den
 
 }  // namespace
 
-// Partial-slot floats of the two configurations (2 slots per CTA x 2 positions x NX x 128).
-size_t gemv_tc_part_floats(bool prefill) {
-  return prefill ? (size_t)2 * num_sms() * 2 * 128 * kRows : (size_t)2 * 2 * num_sms() * 2 * 32 * kRows;
-}
+// Partial-slot floats (2 slots per CTA x 2 CTAs per SM x 2 positions x NX x 128).
+size_t gemv_tc_part_floats() { return (size_t)2 * 2 * num_sms() * 2 * 32 * kRows; }
 // Work-item counters per projection: row blocks x (pairs + passes).
 int64_t gemv_tc_counters(int n_rb, int n_pairs, int64_t n_assign) { return (int64_t)n_rb * (n_pairs + n_assign / 32 + 1); }
 bool gemv_supported(int d, int f) { return d % 64 == 0 && f % 64 == 0 && d <= 65535 * 64 && f <= 65535 * 64; }
 
 // x_rows: [n_assign_cap][d] bf16 in bucket order (TMA source); h: [n_assign_cap][f];
 // y: [n_assign_cap][d]; part: gemv_tc_part_floats(prefill) floats; counters13 / counters2:
-// gemv_tc_counters(row blocks, ...) ints, zero. prefill = the 128-token, one-CTA-per-SM
-// configuration (token-heavy batches), otherwise the decode configuration. pair_dense: NULL or
+// gemv_tc_counters(row blocks, ...) ints, zero. pair_dense: NULL or
 // [n_pairs] device flags (slot holds one unmerged expert's bf16 weights, position 0 only).
 int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_dense, int n_pairs, int d, int f,
                            const uint16_t* x_rows, const int32_t* bucket_off, const int32_t* active_pairs,
-                           const int32_t* n_active, int max_active, int64_t n_assign_cap, bool prefill, float* part,
+                           const int32_t* n_active, int max_active, int64_t n_assign_cap, float* part,
                            int32_t* counters13, int32_t* counters2, uint16_t* h, float* y, cudaStream_t stream) {
-  if (prefill)
-    return launch_both<128, 1>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
-                               n_assign_cap, part, counters13, counters2, h, y, stream);
   return launch_both<32, 2>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
                             n_assign_cap, part, counters13, counters2, h, y, stream);
 }

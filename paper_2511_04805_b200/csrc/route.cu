@@ -385,14 +385,15 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y,
                                                  const int32_t* __restrict__ assign_of,
                                                  const float* __restrict__ gate, int k_rt, int d,
                                                  const uint16_t* __restrict__ residual,
-                                                 uint16_t* __restrict__ out) {
+                                                 uint16_t* __restrict__ out, int64_t T) {
   const int k = K > 0 ? K : k_rt;
-  const int64_t t = blockIdx.y;
   const int c4 = blockIdx.x * blockDim.x + threadIdx.x;  // index of a 4-column group
   pdl_wait();
   PZ_RT(2, false);
   pdl_trigger();
   if (c4 * 4 >= d) return;
+  // tokens stride over gridDim.y (<= 65535 CTAs): any T
+  for (int64_t t = blockIdx.y; t < T; t += gridDim.y) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (residual != nullptr) {
     const uint2 r = *reinterpret_cast<const uint2*>(residual + t * d + c4 * 4);
@@ -412,6 +413,7 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y,
   o.x = f32_to_bf16_rne_bits(acc.x) | (f32_to_bf16_rne_bits(acc.y) << 16);
   o.y = f32_to_bf16_rne_bits(acc.z) | (f32_to_bf16_rne_bits(acc.w) << 16);
   *reinterpret_cast<uint2*>(out + t * d + c4 * 4) = o;
+  }
   PZ_RT(2, true);
 }
 
@@ -580,12 +582,12 @@ int launch_combine(const float* y, const int32_t* assign_of, const float* gate, 
                    int d, const uint16_t* residual, uint16_t* out, cudaStream_t stream) {
   if (T == 0) return PUZZLE_OK;
   const int threads = 256;
-  dim3 grid((unsigned)((d / 4 + threads - 1) / threads), (unsigned)T);
+  dim3 grid((unsigned)((d / 4 + threads - 1) / threads), (unsigned)std::min<int64_t>(T, 65535));
   {
     ProfScope _ps("combine", stream);
     auto kern = k == 1 ? k_combine<1> : k == 2 ? k_combine<2> : k == 4 ? k_combine<4> : k == 6 ? k_combine<6>
               : k == 8 ? k_combine<8> : k_combine<0>;
-    cudaError_t e = launch_pdl(kern, grid, dim3(threads), 0, stream, y, assign_of, gate, k, d, residual, out);
+    cudaError_t e = launch_pdl(kern, grid, dim3(threads), 0, stream, y, assign_of, gate, k, d, residual, out, T);
     if (e != cudaSuccess) return cuda_check(e, "combine launch");
   }
   return cuda_check(cudaGetLastError(), "combine launch");

@@ -157,3 +157,22 @@ def test_rne_matches_torch_cast_on_sweep():
     got = oracle.bf16_round(x)
     want = torch.from_numpy(x.copy()).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(got, want)
+
+
+def test_rne_nan_and_inf_match_torch_cast():
+    """O1 bf16_rne on the non-finite patterns: +-Inf stay Inf, every NaN stays a (quiet) NaN
+    with its sign and top payload bits, as torch's CPU cast does (a NaN rounded
+    by the plain RNE formula became -0)."""
+    rng = np.random.default_rng(7)
+    payload = rng.integers(1, 1 << 23, 4000, dtype=np.uint64).astype(np.uint32)
+    nans = np.concatenate([0x7F800000 | payload, 0xFF800000 | payload,
+                           np.array([0x7FC00000, 0x7FFFFFFF, 0xFFFFFFFF, 0x7F800001, 0x7F810000], np.uint32)])
+    infs = np.array([0x7F800000, 0xFF800000], np.uint32)
+    u = np.concatenate([nans.astype(np.uint32), infs])
+    x = u.view(np.float32)
+    got = oracle.bf16_round(x)
+    want = torch.from_numpy(x.copy()).to(torch.bfloat16)
+    # torch returns one canonical NaN: compare NaN-ness, then the kept sign / quiet bit
+    assert np.array_equal(np.isnan(want.float().numpy()), (got & 0x7FFF) > 0x7F80)
+    assert np.array_equal(got[-2:], want[-2:].view(torch.int16).numpy().view(np.uint16))
+    assert np.array_equal(got[:-2] >> 15, u[:-2] >> 31) and np.all(got[:-2] & 0x0040)
