@@ -167,8 +167,7 @@ int puzzle_quant_gemv(const uint8_t* codes, const float* scales, int64_t rows, i
  *                shape, read without Algorithm 1; only 2*q + 0 may appear in expert_slot
  *                (routing an expert to 2*q + 1 of such a slot gives undefined outputs).
  * Requirements: 1 <= n_experts <= 2*n_pairs <= 512; d_model and d_ff multiples of 64;
- * w13/w2 16-byte aligned. The experimental CTA-pair prefill (PUZZLE_PREFILL_IMPL=pair)
- * rejects pair_dense with PUZZLE_ERR_UNSUPPORTED.
+ * w13/w2 16-byte aligned.
  * ------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_experts;
@@ -185,7 +184,9 @@ typedef struct {
 typedef enum {
   PUZZLE_PATH_AUTO = 0,
   PUZZLE_PATH_GEMV = 1,   /* decode shape: decode into TMEM + tcgen05.mma (weights on M), weights read once per pair */
-  PUZZLE_PATH_TC = 2      /* prefill shape: grouped tcgen05/TMEM GEMM, tiles decoded in shared memory */
+  PUZZLE_PATH_TC = 2,     /* prefill shape: grouped tcgen05/TMEM GEMM, tiles decoded in shared memory */
+  PUZZLE_PATH_TS = 3      /* prefill shape: decoded weights as the TMEM A operand, up to 384 tokens of a
+                             bucket on N per pass (d_model % 128 == 0, d_ff % 64 == 0) */
 } puzzle_path;
 
 /* Bytes of device workspace puzzle_moe_forward needs for up to max_tokens tokens. */

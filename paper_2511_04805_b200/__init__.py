@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PUZZLE_LIB") or os.path.join(_HERE, "libpuzzlemoe.so")
 
 PUZZLE_OK = 0
-PATH_AUTO, PATH_GEMV, PATH_TC = 0, 1, 2
+PATH_AUTO, PATH_GEMV, PATH_TC, PATH_TS = 0, 1, 2, 3
 
 EXPORTED_SYMBOLS = (
     "puzzle_status_string", "puzzle_last_error", "puzzle_abi_version", "puzzle_merge_pack",

@@ -51,6 +51,9 @@ int launch_ep_home_index_peer(const int32_t*, const float*, const int32_t*, int,
 int launch_ep_combine_peer(const int32_t*, const float*, const int32_t*, int, const int32_t*, int, int64_t, int64_t, int,
                            int, const void*, const uint16_t*, uint16_t*, uint32_t*, cudaStream_t);
 bool tc_supported(int d, int f);
+bool ts_supported(int d, int f);
+int launch_ts_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*, const int32_t*,
+                      int64_t, uint16_t*, float*, int32_t*, cudaStream_t);
 int launch_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
                       const int32_t*, int64_t, uint16_t*, float*, int32_t*, cudaStream_t);
 size_t gemv_tc_part_floats();
@@ -226,8 +229,9 @@ size_t workspace_for(const puzzle_moe_layer* L, int64_t max_tokens, int k) {
   // either path for any T <= max_tokens.
   size_t best = 0;
   int64_t knee = (L->n_pairs + k - 1) / k;
-  for (int path : {(int)PUZZLE_PATH_GEMV, (int)PUZZLE_PATH_TC}) {
+  for (int path : {(int)PUZZLE_PATH_GEMV, (int)PUZZLE_PATH_TC, (int)PUZZLE_PATH_TS}) {
     if (path == PUZZLE_PATH_TC && !tc_supported(L->d_model, L->d_ff)) continue;
+    if (path == PUZZLE_PATH_TS && !ts_supported(L->d_model, L->d_ff)) continue;
     for (int64_t t = 1; t <= std::min<int64_t>(max_tokens, knee); ++t)
       best = std::max(best, make_layout(L, make_plan(L, t, k, path)).total);
     if (max_tokens > 0) best = std::max(best, make_layout(L, make_plan(L, max_tokens, k, path)).total);
@@ -392,6 +396,9 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
     if (rc) return rc;
     rows = at<uint16_t>(ws, lay.x_perm);
   }
+  if (plan.path == PUZZLE_PATH_TS)
+    return launch_ts_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
+                             at<uint16_t>(ws, lay.h), y, at<int32_t>(ws, lay.cnt13), s);  // cnt13: zeroed per call
   if (plan.path == PUZZLE_PATH_TC)
     return launch_tc_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, at<int32_t>(ws, lay.cnt13), s);  // cnt13: zeroed per call
@@ -414,7 +421,7 @@ static int forward_impl(const puzzle_moe_layer* L, const uint16_t* hidden, const
   if (int rc = check_layer(L)) return rc;
   if (T < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "T < 0");
   if (k < 1 || k > L->n_experts) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "top_k outside [1, n_experts]");
-  if (path < PUZZLE_PATH_AUTO || path > PUZZLE_PATH_TC) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad path");
+  if (path < PUZZLE_PATH_AUTO || path > PUZZLE_PATH_TS) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad path");
   if (T == 0) return PUZZLE_OK;
   if (!hidden || !logits || !out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL activation pointer");
   if (hidden == out) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "out must not alias hidden");
@@ -423,6 +430,8 @@ static int forward_impl(const puzzle_moe_layer* L, const uint16_t* hidden, const
   if (int rc = check_device()) return rc;
   if (path == PUZZLE_PATH_TC && !tc_supported(L->d_model, L->d_ff))
     return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d_model % 256 == 0 and d_ff % 128 == 0");
+  if (path == PUZZLE_PATH_TS && !ts_supported(L->d_model, L->d_ff))
+    return fail(PUZZLE_ERR_UNSUPPORTED, "TS prefill path needs d_model % 128 == 0 and d_ff % 64 == 0");
   const Plan plan = make_plan(L, T, k, path);
   const Layout lay = make_layout(L, plan);
   const bool calib = sumsq_x || sumsq_h;
@@ -552,9 +561,11 @@ int puzzle_moe_experts(const puzzle_moe_layer* L, const uint16_t* x_rows, const 
   if (!x_rows || !bucket_off || !y_rows) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (!al16(x_rows) || !al16(y_rows)) return fail(PUZZLE_ERR_UNSUPPORTED, "rows must be 16-byte aligned");
   if (int rc = check_device()) return rc;
-  if (path < PUZZLE_PATH_AUTO || path > PUZZLE_PATH_TC) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad path");
+  if (path < PUZZLE_PATH_AUTO || path > PUZZLE_PATH_TS) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "bad path");
   if (path == PUZZLE_PATH_TC && !tc_supported(L->d_model, L->d_ff))
     return fail(PUZZLE_ERR_UNSUPPORTED, "tcgen05 path needs d_model % 256 == 0 and d_ff % 128 == 0");
+  if (path == PUZZLE_PATH_TS && !ts_supported(L->d_model, L->d_ff))
+    return fail(PUZZLE_ERR_UNSUPPORTED, "TS prefill path needs d_model % 128 == 0 and d_ff % 64 == 0");
   // Every pair may be touched: plan with T = n_assign, k = 1 (max_active = min(P, n_assign)).
   Plan plan = make_plan(L, n_assign, 1, path);
   const Layout lay = make_layout(L, plan);

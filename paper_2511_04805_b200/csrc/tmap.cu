@@ -46,5 +46,23 @@ int make_tmap_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, i
   return PUZZLE_OK;
 }
 
+// 3-D map over a [n2][rows][cols] bf16 / u16 tensor whose dim-2 stride is `stride2_rows` rows:
+// a box {box_cols, box_rows, box_n2} lands in shared memory as box_n2 consecutive 2-D boxes
+// (one TMA instruction for several row blocks that are far apart in memory, e.g. the gate and
+// the up rows of the same features of a packed w13 pair).
+int make_tmap_3d(CUtensorMap* m, const void* base, int64_t n2, int64_t rows, int64_t cols, int64_t stride2_rows,
+                 int box_rows, int box_cols, int box_n2) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(PUZZLE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)n2};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)stride2_rows * cols * 2};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, (cuuint32_t)box_n2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PUZZLE_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
+  return PUZZLE_OK;
+}
 
 }  // namespace pz

@@ -1,0 +1,59 @@
+"""Pipeline timeline of the TS prefill kernel (PZ_TRACE build of gemm_ts.cu:
+python scripts/build_variant.py tstrace gemm_ts.cu -DPZ_TRACE=5; run with PUZZLE_LIB=...).
+CTA PZ_TRACE of the w13 kernel: per stage W TMA issue (0), X0 TMA issue (1), decoder words (2),
+decoder A free (3), decoder afull (4), MMA0 xfull (5), MMA0 afull (6), MMA0 issued (7); per
+item epilogue start (8) / end (9). All CTAs: start / end."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import synth  # noqa: E402
+import paper_2511_04805_b200 as pz  # noqa: E402
+
+cfg = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "qwen15"]
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+dev = torch.device("cuda:0")
+layer, _ = bench.build_layer_gpu(pz, cfg, 1, dev)
+hidden, logits = bench.make_inputs(cfg, T, 2, dev)
+for _ in range(3):
+    layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, path=pz.PATH_TS)
+torch.cuda.synchronize()
+lib = pz.load_library()
+ev = np.zeros((14, 4096), np.uint64)
+cc = np.zeros((2, 1024, 2), np.uint64)
+lib.puzzle_debug_ts.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t]
+assert lib.puzzle_debug_ts(ev.ctypes.data, ev.nbytes, cc.ctypes.data, cc.nbytes) == 0
+for name, k in (("w13", 1), ("w2", 0)):
+    v = cc[k].astype(np.int64)
+    n = int((v[:, 1] > 0).sum())
+    v = v[:n]
+    t0 = v[:, 0].min()
+    d = (v[:, 1] - v[:, 0]) / 1e3
+    print(f"{name}: {n} CTAs, start spread {(v[:,0].max()-t0)/1e3:.1f} us, duration min {d.min():.1f} "
+          f"med {np.median(d):.1f} max {d.max():.1f} us; kernel span {(v[:,1].max()-t0)/1e3:.1f} us")
+n = int((ev[7] > 0).sum())
+e = ev[:, :].astype(np.int64)
+t0 = e[0, 0]
+print(f"stages traced {n}; per-stage (us since first W issue):")
+names = ["Wiss", "X0iss", "Dwords", "DAfree", "Dafull", "Mxfull", "Mafull", "Missued"]
+print("  s  " + " ".join(f"{x:>8}" for x in names) + "   dt(Missued)")
+for s in list(range(0, 12)) + list(range(n // 2, n // 2 + 12)) + list(range(n - 6, n)):
+    row = [(e[i, s] - t0) / 1e3 if e[i, s] else float("nan") for i in range(8)]
+    dt = (e[7, s] - e[7, s - 1]) / 1e3 if s > 0 else 0
+    print(f"{s:4d} " + " ".join(f"{x:8.2f}" for x in row) + f"   {dt:.3f}")
+m = e[7, 1:n] - e[7, :n - 1]
+print(f"MMA issue interval: median {np.median(m)/1e3:.3f} us, mean {m.mean()/1e3:.3f} us")
+for a, b, lab in ((0, 2, "W issue -> words"), (1, 5, "X issue -> MMA xfull"), (2, 3, "words -> A free"),
+                  (3, 4, "A free -> afull"), (4, 6, "afull -> MMA sees"), (5, 6, "MMA xfull -> afull"),
+                  (6, 7, "MMA afull -> issued")):
+    dd = (e[b, :n] - e[a, :n]) / 1e3
+    print(f"  {lab:24s} median {np.median(dd):.3f} us  p90 {np.percentile(dd, 90):.3f}")
+ni = int((ev[9] > 0).sum())
+if ni:
+    ep = (e[9, :ni] - e[8, :ni]) / 1e3
+    print(f"items {ni}: epilogue median {np.median(ep):.2f} us, starts at " + " ".join(f"{(x - t0)/1e3:.1f}" for x in e[8, :ni]))
