@@ -538,11 +538,11 @@ def run_ours(args):
                 "duration_ms": dom_ms, "duration_includes": [k for k in (dom, tail) if k in kern],
                 "peak_source": pk["source"],
                 "step_share": kern[dom]["total_ms"] / max(sum(v["total_ms"] for v in kern.values()), 1e-9)}
-    elif dom in ("w13_tc", "w2_tc"):
+    elif dom in ("w13_tc", "w2_tc", "w13_ts", "w2_ts"):
         # prefill: tensor-bound; algorithmic flops = dense-equivalent FFN flops of the routed
         # assignments (unit: one assignment's 2*(2f)*d (w13) or 2*d*f (w2) flop)
         n_assign = T * cfg.top_k
-        unit = 2 * 2 * cfg.d_ff * cfg.d_model if dom == "w13_tc" else 2 * cfg.d_model * cfg.d_ff
+        unit = 2 * 2 * cfg.d_ff * cfg.d_model if dom.startswith("w13") else 2 * cfg.d_model * cfg.d_ff
         achieved = unit * n_assign / (kern[dom]["avg_ms"] / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16_tflops"], "traffic": ncu_traffic(cfg.name, T, dom),
@@ -827,8 +827,8 @@ def sweep(pz, args, device, pk):
                 row.update({"weight_gbs": gbs, "frac_hbm": gbs / pk["hbm_gbs"]})
             else:
                 flops = 2 * 3 * cfg.d_model * cfg.d_ff * T * cfg.top_k
-                tc_ms = sum(v for k, v in kern.items() if k.endswith("_tc"))
-                row.update({"path": "tcgen05", "tflops_step": flops / (ms / 1e3) / 1e12,
+                tc_ms = sum(v for k, v in kern.items() if k.endswith("_tc") or k.endswith("_ts"))
+                row.update({"path": "ts" if any(k.endswith("_ts") for k in kern) else "tc", "tflops_step": flops / (ms / 1e3) / 1e12,
                             "tflops_tc_kernels": flops / (tc_ms / 1e3) / 1e12 if tc_ms else None,
                             "frac_bf16_peak": flops / (tc_ms / 1e3) / 1e12 / pk["bf16_tflops"] if tc_ms else None})
             res.append(row)

@@ -180,7 +180,7 @@ typedef struct {
   const uint8_t* pair_dense;
 } puzzle_moe_layer;
 
-/* Kernel path for puzzle_moe_forward_ex. AUTO picks by token count. */
+/* Kernel path for puzzle_moe_forward_ex. AUTO: GEMV for T <= 64, else TS (else TC, else GEMV). */
 typedef enum {
   PUZZLE_PATH_AUTO = 0,
   PUZZLE_PATH_GEMV = 1,   /* decode shape: decode into TMEM + tcgen05.mma (weights on M), weights read once per pair */

@@ -53,7 +53,7 @@ int launch_ep_combine_peer(const int32_t*, const float*, const int32_t*, int, co
 bool tc_supported(int d, int f);
 bool ts_supported(int d, int f);
 int launch_ts_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*, const int32_t*,
-                      int64_t, uint16_t*, float*, int32_t*, cudaStream_t);
+                      int64_t, uint16_t*, float*, cudaStream_t);
 int launch_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
                       const int32_t*, int64_t, uint16_t*, float*, int32_t*, cudaStream_t);
 size_t gemv_tc_part_floats();
@@ -186,8 +186,13 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   p.k = k;
   p.n_assign = T * k;
   p.max_active = (int)std::min<int64_t>(L->n_pairs, p.n_assign);
+  // token-heavy batches: the decode-into-TMEM prefill kernel (gemm_ts.cu; ahead of or level with
+  // the shared-memory-operand kernel on every config, profiles/r02/prefill_ab.txt), else gemm_tc.cu
   if (path == PUZZLE_PATH_AUTO)
-    path = (T > kGemvMaxTokens && tc_supported(L->d_model, L->d_ff)) ? PUZZLE_PATH_TC : PUZZLE_PATH_GEMV;
+    path = T <= kGemvMaxTokens                  ? PUZZLE_PATH_GEMV
+           : ts_supported(L->d_model, L->d_ff) ? PUZZLE_PATH_TS
+           : tc_supported(L->d_model, L->d_ff) ? PUZZLE_PATH_TC
+                                                : PUZZLE_PATH_GEMV;
   p.path = path;
   return p;
 }
@@ -398,7 +403,7 @@ static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout
   }
   if (plan.path == PUZZLE_PATH_TS)
     return launch_ts_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
-                             at<uint16_t>(ws, lay.h), y, at<int32_t>(ws, lay.cnt13), s);  // cnt13: zeroed per call
+                             at<uint16_t>(ws, lay.h), y, s);
   if (plan.path == PUZZLE_PATH_TC)
     return launch_tc_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, at<int32_t>(ws, lay.cnt13), s);  // cnt13: zeroed per call

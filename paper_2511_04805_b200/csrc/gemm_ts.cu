@@ -43,7 +43,7 @@
 namespace pz {
 
 #ifdef PZ_TRACE  // per-stage pipeline timeline of CTA PZ_TRACE of the w13 launch (scripts/trace_ts.py)
-__device__ unsigned long long g_tst[14][4096];
+__device__ unsigned long long g_tst[14][4096];  // 13: decoder reaches stage (before the W wait)
 __device__ unsigned long long g_tsc[2][1024][2];  // [kernel][cta] {start after wait, end}
 __device__ __forceinline__ unsigned long long ts_gtimer() {
   unsigned long long t;
@@ -85,7 +85,7 @@ constexpr int kNmax = 2 * kNH;             // tokens per work item (multiple of 
 constexpr int kXStages = PZ_TS_XST;
 constexpr int kWStages = PZ_TS_WST;
 constexpr int kXBytes = kNH * kBK * 2;     // token rows of one half-stage
-constexpr int kAStages = 4;                // TMEM A buffers (32 columns = 64 bf16 k each)
+constexpr int kAStages = (512 - 2 * kNH) / 32 > 8 ? 8 : (512 - 2 * kNH) / 32;  // TMEM A buffers (32 columns = 64 k)
 constexpr uint32_t kAccCol = 32 * kAStages;
 constexpr int kSq = 8;                     // stage queue W producer -> X producer
 constexpr int kIq = 4;                     // item queue W producer -> epilogue
@@ -96,10 +96,10 @@ constexpr int kDecWarps = PZ_TS_DECW;
 constexpr int kKH = 8 / kDecWarps;          // K halves per decoder warp
 constexpr int kEpiWarps = 8;                // 4 per accumulator half (one per TMEM lane quarter)
 constexpr int kThreads = 32 * (5 + kDecWarps + kEpiWarps);
-constexpr int kXMaps = kNH / 32;           // X box heights 32, 64, .., kNH rows
+constexpr int kXMaps = kNH / 16;           // X box heights 16, 32, .., kNH rows
 constexpr int kW_DEC0 = 5, kW_EPI0 = 5 + kDecWarps;
 constexpr int kMaxBuckets = kMaxExperts;
-static_assert(kNH % 32 == 0 && kNH <= 256 && kAccCol + 2 * kNH <= 512, "TMEM: A ring + two token halves");
+static_assert(kNH % 16 == 0 && kNH <= 256 && kAccCol + 2 * kNH <= 512, "TMEM: A ring + two token halves");
 
 // X tensor maps of every box height, passed by value (kernel parameter space)
 struct XMaps {
@@ -129,11 +129,13 @@ static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 // A work item: bucket b, row block rb (128 weight rows), token chunk c of the bucket.
 struct Item {
   int b, rb, row0, nvalid, n0, n1;
+  bool ghost;  // rb >= n_rb: the odd row-block count's spare CTA of a cluster (no outputs)
 };
 
-// Item order: pair-major, then row block, then (position, chunk): the CTAs of one wave work on
-// a band of row blocks of ONE pair, whose packed tiles and token rows are re-read from L2.
-__device__ __forceinline__ Item item_info(const Ctl& c, int item, int n_pairs) {
+// Item order: pair-major, then row-block pair, then (position, chunk): the clusters of one wave
+// work on a band of row blocks of ONE pair, whose packed tiles and token rows are re-read from
+// L2. A cluster item is two adjacent row blocks of one token chunk: CTA `rank` takes 2 rbp + rank.
+__device__ __forceinline__ Item item_info(const Ctl& c, int item, int n_pairs, int rank, int n_rb) {
   int lo = 0, hi = n_pairs - 1;  // last pair with pair_off[p] <= item
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -143,8 +145,10 @@ __device__ __forceinline__ Item item_info(const Ctl& c, int item, int n_pairs) {
   const int c0 = c.nch[2 * p], c01 = c0 + c.nch[2 * p + 1];
   const int rem = item - c.pair_off[p];
   Item it;
-  it.rb = rem / c01;
-  const int r2 = rem - it.rb * c01;
+  const int rbp = rem / c01;
+  it.rb = 2 * rbp + rank;
+  it.ghost = it.rb >= n_rb;
+  const int r2 = rem - rbp * c01;
   it.b = 2 * p + (r2 >= c0);
   const int ch = r2 >= c0 ? r2 - c0 : r2;
   const int w = c.ncw[it.b];
@@ -211,11 +215,10 @@ struct Ring {
 template <bool kW13>
 __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
     const __grid_constant__ CUtensorMap tm_w,  // packed w13 [2P][f][d] (3-D, {64, 64, 2} boxes) / w2 [P*d][f] (128-row boxes)
-    const __grid_constant__ XMaps tm_x,        // token rows [n_rows][K] bf16, boxes of 32 (i + 1) rows
+    const __grid_constant__ XMaps tm_x,        // token rows [n_rows][K] bf16, boxes of 16 (i + 1) rows
     const int32_t* __restrict__ bucket_off, int n_pairs, int K, int f, int d, int n_rb,
     uint16_t* __restrict__ h_out,  // w13: [n_assign][f] bf16
     float* __restrict__ y_out,     // w2:  [n_assign][d] f32
-    int32_t* __restrict__ work_ctr,  // zero on entry
     uint32_t mul_one,                // = 1, opaque to ptxas
     const uint8_t* __restrict__ pair_dense) {
   extern __shared__ uint8_t smem_raw[];
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
     for (int h = 0; h < 2; ++h)
       for (int s = 0; s < kXStages; ++s) {
         ptx::mbar_init(&c.xfull[h][s], 1);
-        ptx::mbar_init(&c.xempty[h][s], 1);  // the commit of this half's MMA issuer
+        ptx::mbar_init(&c.xempty[h][s], 2);  // the (multicast) commits of both CTAs' half-h MMA issuers
       }
     for (int s = 0; s < kAStages; ++s) {
       ptx::mbar_init(&c.afull[s], kDecWarps);
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
     int run = 0;
     for (int p = 0; p < n_pairs; ++p) {
       c.pair_off[p] = run;
-      run += n_rb * (c.nch[2 * p] + c.nch[2 * p + 1]);
+      run += ((n_rb + 1) >> 1) * (c.nch[2 * p] + c.nch[2 * p + 1]);
     }
     c.pair_off[n_pairs] = run;
     c.n_items = run;
@@ -284,9 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  ptx::cluster_sync();  // both CTAs' barriers exist before any multicast load / commit reaches them
   const uint32_t tmem = c.tmem_base;
   const int nk = K / kBK;
   const int n_items = c.n_items;
+  const int rank = (int)ptx::cluster_ctarank(), cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
 
   if (warp == 0) {
     // ============================== W producer ==============================
@@ -294,16 +299,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       Ring w{0, 0}, sq{0, 0}, iq{0, 0};
       int tw = 0;
       (void)tw;
-      int next = atomicAdd(work_ctr, 1);
-      for (;;) {
-        const int item = next;
-        if (item >= n_items) break;
-        next = atomicAdd(work_ctr, 1);  // overlaps this item's stream
+      // static round robin over the clusters (both CTAs of a cluster walk the same items)
+      for (int item = cluster; item < n_items; item += n_clusters) {
         mbar_wait_ts(&c.iqempty[iq.i], iq.ph ^ 1);
         c.iq[iq.i] = item;
         ptx::mbar_arrive(&c.iqfull[iq.i]);
         iq.next<kIq>();
-        const Item it = item_info(c, item, n_pairs);
+        const Item it = item_info(c, item, n_pairs, rank, n_rb);
         const int pair = it.b >> 1;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait_ts(&c.wempty[w.i], w.ph ^ 1);
@@ -356,15 +358,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
         }
         if (h.x != cur) {
           cur = h.x;
-          it = item_info(c, cur, n_pairs);
+          it = item_info(c, cur, n_pairs, rank, n_rb);
         }
         const int nh = half ? it.n1 : it.n0;
-        const int box = (nh + 31) >> 5;  // boxes of 32 box rows (the MMA reads the first nh)
+        const int box = nh >> 4;  // one box of exactly nh rows (nh % 16 == 0)
         if (half == 0) PZ_TS(1, tx);
         ++tx;
         uint8_t* sx = smem + (size_t)kWStages * kWBytes + (size_t)(half * kXStages + x.i) * kXBytes;
-        ptx::mbar_arrive_expect_tx(&c.xfull[half][x.i], (uint32_t)box * 32 * (kBK * 2));
-        ptx::tma_load_2d(sx, &tm_x.m[box - 1], &c.xfull[half][x.i], h.y * kBK, it.row0 + half * it.n0);
+        // both CTAs of the cluster need this half's token rows: CTA `half` loads them once,
+        // multicast into the same slot of both (each CTA expects the bytes on its own barrier)
+        ptx::mbar_arrive_expect_tx(&c.xfull[half][x.i], (uint32_t)box * 16 * (kBK * 2));
+        if (rank == half)
+          ptx::tma_load_2d_multicast(sx, &tm_x.m[box - 1], &c.xfull[half][x.i], h.y * kBK, it.row0 + half * it.n0, 0x3);
         x.next<kXStages>();
       }
     }
@@ -382,10 +387,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       mbar_wait_ts(&c.xfull[half][x.i], x.ph);
       const int2 h = c.xhdr[half][x.i];
       if (h.x < 0) break;
-      if (half == 0 && lane == 0) PZ_TS(5, tm_);
+      if (lane == 0) PZ_TS(half ? 10 : 5, tm_);
       if (h.x != cur) {
         cur = h.x;
-        it = item_info(c, cur, n_pairs);
+        it = item_info(c, cur, n_pairs, rank, n_rb);
       }
       const int nh = half ? it.n1 : it.n0;
       if (h.y == 0) {
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
         ptx::tc_fence_after();
       }
       mbar_wait_ts(&c.afull[a.i], a.ph);
-      if (half == 0 && lane == 0) PZ_TS(6, tm_);
+      if (lane == 0) PZ_TS(half ? 11 : 6, tm_);
       ptx::tc_fence_after();
       if (nh > 0) {
         const uint32_t xs = smem_x + (uint32_t)(half * kXStages + x.i) * kXBytes;
@@ -404,12 +409,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
           ptx::mma_bf16_ts_elect(acc, ta + 8 * kk, ptx::smem_desc_sw128(xs + 32 * kk), idesc, (h.y | kk) != 0);
       }
       ptx::mma_commit_elect(&c.aempty[a.i]);  // A buffer free once these MMAs complete
-      ptx::mma_commit_elect(&c.xempty[half][x.i]);  // token slot likewise
+      ptx::mma_commit_multicast_elect(&c.xempty[half][x.i], 0x3);  // token slot: in both CTAs (multicast reload)
       if (h.y == nk - 1) {
         ptx::mma_commit_elect(&c.accfull[half]);
         accph ^= 1;
       }
-      if (half == 0 && lane == 0) PZ_TS(7, tm_);
+      if (lane == 0) PZ_TS(half ? 12 : 7, tm_);
       ++tm_;
       x.next<kXStages>();
       a.next<kAStages>();
@@ -431,12 +436,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
     int td = 0;
     (void)td;
     for (;;) {
+      if (warp == kW_DEC0 && lane == 0) PZ_TS(13, td);  // decoder reaches the stage
       mbar_wait_ts(&c.wfull[w.i], w.ph);
       const int2 h = c.whdr[w.i];
       if (h.x < 0) break;
       if (h.x != cur) {
         cur = h.x;
-        const Item it = item_info(c, cur, n_pairs);
+        const Item it = item_info(c, cur, n_pairs, rank, n_rb);
         mode = c.dense[it.b >> 1] ? 2 : (it.b & 1);  // 0 / 1: packed position, 2: dense slot (pos 0)
       }
       const uint32_t st = smem_w + (uint32_t)w.i * kWBytes;
@@ -447,29 +453,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       if (warp == kW_DEC0 && lane == 0) PZ_TS(2, td);
       if (lane == 0) mbar_arrive_ts(&c.wempty[w.i]);  // words in registers: the slot may refill
       w.next<kWStages>();
+      uint32_t dv[kKH][16];  // decoded while the A buffer may still be in use
+#pragma unroll
+      for (int i = 0; i < 4 * kKH; ++i) {
+        const uint32_t xs[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t xw = xs[j];
+          // |W^| * 2^48 (exponent field e' + 160 = e' | 0xA0, one LOP3); sign S and mask M of the
+          // position form +-2^-63 or +-0: one exact product leaves W^ * 2^-15 (rescaled in the
+          // epilogue); dense slots: the bf16 weight * 2^-15 to match
+          const uint32_t mag = (xw & 0x0FFF0FFFu) | orc;
+          dv[i >> 2][4 * (i & 3) + j] = mode == 2   ? bf16x2_mul(xw, 0x38003800u)
+                                        : mode == 0 ? bf16x2_mul(mag, xw & 0xA000A000u)
+                                                    : bf16x2_mul(mag, (xw * two) & 0xA000A000u);
+        }
+      }
       mbar_wait_ts(&c.aempty[a.i], a.ph ^ 1);  // the MMAs that read this A buffer completed
       if (warp == kW_DEC0 && lane == 0) PZ_TS(3, td);
       ptx::tc_fence_after();
 #pragma unroll
-      for (int k = 0; k < kKH; ++k) {  // one K half (32 k) at a time: 16 registers of decoded pairs
-        uint32_t dv[16];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t xs[4] = {v[4 * k + i].x, v[4 * k + i].y, v[4 * k + i].z, v[4 * k + i].w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t xw = xs[j];
-            // |W^| * 2^48 (exponent field e' + 160 = e' | 0xA0, one LOP3); sign S and mask M of the
-            // position form +-2^-63 or +-0: one exact product leaves W^ * 2^-15 (rescaled in the
-            // epilogue); dense slots: the bf16 weight * 2^-15 to match
-            const uint32_t mag = (xw & 0x0FFF0FFFu) | orc;
-            dv[4 * i + j] = mode == 2   ? bf16x2_mul(xw, 0x38003800u)
-                            : mode == 0 ? bf16x2_mul(mag, xw & 0xA000A000u)
-                                        : bf16x2_mul(mag, (xw * two) & 0xA000A000u);
-          }
-        }
-        ptx::tmem_st_32x32b_x16(lane_tmem + 32u * a.i + 16u * (kh0 + k), dv);
-      }
+      for (int k = 0; k < kKH; ++k) ptx::tmem_st_32x32b_x16(lane_tmem + 32u * a.i + 16u * (kh0 + k), dv[k]);
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
@@ -500,8 +504,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       if (lane == 0) mbar_arrive_ts(&c.iqempty[iq.i]);
       iq.next<kIq>();
       if (item < 0) break;
-      const Item it = item_info(c, item, n_pairs);
-      const int nh = half ? it.n1 : it.n0;
+      const Item it = item_info(c, item, n_pairs, rank, n_rb);
+      const int nh = it.ghost ? 0 : (half ? it.n1 : it.n0);  // a ghost drains nothing
       const int t0 = half * it.n0;  // first token of this half within the chunk
       mbar_wait_ts(&c.accfull[half], accph);
       accph ^= 1;
@@ -572,9 +576,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       ++te;
     }
   }
-  // every MMA completed (the epilogue waited for the last item) and every tcgen05.ld waited on
+  // every MMA completed (the epilogue waited for the last item) and every tcgen05.ld waited on;
+  // no CTA leaves while its peer may still multicast into it or commit to its barriers
   ptx::tc_fence_before();
   __syncthreads();
+  ptx::cluster_sync();
   if (warp == 3) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
@@ -589,10 +595,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
 bool ts_supported(int d, int f) { return d % kRows == 0 && f % kBK == 0 && d % kBK == 0; }
 
 // x_rows: [n_rows_cap][d] bf16 grouped by bucket; h: [n_rows_cap][f]; y: [n_rows_cap][d];
-// work_ctrs: 2 ints, zero on entry (item claim counters of the w13 and the w2 launch).
 int launch_ts_experts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_dense, int n_pairs, int d, int f,
                       const uint16_t* x_rows, const int32_t* bucket_off, int64_t n_rows_cap, uint16_t* h, float* y,
-                      int32_t* work_ctrs, cudaStream_t stream) {
+                      cudaStream_t stream) {
   if (!ts_supported(d, f)) return fail(PUZZLE_ERR_UNSUPPORTED, "prefill TS path needs d_model % 128 == 0 and d_ff % 64 == 0");
   if (n_pairs > kMaxBuckets / 2) return fail(PUZZLE_ERR_UNSUPPORTED, "n_pairs > 256");
   if (n_rows_cap == 0) return PUZZLE_OK;
@@ -605,20 +610,20 @@ int launch_ts_experts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pa
   if ((rc = make_tmap_3d(&tw13, w13, (int64_t)n_pairs * 2, f, d, f, kRows / 2, kBK, 2))) return rc;
   if ((rc = make_tmap_2d(&tw2, w2, (int64_t)n_pairs * d, f, kRows, kBK))) return rc;
   for (int i = 0; i < kXMaps; ++i) {
-    if ((rc = make_tmap_2d(&x13.m[i], x_rows, n_rows_cap, d, 32 * (i + 1), kBK))) return rc;
-    if ((rc = make_tmap_2d(&x2.m[i], h, n_rows_cap, f, 32 * (i + 1), kBK))) return rc;
+    if ((rc = make_tmap_2d(&x13.m[i], x_rows, n_rows_cap, d, 16 * (i + 1), kBK))) return rc;
+    if ((rc = make_tmap_2d(&x2.m[i], h, n_rows_cap, f, 16 * (i + 1), kBK))) return rc;
   }
-  const int grid = num_sms();
+  const int grid = num_sms() & ~1;  // clusters of 2 CTAs, one CTA per SM
   {
     ProfScope _ps("w13_ts", stream);
-    cudaError_t e = launch_pdl(k_ts_experts<true>, dim3(grid), dim3(kThreads), kSmemBytes, stream, tw13, x13, bucket_off, n_pairs, d, f, d, f / (kRows / 2), h, (float*)nullptr, work_ctrs, 1u,
+    cudaError_t e = launch_pdl_cluster2(k_ts_experts<true>, dim3(grid), dim3(kThreads), kSmemBytes, stream, tw13, x13, bucket_off, n_pairs, d, f, d, f / (kRows / 2), h, (float*)nullptr, 1u,
                                pair_dense);
     if (e != cudaSuccess) return cuda_check(e, "w13_ts launch");
   }
   if ((rc = cuda_check(cudaGetLastError(), "w13_ts launch"))) return rc;
   {
     ProfScope _ps("w2_ts", stream);
-    cudaError_t e = launch_pdl(k_ts_experts<false>, dim3(grid), dim3(kThreads), kSmemBytes, stream, tw2, x2, bucket_off, n_pairs, f, f, d, d / kRows, (uint16_t*)nullptr, y, work_ctrs + 1, 1u,
+    cudaError_t e = launch_pdl_cluster2(k_ts_experts<false>, dim3(grid), dim3(kThreads), kSmemBytes, stream, tw2, x2, bucket_off, n_pairs, f, f, d, d / kRows, (uint16_t*)nullptr, y, 1u,
                                pair_dense);
     if (e != cudaSuccess) return cuda_check(e, "w2_ts launch");
   }

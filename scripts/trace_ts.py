@@ -1,5 +1,5 @@
 """Pipeline timeline of the TS prefill kernel (PZ_TRACE build of gemm_ts.cu:
-python scripts/build_variant.py tstrace gemm_ts.cu -DPZ_TRACE=5; run with PUZZLE_LIB=...).
+python scripts/build_variant.py tstrace gemm_ts.cu -DPZ_TRACE=4; run with PUZZLE_LIB=...).
 CTA PZ_TRACE of the w13 kernel: per stage W TMA issue (0), X0 TMA issue (1), decoder words (2),
 decoder A free (3), decoder afull (4), MMA0 xfull (5), MMA0 afull (6), MMA0 issued (7); per
 item epilogue start (8) / end (9). All CTAs: start / end."""
@@ -57,3 +57,20 @@ ni = int((ev[9] > 0).sum())
 if ni:
     ep = (e[9, :ni] - e[8, :ni]) / 1e3
     print(f"items {ni}: epilogue median {np.median(ep):.2f} us, starts at " + " ".join(f"{(x - t0)/1e3:.1f}" for x in e[8, :ni]))
+# A-ring cycle (kAStages = 4): MMA(s) issued -> its completion frees A buffer s % 4, seen by the
+# decoder as "A free" of stage s + 4
+A = int(os.environ.get('TS_ASTAGES', 4))
+ss = np.arange(20, n - 8)
+def med(x):
+    return f"{np.median(x)/1e3:.3f}"
+print("A-ring cycle (us): issue(s)->Afree(s+4)", med(e[3, ss + A] - e[7, ss]),
+      "| Afree->afull(s+4)", med(e[4, ss + A] - e[3, ss + A]),
+      "| afull(s+4)->MMA sees", med(e[6, ss + A] - e[4, ss + A]),
+      "| MMA sees->issued(s+4)", med(e[7, ss + A] - e[6, ss + A]),
+      "| issued(s+4)-issued(s)", med(e[7, ss + A] - e[7, ss]))
+print("X-ring (3 slots) : issued(s)->X issue(s+3)", med(e[1, ss + 3] - e[7, ss]),
+      "| X issue->xfull seen(s+3)", med(e[5, ss + 3] - e[1, ss + 3]))
+print("W: decoder words(s)->W issue(s+4)", med(e[0, ss + 4] - e[2, ss]), "| W issue->words", med(e[2, ss] - e[0, ss]))
+print("decoder: reach(s)->words(s)", med(e[2, ss] - e[13, ss]), "(W wait) | W issue(s)->reach(s)", med(e[13, ss] - e[0, ss]),
+      "| Afree(s)-words(s)", med(e[3, ss] - e[2, ss]), "(A wait) | afull(s)->reach(s+1)", med(e[13, ss + 1] - e[4, ss]))
+print("MMA0: issued(s)->xfull(s+1)", med(e[5, ss + 1] - e[7, ss]), "| xfull->afull", med(e[6, ss] - e[5, ss]))
