@@ -746,10 +746,23 @@ def packer_rates(pz, layer, device):
     ms4 = timed_steps(lambda: pz.quant_unpack(codes, scales, 0), 5) / 5
     del deq
     qg = quant_gemv_rates(pz, w, planes, device)
+    # NEXT-1 fused merge + pack (Eq. 1-7): a Mixtral w1 slot, 4 pairs x [14336, 4096] bf16 experts
+    wi = (torch.randn(4, 14336, 4096, device=device) * 0.0156).to(torch.bfloat16)
+    wj = (torch.randn(4, 14336, 4096, device=device) * 0.0156).to(torch.bfloat16)
+    ni = 1 + torch.randn(4, 4096, device=device).abs()
+    nj = 1 + torch.randn(4, 4096, device=device).abs()
+    mo = pz.merge_experts_pack(wi, wj, ni, nj, 0.4)
+    torch.cuda.synchronize()
+    ms5 = timed_steps(lambda: pz.merge_experts_pack(wi, wj, ni, nj, 0.4, out=mo), 5) / 5
+    me = wi.numel()
+    del wi, wj, mo
+    pk = peaks()
     return {"quant_gemv": qg, "unpack_gbs": unpack_gbs, "unpack_elems": n, "pack_gbs": m * 10 / (ms2 / 1e3) / 1e9, "pack_elems": m,
+            "merge_gbs": me * 6 / (ms5 / 1e3) / 1e9, "merge_frac_hbm": me * 6 / (ms5 / 1e3) / 1e9 / pk["hbm_gbs"],
+            "merge_elems": me, "merge_ms": ms5,
             "quant_pack_gbs": m * (9 + 4 / 128) / (ms3 / 1e3) / 1e9,
             "quant_unpack_gbs": m * (3 + 4 / 128) / (ms4 / 1e3) / 1e9,
-            "note": "algorithmic bytes: unpack 4 B/elem, pack 10 B/elem, quant pack 9 B/elem (+ scales), "
+            "note": "algorithmic bytes: unpack 4 B/elem, pack 10 B/elem, merge+pack 6 B/elem (W_i, W_j in, word out; norms per column), quant pack 9 B/elem (+ scales), "
                     "quant unpack 3 B/elem (+ scales); quant timings include the output allocation"}
 
 

@@ -96,16 +96,19 @@ def test_route_outputs(pz, T):
 @pytest.mark.parametrize("name", ["qwen15", "deepseek"])
 @pytest.mark.parametrize("T", [1, 16, 64])
 def test_forward_full_size_fine_grained(pz, name, T):
+    """BASELINE config 4 decode at full size: EVERY token of the batch against the oracle
+    (all tokens for decode)."""
     cfg = synth.CONFIGS[name]
-    got, ref = _run(pz, cfg, T, pz.PATH_AUTO, sample=min(T, 16))
+    got, ref = _run(pz, cfg, T, pz.PATH_AUTO)
     assert_close(got, ref, f"{name} T={T}")
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("T", [1, 16, 64])
 def test_forward_full_size_mixtral(pz, T):
+    """BASELINE config 2 (the headline workload at T = 64): every token against the oracle."""
     cfg = synth.CONFIGS["mixtral"]
-    got, ref = _run(pz, cfg, T, pz.PATH_AUTO, sample=min(T, 6))
+    got, ref = _run(pz, cfg, T, pz.PATH_AUTO)
     assert_close(got, ref, f"mixtral T={T}")
 
 

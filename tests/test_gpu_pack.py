@@ -108,3 +108,36 @@ def test_merge_experts_pack_edge_values(pz):
                                     torch.from_numpy(w_j).cuda().to(torch.bfloat16),
                                     torch.from_numpy(n_i).cuda(), torch.from_numpy(n_j).cuda(), tau)
         assert np.array_equal(_u16(got), want), tau
+
+
+def test_merge_similarity_decision_near_tau(pz):
+    """Eq. 1-2 at the threshold (reading R17): for every bf16 b within a few percent of the
+    value that puts |a - b| / (a + b) exactly at tau, over many a, the GPU's similarity decision
+    (an approximate quotient with an exact fallback near tau) equals the oracle's correctly
+    rounded f32 division -- the packed words must be bit-identical. Also huge, subnormal-sum
+    and non-finite cases, where the fallback decides."""
+    a_bits = np.arange(0x3C00, 0x4400, 7, dtype=np.uint16)                 # a in ~[2^-7, 2^9)
+    a = (a_bits.astype(np.uint32) << 16).view(np.float32)
+    rows = []
+    for tau in (0.4, 0.6, 0.1, 1.0 / 3.0):
+        tau32 = np.float32(tau)
+        for av in a[:: max(1, len(a) // 96)]:
+            b0 = np.float32(av * (1 - tau32) / (1 + tau32))
+            b_bits = (b0.view(np.uint32) >> 16).astype(np.int64) + np.arange(-24, 24)
+            b = (b_bits.astype(np.uint32) << 16).view(np.float32)
+            rows.append((np.full_like(b, av), b, tau32))
+    extra_i = np.array([3.0e38, 1e-39, -1e-39, np.inf, 2.0 ** -126, 1.0], np.float32)
+    extra_j = np.array([3.0e38, 1e-39, 1e-39, 1.0, 2.0 ** -126, np.nan], np.float32)
+    for tau in (0.4, 0.6, 0.1, 1.0 / 3.0):
+        w_i = np.concatenate([r[0] for r in rows if r[2] == np.float32(tau)] + [extra_i])
+        w_j = np.concatenate([r[1] for r in rows if r[2] == np.float32(tau)] + [extra_j])
+        pad = (-len(w_i)) % 8
+        w_i = np.concatenate([w_i, np.ones(pad, np.float32)])[None, :]
+        w_j = np.concatenate([w_j, np.ones(pad, np.float32)])[None, :]
+        w_i, w_j = synth.to_bf16_values(w_i), synth.to_bf16_values(w_j)
+        n = np.ones(w_i.shape[1], np.float32)
+        want, _ = oracle.pack_artifacts(oracle.merge(w_i, w_j, n, n, float(np.float32(tau))))
+        got = pz.merge_experts_pack(torch.from_numpy(w_i).cuda().to(torch.bfloat16),
+                                    torch.from_numpy(w_j).cuda().to(torch.bfloat16),
+                                    torch.from_numpy(n).cuda(), torch.from_numpy(n).cuda(), float(np.float32(tau)))
+        assert np.array_equal(_u16(got), want), tau
