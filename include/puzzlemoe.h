@@ -54,7 +54,9 @@ typedef enum {
   PUZZLE_ERR_UNSUPPORTED = 3,      /* shape outside the kernels' tiling: d_model or d_ff not a multiple of 64,
                                       E > 512, misaligned pointer (16 B required for weights / activations) */
   PUZZLE_ERR_WORKSPACE = 4,        /* workspace NULL or smaller than puzzle_moe_workspace_size() */
-  PUZZLE_ERR_CUDA = 5              /* CUDA launch / device error (including: no device) */
+  PUZZLE_ERR_CUDA = 5,             /* CUDA launch / device error (including: no device) */
+  PUZZLE_ERR_NCCL = 6              /* NCCL not loadable or an NCCL call failed (the communicator is then
+                                      aborted: every later call on that puzzle_ep returns this code) */
 } puzzle_status;
 
 /* Human-readable name of a status code (static storage). */
@@ -433,6 +435,65 @@ int puzzle_moe_forward_calib(const puzzle_moe_layer* L, const uint16_t* hidden,
  * ------------------------------------------------------------------------------------- */
 int puzzle_profile_begin(void);
 int puzzle_profile_end(char* buf, size_t buflen);
+
+/* ---------------------------------------------------------------------------------------
+ * Expert parallelism behind the boundary (BASELINE.json config 5: "expert-
+ * parallel with NCCL all-to-all at 2/4/8 B200"; the deployment the paper reports is 2 GPUs -> 1,
+ * P:375). One process per GPU. The library owns an NCCL communicator, bootstrapped from a
+ * 128-byte ncclUniqueId that rank 0 creates (puzzle_ep_unique_id) and the caller broadcasts
+ * (e.g. torch.distributed.broadcast_object_list); NCCL itself is loaded at run time
+ * (libnccl.so.2, the copy PyTorch already loaded if any).
+ *
+ * Placement (puzzle_ep_partition): the unit is the merged PAIR, so both experts of a pair stay
+ * on one GPU and each packed tile is still read once. world <= n_pairs: rank r owns
+ * pairs [r*P/world, (r+1)*P/world). world > n_pairs (world % n_pairs == 0): every pair is split
+ * along d_ff into S = world / n_pairs slices, rank r holding slice r % S of pair r / S (SwiGLU is
+ * elementwise in d_ff, so each slice's down projection is an exact partial; the token's home
+ * rank sums the S partials with the gate). A d_ff slice of a packed tensor is a valid packed
+ * tensor (the decode is elementwise).
+ * ------------------------------------------------------------------------------------- */
+#define PUZZLE_EP_UNIQUE_ID_BYTES 128
+typedef struct puzzle_ep puzzle_ep;
+
+/* 128 bytes (ncclUniqueId) for puzzle_ep_create on every rank; call on rank 0 only. */
+int puzzle_ep_unique_id(void* id_out);
+
+/* Collective over the `world` ranks (every rank calls it with the same id): communicator of rank
+ * `rank` on CUDA device `device`. *ep_out = NULL on failure. Errors: INVALID_ARGUMENT, CUDA (no
+ * such device), NCCL. */
+int puzzle_ep_create(puzzle_ep** ep_out, int world, int rank, const void* unique_id, int device);
+/* Destroys the communicator (NULL is a no-op). */
+int puzzle_ep_destroy(puzzle_ep* ep);
+
+/* The placement: dest_pairs HOST int32 [world][2] (rank q owns global pairs [dest_pairs[2q],
+ * dest_pairs[2q+1])) and *slices = S (1, or world / n_pairs). Either output may be NULL. */
+int puzzle_ep_partition(int world, int n_pairs, int32_t* dest_pairs, int* slices);
+
+/* Device workspace bytes of puzzle_moe_forward_ep (0: invalid arguments). */
+size_t puzzle_moe_forward_ep_workspace_size(const puzzle_ep* ep, const puzzle_moe_layer* route_layer,
+                                            const puzzle_moe_layer* local_shard, int64_t cap_tokens, int top_k);
+
+/* puzzle_moe_forward_ep -- the MoE layer (a3)-(a6) expert-parallel over the communicator's ranks,
+ *   with fixed-capacity dispatch: every rank reserves cap = cap_tokens*top_k rows (+1 header row
+ *   carrying the bucket counts) per destination, so both all-to-alls have equal, host-known splits
+ *   and the whole layer runs on the device without host synchronisation (CUDA-graph capturable).
+ *   route_layer  GLOBAL routing metadata: n_experts, n_pairs, d_model, d_ff, expert_slot (device)
+ *                of the whole layer (its weight pointers are not read; they must be non-NULL)
+ *   local_shard  this rank's packed pairs per puzzle_ep_partition (n_pairs = its pair count,
+ *                d_ff = route_layer->d_ff / S; pair_dense as in puzzle_moe_forward)
+ *   hidden, router_logits, residual, out, top_k, renormalize: this rank's T tokens, as in
+ *                puzzle_moe_forward; T <= cap_tokens; cap_tokens must be the same on all ranks;
+ *                a rank with T = 0 (NULL activations allowed) still takes part in both all-to-alls
+ *   path         kernel path of the local experts (AUTO picks by the capacity world*cap)
+ * Steps: puzzle_moe_route -> puzzle_ep_dispatch -> NCCL all-to-all (grouped ncclSend/ncclRecv on
+ * `stream`) -> puzzle_ep_recv_plan -> puzzle_gather_rows -> puzzle_moe_experts -> gather back
+ * -> NCCL all-to-all -> puzzle_ep_home_index -> puzzle_moe_combine. Every rank must call it for
+ * every layer (collective). Errors: as the building blocks; SHAPE_MISMATCH for a local shard
+ * that does not match the partition; WORKSPACE; NCCL. */
+int puzzle_moe_forward_ep(puzzle_ep* ep, const puzzle_moe_layer* route_layer, const puzzle_moe_layer* local_shard,
+                          const uint16_t* hidden, const float* router_logits, int64_t T, int64_t cap_tokens,
+                          int top_k, int renormalize, const uint16_t* residual, uint16_t* out, void* workspace,
+                          size_t workspace_bytes, int path, puzzle_stream_t stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

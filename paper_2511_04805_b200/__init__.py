@@ -23,6 +23,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PUZZLE_LIB") or os.path.join(_HERE, "libpuzzlemoe.so")
 
 PUZZLE_OK = 0
+PUZZLE_ERR_NCCL = 6
+EP_UNIQUE_ID_BYTES = 128
 PATH_AUTO, PATH_GEMV, PATH_TC, PATH_TS = 0, 1, 2, 3
 
 EXPORTED_SYMBOLS = (
@@ -35,6 +37,8 @@ EXPORTED_SYMBOLS = (
     "puzzle_quant_pack", "puzzle_quant_unpack", "puzzle_quant_gemv", "puzzle_ep_dispatch", "puzzle_ep_recv_plan",
     "puzzle_ep_home_index", "puzzle_ep_peer_buffer_size", "puzzle_ep_dispatch_peer", "puzzle_ep_wait_dispatch",
     "puzzle_ep_return_peer", "puzzle_ep_home_index_peer", "puzzle_ep_recv_plan_peer", "puzzle_ep_combine_peer",
+    "puzzle_ep_unique_id", "puzzle_ep_create", "puzzle_ep_destroy", "puzzle_ep_partition",
+    "puzzle_moe_forward_ep_workspace_size", "puzzle_moe_forward_ep",
 )
 
 
@@ -104,6 +108,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_ep_combine_peer": ([P, P, P, I, P, I, I64, I64, I, I, P, P, P, P, P], I),
             "puzzle_ep_return_peer": ([P, P, I, I, I, I64, I, P, P, P], I),
             "puzzle_ep_home_index_peer": ([P, P, P, I, P, I, I64, I64, I, I, P, P, P, P, P], I),
+            "puzzle_ep_unique_id": ([P], I),
+            "puzzle_ep_create": ([ctypes.POINTER(ctypes.c_void_p), I, I, P, I], I),
+            "puzzle_ep_destroy": ([P], I),
+            "puzzle_ep_partition": ([I, I, P, P], I),
+            "puzzle_moe_forward_ep_workspace_size": ([P, P, P, I64, I], SZ),
+            "puzzle_moe_forward_ep": ([P, P, P, P, P, I64, I64, I, I, P, P, P, SZ, I, P], I),
             "puzzle_profile_begin": ([], I),
             "puzzle_profile_end": ([ctypes.c_char_p, SZ], I),
         }
@@ -526,3 +536,70 @@ def quant_gemv(codes, scales, x_i, x_j, stream=None):
     _check(load_library().puzzle_quant_gemv(_p(codes), _p(scales), rows, cols, _p(x_i), x_i.shape[0], _p(x_j),
                                             x_j.shape[0], _p(y_i), _p(y_j), _stream(stream)), "puzzle_quant_gemv")
     return y_i, y_j
+
+
+# ---- expert parallelism behind the C ABI (puzzle_ep_*, puzzle_moe_forward_ep) ----
+def ep_unique_id() -> bytes:
+    """puzzle_ep_unique_id: the 128-byte NCCL bootstrap id (rank 0; broadcast it to the others)."""
+    buf = ctypes.create_string_buffer(EP_UNIQUE_ID_BYTES)
+    _check(load_library().puzzle_ep_unique_id(buf), "puzzle_ep_unique_id")
+    return buf.raw
+
+
+def ep_partition(world: int, n_pairs: int):
+    """puzzle_ep_partition -> (dest_pairs int32 [world][2] numpy, slices)."""
+    import numpy as np
+    dest = np.zeros((world, 2), np.int32)
+    slices = ctypes.c_int(0)
+    _check(load_library().puzzle_ep_partition(int(world), int(n_pairs), dest.ctypes.data_as(ctypes.c_void_p),
+                                              ctypes.byref(slices)), "puzzle_ep_partition")
+    return dest, int(slices.value)
+
+
+class EpComm:
+    """A C-owned NCCL communicator (puzzle_ep_create / puzzle_ep_destroy) and the expert-parallel
+    layer over it (puzzle_moe_forward_ep). Collective: every rank constructs it with the same
+    unique id (from ep_unique_id() on rank 0, broadcast by the caller)."""
+
+    def __init__(self, world: int, rank: int, unique_id: bytes, device: int):
+        assert len(unique_id) == EP_UNIQUE_ID_BYTES
+        self.world, self.rank, self.device = world, rank, device
+        h = ctypes.c_void_p(None)
+        _check(load_library().puzzle_ep_create(ctypes.byref(h), int(world), int(rank), unique_id, int(device)),
+               "puzzle_ep_create")
+        self.handle = h
+        self._ws = None
+
+    def close(self):
+        if self.handle:
+            _check(load_library().puzzle_ep_destroy(self.handle), "puzzle_ep_destroy")
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def workspace(self, route_layer, local_layer, cap_tokens: int, top_k: int) -> torch.Tensor:
+        need = int(load_library().puzzle_moe_forward_ep_workspace_size(
+            self.handle, ctypes.byref(route_layer.desc), ctypes.byref(local_layer.desc), int(cap_tokens), int(top_k)))
+        if need == 0:
+            raise PuzzleError(1, "puzzle_moe_forward_ep_workspace_size", "invalid arguments")
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        return self._ws
+
+    def forward(self, route_layer, local_layer, hidden, router_logits, top_k: int, renormalize: bool,
+                cap_tokens: int | None = None, residual=None, out=None, path: int = PATH_AUTO, workspace=None,
+                stream=None) -> torch.Tensor:
+        """puzzle_moe_forward_ep: this rank's tokens through the expert-parallel layer."""
+        T = hidden.shape[0]
+        cap_tokens = T if cap_tokens is None else int(cap_tokens)
+        out = torch.empty_like(hidden) if out is None else out
+        ws = self.workspace(route_layer, local_layer, cap_tokens, top_k) if workspace is None else workspace
+        _check(load_library().puzzle_moe_forward_ep(
+            self.handle, ctypes.byref(route_layer.desc), ctypes.byref(local_layer.desc), _p(hidden),
+            _p(router_logits), T, cap_tokens, int(top_k), int(bool(renormalize)), _p(residual), _p(out), _p(ws),
+            ws.numel(), int(path), _stream(stream)), "puzzle_moe_forward_ep")
+        return out

@@ -21,8 +21,18 @@ LIB = os.path.join(PKG, "libpuzzlemoe.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_include() -> list[str]:
+    """The NCCL 2.x header (ep_comm.cu loads libnccl at run time; only the header is needed at
+    build time): the one matching PyTorch's bundled NCCL if present, else the system one."""
+    import sysconfig
+    for d in (os.path.join(sysconfig.get_paths()["purelib"], "nvidia", "nccl", "include"), "/usr/include"):
+        if os.path.exists(os.path.join(d, "nccl.h")):
+            return ["-I", d]
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel or /usr/include)")
+
+
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-                "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+                "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), *_nccl_include()]
 
 
 def _sources():

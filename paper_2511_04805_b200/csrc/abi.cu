@@ -264,6 +264,7 @@ const char* puzzle_status_string(int status) {
     case PUZZLE_ERR_UNSUPPORTED: return "PUZZLE_ERR_UNSUPPORTED";
     case PUZZLE_ERR_WORKSPACE: return "PUZZLE_ERR_WORKSPACE";
     case PUZZLE_ERR_CUDA: return "PUZZLE_ERR_CUDA";
+    case PUZZLE_ERR_NCCL: return "PUZZLE_ERR_NCCL";
     default: return "PUZZLE_ERR_UNKNOWN";
   }
 }

@@ -102,3 +102,27 @@ def test_next_row_argument_errors_are_synchronous(lib):
     # both statistics outputs NULL
     assert lib.puzzle_moe_forward_calib(ctypes.byref(desc), None, None, 1, 2, 1, None, None, None, None, None, 0, 0,
                                         None) == 1
+
+
+def test_ep_capi_host_side(lib):
+    """Expert parallelism behind the C ABI: the placement (puzzle_ep_partition) equals the
+    Python partition the gloo tests exercise; the NCCL bootstrap id is 128 bytes; argument
+    errors are synchronous; without a device the communicator is refused loudly."""
+    import paper_2511_04805_b200 as pz
+    from paper_2511_04805_b200.ep import Partition
+    for P, G in [(4, 1), (4, 2), (4, 3), (4, 8), (30, 8), (32, 4), (2, 4), (1, 2), (60, 7)]:
+        dest, S = pz.ep_partition(G, P)
+        part = Partition(P, G)
+        assert S == part.slices
+        assert dest.tolist() == [list(part.pairs_of(q)) for q in range(G)]
+    assert lib.puzzle_ep_partition(8, 3, None, None) == 3            # world > P, world % P != 0
+    assert lib.puzzle_ep_partition(0, 4, None, None) == 1
+    assert len(pz.ep_unique_id()) == pz.EP_UNIQUE_ID_BYTES
+    assert lib.puzzle_moe_forward_ep(None, None, None, None, None, 1, 1, 1, 1, None, None, None, 0, 0, None) == 1
+    assert b"handle" in lib.puzzle_last_error()
+    assert lib.puzzle_ep_destroy(None) == 0
+    assert lib.puzzle_status_string(6) == b"PUZZLE_ERR_NCCL"
+    if not torch.cuda.is_available():
+        h = ctypes.c_void_p(None)
+        assert lib.puzzle_ep_create(ctypes.byref(h), 2, 0, b"\0" * 128, 0) == 5
+        assert not h.value

@@ -401,3 +401,87 @@ def test_ep_peer_world1_symmetric_memory_graph(nccl_group):
         assert_close(out.float().cpu().numpy(), oracle.moe_forward(w13, w2, slot, hb, lb, cfg.top_k, cfg.renormalize),
                      f"peer world 1 replay {seed}")
     assert pb.wait_timeouts() == 0 and int(pb.state[0].item()) == 3
+
+
+# ---- the same layer behind the C ABI: a C-owned NCCL communicator (puzzle_moe_forward_ep) ----
+
+@pytest.fixture(scope="module")
+def ep_comm():
+    import paper_2511_04805_b200 as pz
+    comm = pz.EpComm(1, 0, pz.ep_unique_id(), 0)
+    yield comm
+    comm.close()
+
+
+@pytest.mark.parametrize("cfg", [synth.MoEConfig("ep_small", 30, 256, 512, 8, 2, True),
+                                 synth.MoEConfig("ep_fine", 31, 128, 256, 16, 4, False)], ids=lambda c: c.name)
+@pytest.mark.parametrize("T,path", [(37, 0), (64, 1), (5, 1), (200, 0), (0, 0)])
+def test_ep_capi_world1_matches_oracle_and_python_form(nccl_group, ep_comm, cfg, T, path):
+    """puzzle_moe_forward_ep on a 1-rank communicator: equal to the oracle under the tolerance
+    and bit-identical to the torch.distributed fixed-capacity form (same kernels, same order)."""
+    ep, (w13, w2, slot, _) = _ep_world1(cfg)
+    hb = synth.hidden_bits(cfg, T, seed=7)
+    lg = synth.router_logits(cfg, T, seed=8)
+    rb = synth.hidden_bits(cfg, T, seed=9)
+    h = torch.from_numpy(hb.view(np.int16)).cuda().view(torch.bfloat16)
+    r = torch.from_numpy(rb.view(np.int16)).cuda().view(torch.bfloat16)
+    l = torch.from_numpy(lg).cuda()
+    cap = T + 3
+    out = ep_comm.forward(ep.route_layer, ep.local_layer, h, l, cfg.top_k, cfg.renormalize, cap_tokens=cap,
+                          residual=r, path=path)
+    if T == 0:
+        return
+    py = ep.forward_fixed(h, l, cfg.top_k, cfg.renormalize, residual=r, cap_tokens=cap, path=path)
+    torch.cuda.synchronize()
+    ref = oracle.moe_forward(w13, w2, slot, hb, lg, cfg.top_k, cfg.renormalize, rb)
+    assert_close(out.float().cpu().numpy(), ref, "C-ABI ep vs oracle")
+    assert torch.equal(out.view(torch.int16), py.view(torch.int16))
+
+
+def test_ep_capi_dense_slots_and_graph_capture(nccl_group, ep_comm):
+    """25 % layout through the C-ABI layer, captured into a CUDA graph (NCCL inside) and
+    replayed on new inputs."""
+    cfg = synth.MoEConfig("ep25_capi", 33, 256, 512, 8, 2, True)
+    ep, (w13, w2, slot, dense) = _ep_world1(cfg, n_merged=2)
+    T = 24
+    h = torch.empty((T, cfg.d_model), dtype=torch.bfloat16, device="cuda")
+    lg = torch.empty((T, cfg.n_experts), dtype=torch.float32, device="cuda")
+
+    def load(seed):
+        hb = synth.hidden_bits(cfg, T, seed=seed)
+        lb = synth.router_logits(cfg, T, seed=seed + 1)
+        h.copy_(torch.from_numpy(hb.view(np.int16)).view(torch.bfloat16))
+        lg.copy_(torch.from_numpy(lb))
+        return hb, lb
+
+    load(60)
+    out = torch.empty_like(h)
+    ws = ep_comm.workspace(ep.route_layer, ep.local_layer, T, cfg.top_k)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ep_comm.forward(ep.route_layer, ep.local_layer, h, lg, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ep_comm.forward(ep.route_layer, ep.local_layer, h, lg, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+    hb, lb = load(70)
+    g.replay()
+    torch.cuda.synchronize()
+    ref = oracle.moe_forward(w13, w2, slot, hb, lb, cfg.top_k, cfg.renormalize, pair_dense=dense)
+    assert_close(out.float().cpu().numpy(), ref, "graph-replayed C-ABI ep (dense slots) vs oracle")
+
+
+def test_ep_capi_rejects_mismatched_shard(nccl_group, ep_comm):
+    import paper_2511_04805_b200 as pz
+    cfg = synth.MoEConfig("ep_small", 30, 256, 512, 8, 2, True)
+    ep, _ = _ep_world1(cfg)
+    wrong = pz.PackedMoELayer(ep.local_layer.w13[:1].contiguous(), ep.local_layer.w2[:1].contiguous(),
+                              torch.arange(2, dtype=torch.int32, device="cuda"))
+    h = torch.zeros((4, cfg.d_model), dtype=torch.bfloat16, device="cuda")
+    l = torch.zeros((4, cfg.n_experts), dtype=torch.float32, device="cuda")
+    ws = torch.empty(1 << 26, dtype=torch.uint8, device="cuda")
+    with pytest.raises(pz.PuzzleError) as e:
+        ep_comm.forward(ep.route_layer, wrong, h, l, cfg.top_k, cfg.renormalize, workspace=ws)
+    assert e.value.status == 2
