@@ -174,6 +174,7 @@ struct Plan {
 // Decode shapes (<= 64 tokens) stream each touched pair once through the decode-shape kernels
 // (gemv_tc.cu); larger token counts are tensor-bound and go to the tcgen05 grouped GEMM.
 constexpr int64_t kGemvMaxTokens = 64;
+constexpr int64_t kGemvMaxTokensPerExpert = 64;
 
 struct Layout {
   size_t topk_idx, topk_gate, bucket_off, assign_token, assign_of, active, n_active, cnt13, cnt2, h, y, part,
@@ -186,13 +187,16 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   p.k = k;
   p.n_assign = T * k;
   p.max_active = (int)std::min<int64_t>(L->n_pairs, p.n_assign);
-  // token-heavy batches: the decode-into-TMEM prefill kernel (gemm_ts.cu; ahead of or level with
-  // the shared-memory-operand kernel on every config, profiles/r02/prefill_ab.txt), else gemm_tc.cu
+  // The decode-shape kernels stream each touched pair once per pass of 32 tokens per position:
+  // they win while an expert averages <= 64 tokens (<= 2 passes; measured crossover: Mixtral
+  // T 256 / 512, Qwen1.5 T 512 / 1024, DeepSeek T 512 / 1024, profiles/r02/crossover.txt).
+  // Heavier batches: the decode-into-TMEM prefill kernel (gemm_ts.cu; ahead of or level with the
+  // shared-memory-operand kernel on every config), else gemm_tc.cu.
   if (path == PUZZLE_PATH_AUTO)
-    path = T <= kGemvMaxTokens                  ? PUZZLE_PATH_GEMV
-           : ts_supported(L->d_model, L->d_ff) ? PUZZLE_PATH_TS
-           : tc_supported(L->d_model, L->d_ff) ? PUZZLE_PATH_TC
-                                                : PUZZLE_PATH_GEMV;
+    path = (T <= kGemvMaxTokens || T * k <= kGemvMaxTokensPerExpert * (int64_t)L->n_experts) ? PUZZLE_PATH_GEMV
+           : ts_supported(L->d_model, L->d_ff)                                                ? PUZZLE_PATH_TS
+           : tc_supported(L->d_model, L->d_ff)                                                ? PUZZLE_PATH_TC
+                                                                                              : PUZZLE_PATH_GEMV;
   p.path = path;
   return p;
 }
