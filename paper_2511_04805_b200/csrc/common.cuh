@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include <atomic>
@@ -24,6 +25,24 @@ int cuda_check(cudaError_t e, const char* what);
 int num_sms();
 
 constexpr int kMaxExperts = 512;
+
+// Checked builds (-DPZ_CHECKED, scripts/build_variant.py): device-side invariant checks at the
+// index computations of every kernel (a violated check prints and traps). The substitute for
+// compute-sanitizer, which the GPU pool refuses (profiles/r02/sanitizer_refused.log).
+#ifdef PZ_CHECKED
+#define PZ_DCHECK(cond)                                                                        \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("PZ_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x, #cond);                                                         \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define PZ_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 // The current device (attributes and SM counts below are per device: a process may drive
 // several GPUs, one per thread or one after the other).

@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(1024) k_ep_recv_plan(const uint16_t* __restric
     if (ps[m] <= wi) a = m; else z = m;
   }
   const int32_t l = loff[a] + pre_b[s * lb + a] + (wi - ps[a]);
+  PZ_DCHECK(l >= 0 && l < (int64_t)world * cap && a >= 0 && a < lb);
   return_idx[r] = l;
   gather_idx[l] = (int32_t)r;
 }

@@ -136,6 +136,7 @@ struct Item {
 // work on a band of row blocks of ONE pair, whose packed tiles and token rows are re-read from
 // L2. A cluster item is two adjacent row blocks of one token chunk: CTA `rank` takes 2 rbp + rank.
 __device__ __forceinline__ Item item_info(const Ctl& c, int item, int n_pairs, int rank, int n_rb) {
+  PZ_DCHECK(item >= 0 && item < c.n_items);
   int lo = 0, hi = n_pairs - 1;  // last pair with pair_off[p] <= item
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -157,6 +158,8 @@ __device__ __forceinline__ Item item_info(const Ctl& c, int item, int n_pairs, i
   const int n = (it.nvalid + 31) & ~31;  // MMA width: the live tokens rounded up to 32
   it.n0 = n >> 1;
   it.n1 = n >> 1;
+  PZ_DCHECK(p >= 0 && p < n_pairs && it.b < 2 * n_pairs && it.nvalid >= 1 && it.row0 >= c.off[it.b] &&
+            it.row0 + it.nvalid <= c.off[it.b + 1] && n <= kNmax && it.rb < n_rb + 1);
   return it;
 }
 

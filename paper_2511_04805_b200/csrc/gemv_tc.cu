@@ -219,6 +219,7 @@ __device__ __forceinline__ void locate(const Ctl<WST, XST>& c, int n_active, int
     if (c.s_item[mid] <= item) lo = mid; else hi = mid - 1;
   }
   p = c.s_active[lo];
+  PZ_DCHECK(lo >= 0 && lo < n_active && p >= 0 && item >= c.s_item[lo]);
   pt = load_pair(c.s_off, p);
   const int np = npass_of(pt, nx), rem = item - c.s_item[lo];
   rb = rem / np;
@@ -567,6 +568,8 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       const int offp = (pos ? s.pt.off1 : s.pt.off0) + s.base;  // first assignment of this warp
       float* slot = part + (size_t)(2 * g + (s.item == first_item ? 0 : 1)) * kSlot;
       const uint32_t acc_t = lane_tmem + kAccCol + (uint32_t)NX * pos;
+      PZ_DCHECK(np >= 0 && np <= NX && offp >= 0 && (np == 0 || offp + np <= c.s_off[2 * n_bucket_pairs]));
+      PZ_DCHECK(s.item < n_rb * (n_bucket_pairs + c.s_off[2 * n_bucket_pairs] / 32 + 1));
       // the A operand is W^ * 2^-15 (PZ_TC_ORMAG; dense slots scaled to match): scale back, exact
       constexpr float acc_scale = PZ_TC_ORMAG ? 32768.0f : 1.0f;
       for (int c0 = 0; c0 < np; c0 += 16) {
@@ -585,6 +588,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           // up lanes tokens c0+8..c0+15
           const bool up = lane >= 16;
           const int feat = s.rb * (kRows / 2) + 16 * q + (lane & 15);  // d_ff index of this row
+          PZ_DCHECK(feat < f);
           float o[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] = __shfl_xor_sync(0xffffffffu, __uint_as_float(r[i]), 16);

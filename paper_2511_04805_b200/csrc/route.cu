@@ -162,7 +162,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_route_small(
   __syncthreads();
   const int n_assign = T * k;
   for (int i = threadIdx.x; i < n_assign; i += blockDim.x) {
+    PZ_DCHECK(s_bucket[i] >= 0 && s_bucket[i] < n_buckets);
     const int a = atomicAdd(&s_off[s_bucket[i]], 1);
+    PZ_DCHECK(a >= 0 && a < n_assign);
     assign_token[a] = i / k;
     assign_of[i] = a;
   }
@@ -255,6 +257,7 @@ __global__ void __launch_bounds__(kBigThreads) k_route_scatter(
   __syncthreads();
   if ((int)threadIdx.x < n) {
     const int a = s_base[my_b] + my_local;
+    PZ_DCHECK(my_b >= 0 && my_b < n_buckets && a >= 0);
     assign_token[a] = (int32_t)((i0 + threadIdx.x) / k);
     assign_of[i0 + threadIdx.x] = a;
     s_slotof[threadIdx.x] = a;
@@ -355,6 +358,7 @@ __global__ void __launch_bounds__(kDecThreads) k_route_dec_scatter(
     const int t = i / k, c = t / kDecTokensPerCta;
     const int bp = bpos[i], b = bp & 0xFFFF;
     const int a = s_off[b] + s_pre[c * n_buckets + b] + (bp >> 16);
+    PZ_DCHECK(b < n_buckets && a >= 0 && a < n_assign);
     if (lane == 0) {
       assign_token[a] = t;
       assign_of[i] = a;
