@@ -773,6 +773,10 @@ def run_ours(args):
         if not args.no_extra and not dist_on:  # single-GPU extras (the N = 1 run carries them)
             line["aux"]["host_call"] = host_call_cost(layer, cfg, hidden, logits, out, ws)
             try:
+                line["aux"]["quant_forward"] = quant_forward_rates(pz, device, pk)
+            except Exception as e:  # pragma: no cover
+                line["aux"]["quant_forward"] = {"error": repr(e)}
+            try:
                 ub = unpacked_baseline(pz, layer, cfg, hidden, logits, min(K, 50), W)
                 for arm in ("same_kernels", "cublas"):
                     ub[arm]["packed_speedup"] = ub[arm]["ms_per_step"] / ms
@@ -813,6 +817,54 @@ def ncu_traffic(cfg_name: str, T: int, kernel: str):
     with open(path) as fh:
         tab = json.load(fh)
     return tab.get(f"{cfg_name}/T{T}/{kernel}")
+
+
+def quant_forward_rates(pz, device, pk, cases=(("mixtral", 64), ("mixtral", 1), ("qwen15", 64), ("deepseek", 64))):
+    """NEXT-3: puzzle_moe_forward_quant (the quantised weight class through the decode-shape
+    tcgen05 kernels) on full-size layers with seeded random code bytes (flags + 3-bit codes, bit 3
+    zero) and group scales (timing is data-independent; parity: tests/test_gpu_quant_forward.py).
+    Algorithmic bytes = the touched pairs' code bytes + scales (8.25 bits per merged element)."""
+    import torch
+    res = []
+    g = torch.Generator(device=device)
+    g.manual_seed(2511)
+    for name, T in cases:
+        cfg = synth.CONFIGS[name]
+        P, d, f = cfg.n_pairs, cfg.d_model, cfg.d_ff
+        rnd = lambda *shape: (torch.randint(0, 256, shape, generator=g, device=device, dtype=torch.int32) & 0xF7).to(torch.uint8)
+        c13, c2 = rnd(P, 2, f, d), rnd(P, d, f)
+        s13 = torch.rand((P, 2, f, d // 128), generator=g, device=device) * 0.01 + 1e-3
+        s2 = torch.rand((P, d, f // 128), generator=g, device=device) * 0.01 + 1e-3
+        _, slot = synth.pairing(cfg)
+        layer = pz.QuantMoELayer(c13, s13, c2, s2, torch.from_numpy(slot).to(device))
+        hidden, logits = make_inputs(cfg, T, synth.seeds(cfg)["activations"], device)
+        out = torch.empty_like(hidden)
+        ws = layer.workspace(T, cfg.top_k)
+        fwd = lambda: layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, out=out, workspace=ws)
+        fwd()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fwd()
+        for _ in range(5):
+            gr.replay()
+        torch.cuda.synchronize()
+        K = 50
+        ms = timed_steps(gr.replay, K) / K
+        with pz.profile_window() as prof:
+            timed_steps(fwd, 20)
+        kern = {k: round(t / n * 1e3, 2) for k, (n, t) in prof.kernels.items()}
+        top = torch.topk(logits, cfg.top_k, dim=-1).indices.reshape(-1).cpu().numpy()
+        nt = len(set(int(slot[e]) // 2 for e in top))
+        per_pair = 3 * d * f + (2 * f * d // 128 + d * f // 128) * 4
+        gbs = nt * per_pair / (ms / 1e3) / 1e9
+        res.append({"config": name, "batch": T, "ms_per_step": ms, "tokens_per_s": T / (ms / 1e3),
+                    "touched_pairs": nt, "quant_bytes_per_pair": per_pair, "weight_gbs": gbs,
+                    "frac_hbm": gbs / pk["hbm_gbs"], "kernel_avg_us": kern,
+                    "bits_per_merged_element": 8 + 32 / 128})
+        del layer, c13, c2, s13, s2
+        torch.cuda.empty_cache()
+    return res
 
 
 def host_call_cost(layer, cfg, hidden, logits, out, ws, n: int = 50):

@@ -438,6 +438,32 @@ int puzzle_profile_begin(void);
 int puzzle_profile_end(char* buf, size_t buflen);
 
 /* ---------------------------------------------------------------------------------------
+ * NEXT-3: the quantised PuzzleMoE weight class (App. A.3; R21-R23) in the
+ * forward. Each projection of each merged pair is puzzle_quant_pack's output: one byte per
+ * merged element (S_i S_j M_i M_j 0 c2 c1 c0) and an f32 scale per group of 128 consecutive
+ * columns of a row. The decode-shape kernels stream the code bytes of every touched pair ONCE
+ * for both experts and decode them on the fly into the tcgen05 A operand:
+ *   W^_pos = (-1)^S_pos * M_pos * bf16_rne(f32(code * scale))   (R23; masked entries +0)
+ * -- then SwiGLU, the down projection and the combine exactly as puzzle_moe_forward. Every T is
+ * accepted (passes of 32 tokens per position: the format is for decode-shape batches).
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_experts, n_pairs, d_model, d_ff;   /* d_model, d_ff multiples of 128 */
+  const uint8_t* w13_codes;   /* [n_pairs][2][d_ff][d_model] (gate rows, then up rows), 16-byte aligned */
+  const float* w13_scales;    /* [n_pairs][2][d_ff][d_model / 128] */
+  const uint8_t* w2_codes;    /* [n_pairs][d_model][d_ff], 16-byte aligned */
+  const float* w2_scales;     /* [n_pairs][d_model][d_ff / 128] */
+  const int32_t* expert_slot; /* [n_experts] = 2*pair + pos (device) */
+} puzzle_moe_quant_layer;
+
+size_t puzzle_moe_quant_workspace_size(const puzzle_moe_quant_layer* Q, int64_t max_tokens, int top_k);
+/* Arguments, errors and outputs as puzzle_moe_forward (UNSUPPORTED: d_model or d_ff not a
+ * multiple of 128, scales not 4-byte aligned). */
+int puzzle_moe_forward_quant(const puzzle_moe_quant_layer* Q, const uint16_t* hidden, const float* router_logits,
+                             int64_t T, int top_k, int renormalize, const uint16_t* residual, uint16_t* out,
+                             void* workspace, size_t workspace_bytes, puzzle_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
  * Expert parallelism behind the boundary (BASELINE.json config 5: "expert-
  * parallel with NCCL all-to-all at 2/4/8 B200"; the deployment the paper reports is 2 GPUs -> 1,
  * P:375). One process per GPU. The library owns an NCCL communicator, bootstrapped from a

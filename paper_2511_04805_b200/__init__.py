@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "puzzle_ep_return_peer", "puzzle_ep_home_index_peer", "puzzle_ep_recv_plan_peer", "puzzle_ep_combine_peer",
     "puzzle_ep_unique_id", "puzzle_ep_create", "puzzle_ep_destroy", "puzzle_ep_partition",
     "puzzle_moe_forward_ep_workspace_size", "puzzle_moe_forward_ep",
+    "puzzle_moe_quant_workspace_size", "puzzle_moe_forward_quant",
 )
 
 
@@ -114,6 +115,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "puzzle_ep_partition": ([I, I, P, P], I),
             "puzzle_moe_forward_ep_workspace_size": ([P, P, P, I64, I], SZ),
             "puzzle_moe_forward_ep": ([P, P, P, P, P, I64, I64, I, I, P, P, P, SZ, I, P], I),
+            "puzzle_moe_quant_workspace_size": ([P, I64, I], SZ),
+            "puzzle_moe_forward_quant": ([P, P, P, I64, I, I, P, P, P, SZ, P], I),
             "puzzle_profile_begin": ([], I),
             "puzzle_profile_end": ([ctypes.c_char_p, SZ], I),
         }
@@ -275,6 +278,53 @@ class PackedMoELayer:
                                                  _p(y_rows), _p(workspace), workspace.numel(), int(path),
                                                  _stream(stream)), "puzzle_moe_experts")
         return y_rows
+
+
+class QuantLayerDesc(ctypes.Structure):
+    """puzzle_moe_quant_layer."""
+    _fields_ = [("n_experts", ctypes.c_int32), ("n_pairs", ctypes.c_int32), ("d_model", ctypes.c_int32),
+                ("d_ff", ctypes.c_int32), ("w13_codes", ctypes.c_void_p), ("w13_scales", ctypes.c_void_p),
+                ("w2_codes", ctypes.c_void_p), ("w2_scales", ctypes.c_void_p), ("expert_slot", ctypes.c_void_p)]
+
+
+class QuantMoELayer:
+    """NEXT-3: one MoE layer in the quantised weight class (puzzle_moe_forward_quant).
+
+    w13_codes u8 [P, 2, d_ff, d_model], w13_scales f32 [P, 2, d_ff, d_model/128], w2_codes u8
+    [P, d_model, d_ff], w2_scales f32 [P, d_model, d_ff/128] (puzzle_quant_pack's outputs per
+    projection), expert_slot int32 [E]."""
+
+    def __init__(self, w13_codes, w13_scales, w2_codes, w2_scales, expert_slot):
+        P, two, f, d = w13_codes.shape
+        assert two == 2 and w13_codes.dtype == torch.uint8 and w2_codes.dtype == torch.uint8
+        assert tuple(w2_codes.shape) == (P, d, f) and tuple(w13_scales.shape) == (P, 2, f, d // 128)
+        assert tuple(w2_scales.shape) == (P, d, f // 128) and w13_scales.dtype == torch.float32
+        self.tensors = [t.contiguous() for t in (w13_codes, w13_scales, w2_codes, w2_scales, expert_slot)]
+        self.n_pairs, self.n_experts, self.d_model, self.d_ff = P, expert_slot.numel(), d, f
+        self.desc = QuantLayerDesc(self.n_experts, P, d, f, *[t.data_ptr() for t in self.tensors])
+        self._ws = None
+
+    @property
+    def quant_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.tensors[:4])
+
+    def workspace(self, max_tokens: int, top_k: int) -> torch.Tensor:
+        need = int(load_library().puzzle_moe_quant_workspace_size(ctypes.byref(self.desc), int(max_tokens), int(top_k)))
+        if need == 0:
+            raise PuzzleError(1, "puzzle_moe_quant_workspace_size", "invalid layer")
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.tensors[0].device)
+        return self._ws
+
+    def forward(self, hidden, router_logits, top_k: int, renormalize: bool, residual=None, out=None, workspace=None,
+                stream=None) -> torch.Tensor:
+        T = hidden.shape[0]
+        out = torch.empty_like(hidden) if out is None else out
+        ws = self.workspace(T, top_k) if workspace is None else workspace
+        _check(load_library().puzzle_moe_forward_quant(
+            ctypes.byref(self.desc), _p(hidden), _p(router_logits), T, int(top_k), int(bool(renormalize)),
+            _p(residual), _p(out), _p(ws), ws.numel(), _stream(stream)), "puzzle_moe_forward_quant")
+        return out
 
 
 class RoutingLayer:

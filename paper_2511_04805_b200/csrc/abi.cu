@@ -52,6 +52,9 @@ int launch_ep_combine_peer(const int32_t*, const float*, const int32_t*, int, co
                            int, const void*, const uint16_t*, uint16_t*, uint32_t*, cudaStream_t);
 bool tc_supported(int d, int f);
 bool ts_supported(int d, int f);
+int launch_gemv_tc_experts_quant(const uint8_t*, const float*, const uint8_t*, const float*, int, int, int,
+                                 const uint16_t*, const int32_t*, const int32_t*, const int32_t*, int, int64_t, float*,
+                                 int32_t*, int32_t*, uint16_t*, float*, cudaStream_t);
 int launch_ts_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*, const int32_t*,
                       int64_t, uint16_t*, float*, cudaStream_t);
 int launch_tc_experts(const uint16_t*, const uint16_t*, const uint8_t*, int, int, int, const uint16_t*,
@@ -399,13 +402,19 @@ size_t puzzle_moe_experts_workspace_size(const puzzle_moe_layer* L, int64_t n_as
 
 static int run_experts(const puzzle_moe_layer* L, const Plan& plan, const Layout& lay, void* ws,
                        const uint16_t* x, const int32_t* row_index, const int32_t* bucket_off,
-                       const int32_t* active, const int32_t* n_active, float* y, cudaStream_t s) {
+                       const int32_t* active, const int32_t* n_active, float* y, cudaStream_t s,
+                       const puzzle_moe_quant_layer* Q = nullptr) {
   const uint16_t* rows = x;
   if (row_index) {  // token permutation into bucket order: both paths read rows by TMA
     int rc = launch_gather_rows(x, row_index, plan.n_assign, L->d_model, at<uint16_t>(ws, lay.x_perm), s);
     if (rc) return rc;
     rows = at<uint16_t>(ws, lay.x_perm);
   }
+  if (Q)  // NEXT-3 quantised weight class: the decode-shape kernels over the byte format
+    return launch_gemv_tc_experts_quant(Q->w13_codes, Q->w13_scales, Q->w2_codes, Q->w2_scales, L->n_pairs, L->d_model,
+                                        L->d_ff, rows, bucket_off, active, n_active, plan.max_active, plan.n_assign,
+                                        at<float>(ws, lay.part), at<int32_t>(ws, lay.cnt13), at<int32_t>(ws, lay.cnt2),
+                                        at<uint16_t>(ws, lay.h), y, s);
   if (plan.path == PUZZLE_PATH_TS)
     return launch_ts_experts(L->w13, L->w2, L->pair_dense, L->n_pairs, L->d_model, L->d_ff, rows, bucket_off, plan.n_assign,
                              at<uint16_t>(ws, lay.h), y, s);
@@ -427,7 +436,7 @@ static size_t calib_bytes(const puzzle_moe_layer* L) {
 static int forward_impl(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits,
                         int64_t T, int k, int renorm, const uint16_t* residual, uint16_t* out,
                         void* ws, size_t ws_bytes, int path, puzzle_stream_t stream, double* sumsq_x,
-                        double* sumsq_h) {
+                        double* sumsq_h, const puzzle_moe_quant_layer* Q = nullptr) {
   if (int rc = check_layer(L)) return rc;
   if (T < 0) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "T < 0");
   if (k < 1 || k > L->n_experts) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "top_k outside [1, n_experts]");
@@ -472,7 +481,7 @@ static int forward_impl(const puzzle_moe_layer* L, const uint16_t* hidden, const
   // rows already in bucket order (fused into the large-batch scatter) or gathered now
   rc = run_experts(L, plan, lay, ws, rows_written ? at<uint16_t>(ws, lay.x_perm) : hidden,
                    rows_written ? nullptr : at<int32_t>(ws, lay.assign_token), at<int32_t>(ws, lay.bucket_off),
-                   at<int32_t>(ws, lay.active), at<int32_t>(ws, lay.n_active), at<float>(ws, lay.y), s);
+                   at<int32_t>(ws, lay.active), at<int32_t>(ws, lay.n_active), at<float>(ws, lay.y), s, Q);
   if (rc) return rc;
   // x_perm and h now hold the bucket-ordered x rows and SwiGLU rows of every assignment
   if (sumsq_x && (rc = launch_group_colsumsq(at<uint16_t>(ws, lay.x_perm), at<int32_t>(ws, lay.bucket_off),
@@ -522,6 +531,39 @@ int puzzle_group_colsumsq(const uint16_t* rows, const int32_t* group_off, int n_
   if (!ws || ws_bytes < calib_workspace_bytes(n_groups, cols) || (reinterpret_cast<uintptr_t>(ws) & 15u))
     return fail(PUZZLE_ERR_WORKSPACE, "workspace smaller than puzzle_group_colsumsq_workspace_size");
   return launch_group_colsumsq(rows, group_off, n_groups, cols, sumsq, static_cast<double*>(ws), (cudaStream_t)stream);
+}
+
+// NEXT-3: the quantised weight class through the forward (decode-shape kernels, any T)
+static int quant_view(const puzzle_moe_quant_layer* Q, puzzle_moe_layer& L) {
+  if (!Q) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "quant layer descriptor is NULL");
+  if (!Q->w13_scales || !Q->w2_scales) return fail(PUZZLE_ERR_INVALID_ARGUMENT, "quant scales NULL");
+  if (Q->d_model % 128 || Q->d_ff % 128)
+    return fail(PUZZLE_ERR_UNSUPPORTED, "quantised layers need d_model and d_ff multiples of 128 (groups of 128)");
+  if ((reinterpret_cast<uintptr_t>(Q->w13_scales) | reinterpret_cast<uintptr_t>(Q->w2_scales)) & 3u)
+    return fail(PUZZLE_ERR_UNSUPPORTED, "scales must be 4-byte aligned");
+  L = puzzle_moe_layer{Q->n_experts, Q->n_pairs, Q->d_model, Q->d_ff, reinterpret_cast<const uint16_t*>(Q->w13_codes),
+                       reinterpret_cast<const uint16_t*>(Q->w2_codes), Q->expert_slot, nullptr};
+  return check_layer(&L);
+}
+
+size_t puzzle_moe_quant_workspace_size(const puzzle_moe_quant_layer* Q, int64_t max_tokens, int top_k) {
+  puzzle_moe_layer L;
+  if (quant_view(Q, L) || max_tokens < 0 || top_k < 1 || top_k > L.n_experts) return 0;
+  size_t best = 0;  // the GEMV plan of every T <= max_tokens (split factors depend on min(P, T k))
+  const int64_t knee = (L.n_pairs + top_k - 1) / top_k;
+  for (int64_t t = 1; t <= std::min<int64_t>(max_tokens, knee); ++t)
+    best = std::max(best, make_layout(&L, make_plan(&L, t, top_k, PUZZLE_PATH_GEMV)).total);
+  if (max_tokens > 0) best = std::max(best, make_layout(&L, make_plan(&L, max_tokens, top_k, PUZZLE_PATH_GEMV)).total);
+  return best;
+}
+
+int puzzle_moe_forward_quant(const puzzle_moe_quant_layer* Q, const uint16_t* hidden, const float* logits, int64_t T,
+                             int k, int renorm, const uint16_t* residual, uint16_t* out, void* ws, size_t ws_bytes,
+                             puzzle_stream_t stream) {
+  puzzle_moe_layer L;
+  if (int rc = quant_view(Q, L)) return rc;
+  return forward_impl(&L, hidden, logits, T, k, renorm, residual, out, ws, ws_bytes, PUZZLE_PATH_GEMV, stream, nullptr,
+                      nullptr, Q);
 }
 
 int puzzle_moe_forward(const puzzle_moe_layer* L, const uint16_t* hidden, const float* logits, int64_t T,

@@ -64,12 +64,19 @@ constexpr uint32_t kAccCol = 64 * kAStages;      // 192: accumulators of positio
 
 // Configuration: NX = 32 tokens per position per pass, 2 CTAs per SM, 256 TMEM columns
 // (batches of 1-64 tokens; larger batches go to the prefill kernels).
-template <int NX, int CTAS>
+#ifndef PZ_TC_WST_Q  // W ring depth of the quantised class (half-size slots)
+#define PZ_TC_WST_Q PZ_TC_WST
+#endif
+template <int NX, int CTAS, int FMT = 0>
 struct Cfg {
   static constexpr int kNX = NX;                          // tokens per position per pass (UMMA N <= NX)
   static constexpr int kXPos = NX * kBK * 2;              // one position's activation rows per stage
   static constexpr int kXBytes = 2 * kXPos;               // X stage: both positions
-  static constexpr int kWStages = NX == 32 ? PZ_TC_WST : 4;
+  // W slots: a stage of 128 rows x 64 k -- 16 KB of packed words, or 8 KB of quantised code bytes
+  // (a deeper ring of half-size slots, 6 / 8, measured neutral: the quantised class is bound by
+  // its decode on the ALU pipe, profiles/r02/quant_forward.txt)
+  static constexpr int kWSlot = FMT ? kRows * kBK : kWBytes;
+  static constexpr int kWStages = FMT ? PZ_TC_WST_Q : (NX == 32 ? PZ_TC_WST : 4);
   static constexpr int kXStages = NX == 32 ? PZ_TC_XST : 4;
   static constexpr uint32_t kTmemCols = CTAS == 2 ? 256 : 512;
   static_assert(kAccCol + 2 * NX <= kTmemCols, "TMEM: A ring + accumulators");
@@ -113,10 +120,11 @@ struct alignas(16) Ctl {
 
 template <class C>
 constexpr size_t smem_bytes() {
-  return 1024 + (size_t)C::kWStages * kWBytes + (size_t)C::kXStages * C::kXBytes +
+  return 1024 + (size_t)C::kWStages * C::kWSlot + (size_t)C::kXStages * C::kXBytes +
          sizeof(Ctl<C::kWStages, C::kXStages>);
 }
 static_assert(2 * (smem_bytes<Cfg<32, 2>>() + 1024) <= 228 * 1024, "decode: two CTAs per SM");
+static_assert(2 * (smem_bytes<Cfg<32, 2, 1>>() + 1024) <= 228 * 1024, "decode (quantised): two CTAs per SM");
 
 struct PairTokens {
   int off0, cnt0, off1, cnt1;
@@ -297,24 +305,98 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST>& c, uint32_t smem_w, u
   }
 }
 
+// NEXT-3, the quantised weight class (R21-R23): one byte per merged element, S_i S_j M_i M_j 0 c2
+// c1 c0, and an f32 scale per group of 128 columns. Decoded element of position p:
+// (-1)^S_p * M_p * bf16_rne(f32(c * scale)) (R23), bit-exact: the 8 magnitudes of the thread's
+// group (its 32 k of a stage lie in one group) are formed once per stage with the same f32
+// product and RNE, then selected per byte pair with byte permutes (prmt); sign and mask are
+// integer ops (no scaling trick: exact for every finite scale).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ uint32_t bf16x2_of(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// two code bytes (bits 0-15 of y) -> bf16x2 of position 0 / 1 (MODE bits 0 / 1)
+template <int MODE>
+__device__ __forceinline__ void qdecode2(uint32_t y, const uint32_t (&L)[4], uint32_t& o0, uint32_t& o1) {
+  const uint32_t sel = (y & 0x0303u) * 0x22u + 0x1010u;        // bytes 2(c & 3), 2(c & 3) + 1
+  const uint32_t lo = prmt(L[0], L[1], sel), hi = prmt(L[2], L[3], sel);
+  const uint32_t m3 = prmt(y << 5, 0u, 0x9988u);                // code bit 2 -> 16-bit lane mask
+  const uint32_t mag = (lo & ~m3) | (hi & m3);                   // |W^| as bf16x2
+  const uint32_t p = prmt(y, 0u, 0x1404u);                       // byte k -> bits 16k + 8 .. 16k + 15
+  if (MODE & 1) o0 = (mag | (p & 0x80008000u)) & prmt(y << 2, 0u, 0x9988u);         // S_i bit 7, M_i bit 5
+  if (MODE & 2) o1 = (mag | ((p << 1) & 0x80008000u)) & prmt(y << 3, 0u, 0x9988u);  // S_j bit 6, M_j bit 4
+}
+
+template <int MODE, int WST, int XST, class Epi>
+__device__ __forceinline__ void decode_pass_q(Ctl<WST, XST>& c, uint32_t smem_w, uint32_t lane_tmem,
+                                              const uint32_t (&w_off)[2], int kh, int n_stages, Ring& w, Ring& a,
+                                              const float* __restrict__ row_scales, int kb0, int& tcount, int ep_at,
+                                              Epi&& epi) {
+  const int lane = threadIdx.x & 31;
+  (void)tcount;
+  float sc_next = __ldg(row_scales + (kb0 >> 1));  // a group = 2 stages of 64
+  for (int kb = 0; kb < n_stages; ++kb) {
+    if (kb) ptx::mbar_wait(&c.wfull[w.i], w.ph);
+    const uint32_t st = smem_w + (uint32_t)w.i * (kRows * kBK);  // quantised W slots: 8 KB
+    const uint4 v0 = lds128(st + w_off[0]), v1 = lds128(st + w_off[1]);
+    const float sc = sc_next;
+    if (kb + 1 < n_stages) sc_next = __ldg(row_scales + ((kb0 + kb + 1) >> 1));  // in flight meanwhile
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&c.wempty[w.i]);  // bytes in registers: the slot may refill
+    w.next<WST>();
+    uint32_t L[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) L[j] = bf16x2_of(__fmul_rn((float)(2 * j), sc), __fmul_rn((float)(2 * j + 1), sc));
+    uint32_t d0[16], d1[16];
+    const uint32_t words[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      qdecode2<MODE>(words[i], L, d0[2 * i], d1[2 * i]);
+      qdecode2<MODE>(words[i] >> 16, L, d0[2 * i + 1], d1[2 * i + 1]);
+    }
+    ptx::mbar_wait(&c.a_empty[a.i], a.ph ^ 1);  // the MMAs that read A buffer a.i have completed
+    ptx::tc_fence_after();
+    const uint32_t t0 = lane_tmem + 64u * a.i + 16u * kh;
+    if (MODE & 1) ptx::tmem_st_32x32b_x16(t0, d0);
+    if (MODE & 2) ptx::tmem_st_32x32b_x16(t0 + 32u, d1);
+    ptx::tmem_st_wait();
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&c.a_full[a.i]);
+    ++tcount;
+    a.next<kAStages>();
+    if (kb == ep_at) epi();
+  }
+}
+
 // part: 2 slots per CTA ([g][0] = its first piece, [g][1] = its last piece), each
 // [2 positions][NX tokens of the pass][128 tile rows] fp32 (w13 rows 0-63 = g, 64-127 = u);
 // counters: one per work item, zero on entry.
-template <bool kW13, int NX, int CTAS>
+// FMT 0: packed 16-bit words (Algorithm 1); FMT 1: the quantised byte format (NEXT-3) with
+// qscales f32 [weight rows][K / 128].
+template <bool kW13, int NX, int CTAS, int FMT = 0>
 __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM sub-partition
     const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
     const int32_t* __restrict__ bucket_off, const int32_t* __restrict__ active_pairs,
     const int32_t* __restrict__ n_active_ptr, int K, int f, int d, int n_rb,
     float* __restrict__ part, int32_t* __restrict__ counters, uint16_t* __restrict__ h_out,
-    float* __restrict__ y_out, uint32_t mul_one, int n_bucket_pairs, const uint8_t* __restrict__ pair_dense) {
-  using C = Cfg<NX, CTAS>;
+    float* __restrict__ y_out, uint32_t mul_one, int n_bucket_pairs, const uint8_t* __restrict__ pair_dense,
+    const float* __restrict__ qscales = nullptr) {
+  using C = Cfg<NX, CTAS, FMT>;
+  constexpr uint32_t kWStageBytes = C::kWSlot;  // bytes of one W stage (codes: 1 B each)
   constexpr int kWStages = C::kWStages, kXStages = C::kXStages, kXBytes = C::kXBytes, kXPos = C::kXPos;
   constexpr int kSlot = 2 * NX * kRows;  // floats per partial slot
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_w = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;  // == smem, shared window
-  const uint32_t smem_x = smem_w + kWStages * kWBytes;
-  auto& c = *reinterpret_cast<Ctl<kWStages, kXStages>*>(smem + (size_t)kWStages * kWBytes +
+  const uint32_t smem_x = smem_w + kWStages * kWStageBytes;
+  auto& c = *reinterpret_cast<Ctl<kWStages, kXStages>*>(smem + (size_t)kWStages * kWStageBytes +
                                                          (size_t)kXStages * kXBytes);
   const uint32_t whdr_s = ptx::smem_u32(&c.whdr[0]), xhdr_s = ptx::smem_u32(&c.xhdr[0]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -408,11 +490,11 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           if (tw == 0) g_cta[kW13][blockIdx.x][1] = gtimer();
 #endif
           c.whdr[w.i] = hv;
-          uint8_t* sw = smem + (size_t)w.i * kWBytes;
-          ptx::mbar_arrive_expect_tx(&c.wfull[w.i], kWBytes);
+          uint8_t* sw = smem + (size_t)w.i * kWStageBytes;
+          ptx::mbar_arrive_expect_tx(&c.wfull[w.i], kWStageBytes);
           if (kW13) {  // 64 gate rows, then the same features' 64 up rows
             ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
-            ptx::tma_load_2d(sw + kWBytes / 2, &tm_w, &c.wfull[w.i], kc, wrow + f);
+            ptx::tma_load_2d(sw + kWStageBytes / 2, &tm_w, &c.wfull[w.i], kc, wrow + f);
           } else {
             ptx::tma_load_2d(sw, &tm_w, &c.wfull[w.i], kc, wrow);
           }
@@ -480,7 +562,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       PZ_TR(1, tx);
       ++tx;
       const bool a0 = (q.y >> 28) & 1, a1 = (q.z >> 28) & 1;
-      uint8_t* sx = smem + (size_t)kWStages * kWBytes + (size_t)x.i * kXBytes;
+      uint8_t* sx = smem + (size_t)kWStages * kWStageBytes + (size_t)x.i * kXBytes;
       ptx::mbar_arrive_expect_tx(&c.xfull[x.i], (uint32_t)(a0 + a1) * kXPos);
       if (a0) ptx::tma_load_2d(sx, &tm_x, &c.xfull[x.i], q.x, q.y & 0x0FFFFFFF);
       if (a1) ptx::tma_load_2d(sx + kXPos, &tm_x, &c.xfull[x.i], q.x, q.z & 0x0FFFFFFF);
@@ -553,6 +635,12 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     uint32_t w_off[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) w_off[i] = swz(srow, 4 * kh + i);
+    // quant stages: 64-byte rows under the 64-byte swizzle (16-byte chunk c of row r at chunk
+    // c ^ ((r >> 1) & 3)); this thread reads chunks 2 kh, 2 kh + 1 (its 32 k)
+    uint32_t wq_off[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) wq_off[i] = (uint32_t)(srow * 64 + (((2 * kh + i) ^ ((srow >> 1) & 3)) << 4));
+    (void)wq_off;
     Ring w{0, 0}, a{0, 0};
     uint32_t accph = 0;
     int tcount = 0;
@@ -571,7 +659,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       PZ_DCHECK(np >= 0 && np <= NX && offp >= 0 && (np == 0 || offp + np <= c.s_off[2 * n_bucket_pairs]));
       PZ_DCHECK(s.item < n_rb * (n_bucket_pairs + c.s_off[2 * n_bucket_pairs] / 32 + 1));
       // the A operand is W^ * 2^-15 (PZ_TC_ORMAG; dense slots scaled to match): scale back, exact
-      constexpr float acc_scale = PZ_TC_ORMAG ? 32768.0f : 1.0f;
+      constexpr float acc_scale = (PZ_TC_ORMAG && FMT == 0) ? 32768.0f : 1.0f;  // quant bytes decode exactly
       for (int c0 = 0; c0 < np; c0 += 16) {
         uint32_t r[16];
         ptx::tmem_ld_32x32b_x16(acc_t + c0, r);
@@ -677,10 +765,20 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       // completed by then; the A ring lets the decoders run ahead meanwhile)
       const int ep_at = PZ_TC_DEFER ? min(1, n_st - 1) : -1;
       // a dense slot (R20) is only ever routed at position 0
+      if constexpr (FMT == 1) {
+        // this thread's weight row (global) and its group scales [K / 128]
+        const int64_t grow = kW13 ? (int64_t)s.p * 2 * f + (srow < 64 ? 0 : f) + s.rb * (kRows / 2) + (srow & 63)
+                                  : (int64_t)s.p * d + s.rb * kRows + row;
+        const float* rs = qscales + grow * (K / 128);
+        if (s.n0 > 0 && s.n1 > 0) decode_pass_q<3>(c, smem_w, lane_tmem, wq_off, kh, n_st, w, a, rs, s.kb0, tcount, ep_at, flush);
+        else if (s.n0 > 0) decode_pass_q<1>(c, smem_w, lane_tmem, wq_off, kh, n_st, w, a, rs, s.kb0, tcount, ep_at, flush);
+        else decode_pass_q<2>(c, smem_w, lane_tmem, wq_off, kh, n_st, w, a, rs, s.kb0, tcount, ep_at, flush);
+      } else {
       if (pair_dense != nullptr && pair_dense[s.p]) decode_pass<4>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
       else if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
       else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
       else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      }
       if (PZ_TC_DEFER) {
         pend = s;
         have_pend = true;
@@ -701,13 +799,13 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
 #endif
 }
 
-template <bool kW13, int NX, int CTAS>
+template <bool kW13, int NX, int CTAS, int FMT = 0>
 int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* bucket_off, const int32_t* active,
                const int32_t* n_active, int K, int f, int d, int n_rb, int max_active, int64_t n_assign, float* part,
                int32_t* counters, uint16_t* h, float* y, int n_pairs, const uint8_t* pair_dense,
-               cudaStream_t stream) {
-  using C = Cfg<NX, CTAS>;
-  auto kern = k_gemv_tc<kW13, NX, CTAS>;
+               cudaStream_t stream, const float* qscales = nullptr) {
+  using C = Cfg<NX, CTAS, FMT>;
+  auto kern = k_gemv_tc<kW13, NX, CTAS, FMT>;
   constexpr size_t kSmem = smem_bytes<C>();
   static std::atomic<uint64_t> attr{0};
   if (int rc = cuda_check(ensure_smem_attr(kern, kSmem, attr), "gemv smem attribute")) return rc;
@@ -715,11 +813,11 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
   // recomputes the partition from the actual active pairs and passes)
   const int64_t S = ((int64_t)max_active + n_assign / NX) * n_rb * (K / kBK);  // >= the real stage count
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)CTAS * num_sms(), S / kMinStages));
-  const char* name = NX == 32 ? (kW13 ? "w13_gemv" : "w2_gemv") : (kW13 ? "w13_tc" : "w2_tc");
+  const char* name = FMT ? (kW13 ? "w13_gemv_q" : "w2_gemv_q") : (kW13 ? "w13_gemv" : "w2_gemv");
   {
     ProfScope _ps(name, stream);
     cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kThreads), kSmem, stream, tw, tx, bucket_off, active, n_active,
-                               K, f, d, n_rb, part, counters, h, y, 1u, n_pairs, pair_dense);
+                               K, f, d, n_rb, part, counters, h, y, 1u, n_pairs, pair_dense, qscales);
     if (e != cudaSuccess) return cuda_check(e, name);
   }
   return cuda_check(cudaGetLastError(), name);
@@ -745,7 +843,38 @@ int launch_both(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_den
                                      n_assign_cap, part, counters2, h, y, n_pairs, pair_dense, stream);
 }
 
+// NEXT-3: the same two launches over the quantised byte format (codes u8 [rows][K] + f32
+// scales [rows][K / 128] per projection; no dense slots)
+int launch_both_quant(const uint8_t* c13, const float* s13, const uint8_t* c2, const float* s2, int n_pairs, int d, int f,
+                      const uint16_t* x_rows, const int32_t* bucket_off, const int32_t* active_pairs,
+                      const int32_t* n_active, int max_active, int64_t n_assign_cap, float* part, int32_t* counters13,
+                      int32_t* counters2, uint16_t* h, float* y, cudaStream_t stream) {
+  constexpr int NX = 32, CTAS = 2;
+  if (max_active == 0 || n_assign_cap == 0) return PUZZLE_OK;
+  CUtensorMap tw13, tx13, tw2, tx2;
+  int rc;
+  if ((rc = make_tmap_2d_u8(&tw13, c13, (int64_t)n_pairs * 2 * f, d, kRows / 2, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx13, x_rows, n_assign_cap, d, NX, kBK))) return rc;
+  if ((rc = make_tmap_2d_u8(&tw2, c2, (int64_t)n_pairs * d, f, kRows, kBK))) return rc;
+  if ((rc = make_tmap_2d(&tx2, h, n_assign_cap, f, NX, kBK))) return rc;
+  const int rb13 = f / (kRows / 2), rb2 = (d + kRows - 1) / kRows;
+  if ((rc = launch_one<true, NX, CTAS, 1>(tw13, tx13, bucket_off, active_pairs, n_active, d, f, d, rb13, max_active,
+                                          n_assign_cap, part, counters13, h, y, n_pairs, nullptr, stream, s13)))
+    return rc;
+  return launch_one<false, NX, CTAS, 1>(tw2, tx2, bucket_off, active_pairs, n_active, f, f, d, rb2, max_active,
+                                        n_assign_cap, part, counters2, h, y, n_pairs, nullptr, stream, s2);
+}
+
 }  // namespace
+
+int launch_gemv_tc_experts_quant(const uint8_t* c13, const float* s13, const uint8_t* c2, const float* s2, int n_pairs,
+                                 int d, int f, const uint16_t* x_rows, const int32_t* bucket_off,
+                                 const int32_t* active_pairs, const int32_t* n_active, int max_active,
+                                 int64_t n_assign_cap, float* part, int32_t* counters13, int32_t* counters2, uint16_t* h,
+                                 float* y, cudaStream_t stream) {
+  return launch_both_quant(c13, s13, c2, s2, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
+                           n_assign_cap, part, counters13, counters2, h, y, stream);
+}
 
 // Partial-slot floats (2 slots per CTA x 2 CTAs per SM x 2 positions x NX x 128).
 size_t gemv_tc_part_floats() { return (size_t)2 * 2 * num_sms() * 2 * 32 * kRows; }

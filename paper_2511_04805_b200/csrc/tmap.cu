@@ -87,6 +87,31 @@ int make_tmap_2d_uncached(CUtensorMap* m, const void* base, int64_t rows, int64_
   return PUZZLE_OK;
 }
 
+// 2-D map over a u8 [rows][cols] tensor, box [box_rows][box_cols = 64 bytes], 64-byte swizzle
+// (16-byte chunk c of smem row r at chunk c ^ ((r >> 1) & 3): conflict-free 16-byte row reads)
+int make_tmap_2d_u8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows, int box_cols) {
+  const TmapKey k{reinterpret_cast<uintptr_t>(base), rows, cols, 0, 0, box_rows, box_cols, 100};
+  const int i = TmapCache::slot(k);
+  if (g_tmaps.used[i] && g_tmaps.key[i] == k) {
+    *m = g_tmaps.map[i];
+    return PUZZLE_OK;
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(PUZZLE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PUZZLE_ERR_CUDA, "cuTensorMapEncodeTiled (u8) failed: " + std::to_string((int)r));
+  g_tmaps.key[i] = k;
+  g_tmaps.map[i] = *m;
+  g_tmaps.used[i] = true;
+  return PUZZLE_OK;
+}
+
 // 3-D map over a [n2][rows][cols] bf16 / u16 tensor whose dim-2 stride is `stride2_rows` rows:
 // a box {box_cols, box_rows, box_n2} lands in shared memory as box_n2 consecutive 2-D boxes
 // (one TMA instruction for several row blocks that are far apart in memory, e.g. the gate and
