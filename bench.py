@@ -1053,7 +1053,8 @@ def sweep(pz, args, device, pk):
                 row.update({"weight_gbs_step": gbs, "frac_hbm_step": gbs / pk["hbm_gbs"]})
                 flops = 2 * 3 * cfg.d_model * cfg.d_ff * T * cfg.top_k
                 tc_ms = sum(v for k, v in kern.items() if k.endswith("_tc") or k.endswith("_ts"))
-                row.update({"path": "ts" if any(k.endswith("_ts") for k in kern) else "tc", "tflops_step": flops / (ms / 1e3) / 1e12,
+                row.update({"path": "ts" if any(k.endswith("_ts") for k in kern) else
+                                    "gemv" if any(k.endswith("_gemv") for k in kern) else "tc", "tflops_step": flops / (ms / 1e3) / 1e12,
                             "tflops_tc_kernels": flops / (tc_ms / 1e3) / 1e12 if tc_ms else None,
                             "frac_bf16_peak": flops / (tc_ms / 1e3) / 1e12 / pk["bf16_tflops"] if tc_ms else None})
             res.append(row)
