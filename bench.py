@@ -763,7 +763,7 @@ def run_ours(args):
         line.setdefault("aux", {})["strong_scaling"] = ep_strong_scaling(
             pz, args, cfg, device, rank, world, routing, local, ep, ep_capi, global_batch=args.batch)
     if dist_on and ((world > 1 and not args.no_extra) or args.stack_ep):
-        stack_ep = stack_runs_ep(pz, args, device, part, rank, world)
+        stack_ep = stack_runs_ep(pz, args, device, part, rank, world, ep_capi)
         line.setdefault("aux", {})["stack32_ep"] = stack_ep
     if rank == 0:
         line["clocks"] = clocks.summary(t0, t1)
@@ -1156,7 +1156,7 @@ def stack_runs(pz, args, device, pk):
     return res
 
 
-def stack_runs_ep(pz, args, device, part, rank, world):
+def stack_runs_ep(pz, args, device, part, rank, world, ep_capi=None):
     """BASELINE.json configs[4] as named: the 32-layer Mixtral-8x7B MoE stack at 50%
     compression, EXPERT-PARALLEL -- every rank holds its share of each layer's merged pairs and
     its own tokens (weak scaling), x_{l+1} = x_l + MoE_l(x_l). Batch-64 decode runs the
@@ -1195,10 +1195,17 @@ def stack_runs_ep(pz, args, device, part, rank, world):
         logits = [torch.randn((T, cfg.n_experts), generator=g, device=device) for _ in range(n_layers)]
         fixed = T <= 64
 
+        ws_c = None
+        if fixed and ep_capi is not None:  # one communicator and workspace serve every layer
+            ws_c = ep_capi.workspace(eps[0].route_layer, eps[0].local_layer, T, cfg.top_k)
+
         def step():
             x = x0
             for l, ep in enumerate(eps):
-                if fixed and pb is not None:
+                if fixed and ws_c is not None:
+                    x = ep_capi.forward(ep.route_layer, ep.local_layer, x, logits[l], cfg.top_k, cfg.renormalize,
+                                        cap_tokens=T, residual=x, workspace=ws_c, path=pz.PATH_GEMV)
+                elif fixed and pb is not None:
                     x = ep.forward_peer(x, logits[l], cfg.top_k, cfg.renormalize, residual=x, path=pz.PATH_GEMV)
                 elif fixed:
                     x = ep.forward_fixed(x, logits[l], cfg.top_k, cfg.renormalize, residual=x, path=pz.PATH_GEMV)
@@ -1225,7 +1232,8 @@ def stack_runs_ep(pz, args, device, part, rank, world):
         ms = float(t.item())
         row = {"config": f"mixtral_stack32_ep{world}", "batch_per_rank": T, "ms_per_step": ms,
                "tokens_per_s": T * world / (ms / 1e3), "layers": n_layers,
-               "dispatch": (("fixed-capacity over NVLink peer memory" if pb is not None else "fixed-capacity, NCCL")
+               "dispatch": (("fixed-capacity, C-ABI NCCL communicator" if ws_c is not None else
+                             "fixed-capacity over NVLink peer memory" if pb is not None else "fixed-capacity, NCCL")
                             + (", one CUDA graph of 32 layers" if not args.no_graph else ", eager")
                             if fixed else "variable-split, NCCL, eager")}
         if fixed and pb is not None:
