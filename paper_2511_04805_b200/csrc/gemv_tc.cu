@@ -87,6 +87,7 @@ __device__ unsigned long long g_trace[8][4096];
 __device__ unsigned long long g_cta[2][1024][4];  // [kernel][cta] {start, first W issue, producer done, end}
 __device__ unsigned long long g_after_wait[2][1024];  // [kernel][cta] pdl_wait returned
 __device__ unsigned int g_smid[2][1024];
+__device__ unsigned long long g_red[2][1024][8];  // [kernel][cta] reducer: {epilogue start, wait start, counter seen, end}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -111,6 +112,7 @@ struct alignas(16) Ctl {
   uint64_t sqfull[kSq], sqempty[kSq];
   uint64_t pdone;  // decoders -> X producer: partials of this CTA's first (signalling) piece stored
   uint64_t acc_full, acc_empty;
+  uint64_t red_bar;  // reducer: staged partials landed (bulk copies)
   uint32_t tmem_base;
   int s_last;
   int32_t s_off[kMaxExperts + 1];       // bucket_off[0 .. 2P]
@@ -143,6 +145,34 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 1-D bulk copy global -> this CTA's shared memory, completion on an mbarrier (tx bytes)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_f32_hint(float* a, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ float4 ptx_lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void ptx_sts_f4(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 __device__ __forceinline__ int4 lds_int4(uint32_t addr) {
   int4 v;
@@ -420,6 +450,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     ptx::mbar_init(&c.pdone, kDecWarps);
     ptx::mbar_init(&c.acc_full, 2);
     ptx::mbar_init(&c.acc_empty, kDecWarps);
+    ptx::mbar_init(&c.red_bar, 1);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tm_w);
     ptx::tma_prefetch_desc(&tm_x);
@@ -647,6 +678,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     const int first_item = s_begin / nk;  // pieces of this CTA: [g][0] = first, [g][1] = last
     // ---- epilogue of pass s: warp (q, pos = kh) reads its rows' accumulators ----
     auto finish = [&](const Pass& s) {
+#ifdef PZ_TRACE
+      if (dtid == 0 && !(s.kb0 == 0 && s.kb1 == nk) && g == sk.owner(s.item * nk)) g_red[kW13][blockIdx.x][0] = gtimer();
+#endif
       ptx::mbar_wait(&c.acc_full, accph);
       accph ^= 1;
       ptx::tc_fence_after();
@@ -667,10 +701,14 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
 #pragma unroll
         for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * acc_scale);
         if (!whole) {
+          // evict_last: the reducer reads these back up to a whole range later, after hundreds
+          // of MB of weights have streamed through L2; from HBM, behind the weight stream's
+          // queues, that read took ~5 us (scripts/red_stats.py)
+          const uint64_t keep = l2_policy_evict_last();
           const int t0 = pos * NX + c0;  // (position, token of the pass)
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (c0 + i < np) slot[(size_t)(t0 + i) * kRows + prow] = __uint_as_float(r[i]);
+            if (c0 + i < np) st_f32_hint(slot + (size_t)(t0 + i) * kRows + prow, __uint_as_float(r[i]), keep);
         } else if (kW13) {
           // exchange g <-> u with the partner lane; gate lanes finish tokens c0..c0+7,
           // up lanes tokens c0+8..c0+15
@@ -709,43 +747,103 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         } else {
           // the reducer (this CTA's last piece): wait for the other pieces' signals, then sum
           // the partials in CTA order (own slot included)
+#ifdef PZ_TRACE
+          if (dtid == 0) g_red[kW13][blockIdx.x][1] = gtimer();
+#endif
           named_bar_sync(1, kDecWarps * 32);
           if (dtid == 0) {
             __threadfence();
             while (ld_acquire_gpu(&counters[s.item]) < g_last - g_first) __nanosleep(64);
             counters[s.item] = 0;  // ready for the next call on this stream
+#ifdef PZ_TRACE
+            g_red[kW13][blockIdx.x][2] = gtimer();
+#endif
           }
           named_bar_sync(1, kDecWarps * 32);
+          // Sum the slots of CTAs g_first .. g_last in CTA order (from 0). The active rows of
+          // every slot are staged into the idle W / X rings by two TMA bulk copies per slot (one
+          // thread, all in flight at once), then summed from shared memory; slots beyond the
+          // rings' capacity are staged in further rounds, the running sum carried in staged slot
+          // 0. The rings are idle: this is the CTA's last piece and its MMAs have completed.
+          // Mixtral w2 (3 slots x 35 rows): 8.6 us with per-thread float4 loads, 5.6 us staged
+          // with 16-byte cp.async (LSU issue bound beside the co-resident CTA's decode), 2.0 us
+          // with bulk copies (scripts/red_stats.py; profiles/r02/reduce_ab.txt).
           const int r0 = s.rb * (kW13 ? kRows / 2 : kRows);
           const int cols = kW13 ? kRows / 2 : min(kRows, d - r0);  // outputs of this tile, multiple of 4
           const int q4 = cols / 4;
-          const int n_tot = 2 * NX;  // slot rows: (position, token of the pass)
-          for (int i = dtid; i < n_tot * q4; i += kDecWarps * 32) {
-            const int t = i / q4, cq = 4 * (i % q4);
-            const int pos = t / NX, tk = t % NX;
-            if (tk >= (pos ? s.n1 : s.n0)) continue;
-            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
-            for (int gg = g_first; gg <= g_last; ++gg) {
-              const int sl = 2 * gg + (s.item == sk.begin(gg) / nk ? 0 : 1);
-              const float* src = part + (size_t)sl * kSlot + (size_t)t * kRows + cq;
-              const float4 v4 = __ldcg(reinterpret_cast<const float4*>(src));
-              s0.x += v4.x; s0.y += v4.y; s0.z += v4.z; s0.w += v4.w;
-              if (kW13) {
-                const float4 u = __ldcg(reinterpret_cast<const float4*>(src + kRows / 2));
-                s1.x += u.x; s1.y += u.y; s1.z += u.z; s1.w += u.w;
+          const int n_rows = s.n0 + s.n1;                           // active (position, token) rows
+          constexpr uint32_t kRowB = kRows * 4;                     // one slot row: 512 bytes
+          constexpr uint32_t kRing = kWStages * kWStageBytes + kXStages * kXBytes;
+          static_assert(kRing >= 2u * (2 * NX) * kRowB, "reducer: two full slots fit the rings");
+          const int m = min(g_last - g_first + 1, (int)(kRing / (n_rows * kRowB)));  // >= 2 slots
+          const int n_units = n_rows * q4;
+          const uint64_t drop = l2_policy_evict_first();  // the partials are dead once read
+          uint32_t red_ph = 0;  // one reduction per CTA (its last piece): red_bar phases from 0
+          for (int gg = g_first, k0 = 0; gg <= g_last; k0 = 1) {
+            const int cnt = min(m - k0, g_last - gg + 1);
+            if (dtid == 0) {  // two bulk copies per slot: its position-0 rows, its position-1 rows
+              // generic-proxy data (the acquired partials; staged rows read by the last round)
+              // before async-proxy accesses
+              asm volatile("fence.proxy.async;" ::: "memory");
+              ptx::mbar_arrive_expect_tx(&c.red_bar, (uint32_t)(cnt * n_rows) * kRowB);
+              for (int k = 0; k < cnt; ++k) {
+                const int gk = gg + k;
+                const float* src = part + (size_t)(2 * gk + (s.item == sk.begin(gk) / nk ? 0 : 1)) * kSlot;
+                const uint32_t dst = smem_w + (uint32_t)(k0 + k) * n_rows * kRowB;
+                if (s.n0) bulk_g2s(dst, src, (uint32_t)s.n0 * kRowB, &c.red_bar, drop);
+                if (s.n1) bulk_g2s(dst + (uint32_t)s.n0 * kRowB, src + (size_t)NX * kRows, (uint32_t)s.n1 * kRowB,
+                                   &c.red_bar, drop);
               }
             }
-            const size_t aa = (size_t)((pos ? s.pt.off1 : s.pt.off0) + s.base + tk);
-            if (kW13) {
-              uint2 o;
-              o.x = f32_to_bf16_rne_bits(silu_mul(s0.x, s1.x)) | (f32_to_bf16_rne_bits(silu_mul(s0.y, s1.y)) << 16);
-              o.y = f32_to_bf16_rne_bits(silu_mul(s0.z, s1.z)) | (f32_to_bf16_rne_bits(silu_mul(s0.w, s1.w)) << 16);
-              *reinterpret_cast<uint2*>(h_out + aa * f + r0 + cq) = o;
-            } else {
-              *reinterpret_cast<float4*>(y_out + aa * d + r0 + cq) = s0;
+            ptx::mbar_wait(&c.red_bar, red_ph);
+            red_ph ^= 1;
+#ifdef PZ_TRACE
+            if (k0 == 0 && (dtid & 31) == 0) g_red[kW13][blockIdx.x][4 + (dtid >> 7)] = gtimer();  // warps 0 / 4 loads landed
+#endif
+            named_bar_sync(1, kDecWarps * 32);
+#ifdef PZ_TRACE
+            if (k0 == 0 && dtid == 0) g_red[kW13][blockIdx.x][6] = gtimer();
+#endif
+            const bool last = gg + cnt > g_last;
+            for (int u = dtid; u < n_units; u += kDecWarps * 32) {
+              const int r = u / q4, cq = 4 * (u % q4);
+              const uint32_t a0 = smem_w + (uint32_t)r * kRowB + 16u * (cq / 4);
+              float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+              if (k0) {  // the running sum of the earlier rounds
+                s0 = ptx_lds_f4(a0);
+                if (kW13) s1 = ptx_lds_f4(a0 + kRowB / 2);
+              }
+              for (int k = k0; k < k0 + cnt; ++k) {
+                const uint32_t ak = a0 + (uint32_t)k * n_rows * kRowB;
+                const float4 v4 = ptx_lds_f4(ak);
+                s0.x += v4.x; s0.y += v4.y; s0.z += v4.z; s0.w += v4.w;
+                if (kW13) {
+                  const float4 u4 = ptx_lds_f4(ak + kRowB / 2);
+                  s1.x += u4.x; s1.y += u4.y; s1.z += u4.z; s1.w += u4.w;
+                }
+              }
+              if (!last) {
+                ptx_sts_f4(a0, s0);
+                if (kW13) ptx_sts_f4(a0 + kRowB / 2, s1);
+                continue;
+              }
+              const size_t aa = (size_t)((r < s.n0 ? s.pt.off0 + r : s.pt.off1 + r - s.n0) + s.base);
+              if (kW13) {
+                uint2 o;
+                o.x = f32_to_bf16_rne_bits(silu_mul(s0.x, s1.x)) | (f32_to_bf16_rne_bits(silu_mul(s0.y, s1.y)) << 16);
+                o.y = f32_to_bf16_rne_bits(silu_mul(s0.z, s1.z)) | (f32_to_bf16_rne_bits(silu_mul(s0.w, s1.w)) << 16);
+                *reinterpret_cast<uint2*>(h_out + aa * f + r0 + cq) = o;
+              } else {
+                *reinterpret_cast<float4*>(y_out + aa * d + r0 + cq) = s0;
+              }
             }
+            gg += cnt;
+            named_bar_sync(1, kDecWarps * 32);  // staged slots read before the next round refills them
           }
           named_bar_sync(1, kDecWarps * 32);
+#ifdef PZ_TRACE
+          if (dtid == 0) g_red[kW13][blockIdx.x][3] = gtimer();
+#endif
         }
       }
     };
@@ -897,6 +995,9 @@ int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, const uint8_
 #ifdef PZ_TRACE
 extern "C" __attribute__((visibility("default"))) int puzzle_debug_trace(void* dst, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(dst, g_trace, bytes);
+}
+extern "C" __attribute__((visibility("default"))) int puzzle_debug_red(void* dst, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(dst, g_red, bytes);
 }
 extern "C" __attribute__((visibility("default"))) int puzzle_debug_cta(void* dst, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(dst, g_cta, bytes);

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <vector>
+#include <string>
 #include "../../paper_2511_04805_b200/csrc/tc_ptx.cuh"
 using namespace pz;
 
@@ -45,12 +46,14 @@ __global__ void k_stream(const __grid_constant__ CUtensorMap tm, int rows_total,
 typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-int main() {
+int main(int argc, char** argv) {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   void* fnp; cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q);
   EncFn enc = (EncFn)fnp;
-  const long rows = 4 * 2 * 14336, cols = 4096;  // Mixtral w13 packed: 940 MB
+  // Mixtral w13 packed [4 x 2 x 14336, 4096] (940 MB) or, with argv[1] = "w2", w2 [4 x 4096, 14336]
+  const bool w2 = argc > 1 && std::string(argv[1]) == "w2";
+  const long rows = w2 ? 4 * 4096 : 4 * 2 * 14336, cols = w2 ? 14336 : 4096;
   uint16_t* buf; cudaMalloc(&buf, rows * cols * 2); cudaMemset(buf, 1, rows * cols * 2);
   int* sink; cudaMalloc(&sink, 4);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);

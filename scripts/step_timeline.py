@@ -101,3 +101,13 @@ if len(sys.argv) > 3:
         for s_, d_ in per_sm.items():
             gpc.setdefault(s_ // 18, []).append(np.mean(d_))
         print("  by SM-id block of 18:", {k2: round(float(np.mean(v2)), 1) for k2, v2 in sorted(gpc.items())})
+
+if os.environ.get("TIMELINE_DUMP"):
+    sm = np.zeros((2, 1024), np.uint32)
+    lib.puzzle_debug_smid.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    assert lib.puzzle_debug_smid(sm.ctypes.data, sm.nbytes) == 0
+    red = np.zeros((2, 1024, 8), np.uint64)
+    lib.puzzle_debug_red.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    assert lib.puzzle_debug_red(red.ctypes.data, red.nbytes) == 0
+    np.savez(os.environ["TIMELINE_DUMP"], cta=cta, wt=wt, sm=sm, rt=rt, red=red,
+             logits=logits.float().cpu().numpy(), slot=layer.expert_slot.cpu().numpy())
