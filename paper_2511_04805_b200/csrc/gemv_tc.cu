@@ -54,6 +54,9 @@ constexpr int kWBytes = kRows * kBK * 2;         // 16 KB packed words per stage
 #ifndef PZ_TC_WST  // W ring depth of the decode configuration (tuning knob)
 #define PZ_TC_WST 4
 #endif
+#ifndef PZ_W2_EARLY  // w2: only the X producer waits for w13 (weights stream during w13's tail)
+#define PZ_W2_EARLY 1
+#endif
 #ifndef PZ_TC_XST  // X ring depth of the decode configuration (tuning knob)
 #define PZ_TC_XST 5
 #endif
@@ -459,7 +462,13 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   if (threadIdx.x == 0) g_cta[kW13][blockIdx.x][0] = gtimer();
 #endif
   if (warp == 1) ptx::tmem_alloc<C::kTmemCols>(&c.tmem_base);
-  pdl_wait();     // route / gather / previous projection complete and visible
+  // w13 reads the routing tables below: wait for the route kernel. w2 (PZ_W2_EARLY) only waits
+  // in its X producer, before the first load of h (the one input w13 writes): its weight stream,
+  // decode and TMEM A buffers fill during w13's tail. The routing tables are complete by then:
+  // this grid launches only once every w13 CTA has passed its own wait (route complete) and
+  // triggered; they are read through L2 (__ldcg). Partial slots (shared with w13) are written
+  // only after an MMA, i.e. after that wait.
+  if (kW13 || !PZ_W2_EARLY) pdl_wait();
 #ifdef PZ_TRACE
   if (threadIdx.x == 0) {
     g_after_wait[kW13][blockIdx.x] = gtimer();
@@ -469,9 +478,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   }
 #endif
   pdl_trigger();  // the next kernel may begin its prologue as CTAs of this one retire
-  const int n_active = *n_active_ptr;
-  for (int i = threadIdx.x; i < n_active; i += blockDim.x) c.s_active[i] = active_pairs[i];
-  for (int i = threadIdx.x; i <= 2 * n_bucket_pairs; i += blockDim.x) c.s_off[i] = bucket_off[i];
+  const int n_active = __ldcg(n_active_ptr);
+  for (int i = threadIdx.x; i < n_active; i += blockDim.x) c.s_active[i] = __ldcg(active_pairs + i);
+  for (int i = threadIdx.x; i <= 2 * n_bucket_pairs; i += blockDim.x) c.s_off[i] = __ldcg(bucket_off + i);
   __syncthreads();
   if (threadIdx.x == 0) {  // work items per active pair: row blocks x token passes
     int run = 0;
@@ -559,6 +568,12 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     Ring sq{0, 0}, x{0, 0};
     int tx = 0;
     (void)tx;
+    if (!kW13 && PZ_W2_EARLY) {
+      pdl_wait();  // h (w13's output) complete and visible
+#ifdef PZ_TRACE
+      g_after_wait[kW13][blockIdx.x] = gtimer();
+#endif
+    }
     // this CTA's first piece signals its item's reducer when the item is split and started
     // in an earlier CTA's range
     int sig_item = s_begin < s_end && s_begin % nk != 0 ? s_begin / nk : -1;
