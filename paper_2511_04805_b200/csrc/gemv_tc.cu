@@ -478,17 +478,27 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   }
 #endif
   pdl_trigger();  // the next kernel may begin its prologue as CTAs of this one retire
-  const int n_active = __ldcg(n_active_ptr);
-  for (int i = threadIdx.x; i < n_active; i += blockDim.x) c.s_active[i] = __ldcg(active_pairs + i);
+  // routing tables in one round trip (all P slots of active_pairs, whatever n_active is; this
+  // setup is on w13's critical path: ~4 us from the wait to the first weight load before)
   for (int i = threadIdx.x; i <= 2 * n_bucket_pairs; i += blockDim.x) c.s_off[i] = __ldcg(bucket_off + i);
+  for (int i = threadIdx.x; i < n_bucket_pairs; i += blockDim.x) c.s_active[i] = __ldcg(active_pairs + i);
+  const int n_active = __ldcg(n_active_ptr);
   __syncthreads();
-  if (threadIdx.x == 0) {  // work items per active pair: row blocks x token passes
+  if (warp == 0) {  // work items per active pair (row blocks x token passes): warp prefix sum
     int run = 0;
-    for (int z = 0; z < n_active; ++z) {
-      c.s_item[z] = run;
-      run += n_rb * npass_of(load_pair(c.s_off, c.s_active[z]), NX);
+    for (int z0 = 0; z0 < n_active; z0 += 32) {
+      const int z = z0 + lane;
+      const int own = z < n_active ? n_rb * npass_of(load_pair(c.s_off, c.s_active[z]), NX) : 0;
+      int v = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      if (z < n_active) c.s_item[z] = run + v - own;
+      run += __shfl_sync(0xffffffffu, v, 31);
     }
-    c.s_item[n_active] = run;
+    if (lane == 0) c.s_item[n_active] = run;
   }
   ptx::tc_fence_before();
   __syncthreads();
