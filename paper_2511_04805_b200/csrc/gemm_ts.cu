@@ -43,7 +43,7 @@
 namespace pz {
 
 #ifdef PZ_TRACE  // per-stage pipeline timeline of CTA PZ_TRACE of the w13 launch (scripts/trace_ts.py)
-__device__ unsigned long long g_tst[14][4096];  // 13: decoder reaches stage (before the W wait)
+__device__ unsigned long long g_tst[18][4096];  // 14-17: epilogue internals (see the epilogue)  // 13: decoder reaches stage (before the W wait)
 __device__ unsigned long long g_tsc[2][1024][2];  // [kernel][cta] {start after wait, end}
 __device__ __forceinline__ unsigned long long ts_gtimer() {
   unsigned long long t;
@@ -513,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       mbar_wait_ts(&c.accfull[half], accph);
       accph ^= 1;
       if (warp == kW_EPI0 && lane == 0) PZ_TS(8, te);
+      if (warp == kW_EPI0 + 4 && lane == 0) PZ_TS(17, te);  // half 1's accumulator seen
       ptx::tc_fence_after();
       auto process = [&](const uint32_t(&v)[16], int c0) {
         if (kW13) {
@@ -556,12 +557,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
           }
         }
       };
+      {
       // 16 token columns per step, the next step's TMEM load in flight while this one is
       // processed (nh is a multiple of 16)
       uint32_t ra[16], rb[16];
       if (nh > 0) ptx::tmem_ld_32x32b_x16(acc_t, ra);
       for (int c0 = 0; c0 < nh; c0 += 32) {
         ptx::tmem_ld_wait();
+        if (c0 == 0 && warp == kW_EPI0 && lane == 0) PZ_TS(14, te);  // first TMEM load landed
         if (c0 + 16 < nh) ptx::tmem_ld_32x32b_x16(acc_t + c0 + 16, rb);
         process(ra, c0);
         if (c0 + 16 >= nh) break;
@@ -569,6 +572,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
         if (c0 + 32 < nh) ptx::tmem_ld_32x32b_x16(acc_t + c0 + 32, ra);
         process(rb, c0 + 16);
       }
+      }
+      if (warp == kW_EPI0 && lane == 0) PZ_TS(15, te);      // half 0 (quarter 0) processed
+      if (warp == kW_EPI0 + 4 && lane == 0) PZ_TS(16, te);  // half 1 (quarter 0) processed
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_ts(&c.accempty[half]);

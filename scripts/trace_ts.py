@@ -24,7 +24,7 @@ for _ in range(3):
     layer.forward(hidden, logits, cfg.top_k, cfg.renormalize, path=pz.PATH_TS)
 torch.cuda.synchronize()
 lib = pz.load_library()
-ev = np.zeros((14, 4096), np.uint64)
+ev = np.zeros((18, 4096), np.uint64)
 cc = np.zeros((2, 1024, 2), np.uint64)
 lib.puzzle_debug_ts.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t]
 assert lib.puzzle_debug_ts(ev.ctypes.data, ev.nbytes, cc.ctypes.data, cc.nbytes) == 0
@@ -74,3 +74,13 @@ print("W: decoder words(s)->W issue(s+4)", med(e[0, ss + 4] - e[2, ss]), "| W is
 print("decoder: reach(s)->words(s)", med(e[2, ss] - e[13, ss]), "(W wait) | W issue(s)->reach(s)", med(e[13, ss] - e[0, ss]),
       "| Afree(s)-words(s)", med(e[3, ss] - e[2, ss]), "(A wait) | afull(s)->reach(s+1)", med(e[13, ss + 1] - e[4, ss]))
 print("MMA0: issued(s)->xfull(s+1)", med(e[5, ss + 1] - e[7, ss]), "| xfull->afull", med(e[6, ss] - e[5, ss]))
+
+# epilogue internals per item (events 8 accfull[0] seen, 14 first TMEM load landed, 15 half 0
+# processed, 17 accfull[1] seen, 16 half 1 processed, 9 item end); MMA0 first issue of the next item
+ni = int((ev[9] > 0).sum())
+if ni and (ev[15, :ni] > 0).all():
+    E = ev[:, :ni].astype(np.int64)
+    print("epilogue internals (median us): accfull0->first load %.2f | first load->half0 processed %.2f | "
+          "half0 processed->item end %.2f | accfull1 - accfull0 %.2f | accfull1->half1 processed %.2f" % (
+              np.median(E[14] - E[8]) / 1e3, np.median(E[15] - E[14]) / 1e3, np.median(E[9] - E[15]) / 1e3,
+              np.median(E[17] - E[8]) / 1e3, np.median(E[16] - E[17]) / 1e3))
