@@ -63,6 +63,17 @@ def test_tiny_config_exact_shape(pz):
     assert_close(got, ref, "tiny")
 
 
+@pytest.mark.parametrize("T", [48, 64])
+def test_decode_split_item_many_pieces(pz, T):
+    """Stream-K reduction with many pieces per item (gemv_tc.cu reducer): one pair and
+    d_ff = 8192, so a w2 item (128 rows x 128 K-stages) spans ~16 CTAs of ~8 stages and the
+    pieces' slots (up to 64 rows each) exceed the W / X rings -- staged in several rounds
+    with the running sum carried in staged slot 0."""
+    cfg = synth.MoEConfig("many_pieces", 23, 256, 8192, 2, 1, True)
+    got, ref = _run(pz, cfg, T, pz.PATH_GEMV)
+    assert_close(got, ref, f"many pieces T={T}")
+
+
 def test_skewed_routing_all_tokens_one_pair(pz):
     """Every token routed to the same pair (>64 tokens per position: multiple passes)."""
     cfg = synth.MoEConfig("skew", 8, 128, 256, 8, 2, True)

@@ -84,6 +84,14 @@ def test_quant_forward_matches_oracle(pz, cfg, T):
     assert_close(got, ref, f"quant {cfg.name} T={T}")
 
 
+def test_quant_forward_split_item_many_pieces(pz):
+    """The reducer's multi-round staging with the quantised class's smaller rings (72 KB):
+    one pair, d_ff = 8192 (w2 items of 128 K-stages over CTAs of ~8 stages)."""
+    cfg = synth.MoEConfig("q_many_pieces", 24, 256, 8192, 2, 1, True)
+    got, ref = _run(pz, cfg, 64)
+    assert_close(got, ref, "quant many pieces")
+
+
 def test_quant_forward_skewed_multi_pass(pz):
     """One pair takes most tokens: several passes of 32 per position, split work items."""
     cfg = CFGS[0]
