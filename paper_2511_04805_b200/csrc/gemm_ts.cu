@@ -11,8 +11,7 @@
 // TMEM, the MMA reads it from there), and the packed slot is released as soon as the decoders
 // hold the words in registers.
 //
-// Persistent, one CTA per SM (512 TMEM columns), 13 warps (<= 4 per SM sub-partition, so up
-// to 128 registers per thread). A TMA instruction costs its issuing
+// Persistent, one CTA per SM (512 TMEM columns), 25 warps (72 registers per thread). A TMA instruction costs its issuing
 // thread ~165 ns whatever the box size (scripts/micro/tma_l2.cu, profiles/r02), so every
 // producer thread issues ONE box per stage:
 //   warp 0      W producer: claims work items (atomic ticket), TMA of each 64-wide K stage of
@@ -26,9 +25,10 @@
 //   warps 5-8   decoders: warp q = warp % 4 decodes tile rows 32q..32q+31 of a stage (Algorithm
 //               1 as one LOP3 + one exact bf16x2 multiply per 2 words, as in gemv_tc.cu) and
 //               stores them with tcgen05.st into A buffer j (of kAStages)
-//   warps 9-12  epilogue: drain the accumulators half by half (tcgen05.ld), SwiGLU (w13) or
-//               fp32 rows (w2) -> global; each half is released as soon as it is read, so the
-//               next item's MMAs on that half overlap the drain of the other
+//   warps 9-24  epilogue: drain the accumulators (tcgen05.ld), SwiGLU (w13) or fp32 rows (w2)
+//               -> global; two warps per (half, TMEM lane quarter) take alternate 16-column
+//               chunks (a half drains in 4.6 us instead of 5.3 with one warp each,
+//               profiles/r02/ts_epilogue.txt); each half is released as soon as it is read
 // TMEM columns: A buffers [0, 32 kAStages); accumulator half h at kAccCol + kNH h.
 // w13 tiles: TMEM lane quarter q = 16 gate rows (features f0 + 16q ..) then the same 16
 // features' up rows, so g and u of one d_ff index meet in lanes i, i + 16 of one warp.
@@ -94,7 +94,13 @@ constexpr int kIq = 4;                     // item queue W producer -> epilogue
 #endif
 constexpr int kDecWarps = PZ_TS_DECW;
 constexpr int kKH = 8 / kDecWarps;          // K halves per decoder warp
-constexpr int kEpiWarps = 8;                // 4 per accumulator half (one per TMEM lane quarter)
+#ifndef PZ_TS_EPIW
+#define PZ_TS_EPIW 16
+#endif
+// 4 or 8 per accumulator half: one or two per TMEM lane quarter (two split a half's 16-column
+// chunks between them, alternately)
+constexpr int kEpiWarps = PZ_TS_EPIW;
+constexpr int kEpiSplit = kEpiWarps / 8;
 constexpr int kThreads = 32 * (5 + kDecWarps + kEpiWarps);
 constexpr int kXMaps = kNH / 16;           // X box heights 16, 32, .., kNH rows
 constexpr int kW_DEC0 = 5, kW_EPI0 = 5 + kDecWarps;
@@ -490,7 +496,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
     // warp (q, half): TMEM lane quarter q of accumulator half `half`; the two halves drain in
     // parallel and are released independently
     const int q = warp & 3;
-    const int half = (warp - kW_EPI0) >> 2;
+    const int half = ((warp - kW_EPI0) >> 2) & 1;
+    const int part = (warp - kW_EPI0) >> 3;  // which of the quarter's kEpiSplit chunk streams
     const int row = 32 * q + lane;  // tile row == TMEM lane
     const uint32_t acc_t = tmem + ((uint32_t)(32 * q) << 16) + kAccCol + (uint32_t)(kNH * half);
     const bool up = lane >= 16;  // w13: lanes 16-31 hold the up rows of lanes 0-15's features
@@ -560,17 +567,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       {
       // 16 token columns per step, the next step's TMEM load in flight while this one is
       // processed (nh is a multiple of 16)
+      // this warp's chunks: 16 part, 16 part + cs, ... (cs = 16 kEpiSplit)
       uint32_t ra[16], rb[16];
-      if (nh > 0) ptx::tmem_ld_32x32b_x16(acc_t, ra);
-      for (int c0 = 0; c0 < nh; c0 += 32) {
+      constexpr int cs = 16 * kEpiSplit;
+      if (16 * part < nh) ptx::tmem_ld_32x32b_x16(acc_t + 16 * part, ra);
+      for (int c0 = 16 * part; c0 < nh; c0 += 2 * cs) {
         ptx::tmem_ld_wait();
         if (c0 == 0 && warp == kW_EPI0 && lane == 0) PZ_TS(14, te);  // first TMEM load landed
-        if (c0 + 16 < nh) ptx::tmem_ld_32x32b_x16(acc_t + c0 + 16, rb);
+        if (c0 + cs < nh) ptx::tmem_ld_32x32b_x16(acc_t + c0 + cs, rb);
         process(ra, c0);
-        if (c0 + 16 >= nh) break;
+        if (c0 + cs >= nh) break;
         ptx::tmem_ld_wait();
-        if (c0 + 32 < nh) ptx::tmem_ld_32x32b_x16(acc_t + c0 + 32, ra);
-        process(rb, c0 + 16);
+        if (c0 + 2 * cs < nh) ptx::tmem_ld_32x32b_x16(acc_t + c0 + 2 * cs, ra);
+        process(rb, c0 + cs);
       }
       }
       if (warp == kW_EPI0 && lane == 0) PZ_TS(15, te);      // half 0 (quarter 0) processed
