@@ -11,15 +11,17 @@
 // TMEM, the MMA reads it from there), and the packed slot is released as soon as the decoders
 // hold the words in registers.
 //
-// Persistent, one CTA per SM (512 TMEM columns), 25 warps (72 registers per thread). A TMA instruction costs its issuing
-// thread ~165 ns whatever the box size (scripts/micro/tma_l2.cu, profiles/r02), so every
-// producer thread issues ONE box per stage:
-//   warp 0      W producer: claims work items (atomic ticket), TMA of each 64-wide K stage of
+// Persistent, one CTA per SM (512 TMEM columns) in clusters of two, 25 warps (72 registers per
+// thread). A TMA instruction costs its issuing thread ~165 ns whatever the box size
+// (scripts/micro/tma_l2.cu, profiles/r02), so every producer thread issues ONE box per stage:
+//   warp 0      W producer: walks the cluster's items (static round robin over clusters; the
+//               two CTAs take adjacent row blocks of one token chunk), TMA of each 64-wide K stage of
 //               the PACKED 128-row weight tile (w13: one 3-D box = 64 gate + the same features'
 //               64 up rows) into a kWStages ring (released by the decoders once read); queues
 //               every stage for the X producers and every item for the epilogue
-//   warps 1, 2  X producers, one per token half h: the half's token rows (one box of 32..kNH
-//               rows) into its own kXStages ring (released by that half's MMA commits)
+//   warps 1, 2  X producers, one per token half h: the half's token rows (one box of 16..kNH
+//               rows, loaded by CTA h of the cluster and multicast into both) into its own
+//               kXStages ring (released by both CTAs' half-h MMA commits)
 //   warps 3, 4  MMA issuers, one per token half (N = N0 + N1, fixed TMEM column ranges):
 //               tcgen05.mma.kind::f16, A = decoded stage in TMEM, B = token rows from smem
 //   warps 5-8   decoders: warp q = warp % 4 decodes tile rows 32q..32q+31 of a stage (Algorithm
