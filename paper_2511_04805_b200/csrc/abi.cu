@@ -191,12 +191,13 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   p.n_assign = T * k;
   p.max_active = (int)std::min<int64_t>(L->n_pairs, p.n_assign);
   // The decode-shape kernels stream each touched pair once per pass of 32 tokens per position:
-  // they win while an expert averages <= 64 tokens (<= 2 passes; measured crossover: Mixtral
-  // T 256 / 512, Qwen1.5 T 512 / 1024, DeepSeek T 512 / 1024, profiles/r02/crossover.txt).
+  // they win while an expert averages < 64 tokens (<= 2 passes; measured crossover: Mixtral
+  // T 128 / 256, Qwen1.5 T 512 / 1024, DeepSeek T 512 / 1024, profiles/r02/crossover.txt and,
+  // after the routing fix, route_threshold.txt: at exactly 64 (Mixtral T 256) TS is 7 % ahead).
   // Heavier batches: the decode-into-TMEM prefill kernel (gemm_ts.cu; ahead of or level with the
   // shared-memory-operand kernel on every config), else gemm_tc.cu.
   if (path == PUZZLE_PATH_AUTO)
-    path = (T <= kGemvMaxTokens || T * k <= kGemvMaxTokensPerExpert * (int64_t)L->n_experts) ? PUZZLE_PATH_GEMV
+    path = (T <= kGemvMaxTokens || T * k < kGemvMaxTokensPerExpert * (int64_t)L->n_experts) ? PUZZLE_PATH_GEMV
            : ts_supported(L->d_model, L->d_ff)                                                ? PUZZLE_PATH_TS
            : tc_supported(L->d_model, L->d_ff)                                                ? PUZZLE_PATH_TC
                                                                                               : PUZZLE_PATH_GEMV;

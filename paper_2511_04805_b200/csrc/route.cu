@@ -36,7 +36,12 @@ namespace {
 
 constexpr int kMaxTopK = 16;
 constexpr int kSmallThreads = 1024;
-constexpr int kSmallMaxAssign = 4096;  // single-CTA path keeps the assignment list in smem
+// One CTA routes while T x k <= kSmallMaxAssign and T x E <= kSmallMaxScores (its top-k is T
+// warp-serial selections over E logits); beyond, the three grids. Measured (profiles/r02/
+// route_threshold.txt): the single CTA took 33 / 71 / 134 us at Mixtral T 512, Qwen1.5 T 512 /
+// 1024 (the old bound T k <= 4096), the three grids ~30-35 us at every T <= 1024.
+constexpr int kSmallMaxAssign = 512;
+constexpr int kSmallMaxScores = 4096;
 constexpr int64_t kDecMaxTokens = 64;   // two-grid decode routing
 
 // One warp routes token t. Rank selection: lane l holds the logits of experts 32 i + l
@@ -476,7 +481,7 @@ static int per_lane(int E) {
   return per;
 }
 
-bool route_is_small(int64_t T, int k) { return T * k <= kSmallMaxAssign; }
+bool route_is_small(int64_t T, int k, int E) { return T * k <= kSmallMaxAssign && T * E <= kSmallMaxScores; }
 
 // Decode-batch routing scratch: per-CTA histograms + packed bucket positions (ints).
 int64_t route_dec_scratch_ints(int64_t T, int k, int n_pairs) {
@@ -531,7 +536,7 @@ int launch_route(const float* logits, int64_t T, int E, int k, int renorm, const
   if (E > kMaxExperts) return fail(PUZZLE_ERR_UNSUPPORTED, "n_experts > 512");
   const int nb = 2 * n_pairs;
   if (rows_written) *rows_written = false;
-  if (route_is_small(T, k)) {
+  if (route_is_small(T, k, E)) {
     {
       ProfScope _ps("route", stream);
       const int per = per_lane(E);
