@@ -27,6 +27,7 @@ int launch_route(const float*, int64_t, int, int, int, const int32_t*, int, int3
                  bool*, cudaStream_t);
 int launch_active_pairs(const int32_t*, int, int32_t*, int32_t*, cudaStream_t);
 int64_t route_dec_scratch_ints(int64_t T, int k, int n_pairs);
+bool route_dec_fits(int64_t T, int n_pairs);
 int launch_route_dec(const float*, int64_t, int, int, int, const int32_t*, int, int32_t*, float*, int32_t*, int32_t*,
                      int32_t*, int32_t*, int32_t*, int32_t*, int, int32_t*, const uint16_t*, int, uint16_t*,
                      cudaStream_t);
@@ -230,7 +231,7 @@ Layout make_layout(const puzzle_moe_layer* L, const Plan& p) {
   // stream-K partial slots: 2 per CTA x 2 positions x tokens of a pass x 128 fp32
   o.part = take(p.path == PUZZLE_PATH_GEMV ? gemv_tc_part_floats() * 4 : 0);
   o.x_perm = take(na * d * 2);
-  o.route_scratch = take((size_t)std::max<int64_t>(2 * 2 * (int64_t)P, p.T <= kGemvMaxTokens
+  o.route_scratch = take((size_t)std::max<int64_t>(2 * 2 * (int64_t)P, route_dec_fits(p.T, (int)P)
                                                                           ? route_dec_scratch_ints(p.T, p.k, (int)P)
                                                                           : 0) * 4);
   o.total = off;
@@ -461,7 +462,9 @@ static int forward_impl(const puzzle_moe_layer* L, const uint16_t* hidden, const
   cudaStream_t s = (cudaStream_t)stream;
   bool rows_written = false;
   int rc;
-  if (T <= kGemvMaxTokens) {  // decode batches: two-grid routing with the row gather fused
+  // two-grid routing with the row gather fused (decode and intermediate batches: one top-k CTA per
+  // 8 tokens, the slots from per-CTA histograms); larger batches: route.cu's single CTA / three grids
+  if (route_dec_fits(T, L->n_pairs)) {
     rc = launch_route_dec(logits, T, L->n_experts, k, renorm, L->expert_slot, L->n_pairs,
                           at<int32_t>(ws, lay.topk_idx), at<float>(ws, lay.topk_gate), at<int32_t>(ws, lay.bucket_off),
                           at<int32_t>(ws, lay.assign_token), at<int32_t>(ws, lay.assign_of),

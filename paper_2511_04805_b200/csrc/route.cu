@@ -42,7 +42,10 @@ constexpr int kSmallThreads = 1024;
 // 1024 (the old bound T k <= 4096), the three grids ~30-35 us at every T <= 1024.
 constexpr int kSmallMaxAssign = 512;
 constexpr int kSmallMaxScores = 4096;
-constexpr int64_t kDecMaxTokens = 64;   // two-grid decode routing
+// Two-grid routing (top-k grid + scatter grid, deterministic slot order, row gather fused) up to
+// kDecMaxTokens tokens while the scatter grid's per-CTA histogram prefix fits the default 48 KB
+// of dynamic shared memory (route_dec_fits); the forward's larger batches take the three grids.
+constexpr int64_t kDecMaxTokens = 512;
 
 // One warp routes token t. Rank selection: lane l holds the logits of experts 32 i + l
 // (i < PER); each counts how many of the E logits rank above each of its own (larger logit,
@@ -489,13 +492,18 @@ int64_t route_dec_scratch_ints(int64_t T, int k, int n_pairs) {
 }
 
 // Routing + fused row gather for T <= kDecMaxTokens: two multi-CTA kernels (see above).
+bool route_dec_fits(int64_t T, int n_pairs) {
+  const int64_t n_hist = (T + kDecTokensPerCta - 1) / kDecTokensPerCta;
+  return T <= kDecMaxTokens && n_hist * 2 * n_pairs * (int64_t)sizeof(int32_t) <= 48 * 1024;
+}
+
 int launch_route_dec(const float* logits, int64_t T, int E, int k, int renorm, const int32_t* expert_slot,
                      int n_pairs, int32_t* topk_idx, float* topk_gate, int32_t* bucket_off, int32_t* assign_token,
                      int32_t* assign_of, int32_t* active_pairs, int32_t* n_active, int32_t* zero_ptr, int n_zero,
                      int32_t* scratch, const uint16_t* hidden, int d, uint16_t* x_perm, cudaStream_t stream) {
   if (k > kMaxTopK) return fail(PUZZLE_ERR_UNSUPPORTED, "top_k > 16 is not supported by the route kernel");
   if (E > kMaxExperts) return fail(PUZZLE_ERR_UNSUPPORTED, "n_experts > 512");
-  if (T > kDecMaxTokens) return fail(PUZZLE_ERR_UNSUPPORTED, "decode routing takes <= 64 tokens");
+  if (!route_dec_fits(T, n_pairs)) return fail(PUZZLE_ERR_UNSUPPORTED, "two-grid routing: too many tokens");
   const int nb = 2 * n_pairs;
   const int n_hist = (int)((T + kDecTokensPerCta - 1) / kDecTokensPerCta);
   int32_t* hist = scratch;
