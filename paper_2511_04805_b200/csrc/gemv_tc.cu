@@ -787,7 +787,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           named_bar_sync(1, kDecWarps * 32);
           // Sum the slots of CTAs g_first .. g_last in CTA order (from 0). The active rows of
           // every slot are staged into the idle W / X rings by two TMA bulk copies per slot (one
-          // thread, all in flight at once), then summed from shared memory; slots beyond the
+          // per lane of the first decoder warp, all in flight at once), then summed from shared memory; slots beyond the
           // rings' capacity are staged in further rounds, the running sum carried in staged slot
           // 0. The rings are idle: this is the CTA's last piece and its MMAs have completed.
           // Mixtral w2 (3 slots x 35 rows): 8.6 us with per-thread float4 loads, 5.6 us staged
@@ -806,18 +806,21 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           uint32_t red_ph = 0;  // one reduction per CTA (its last piece): red_bar phases from 0
           for (int gg = g_first, k0 = 0; gg <= g_last; k0 = 1) {
             const int cnt = min(m - k0, g_last - gg + 1);
-            if (dtid == 0) {  // two bulk copies per slot: its position-0 rows, its position-1 rows
-              // generic-proxy data (the acquired partials; staged rows read by the last round)
-              // before async-proxy accesses
-              asm volatile("fence.proxy.async;" ::: "memory");
-              ptx::mbar_arrive_expect_tx(&c.red_bar, (uint32_t)(cnt * n_rows) * kRowB);
-              for (int k = 0; k < cnt; ++k) {
-                const int gk = gg + k;
-                const float* src = part + (size_t)(2 * gk + (s.item == sk.begin(gk) / nk ? 0 : 1)) * kSlot;
-                const uint32_t dst = smem_w + (uint32_t)(k0 + k) * n_rows * kRowB;
-                if (s.n0) bulk_g2s(dst, src, (uint32_t)s.n0 * kRowB, &c.red_bar, drop);
-                if (s.n1) bulk_g2s(dst + (uint32_t)s.n0 * kRowB, src + (size_t)NX * kRows, (uint32_t)s.n1 * kRowB,
-                                   &c.red_bar, drop);
+            if (dtid < 32) {  // two bulk copies per slot (its position-0 rows, its position-1 rows),
+                              // one per lane: a TMA instruction costs its issuing thread ~165 ns
+              if (dtid == 0) ptx::mbar_arrive_expect_tx(&c.red_bar, (uint32_t)(cnt * n_rows) * kRowB);
+              __syncwarp();
+              for (int l = dtid; l < 2 * cnt; l += 32) {
+                const int k = l >> 1, pos = l & 1, gk = gg + k;
+                const int rows = pos ? s.n1 : s.n0;
+                if (rows == 0) continue;
+                // generic-proxy data (the acquired partials; staged rows read by the last round)
+                // before async-proxy accesses
+                asm volatile("fence.proxy.async;" ::: "memory");
+                const float* src = part + (size_t)(2 * gk + (s.item == sk.begin(gk) / nk ? 0 : 1)) * kSlot +
+                                   (size_t)pos * NX * kRows;
+                const uint32_t dst = smem_w + (uint32_t)(k0 + k) * n_rows * kRowB + (uint32_t)(pos * s.n0) * kRowB;
+                bulk_g2s(dst, src, (uint32_t)rows * kRowB, &c.red_bar, drop);
               }
             }
             ptx::mbar_wait(&c.red_bar, red_ph);
