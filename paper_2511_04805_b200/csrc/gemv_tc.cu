@@ -169,6 +169,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ void st_f32_hint(float* a, float v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void ptx_sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
 __device__ __forceinline__ float4 ptx_lds_f4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
@@ -425,6 +428,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   constexpr uint32_t kWStageBytes = C::kWSlot;  // bytes of one W stage (codes: 1 B each)
   constexpr int kWStages = C::kWStages, kXStages = C::kXStages, kXBytes = C::kXBytes, kXPos = C::kXPos;
   constexpr int kSlot = 2 * NX * kRows;  // floats per partial slot
+  constexpr uint32_t kRowB = kRows * 4;   // one slot row (a (position, token) of 128 outputs): 512 bytes
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_w = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;  // == smem, shared window
@@ -710,6 +714,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       accph ^= 1;
       ptx::tc_fence_after();
       const bool whole = s.kb0 == 0 && s.kb1 == nk;  // the item is not split: final outputs
+      const bool reducer = !whole && g == sk.owner(s.item * nk);  // the item's first piece: this CTA sums
       const int pos = kh;
       const int np = pos ? s.n1 : s.n0;
       const int offp = (pos ? s.pt.off1 : s.pt.off0) + s.base;  // first assignment of this warp
@@ -725,7 +730,14 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * acc_scale);
-        if (!whole) {
+        if (!whole && reducer) {
+          // the reducer's own piece (the sum's first term): straight into staged slot 0 of the
+          // W ring -- idle now: every stage was decoded before the MMAs completed
+          const uint32_t a0 = smem_w + (uint32_t)((pos ? s.n0 : 0) + c0) * kRowB + (uint32_t)prow * 4u;
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < np) ptx_sts_f32(a0 + (uint32_t)i * kRowB, __uint_as_float(r[i]));
+        } else if (!whole) {
           // evict_last: the reducer reads these back up to a whole range later, after hundreds
           // of MB of weights have streamed through L2; from HBM, behind the weight stream's
           // queues, that read took ~5 us (scripts/red_stats.py)
@@ -777,7 +789,6 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
 #endif
           named_bar_sync(1, kDecWarps * 32);
           if (dtid == 0) {
-            __threadfence();
             while (ld_acquire_gpu(&counters[s.item]) < g_last - g_first) __nanosleep(64);
             counters[s.item] = 0;  // ready for the next call on this stream
 #ifdef PZ_TRACE
@@ -797,20 +808,23 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           const int cols = kW13 ? kRows / 2 : min(kRows, d - r0);  // outputs of this tile, multiple of 4
           const int q4 = cols / 4;
           const int n_rows = s.n0 + s.n1;                           // active (position, token) rows
-          constexpr uint32_t kRowB = kRows * 4;                     // one slot row: 512 bytes
           constexpr uint32_t kRing = kWStages * kWStageBytes + kXStages * kXBytes;
           static_assert(kRing >= 2u * (2 * NX) * kRowB, "reducer: two full slots fit the rings");
           const int m = min(g_last - g_first + 1, (int)(kRing / (n_rows * kRowB)));  // >= 2 slots
           const int n_units = n_rows * q4;
           const uint64_t drop = l2_policy_evict_first();  // the partials are dead once read
           uint32_t red_ph = 0;  // one reduction per CTA (its last piece): red_bar phases from 0
+          // staged position 0 of the first round already holds this CTA's own piece (stored from
+          // TMEM above); every other slot comes in by bulk copies
           for (int gg = g_first, k0 = 0; gg <= g_last; k0 = 1) {
             const int cnt = min(m - k0, g_last - gg + 1);
-            if (dtid < 32) {  // two bulk copies per slot (its position-0 rows, its position-1 rows),
-                              // one per lane: a TMA instruction costs its issuing thread ~165 ns
-              if (dtid == 0) ptx::mbar_arrive_expect_tx(&c.red_bar, (uint32_t)(cnt * n_rows) * kRowB);
+            const int skip = gg == g_first ? 1 : 0;  // own piece: not copied
+            if (dtid < 32 && cnt > skip) {  // two bulk copies per slot (its position-0 rows, its
+                                            // position-1 rows), one per lane: a TMA instruction
+                                            // costs its issuing thread ~165 ns
+              if (dtid == 0) ptx::mbar_arrive_expect_tx(&c.red_bar, (uint32_t)((cnt - skip) * n_rows) * kRowB);
               __syncwarp();
-              for (int l = dtid; l < 2 * cnt; l += 32) {
+              for (int l = dtid + 2 * skip; l < 2 * cnt; l += 32) {
                 const int k = l >> 1, pos = l & 1, gk = gg + k;
                 const int rows = pos ? s.n1 : s.n0;
                 if (rows == 0) continue;
@@ -823,8 +837,10 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
                 bulk_g2s(dst, src, (uint32_t)rows * kRowB, &c.red_bar, drop);
               }
             }
-            ptx::mbar_wait(&c.red_bar, red_ph);
-            red_ph ^= 1;
+            if (cnt > skip) {
+              ptx::mbar_wait(&c.red_bar, red_ph);
+              red_ph ^= 1;
+            }
 #ifdef PZ_TRACE
             if (k0 == 0 && (dtid & 31) == 0) g_red[kW13][blockIdx.x][4 + (dtid >> 7)] = gtimer();  // warps 0 / 4 loads landed
 #endif
