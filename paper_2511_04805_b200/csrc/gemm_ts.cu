@@ -37,6 +37,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -96,6 +97,9 @@ constexpr int kIq = 4;                     // item queue W producer -> epilogue
 #endif
 constexpr int kDecWarps = PZ_TS_DECW;
 constexpr int kKH = 8 / kDecWarps;          // K halves per decoder warp
+#ifndef PZ_TS_PAIR  // a pair whose two buckets each fit a half (<= kNH tokens) is ONE item: half h
+#define PZ_TS_PAIR 1  // = bucket 2p + h, each weight stage streamed and decoded once for both experts
+#endif
 #ifndef PZ_TS_EPIW
 #define PZ_TS_EPIW 16
 #endif
@@ -129,20 +133,27 @@ struct alignas(16) Ctl {
   int16_t ncw[kMaxBuckets];              // chunk width (multiple of 32, <= kNmax)
   int32_t pair_off[kMaxBuckets / 2 + 1]; // first item of each pair (pair-major order)
   uint8_t dense[kMaxBuckets / 2];        // slot holds plain bf16 weights: no decode (R20)
+  uint8_t paired[kMaxBuckets / 2];       // PZ_TS_PAIR: the pair's two buckets form one item per row block
 };
 
 constexpr size_t kSmemBytes = 1024 + (size_t)kWStages * kWBytes + 2 * (size_t)kXStages * kXBytes + sizeof(Ctl);
 static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 
-// A work item: bucket b, row block rb (128 weight rows), token chunk c of the bucket.
+// A work item: row block rb (128 weight rows) of the pair b / 2 and either a token chunk of bucket
+// b (its tokens split over the two halves) or, `paired`, both buckets of the pair (half h = bucket
+// 2 (b / 2) + h, decoded for its own position). Half h: rows [base_h, base_h + nv_h) of the
+// bucket-ordered token rows, MMA width n_h (a multiple of 16 >= nv_h).
 struct Item {
   int b, rb, row0, nvalid, n0, n1;
-  bool ghost;  // rb >= n_rb: the odd row-block count's spare CTA of a cluster (no outputs)
+  int base1, nv0, nv1;  // half 1's first row; valid tokens of half 0 / 1 (half 0 starts at row0)
+  bool ghost;   // rb >= n_rb: the odd row-block count's spare CTA of a cluster (no outputs)
+  bool paired;
 };
 
 // Item order: pair-major, then row-block pair, then (position, chunk): the clusters of one wave
 // work on a band of row blocks of ONE pair, whose packed tiles and token rows are re-read from
 // L2. A cluster item is two adjacent row blocks of one token chunk: CTA `rank` takes 2 rbp + rank.
+template <bool kPair>
 __device__ __forceinline__ Item item_info(const Ctl& c, int item, int n_pairs, int rank, int n_rb) {
   PZ_DCHECK(item >= 0 && item < c.n_items);
   int lo = 0, hi = n_pairs - 1;  // last pair with pair_off[p] <= item
@@ -151,12 +162,26 @@ __device__ __forceinline__ Item item_info(const Ctl& c, int item, int n_pairs, i
     if (c.pair_off[mid] <= item) lo = mid; else hi = mid - 1;
   }
   const int p = lo;
-  const int c0 = c.nch[2 * p], c01 = c0 + c.nch[2 * p + 1];
+  const bool paired = kPair && c.paired[p];
+  const int c0 = c.nch[2 * p], c01 = paired ? 1 : c0 + c.nch[2 * p + 1];
   const int rem = item - c.pair_off[p];
   Item it;
   const int rbp = rem / c01;
   it.rb = 2 * rbp + rank;
   it.ghost = it.rb >= n_rb;
+  it.paired = paired;
+  if (paired) {
+    it.b = 2 * p;
+    it.row0 = c.off[2 * p];
+    it.base1 = c.off[2 * p + 1];
+    it.nv0 = c.off[2 * p + 1] - c.off[2 * p];
+    it.nv1 = c.off[2 * p + 2] - c.off[2 * p + 1];
+    it.nvalid = it.nv0 + it.nv1;
+    it.n0 = (it.nv0 + 15) & ~15;
+    it.n1 = (it.nv1 + 15) & ~15;
+    PZ_DCHECK(it.nv0 >= 1 && it.nv1 >= 1 && it.n0 <= kNH && it.n1 <= kNH && it.rb < n_rb + 1);
+    return it;
+  }
   const int r2 = rem - rbp * c01;
   it.b = 2 * p + (r2 >= c0);
   const int ch = r2 >= c0 ? r2 - c0 : r2;
@@ -166,6 +191,9 @@ __device__ __forceinline__ Item item_info(const Ctl& c, int item, int n_pairs, i
   const int n = (it.nvalid + 31) & ~31;  // MMA width: the live tokens rounded up to 32
   it.n0 = n >> 1;
   it.n1 = n >> 1;
+  it.base1 = it.row0 + it.n0;
+  it.nv0 = min(it.n0, it.nvalid);
+  it.nv1 = it.nvalid - it.nv0;
   PZ_DCHECK(p >= 0 && p < n_pairs && it.b < 2 * n_pairs && it.nvalid >= 1 && it.row0 >= c.off[it.b] &&
             it.row0 + it.nvalid <= c.off[it.b + 1] && n <= kNmax && it.rb < n_rb + 1);
   return it;
@@ -223,8 +251,15 @@ struct Ring {
   }
 };
 
-template <bool kW13>
-__global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
+// kPair: paired items (PZ_TS_PAIR) compiled in, with 8 epilogue warps (the pair decode needs the
+// registers); without, the kernel is the unpaired form with kEpiWarps epilogue warps
+template <bool kPair>
+constexpr int ts_epi_warps() { return kPair ? 8 : kEpiWarps; }
+template <bool kPair>
+constexpr int ts_threads() { return 32 * (5 + kDecWarps + ts_epi_warps<kPair>()); }
+
+template <bool kW13, bool kPair>
+__global__ void __launch_bounds__(ts_threads<kPair>(), 1) k_ts_experts(
     const __grid_constant__ CUtensorMap tm_w,  // packed w13 [2P][f][d] (3-D, {64, 64, 2} boxes) / w2 [P*d][f] (128-row boxes)
     const __grid_constant__ XMaps tm_x,        // token rows [n_rows][K] bf16, boxes of 16 (i + 1) rows
     const int32_t* __restrict__ bucket_off, int n_pairs, int K, int f, int d, int n_rb,
@@ -239,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
   Ctl& c = *reinterpret_cast<Ctl*>(smem + (size_t)kWStages * kWBytes + 2 * (size_t)kXStages * kXBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_buckets = 2 * n_pairs;
+  constexpr int kEW = ts_epi_warps<kPair>(), kES = kEW / 8;  // epilogue warps, chunk streams per quarter
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kWStages; ++s) {
@@ -260,11 +296,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
     }
     for (int s = 0; s < kIq; ++s) {
       ptx::mbar_init(&c.iqfull[s], 1);
-      ptx::mbar_init(&c.iqempty[s], kEpiWarps);
+      ptx::mbar_init(&c.iqempty[s], kEW);
     }
     for (int h = 0; h < 2; ++h) {
       ptx::mbar_init(&c.accfull[h], 1);
-      ptx::mbar_init(&c.accempty[h], kEpiWarps / 2);
+      ptx::mbar_init(&c.accempty[h], kEW / 2);
     }
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tm_w);
@@ -279,6 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
   for (int i = threadIdx.x; i <= n_buckets; i += blockDim.x) c.off[i] = bucket_off[i];
   for (int i = threadIdx.x; i < n_pairs; i += blockDim.x) c.dense[i] = pair_dense ? pair_dense[i] : 0;
   __syncthreads();
+  for (int i = threadIdx.x; i < n_pairs; i += blockDim.x) {
+    const int c0 = c.off[2 * i + 1] - c.off[2 * i], c1 = c.off[2 * i + 2] - c.off[2 * i + 1];
+    c.paired[i] = kPair && !c.dense[i] && c0 > 0 && c1 > 0 && c0 <= kNH && c1 <= kNH;
+  }
   for (int b = threadIdx.x; b < n_buckets; b += blockDim.x) {  // token chunks of each bucket
     const int cnt = c.off[b + 1] - c.off[b];
     const int nch = (cnt + kNmax - 1) / kNmax;
@@ -290,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
     int run = 0;
     for (int p = 0; p < n_pairs; ++p) {
       c.pair_off[p] = run;
-      run += ((n_rb + 1) >> 1) * (c.nch[2 * p] + c.nch[2 * p + 1]);
+      run += ((n_rb + 1) >> 1) * (c.paired[p] ? 1 : c.nch[2 * p] + c.nch[2 * p + 1]);
     }
     c.pair_off[n_pairs] = run;
     c.n_items = run;
@@ -316,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
         c.iq[iq.i] = item;
         ptx::mbar_arrive(&c.iqfull[iq.i]);
         iq.next<kIq>();
-        const Item it = item_info(c, item, n_pairs, rank, n_rb);
+        const Item it = item_info<kPair>(c, item, n_pairs, rank, n_rb);
         const int pair = it.b >> 1;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait_ts(&c.wempty[w.i], w.ph ^ 1);
@@ -369,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
         }
         if (h.x != cur) {
           cur = h.x;
-          it = item_info(c, cur, n_pairs, rank, n_rb);
+          it = item_info<kPair>(c, cur, n_pairs, rank, n_rb);
         }
         const int nh = half ? it.n1 : it.n0;
         const int box = nh >> 4;  // one box of exactly nh rows (nh % 16 == 0)
@@ -380,7 +420,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
         // multicast into the same slot of both (each CTA expects the bytes on its own barrier)
         ptx::mbar_arrive_expect_tx(&c.xfull[half][x.i], (uint32_t)box * 16 * (kBK * 2));
         if (rank == half)
-          ptx::tma_load_2d_multicast(sx, &tm_x.m[box - 1], &c.xfull[half][x.i], h.y * kBK, it.row0 + half * it.n0, 0x3);
+          ptx::tma_load_2d_multicast(sx, &tm_x.m[box - 1], &c.xfull[half][x.i], h.y * kBK,
+                                     kPair ? (half ? it.base1 : it.row0) : it.row0 + half * it.n0, 0x3);
         x.next<kXStages>();
       }
     }
@@ -401,25 +442,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       if (lane == 0) PZ_TS(half ? 10 : 5, tm_);
       if (h.x != cur) {
         cur = h.x;
-        it = item_info(c, cur, n_pairs, rank, n_rb);
+        it = item_info<kPair>(c, cur, n_pairs, rank, n_rb);
       }
       const int nh = half ? it.n1 : it.n0;
       if (h.y == 0) {
         mbar_wait_ts(&c.accempty[half], accph ^ 1);  // the previous item's half drained
         ptx::tc_fence_after();
       }
-      mbar_wait_ts(&c.afull[a.i], a.ph);
+      // a paired item's stage fills two A buffers (position 0, position 1): half h reads buffer h
+      Ring a1 = a;
+      if (kPair && it.paired) a1.next<kAStages>();
+      const Ring am = (kPair && it.paired && half) ? a1 : a;
+      mbar_wait_ts(&c.afull[am.i], am.ph);
       if (lane == 0) PZ_TS(half ? 11 : 6, tm_);
       ptx::tc_fence_after();
       if (nh > 0) {
         const uint32_t xs = smem_x + (uint32_t)(half * kXStages + x.i) * kXBytes;
-        const uint32_t ta = tmem + 32u * a.i;
+        const uint32_t ta = tmem + 32u * am.i;
         const uint32_t idesc = ptx::idesc_bf16_f32(128, (uint32_t)nh);
 #pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk)
           ptx::mma_bf16_ts_elect(acc, ta + 8 * kk, ptx::smem_desc_sw128(xs + 32 * kk), idesc, (h.y | kk) != 0);
       }
       ptx::mma_commit_elect(&c.aempty[a.i]);  // A buffer free once these MMAs complete
+      if (kPair && it.paired) ptx::mma_commit_elect(&c.aempty[a1.i]);  // both buffers: two commits each
       ptx::mma_commit_multicast_elect(&c.xempty[half][x.i], 0x3);  // token slot: in both CTAs (multicast reload)
       if (h.y == nk - 1) {
         ptx::mma_commit_elect(&c.accfull[half]);
@@ -429,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       ++tm_;
       x.next<kXStages>();
       a.next<kAStages>();
+      if (kPair && it.paired) a.next<kAStages>();
     }
   } else if (warp < kW_EPI0) {
     // ============================== decoders ==============================
@@ -453,8 +500,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       if (h.x < 0) break;
       if (h.x != cur) {
         cur = h.x;
-        const Item it = item_info(c, cur, n_pairs, rank, n_rb);
-        mode = c.dense[it.b >> 1] ? 2 : (it.b & 1);  // 0 / 1: packed position, 2: dense slot (pos 0)
+        const Item it = item_info<kPair>(c, cur, n_pairs, rank, n_rb);
+        // 0 / 1: packed position, 2: dense slot (pos 0), 3: paired item (both positions)
+        mode = (kPair && it.paired) ? 3 : c.dense[it.b >> 1] ? 2 : (it.b & 1);
       }
       const uint32_t st = smem_w + (uint32_t)w.i * kWBytes;
       uint4 v[4 * kKH];
@@ -464,34 +512,84 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       if (warp == kW_DEC0 && lane == 0) PZ_TS(2, td);
       if (lane == 0) mbar_arrive_ts(&c.wempty[w.i]);  // words in registers: the slot may refill
       w.next<kWStages>();
-      uint32_t dv[kKH][16];  // decoded while the A buffer may still be in use
+      // decode the stage for one position (MD: 0 / 1 packed position, 2 dense slot) into the next
+      // A buffer. The unpaired kernel keeps one copy with the position chosen at run time; the
+      // paired one (kPair) instantiates a copy per position -- a paired stage decodes position 0,
+      // then position 1 (the words stay in v) -- since a run-time choice costs the selects of all
+      // three forms per word (measured: paired Mixtral T 256 0.44 ms specialised, 0.66 not)
+      if constexpr (kPair) {
+        auto emit = [&](auto mdc) {
+          constexpr int MD = decltype(mdc)::value;
+          uint32_t dv[kKH][16];  // decoded while the A buffer may still be in use
 #pragma unroll
-      for (int i = 0; i < 4 * kKH; ++i) {
-        const uint32_t xs[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+          for (int i = 0; i < 4 * kKH; ++i) {
+            const uint32_t xs[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t xw = xs[j];
-          // |W^| * 2^48 (exponent field e' + 160 = e' | 0xA0, one LOP3); sign S and mask M of the
-          // position form +-2^-63 or +-0: one exact product leaves W^ * 2^-15 (rescaled in the
-          // epilogue); dense slots: the bf16 weight * 2^-15 to match
-          const uint32_t mag = (xw & 0x0FFF0FFFu) | orc;
-          dv[i >> 2][4 * (i & 3) + j] = mode == 2   ? bf16x2_mul(xw, 0x38003800u)
-                                        : mode == 0 ? bf16x2_mul(mag, xw & 0xA000A000u)
-                                                    : bf16x2_mul(mag, (xw * two) & 0xA000A000u);
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t xw = xs[j];
+              // |W^| * 2^48 (exponent field e' + 160 = e' | 0xA0, one LOP3); sign S and mask M of the
+              // position form +-2^-63 or +-0: one exact product leaves W^ * 2^-15 (rescaled in the
+              // epilogue); dense slots: the bf16 weight * 2^-15 to match
+              const uint32_t mag = (xw & 0x0FFF0FFFu) | orc;
+              dv[i >> 2][4 * (i & 3) + j] = MD == 2   ? bf16x2_mul(xw, 0x38003800u)
+                                            : MD == 0 ? bf16x2_mul(mag, xw & 0xA000A000u)
+                                                      : bf16x2_mul(mag, (xw * two) & 0xA000A000u);
+            }
+          }
+          mbar_wait_ts(&c.aempty[a.i], a.ph ^ 1);  // the MMAs that read this A buffer completed
+          if (warp == kW_DEC0 && lane == 0) PZ_TS(3, td);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < kKH; ++k) ptx::tmem_st_32x32b_x16(lane_tmem + 32u * a.i + 16u * (kh0 + k), dv[k]);
+          ptx::tmem_st_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_ts(&c.afull[a.i]);
+          a.next<kAStages>();
+        };
+        using P0 = std::integral_constant<int, 0>;
+        using P1 = std::integral_constant<int, 1>;
+        if (mode == 3) {
+          emit(P0{});
+          emit(P1{});
+        } else if (mode == 0) {
+          emit(P0{});
+        } else if (mode == 1) {
+          emit(P1{});
+        } else {
+          emit(std::integral_constant<int, 2>{});
         }
-      }
-      mbar_wait_ts(&c.aempty[a.i], a.ph ^ 1);  // the MMAs that read this A buffer completed
-      if (warp == kW_DEC0 && lane == 0) PZ_TS(3, td);
-      ptx::tc_fence_after();
+      } else {
+        const int MD = mode;
+        uint32_t dv[kKH][16];  // decoded while the A buffer may still be in use
 #pragma unroll
-      for (int k = 0; k < kKH; ++k) ptx::tmem_st_32x32b_x16(lane_tmem + 32u * a.i + 16u * (kh0 + k), dv[k]);
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_ts(&c.afull[a.i]);
+        for (int i = 0; i < 4 * kKH; ++i) {
+          const uint32_t xs[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t xw = xs[j];
+            // |W^| * 2^48 (exponent field e' + 160 = e' | 0xA0, one LOP3); sign S and mask M of the
+            // position form +-2^-63 or +-0: one exact product leaves W^ * 2^-15 (rescaled in the
+            // epilogue); dense slots: the bf16 weight * 2^-15 to match
+            const uint32_t mag = (xw & 0x0FFF0FFFu) | orc;
+            dv[i >> 2][4 * (i & 3) + j] = MD == 2   ? bf16x2_mul(xw, 0x38003800u)
+                                          : MD == 0 ? bf16x2_mul(mag, xw & 0xA000A000u)
+                                                    : bf16x2_mul(mag, (xw * two) & 0xA000A000u);
+          }
+        }
+        mbar_wait_ts(&c.aempty[a.i], a.ph ^ 1);  // the MMAs that read this A buffer completed
+        if (warp == kW_DEC0 && lane == 0) PZ_TS(3, td);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kKH; ++k) ptx::tmem_st_32x32b_x16(lane_tmem + 32u * a.i + 16u * (kh0 + k), dv[k]);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_ts(&c.afull[a.i]);
+        a.next<kAStages>();
+      }
       if (warp == kW_DEC0 && lane == 0) PZ_TS(4, td);
       ++td;
-      a.next<kAStages>();
     }
   } else {
     // ============================== epilogue ==============================
@@ -516,9 +614,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       if (lane == 0) mbar_arrive_ts(&c.iqempty[iq.i]);
       iq.next<kIq>();
       if (item < 0) break;
-      const Item it = item_info(c, item, n_pairs, rank, n_rb);
+      const Item it = item_info<kPair>(c, item, n_pairs, rank, n_rb);
       const int nh = it.ghost ? 0 : (half ? it.n1 : it.n0);  // a ghost drains nothing
-      const int t0 = half * it.n0;  // first token of this half within the chunk
+      // this half's first row and valid tokens
+      const int hb = kPair ? (half ? it.base1 : it.row0) : it.row0 + half * it.n0;
+      const int hv = kPair ? (half ? it.nv1 : it.nv0) : it.nvalid - half * it.n0;
       mbar_wait_ts(&c.accfull[half], accph);
       accph ^= 1;
       if (warp == kW_EPI0 && lane == 0) PZ_TS(8, te);
@@ -529,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
           // lanes 0-15 hold g, lanes 16-31 u of the same 16 features: each lane sends its partner
           // the half of the 16 tokens it does not finish (gate lanes finish c0..c0+7, up lanes
           // c0+8..c0+15); independent chains per token (shuffles, then SFU math, then stores)
-          const int tok0 = t0 + c0 + (up ? 8 : 0);
+          const int tok0 = c0 + (up ? 8 : 0);  // first token (of this half) this lane finishes
           float gv[8], uv[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -541,8 +641,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
           float hf[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) hf[i] = silu_mul_fast(gv[i], uv[i]);
-          const int lim = min(min(8, it.nvalid - tok0), nh - c0 - (up ? 8 : 0));
-          uint16_t* dst = h_out + (size_t)(it.row0 + tok0) * f + it.rb * (kRows / 2) + 16 * q + (lane & 15);
+          const int lim = min(min(8, hv - tok0), nh - tok0);
+          uint16_t* dst = h_out + (size_t)(hb + tok0) * f + it.rb * (kRows / 2) + 16 * q + (lane & 15);
 #pragma unroll
           for (int i = 0; i < 8; i += 2) {
             const uint32_t pk = f32x2_to_bf16x2_rn(hf[i], hf[i + 1]);
@@ -554,8 +654,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
 #endif
           }
         } else {
-          float* dst = y_out + (size_t)(it.row0 + t0 + c0) * d + it.rb * kRows + row;  // d_model row
-          const int lim = min(min(16, it.nvalid - t0 - c0), nh - c0);
+          float* dst = y_out + (size_t)(hb + c0) * d + it.rb * kRows + row;  // d_model row
+          const int lim = min(min(16, hv - c0), nh - c0);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
 #ifdef PZ_TS_NOSTORE
@@ -571,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
       // processed (nh is a multiple of 16)
       // this warp's chunks: 16 part, 16 part + cs, ... (cs = 16 kEpiSplit)
       uint32_t ra[16], rb[16];
-      constexpr int cs = 16 * kEpiSplit;
+      constexpr int cs = 16 * kES;
       if (16 * part < nh) ptx::tmem_ld_32x32b_x16(acc_t + 16 * part, ra);
       for (int c0 = 16 * part; c0 < nh; c0 += 2 * cs) {
         ptx::tmem_ld_wait();
@@ -610,20 +710,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_ts_experts(
 #endif
 }
 
-}  // namespace
-
-bool ts_supported(int d, int f) { return d % kRows == 0 && f % kBK == 0 && d % kBK == 0; }
-
-// x_rows: [n_rows_cap][d] bf16 grouped by bucket; h: [n_rows_cap][f]; y: [n_rows_cap][d];
-int launch_ts_experts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_dense, int n_pairs, int d, int f,
-                      const uint16_t* x_rows, const int32_t* bucket_off, int64_t n_rows_cap, uint16_t* h, float* y,
-                      cudaStream_t stream) {
-  if (!ts_supported(d, f)) return fail(PUZZLE_ERR_UNSUPPORTED, "prefill TS path needs d_model % 128 == 0 and d_ff % 64 == 0");
-  if (n_pairs > kMaxBuckets / 2) return fail(PUZZLE_ERR_UNSUPPORTED, "n_pairs > 256");
-  if (n_rows_cap == 0) return PUZZLE_OK;
-  static std::atomic<uint64_t> attr13{0}, attr2{0};
-  if (int rc = cuda_check(ensure_smem_attr(k_ts_experts<true>, kSmemBytes, attr13), "w13_ts smem attribute")) return rc;
-  if (int rc = cuda_check(ensure_smem_attr(k_ts_experts<false>, kSmemBytes, attr2), "w2_ts smem attribute")) return rc;
+template <bool kPair>
+int launch_ts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_dense, int n_pairs, int d, int f,
+              const uint16_t* x_rows, const int32_t* bucket_off, int64_t n_rows_cap, uint16_t* h, float* y,
+              cudaStream_t stream) {
+  static std::atomic<uint64_t> attr13{0}, attr2{0};  // per instantiation
+  if (int rc = cuda_check(ensure_smem_attr(k_ts_experts<true, kPair>, kSmemBytes, attr13), "w13_ts smem attribute")) return rc;
+  if (int rc = cuda_check(ensure_smem_attr(k_ts_experts<false, kPair>, kSmemBytes, attr2), "w2_ts smem attribute")) return rc;
   CUtensorMap tw13, tw2;
   XMaps x13, x2;
   int rc;
@@ -636,18 +729,37 @@ int launch_ts_experts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pa
   const int grid = num_sms() & ~1;  // clusters of 2 CTAs, one CTA per SM
   {
     ProfScope _ps("w13_ts", stream);
-    cudaError_t e = launch_pdl_cluster2(k_ts_experts<true>, dim3(grid), dim3(kThreads), kSmemBytes, stream, tw13, x13, bucket_off, n_pairs, d, f, d, f / (kRows / 2), h, (float*)nullptr, 1u,
+    cudaError_t e = launch_pdl_cluster2(k_ts_experts<true, kPair>, dim3(grid), dim3(ts_threads<kPair>()), kSmemBytes, stream, tw13, x13, bucket_off, n_pairs, d, f, d, f / (kRows / 2), h, (float*)nullptr, 1u,
                                pair_dense);
     if (e != cudaSuccess) return cuda_check(e, "w13_ts launch");
   }
   if ((rc = cuda_check(cudaGetLastError(), "w13_ts launch"))) return rc;
   {
     ProfScope _ps("w2_ts", stream);
-    cudaError_t e = launch_pdl_cluster2(k_ts_experts<false>, dim3(grid), dim3(kThreads), kSmemBytes, stream, tw2, x2, bucket_off, n_pairs, f, f, d, d / kRows, (uint16_t*)nullptr, y, 1u,
+    cudaError_t e = launch_pdl_cluster2(k_ts_experts<false, kPair>, dim3(grid), dim3(ts_threads<kPair>()), kSmemBytes, stream, tw2, x2, bucket_off, n_pairs, f, f, d, d / kRows, (uint16_t*)nullptr, y, 1u,
                                pair_dense);
     if (e != cudaSuccess) return cuda_check(e, "w2_ts launch");
   }
   return cuda_check(cudaGetLastError(), "w2_ts launch");
 }
+
+}  // namespace
+
+bool ts_supported(int d, int f) { return d % kRows == 0 && f % kBK == 0 && d % kBK == 0; }
+
+// x_rows: [n_rows_cap][d] bf16 grouped by bucket; h: [n_rows_cap][f]; y: [n_rows_cap][d];
+int launch_ts_experts(const uint16_t* w13, const uint16_t* w2, const uint8_t* pair_dense, int n_pairs, int d, int f,
+                      const uint16_t* x_rows, const int32_t* bucket_off, int64_t n_rows_cap, uint16_t* h, float* y,
+                      cudaStream_t stream) {
+  if (!ts_supported(d, f)) return fail(PUZZLE_ERR_UNSUPPORTED, "prefill TS path needs d_model % 128 == 0 and d_ff % 64 == 0");
+  if (n_pairs > kMaxBuckets / 2) return fail(PUZZLE_ERR_UNSUPPORTED, "n_pairs > 256");
+  if (n_rows_cap == 0) return PUZZLE_OK;
+  // paired items while the buckets average <= 160 tokens (most pairs then have both buckets
+  // within a half); profiles/r02/ts_pair_ab.txt
+  const bool pair = PZ_TS_PAIR && n_rows_cap <= (int64_t)160 * 2 * n_pairs;
+  return pair ? launch_ts<true>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, n_rows_cap, h, y, stream)
+              : launch_ts<false>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, n_rows_cap, h, y, stream);
+}
+
 
 }  // namespace pz
