@@ -178,7 +178,7 @@ struct Plan {
 // Decode shapes (<= 64 tokens) stream each touched pair once through the decode-shape kernels
 // (gemv_tc.cu); larger token counts are tensor-bound and go to the tcgen05 grouped GEMM.
 constexpr int64_t kGemvMaxTokens = 64;
-constexpr int64_t kGemvMaxTokensPerExpert = 32;
+constexpr int64_t kGemvMaxTokensPerExpert = 56;
 
 struct Layout {
   size_t topk_idx, topk_gate, bucket_off, assign_token, assign_of, active, n_active, cnt13, cnt2, h, y, part,
@@ -191,10 +191,10 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   p.k = k;
   p.n_assign = T * k;
   p.max_active = (int)std::min<int64_t>(L->n_pairs, p.n_assign);
-  // The decode-shape kernels stream each touched pair once per pass of 32 tokens per position:
-  // they win while an expert averages < 32 tokens (one pass of 32 per position; measured with
-  // the TS kernel's paired items: GEMV ahead up to 25.6 tokens per expert, TS from 32 --
-  // profiles/r02/crossover_paired.log).
+  // The decode-shape kernels stream each touched pair once per pass of 32 (or, above 20 tokens
+  // per expert on average, 64) tokens per position: they win while an expert averages < 56
+  // tokens (GEMV ahead at 48-51 tokens per expert on every config, TS from 64-72 --
+  // profiles/r02/nx64_crossover.log).
   // Heavier batches: the decode-into-TMEM prefill kernel (gemm_ts.cu; ahead of or level with the
   // shared-memory-operand kernel on every config), else gemm_tc.cu.
   if (path == PUZZLE_PATH_AUTO)

@@ -60,13 +60,13 @@ constexpr int kWBytes = kRows * kBK * 2;         // 16 KB packed words per stage
 #ifndef PZ_TC_XST  // X ring depth of the decode configuration (tuning knob)
 #define PZ_TC_XST 5
 #endif
-constexpr int kAStages = 3;  // TMEM A buffers (64 columns each: 64 k of both positions)
 constexpr int kSq = 8;       // stage queue W producer -> X producer
 constexpr int kMinStages = 8;  // stream-K: minimum stages per CTA
-constexpr uint32_t kAccCol = 64 * kAStages;      // 192: accumulators of position p at 192 + NX p
 
-// Configuration: NX = 32 tokens per position per pass, 2 CTAs per SM, 256 TMEM columns
-// (batches of 1-64 tokens; larger batches go to the prefill kernels).
+// Configurations (2 CTAs per SM, 256 TMEM columns each): NX = 32 tokens per position per pass
+// with 3 TMEM A buffers (decode batches: <= 24 tokens per expert on average), or NX = 64 with 2
+// A buffers and shallower rings (intermediate batches: one pass of up to 64 tokens per position
+// instead of two passes of 32, each of which streams the pair's weights again).
 #ifndef PZ_TC_WST_Q  // W ring depth of the quantised class (half-size slots)
 #define PZ_TC_WST_Q PZ_TC_WST
 #endif
@@ -79,8 +79,10 @@ struct Cfg {
   // (a deeper ring of half-size slots, 6 / 8, measured neutral: the quantised class is bound by
   // its decode on the ALU pipe, profiles/r02/quant_forward.txt)
   static constexpr int kWSlot = FMT ? kRows * kBK : kWBytes;
-  static constexpr int kWStages = FMT ? PZ_TC_WST_Q : (NX == 32 ? PZ_TC_WST : 4);
-  static constexpr int kXStages = NX == 32 ? PZ_TC_XST : 4;
+  static constexpr int kWStages = FMT ? PZ_TC_WST_Q : (NX == 32 ? PZ_TC_WST : 3);
+  static constexpr int kXStages = NX == 32 ? PZ_TC_XST : 3;
+  static constexpr int kAStages = NX == 32 ? 3 : 2;  // TMEM A buffers (64 columns: 64 k of both positions)
+  static constexpr uint32_t kAccCol = 64 * kAStages;  // accumulators of position p at kAccCol + NX p
   static constexpr uint32_t kTmemCols = CTAS == 2 ? 256 : 512;
   static_assert(kAccCol + 2 * NX <= kTmemCols, "TMEM: A ring + accumulators");
 };
@@ -105,13 +107,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PZ_TRD(ev, idx)
 #endif
 
-template <int WST, int XST>
+template <int WST, int XST, int AST>
 struct alignas(16) Ctl {
   int4 whdr[WST];  // stage headers (see Pass); item -1 = no more work
   int4 xhdr[XST];
   int4 sq[kSq];         // W producer -> X producer: {k column, row0 | active0 << 28, row1 | ...}
   int4 sqh[kSq];        //   ... and the stage headers
-  uint64_t wfull[WST], wempty[WST], xfull[XST], xempty[XST], a_full[kAStages], a_empty[kAStages];
+  uint64_t wfull[WST], wempty[WST], xfull[XST], xempty[XST], a_full[AST], a_empty[AST];
   uint64_t sqfull[kSq], sqempty[kSq];
   uint64_t pdone;  // decoders -> X producer: partials of this CTA's first (signalling) piece stored
   uint64_t acc_full, acc_empty;
@@ -126,7 +128,7 @@ struct alignas(16) Ctl {
 template <class C>
 constexpr size_t smem_bytes() {
   return 1024 + (size_t)C::kWStages * C::kWSlot + (size_t)C::kXStages * C::kXBytes +
-         sizeof(Ctl<C::kWStages, C::kXStages>);
+         sizeof(Ctl<C::kWStages, C::kXStages, C::kAStages>);
 }
 static_assert(2 * (smem_bytes<Cfg<32, 2>>() + 1024) <= 228 * 1024, "decode: two CTAs per SM");
 static_assert(2 * (smem_bytes<Cfg<32, 2, 1>>() + 1024) <= 228 * 1024, "decode (quantised): two CTAs per SM");
@@ -254,8 +256,8 @@ __device__ __forceinline__ int npass_of(const PairTokens& pt, int nx) {
 }
 
 // item -> (active pair z, row block, pass): binary search over the per-pair item prefix
-template <int WST, int XST>
-__device__ __forceinline__ void locate(const Ctl<WST, XST>& c, int n_active, int item, int nx, int& p,
+template <int WST, int XST, int AST>
+__device__ __forceinline__ void locate(const Ctl<WST, XST, AST>& c, int n_active, int item, int nx, int& p,
                                       PairTokens& pt, int& rb, int& base) {
   int lo = 0, hi = n_active - 1;
   while (lo < hi) {
@@ -270,8 +272,8 @@ __device__ __forceinline__ void locate(const Ctl<WST, XST>& c, int n_active, int
   base = (rem % np) * nx;
 }
 
-template <int WST, int XST>
-__device__ __forceinline__ Pass make_pass(const Ctl<WST, XST>& c, int4 h, int n_active, int nx) {
+template <int WST, int XST, int AST>
+__device__ __forceinline__ Pass make_pass(const Ctl<WST, XST, AST>& c, int4 h, int n_active, int nx) {
   Pass s;
   s.item = h.x;
   s.kb0 = h.w >> 16;
@@ -286,8 +288,8 @@ __device__ __forceinline__ Pass make_pass(const Ctl<WST, XST>& c, int4 h, int n_
 // pos 0, bit 1 = pos 1, bit 2 = pos 0 of a dense slot: the words are the bf16 weights): decode this thread's 32 packed words per stage (16 registers, k =
 // 32 kh .. 32 kh + 31 of its row) and store the bf16 rows into the TMEM A buffer: register r
 // of chunk i -> column 16 kh + 4 i + r (k pair 32 kh + 8 i + 2 r).
-template <int MODE, int WST, int XST, class Epi>
-__device__ __forceinline__ void decode_pass(Ctl<WST, XST>& c, uint32_t smem_w, uint32_t lane_tmem,
+template <int MODE, int WST, int XST, int AST, class Epi>
+__device__ __forceinline__ void decode_pass(Ctl<WST, XST, AST>& c, uint32_t smem_w, uint32_t lane_tmem,
                                             const uint32_t (&w_off)[4],
                                             int kh, int n_stages, Ring& w, Ring& a, const Muls& mu, int& tcount,
                                             bool kW13, int ep_at, Epi&& epi) {
@@ -336,7 +338,7 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST>& c, uint32_t smem_w, u
     if (lane == 0) ptx::mbar_arrive(&c.a_full[a.i]);
     PZ_TRD(4, tcount);
     ++tcount;
-    a.next<kAStages>();
+    a.next<AST>();
     if (kb == ep_at) epi();  // the previous pass's epilogue, once the tensor pipe has work queued
   }
 }
@@ -369,8 +371,8 @@ __device__ __forceinline__ void qdecode2(uint32_t y, const uint32_t (&L)[4], uin
   if (MODE & 2) o1 = (mag | ((p << 1) & 0x80008000u)) & prmt(y << 3, 0u, 0x9988u);  // S_j bit 6, M_j bit 4
 }
 
-template <int MODE, int WST, int XST, class Epi>
-__device__ __forceinline__ void decode_pass_q(Ctl<WST, XST>& c, uint32_t smem_w, uint32_t lane_tmem,
+template <int MODE, int WST, int XST, int AST, class Epi>
+__device__ __forceinline__ void decode_pass_q(Ctl<WST, XST, AST>& c, uint32_t smem_w, uint32_t lane_tmem,
                                               const uint32_t (&w_off)[2], int kh, int n_stages, Ring& w, Ring& a,
                                               const float* __restrict__ row_scales, int kb0, int& tcount, int ep_at,
                                               Epi&& epi) {
@@ -406,7 +408,7 @@ __device__ __forceinline__ void decode_pass_q(Ctl<WST, XST>& c, uint32_t smem_w,
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&c.a_full[a.i]);
     ++tcount;
-    a.next<kAStages>();
+    a.next<AST>();
     if (kb == ep_at) epi();
   }
 }
@@ -429,11 +431,15 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   constexpr int kWStages = C::kWStages, kXStages = C::kXStages, kXBytes = C::kXBytes, kXPos = C::kXPos;
   constexpr int kSlot = 2 * NX * kRows;  // floats per partial slot
   constexpr uint32_t kRowB = kRows * 4;   // one slot row (a (position, token) of 128 outputs): 512 bytes
+  // the reducer stages the partial slots in the idle W / X rings when two full slots fit
+  // (NX = 32); otherwise (NX = 64: 64 KB slots, 96 KB of rings) it sums them from L2 directly
+  constexpr uint32_t kRing = kWStages * kWStageBytes + kXStages * kXBytes;
+  constexpr bool kStagedRed = kRing >= 2u * (2 * NX) * kRowB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_w = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;  // == smem, shared window
   const uint32_t smem_x = smem_w + kWStages * kWStageBytes;
-  auto& c = *reinterpret_cast<Ctl<kWStages, kXStages>*>(smem + (size_t)kWStages * kWStageBytes +
+  auto& c = *reinterpret_cast<Ctl<kWStages, kXStages, C::kAStages>*>(smem + (size_t)kWStages * kWStageBytes +
                                                          (size_t)kXStages * kXBytes);
   const uint32_t whdr_s = ptx::smem_u32(&c.whdr[0]), xhdr_s = ptx::smem_u32(&c.xhdr[0]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -446,7 +452,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       ptx::mbar_init(&c.xfull[j], 1);
       ptx::mbar_init(&c.xempty[j], 2);  // commits of both MMA warps
     }
-    for (int j = 0; j < kAStages; ++j) {
+    for (int j = 0; j < C::kAStages; ++j) {
       ptx::mbar_init(&c.a_full[j], kDecWarps);
       ptx::mbar_init(&c.a_empty[j], 2);
     }
@@ -651,7 +657,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       const Pass s = make_pass(c, h, n_active, NX);
       const int np = mypos ? s.n1 : s.n0;
       const uint32_t idp = ptx::idesc_bf16_f32(128, (uint32_t)((np + 15) & ~15));
-      const uint32_t acc_col = tmem + kAccCol + (uint32_t)NX * mypos;
+      const uint32_t acc_col = tmem + C::kAccCol + (uint32_t)NX * mypos;
       ptx::mbar_wait(&c.acc_empty, accph ^ 1);  // the previous pass's epilogue drained TMEM
       ptx::tc_fence_after();
       for (int kb = s.kb0; kb < s.kb1; ++kb) {
@@ -674,7 +680,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         if (mypos == 0) PZ_TR(7, tcount);
         ++tcount;
         x.next<kXStages>();
-        a.next<kAStages>();
+        a.next<C::kAStages>();
       }
       accph ^= 1;
     }
@@ -719,7 +725,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       const int np = pos ? s.n1 : s.n0;
       const int offp = (pos ? s.pt.off1 : s.pt.off0) + s.base;  // first assignment of this warp
       float* slot = part + (size_t)(2 * g + (s.item == first_item ? 0 : 1)) * kSlot;
-      const uint32_t acc_t = lane_tmem + kAccCol + (uint32_t)NX * pos;
+      const uint32_t acc_t = lane_tmem + C::kAccCol + (uint32_t)NX * pos;
       PZ_DCHECK(np >= 0 && np <= NX && offp >= 0 && (np == 0 || offp + np <= c.s_off[2 * n_bucket_pairs]));
       PZ_DCHECK(s.item < n_rb * (n_bucket_pairs + c.s_off[2 * n_bucket_pairs] / 32 + 1));
       // the A operand is W^ * 2^-15 (PZ_TC_ORMAG; dense slots scaled to match): scale back, exact
@@ -730,7 +736,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * acc_scale);
-        if (!whole && reducer) {
+        if (!whole && reducer && kStagedRed) {
           // the reducer's own piece (the sum's first term): straight into staged slot 0 of the
           // W ring -- idle now: every stage was decoded before the MMAs completed
           const uint32_t a0 = smem_w + (uint32_t)((pos ? s.n0 : 0) + c0) * kRowB + (uint32_t)prow * 4u;
@@ -808,8 +814,35 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           const int cols = kW13 ? kRows / 2 : min(kRows, d - r0);  // outputs of this tile, multiple of 4
           const int q4 = cols / 4;
           const int n_rows = s.n0 + s.n1;                           // active (position, token) rows
-          constexpr uint32_t kRing = kWStages * kWStageBytes + kXStages * kXBytes;
-          static_assert(kRing >= 2u * (2 * NX) * kRowB, "reducer: two full slots fit the rings");
+          if constexpr (!kStagedRed) {
+            // every piece (own included) is in its global slot: sum them in CTA order from L2
+            for (int u = dtid; u < n_rows * q4; u += kDecWarps * 32) {
+              const int r = u / q4, cq = 4 * (u % q4);
+              const int t = r < s.n0 ? r : NX + r - s.n0;  // (position, token) row of a slot
+              float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+              for (int gg = g_first; gg <= g_last; ++gg) {
+                const float* src = part + (size_t)(2 * gg + (s.item == sk.begin(gg) / nk ? 0 : 1)) * kSlot +
+                                   (size_t)t * kRows + cq;
+                const float4 v4 = __ldcg(reinterpret_cast<const float4*>(src));
+                s0.x += v4.x; s0.y += v4.y; s0.z += v4.z; s0.w += v4.w;
+                if (kW13) {
+                  const float4 u4 = __ldcg(reinterpret_cast<const float4*>(src + kRows / 2));
+                  s1.x += u4.x; s1.y += u4.y; s1.z += u4.z; s1.w += u4.w;
+                }
+              }
+              const size_t aa = (size_t)((r < s.n0 ? s.pt.off0 + r : s.pt.off1 + r - s.n0) + s.base);
+              if (kW13) {
+                uint2 o;
+                o.x = f32_to_bf16_rne_bits(silu_mul(s0.x, s1.x)) | (f32_to_bf16_rne_bits(silu_mul(s0.y, s1.y)) << 16);
+                o.y = f32_to_bf16_rne_bits(silu_mul(s0.z, s1.z)) | (f32_to_bf16_rne_bits(silu_mul(s0.w, s1.w)) << 16);
+                *reinterpret_cast<uint2*>(h_out + aa * f + r0 + cq) = o;
+              } else {
+                *reinterpret_cast<float4*>(y_out + aa * d + r0 + cq) = s0;
+              }
+            }
+            named_bar_sync(1, kDecWarps * 32);
+            return;
+          }
           const int m = min(g_last - g_first + 1, (int)(kRing / (n_rows * kRowB)));  // >= 2 slots
           const int n_units = n_rows * q4;
           const uint64_t drop = l2_policy_evict_first();  // the partials are dead once read
@@ -1018,11 +1051,16 @@ int launch_gemv_tc_experts_quant(const uint8_t* c13, const float* s13, const uin
                            n_assign_cap, part, counters13, counters2, h, y, stream);
 }
 
-// Partial-slot floats (2 slots per CTA x 2 CTAs per SM x 2 positions x NX x 128).
-size_t gemv_tc_part_floats() { return (size_t)2 * 2 * num_sms() * 2 * 32 * kRows; }
+// Partial-slot floats (2 slots per CTA x 2 CTAs per SM x 2 positions x NX x 128, NX <= 64).
+size_t gemv_tc_part_floats() { return (size_t)2 * 2 * num_sms() * 2 * 64 * kRows; }
 // Work-item counters per projection: row blocks x (pairs + passes).
 int64_t gemv_tc_counters(int n_rb, int n_pairs, int64_t n_assign) { return (int64_t)n_rb * (n_pairs + n_assign / 32 + 1); }
 bool gemv_supported(int d, int f) { return d % 64 == 0 && f % 64 == 0 && d <= 65535 * 64 && f <= 65535 * 64; }
+
+#ifndef PZ_NX64_TOKENS  // average tokens per expert above which the NX = 64 configuration runs
+#define PZ_NX64_TOKENS 20
+#endif
+constexpr int kNx64Tokens = PZ_NX64_TOKENS;
 
 // x_rows: [n_assign_cap][d] bf16 in bucket order (TMA source); h: [n_assign_cap][f];
 // y: [n_assign_cap][d]; part: gemv_tc_part_floats(prefill) floats; counters13 / counters2:
@@ -1032,6 +1070,11 @@ int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, const uint8_
                            const uint16_t* x_rows, const int32_t* bucket_off, const int32_t* active_pairs,
                            const int32_t* n_active, int max_active, int64_t n_assign_cap, float* part,
                            int32_t* counters13, int32_t* counters2, uint16_t* h, float* y, cudaStream_t stream) {
+  // one pass of 64 tokens per position instead of two of 32 once experts average more than
+  // kNx64Tokens tokens (profiles/r02/nx64_crossover.log)
+  if (n_assign_cap > (int64_t)kNx64Tokens * 2 * n_pairs)
+    return launch_both<64, 2>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
+                              n_assign_cap, part, counters13, counters2, h, y, stream);
   return launch_both<32, 2>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
                             n_assign_cap, part, counters13, counters2, h, y, stream);
 }
