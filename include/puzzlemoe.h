@@ -183,7 +183,8 @@ typedef struct {
 } puzzle_moe_layer;
 
 /* Kernel path for puzzle_moe_forward_ex. AUTO: GEMV while T <= 64 or the experts average
- * fewer than 56 tokens (T*top_k < 56*n_experts), else TS (else TC, else GEMV). */
+ * fewer than 72 tokens (T*top_k < 72*n_experts; 100 when d_ff >= 8192), else TS (else TC,
+ * else GEMV). */
 typedef enum {
   PUZZLE_PATH_AUTO = 0,
   PUZZLE_PATH_GEMV = 1,   /* decode shape: decode into TMEM + tcgen05.mma (weights on M), weights read once per pair */

@@ -79,8 +79,14 @@ struct Cfg {
   // (a deeper ring of half-size slots, 6 / 8, measured neutral: the quantised class is bound by
   // its decode on the ALU pipe, profiles/r02/quant_forward.txt)
   static constexpr int kWSlot = FMT ? kRows * kBK : kWBytes;
-  static constexpr int kWStages = FMT ? PZ_TC_WST_Q : (NX == 32 ? PZ_TC_WST : 3);
+  // decoder warps: 8 per CTA at 2 CTAs per SM; 16 in the one-CTA-per-SM configuration (each
+  // decodes a K quarter of a stage instead of a K half: the same 16 decoder warps per SM)
+  static constexpr int kDec = CTAS == 1 ? 16 : 8;
+  static constexpr int kThreads = 128 + 32 * kDec;
+  static constexpr int kKC = 32 / kDec;  // 16-byte chunks (8 packed words) per decoder thread per stage
+  static constexpr int kWStages = FMT ? PZ_TC_WST_Q : (NX == 32 ? PZ_TC_WST : CTAS == 1 ? 6 : 3);
   static constexpr int kXStages = NX == 32 ? PZ_TC_XST : 3;
+  static_assert(FMT == 0 || CTAS == 2, "the quantised class runs the two-CTA configuration");
   static constexpr int kAStages = NX == 32 ? 3 : 2;  // TMEM A buffers (64 columns: 64 k of both positions)
   static constexpr uint32_t kAccCol = 64 * kAStages;  // accumulators of position p at kAccCol + NX p
   static constexpr uint32_t kTmemCols = CTAS == 2 ? 256 : 512;
@@ -132,6 +138,8 @@ constexpr size_t smem_bytes() {
 }
 static_assert(2 * (smem_bytes<Cfg<32, 2>>() + 1024) <= 228 * 1024, "decode: two CTAs per SM");
 static_assert(2 * (smem_bytes<Cfg<32, 2, 1>>() + 1024) <= 228 * 1024, "decode (quantised): two CTAs per SM");
+static_assert(2 * (smem_bytes<Cfg<64, 2>>() + 1024) <= 228 * 1024, "NX 64: two CTAs per SM");
+static_assert(smem_bytes<Cfg<128, 1>>() <= 227 * 1024, "NX 128: one CTA per SM");
 
 struct PairTokens {
   int off0, cnt0, off1, cnt1;
@@ -288,9 +296,9 @@ __device__ __forceinline__ Pass make_pass(const Ctl<WST, XST, AST>& c, int4 h, i
 // pos 0, bit 1 = pos 1, bit 2 = pos 0 of a dense slot: the words are the bf16 weights): decode this thread's 32 packed words per stage (16 registers, k =
 // 32 kh .. 32 kh + 31 of its row) and store the bf16 rows into the TMEM A buffer: register r
 // of chunk i -> column 16 kh + 4 i + r (k pair 32 kh + 8 i + 2 r).
-template <int MODE, int WST, int XST, int AST, class Epi>
+template <int MODE, int KC, int WST, int XST, int AST, class Epi>
 __device__ __forceinline__ void decode_pass(Ctl<WST, XST, AST>& c, uint32_t smem_w, uint32_t lane_tmem,
-                                            const uint32_t (&w_off)[4],
+                                            const uint32_t (&w_off)[KC],
                                             int kh, int n_stages, Ring& w, Ring& a, const Muls& mu, int& tcount,
                                             bool kW13, int ep_at, Epi&& epi) {
   const int lane = threadIdx.x & 31;
@@ -300,12 +308,12 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST, AST>& c, uint32_t smem
     if (kb) ptx::mbar_wait(&c.wfull[w.i], w.ph);
     PZ_TRD(2, tcount);
     const uint32_t st = smem_w + (uint32_t)w.i * kWBytes;
-    uint4 v[4];
+    uint4 v[KC];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = lds128(st + w_off[i]);
-    uint32_t d0[16], d1[16];
+    for (int i = 0; i < KC; ++i) v[i] = lds128(st + w_off[i]);
+    uint32_t d0[4 * KC], d1[4 * KC];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < KC; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t x = comp(v[i], j);
@@ -329,9 +337,14 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST, AST>& c, uint32_t smem
     ptx::mbar_wait(&c.a_empty[a.i], a.ph ^ 1);  // the MMAs that read A buffer a.i have completed
     PZ_TRD(3, tcount);
     ptx::tc_fence_after();
-    const uint32_t t0 = lane_tmem + 64u * a.i + 16u * kh;
-    if (MODE & 5) ptx::tmem_st_32x32b_x16(t0, d0);
-    if (MODE & 2) ptx::tmem_st_32x32b_x16(t0 + 32u, d1);
+    const uint32_t t0 = lane_tmem + 64u * a.i + 4u * KC * kh;
+    if constexpr (KC == 4) {
+      if (MODE & 5) ptx::tmem_st_32x32b_x16(t0, d0);
+      if (MODE & 2) ptx::tmem_st_32x32b_x16(t0 + 32u, d1);
+    } else {
+      if (MODE & 5) ptx::tmem_st_32x32b_x8(t0, d0);
+      if (MODE & 2) ptx::tmem_st_32x32b_x8(t0 + 32u, d1);
+    }
     ptx::tmem_st_wait();
     ptx::tc_fence_before();
     __syncwarp();
@@ -427,6 +440,8 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     float* __restrict__ y_out, uint32_t mul_one, int n_bucket_pairs, const uint8_t* __restrict__ pair_dense,
     const float* __restrict__ qscales = nullptr) {
   using C = Cfg<NX, CTAS, FMT>;
+  constexpr int kDecWarps = C::kDec;  // (shadows the two-CTA default)
+  constexpr int kKC = C::kKC;
   constexpr uint32_t kWStageBytes = C::kWSlot;  // bytes of one W stage (codes: 1 B each)
   constexpr int kWStages = C::kWStages, kXStages = C::kXStages, kXBytes = C::kXBytes, kXPos = C::kXPos;
   constexpr int kSlot = 2 * NX * kRows;  // floats per partial slot
@@ -688,7 +703,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     // ============================== decoders + epilogue ==============================
     const int dtid = threadIdx.x - 64;
     const int q = warp & 3;          // TMEM lane quarter this warp may access
-    const int kh = (warp - 2) >> 2;  // K half of a stage; position handled in the epilogue
+    const int kh = (warp - 2) >> 2;  // K half (quarter: 16 decoders) of a stage
     const int row = 32 * q + lane;   // tile row == TMEM lane
     // shared-memory row this thread decodes. w13: the stage holds 64 gate rows then the same
     // features' 64 up rows; lanes 0-15 of quarter q take gate rows 16q.., lanes 16-31 the up
@@ -698,9 +713,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     const int prow = kW13 ? (lane < 16 ? 16 * q + lane : 64 + 16 * q + lane - 16) : row;
     const uint32_t lane_tmem = tmem + ((uint32_t)(32 * q) << 16);
     const Muls mu{mul_one, mul_one * 2u, mul_one * 4u, mul_one * 8u, mul_one * 0x50005000u};
-    uint32_t w_off[4];
+    uint32_t w_off[kKC];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) w_off[i] = swz(srow, 4 * kh + i);
+    for (int i = 0; i < kKC; ++i) w_off[i] = swz(srow, kKC * kh + i);
     // quant stages: 64-byte rows under the 64-byte swizzle (16-byte chunk c of row r at chunk
     // c ^ ((r >> 1) & 3)); this thread reads chunks 2 kh, 2 kh + 1 (its 32 k)
     uint32_t wq_off[2];
@@ -721,7 +736,9 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       ptx::tc_fence_after();
       const bool whole = s.kb0 == 0 && s.kb1 == nk;  // the item is not split: final outputs
       const bool reducer = !whole && g == sk.owner(s.item * nk);  // the item's first piece: this CTA sums
-      const int pos = kh;
+      // warp (q, kh): position kh & 1; with 16 decoders, token chunks of 16 alternate between
+      // the warps kh and kh + 2
+      const int pos = kh & 1;
       const int np = pos ? s.n1 : s.n0;
       const int offp = (pos ? s.pt.off1 : s.pt.off0) + s.base;  // first assignment of this warp
       float* slot = part + (size_t)(2 * g + (s.item == first_item ? 0 : 1)) * kSlot;
@@ -730,7 +747,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       PZ_DCHECK(s.item < n_rb * (n_bucket_pairs + c.s_off[2 * n_bucket_pairs] / 32 + 1));
       // the A operand is W^ * 2^-15 (PZ_TC_ORMAG; dense slots scaled to match): scale back, exact
       constexpr float acc_scale = (PZ_TC_ORMAG && FMT == 0) ? 32768.0f : 1.0f;  // quant bytes decode exactly
-      for (int c0 = 0; c0 < np; c0 += 16) {
+      for (int c0 = 16 * (kh >> 1); c0 < np; c0 += 16 * (kDecWarps / 8)) {
         uint32_t r[16];
         ptx::tmem_ld_32x32b_x16(acc_t + c0, r);
         ptx::tmem_ld_wait();
@@ -949,10 +966,10 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         else if (s.n0 > 0) decode_pass_q<1>(c, smem_w, lane_tmem, wq_off, kh, n_st, w, a, rs, s.kb0, tcount, ep_at, flush);
         else decode_pass_q<2>(c, smem_w, lane_tmem, wq_off, kh, n_st, w, a, rs, s.kb0, tcount, ep_at, flush);
       } else {
-      if (pair_dense != nullptr && pair_dense[s.p]) decode_pass<4>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
-      else if (s.n0 > 0 && s.n1 > 0) decode_pass<3>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
-      else if (s.n0 > 0) decode_pass<1>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
-      else decode_pass<2>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      if (pair_dense != nullptr && pair_dense[s.p]) decode_pass<4, kKC>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      else if (s.n0 > 0 && s.n1 > 0) decode_pass<3, kKC>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      else if (s.n0 > 0) decode_pass<1, kKC>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
+      else decode_pass<2, kKC>(c, smem_w, lane_tmem, w_off, kh, n_st, w, a, mu, tcount, kW13, ep_at, flush);
       }
       if (PZ_TC_DEFER) {
         pend = s;
@@ -991,7 +1008,7 @@ int launch_one(const CUtensorMap& tw, const CUtensorMap& tx, const int32_t* buck
   const char* name = FMT ? (kW13 ? "w13_gemv_q" : "w2_gemv_q") : (kW13 ? "w13_gemv" : "w2_gemv");
   {
     ProfScope _ps(name, stream);
-    cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kThreads), kSmem, stream, tw, tx, bucket_off, active, n_active,
+    cudaError_t e = launch_pdl(kern, dim3(grid), dim3(C::kThreads), kSmem, stream, tw, tx, bucket_off, active, n_active,
                                K, f, d, n_rb, part, counters, h, y, 1u, n_pairs, pair_dense, qscales);
     if (e != cudaSuccess) return cuda_check(e, name);
   }
@@ -1051,7 +1068,8 @@ int launch_gemv_tc_experts_quant(const uint8_t* c13, const float* s13, const uin
                            n_assign_cap, part, counters13, counters2, h, y, stream);
 }
 
-// Partial-slot floats (2 slots per CTA x 2 CTAs per SM x 2 positions x NX x 128, NX <= 64).
+// Partial-slot floats (2 slots per CTA x 2 CTAs per SM x 2 positions x NX x 128 with NX <= 64,
+// or 2 slots x 1 CTA per SM x 2 positions x 128 x 128: the same size).
 size_t gemv_tc_part_floats() { return (size_t)2 * 2 * num_sms() * 2 * 64 * kRows; }
 // Work-item counters per projection: row blocks x (pairs + passes).
 int64_t gemv_tc_counters(int n_rb, int n_pairs, int64_t n_assign) { return (int64_t)n_rb * (n_pairs + n_assign / 32 + 1); }
@@ -1061,6 +1079,10 @@ bool gemv_supported(int d, int f) { return d % 64 == 0 && f % 64 == 0 && d <= 65
 #define PZ_NX64_TOKENS 20
 #endif
 constexpr int kNx64Tokens = PZ_NX64_TOKENS;
+#ifndef PZ_NX128_TOKENS  // ... and the NX = 128 configuration (one CTA per SM; NX 64 ahead at 48)
+#define PZ_NX128_TOKENS 56
+#endif
+constexpr int kNx128Tokens = PZ_NX128_TOKENS;
 
 // x_rows: [n_assign_cap][d] bf16 in bucket order (TMA source); h: [n_assign_cap][f];
 // y: [n_assign_cap][d]; part: gemv_tc_part_floats(prefill) floats; counters13 / counters2:
@@ -1071,7 +1093,11 @@ int launch_gemv_tc_experts(const uint16_t* w13, const uint16_t* w2, const uint8_
                            const int32_t* n_active, int max_active, int64_t n_assign_cap, float* part,
                            int32_t* counters13, int32_t* counters2, uint16_t* h, float* y, cudaStream_t stream) {
   // one pass of 64 tokens per position instead of two of 32 once experts average more than
-  // kNx64Tokens tokens (profiles/r02/nx64_crossover.log)
+  // kNx64Tokens tokens, of 128 above kNx128Tokens (profiles/r02/nx64_crossover.log,
+  // nx128_crossover.log)
+  if (n_assign_cap > (int64_t)kNx128Tokens * 2 * n_pairs)  // one CTA per SM, 512 TMEM columns
+    return launch_both<128, 1>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active,
+                               max_active, n_assign_cap, part, counters13, counters2, h, y, stream);
   if (n_assign_cap > (int64_t)kNx64Tokens * 2 * n_pairs)
     return launch_both<64, 2>(w13, w2, pair_dense, n_pairs, d, f, x_rows, bucket_off, active_pairs, n_active, max_active,
                               n_assign_cap, part, counters13, counters2, h, y, stream);
