@@ -1017,10 +1017,10 @@ def sweep(pz, args, device, pk):
     res = []
     layers = {}
     for name, T, ratio in (("mixtral", 1, 0.5), ("mixtral", 16, 0.5), ("mixtral", 128, 0.5), ("mixtral", 256, 0.5),
-                           ("mixtral", 512, 0.5), ("mixtral", 1024, 0.5), ("mixtral", 4096, 0.5),
+                           ("mixtral", 384, 0.5), ("mixtral", 512, 0.5), ("mixtral", 1024, 0.5), ("mixtral", 4096, 0.5),
                            ("qwen15", 1, 0.5), ("qwen15", 16, 0.5), ("qwen15", 64, 0.5), ("qwen15", 128, 0.5),
                            ("qwen15", 256, 0.5), ("qwen15", 512, 0.5), ("qwen15", 1024, 0.5), ("qwen15", 4096, 0.5),
-                           ("deepseek", 1, 0.5), ("deepseek", 16, 0.5), ("deepseek", 64, 0.5), ("deepseek", 1024, 0.5),
+                           ("deepseek", 1, 0.5), ("deepseek", 16, 0.5), ("deepseek", 64, 0.5), ("deepseek", 512, 0.5), ("deepseek", 1024, 0.5),
                            ("deepseek", 4096, 0.5),
                            ("mixtral", 64, 0.25), ("mixtral", 4096, 0.25), ("deepseek", 64, 0.25)):
         cfg = synth.CONFIGS[name]
