@@ -67,6 +67,13 @@ constexpr int kMinStages = 8;  // stream-K: minimum stages per CTA
 // with 3 TMEM A buffers (decode batches: <= 24 tokens per expert on average), or NX = 64 with 2
 // A buffers and shallower rings (intermediate batches: one pass of up to 64 tokens per position
 // instead of two passes of 32, each of which streams the pair's weights again).
+#ifndef PZ_TC_WST1  // W / X ring depths of the one-CTA-per-SM (NX 128) configuration: 32 KB X slots
+// (profiles/r02/nx128_rings_ab.txt: 5 / 4 ahead of 6 / 3, 3 / 5, 4 / 4 by 1-5 %)
+#define PZ_TC_WST1 5
+#endif
+#ifndef PZ_TC_XST1
+#define PZ_TC_XST1 4
+#endif
 #ifndef PZ_TC_WST_Q  // W ring depth of the quantised class (half-size slots)
 #define PZ_TC_WST_Q PZ_TC_WST
 #endif
@@ -84,8 +91,8 @@ struct Cfg {
   static constexpr int kDec = CTAS == 1 ? 16 : 8;
   static constexpr int kThreads = 128 + 32 * kDec;
   static constexpr int kKC = 32 / kDec;  // 16-byte chunks (8 packed words) per decoder thread per stage
-  static constexpr int kWStages = FMT ? PZ_TC_WST_Q : (NX == 32 ? PZ_TC_WST : CTAS == 1 ? 6 : 3);
-  static constexpr int kXStages = NX == 32 ? PZ_TC_XST : 3;
+  static constexpr int kWStages = FMT ? PZ_TC_WST_Q : (NX == 32 ? PZ_TC_WST : CTAS == 1 ? PZ_TC_WST1 : 3);
+  static constexpr int kXStages = NX == 32 ? PZ_TC_XST : CTAS == 1 ? PZ_TC_XST1 : 3;
   static_assert(FMT == 0 || CTAS == 2, "the quantised class runs the two-CTA configuration");
   static constexpr int kAStages = NX == 32 ? 3 : 2;  // TMEM A buffers (64 columns: 64 k of both positions)
   static constexpr uint32_t kAccCol = 64 * kAStages;  // accumulators of position p at kAccCol + NX p
