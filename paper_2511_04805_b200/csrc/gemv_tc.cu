@@ -391,6 +391,23 @@ __device__ __forceinline__ void qdecode2(uint32_t y, const uint32_t (&L)[4], uin
   if (MODE & 2) o1 = (mag | ((p << 1) & 0x80008000u)) & prmt(y << 3, 0u, 0x9988u);  // S_j bit 6, M_j bit 4
 }
 
+// The same two bytes through byte tables and the exact-product sign / mask of the packed words
+// (about 2.4x fewer integer-pipe instructions): Tl / Th hold the low / high bytes of the 8
+// magnitudes x 2^63, indexed by the code nibble of each byte (bit 3 of the format is 0), and
+// (-1)^S * M * 2^-63 is formed from the flag bits as a bf16 factor (S_p -> bit 15, M_p -> bit
+// 13: +-2^-63 or +-0), one exact bf16x2 product per position. Exact while every magnitude
+// times 2^63 is finite and every non-zero product normal: 2^-126 <= scale <= 2^61 (the
+// caller keeps qdecode2 for other groups).
+template <int MODE>
+__device__ __forceinline__ void qdecode2_tab(uint32_t y, const uint32_t (&Tl)[2], const uint32_t (&Th)[2], uint32_t& o0,
+                                            uint32_t& o1) {
+  const uint32_t lo = prmt(Tl[0], Tl[1], y), hi = prmt(Th[0], Th[1], y);  // selector nibbles 0 / 2: the codes
+  const uint32_t mag = prmt(lo, hi, 0x6240u);                              // bf16x2 |W^| * 2^63
+  const uint32_t p = prmt(y, 0u, 0x1404u);  // byte k -> bits 16k + 8 .. 16k + 15: S_i S_j M_i M_j at 15 .. 12
+  if (MODE & 1) o0 = bf16x2_mul(mag, p & 0xA000A000u);
+  if (MODE & 2) o1 = bf16x2_mul(mag, (p << 1) & 0xA000A000u);
+}
+
 template <int MODE, int WST, int XST, int AST, class Epi>
 __device__ __forceinline__ void decode_pass_q(Ctl<WST, XST, AST>& c, uint32_t smem_w, uint32_t lane_tmem,
                                               const uint32_t (&w_off)[2], int kh, int n_stages, Ring& w, Ring& a,
@@ -408,15 +425,29 @@ __device__ __forceinline__ void decode_pass_q(Ctl<WST, XST, AST>& c, uint32_t sm
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&c.wempty[w.i]);  // bytes in registers: the slot may refill
     w.next<WST>();
-    uint32_t L[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) L[j] = bf16x2_of(__fmul_rn((float)(2 * j), sc), __fmul_rn((float)(2 * j + 1), sc));
     uint32_t d0[16], d1[16];
     const uint32_t words[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    if (sc >= 0x1p-126f && sc <= 0x1p61f) {  // byte-table decode (exact in this scale range)
+      uint32_t L[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      qdecode2<MODE>(words[i], L, d0[2 * i], d1[2 * i]);
-      qdecode2<MODE>(words[i] >> 16, L, d0[2 * i + 1], d1[2 * i + 1]);
+      for (int j = 0; j < 4; ++j)
+        L[j] = bf16x2_of(__fmul_rn(__fmul_rn((float)(2 * j), sc), 0x1p63f), __fmul_rn(__fmul_rn((float)(2 * j + 1), sc), 0x1p63f));
+      const uint32_t Tl[2] = {prmt(L[0], L[1], 0x6420u), prmt(L[2], L[3], 0x6420u)};
+      const uint32_t Th[2] = {prmt(L[0], L[1], 0x7531u), prmt(L[2], L[3], 0x7531u)};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        qdecode2_tab<MODE>(words[i], Tl, Th, d0[2 * i], d1[2 * i]);
+        qdecode2_tab<MODE>(words[i] >> 16, Tl, Th, d0[2 * i + 1], d1[2 * i + 1]);
+      }
+    } else {  // any other finite scale: integer sign / mask (exact for every scale)
+      uint32_t L[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) L[j] = bf16x2_of(__fmul_rn((float)(2 * j), sc), __fmul_rn((float)(2 * j + 1), sc));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        qdecode2<MODE>(words[i], L, d0[2 * i], d1[2 * i]);
+        qdecode2<MODE>(words[i] >> 16, L, d0[2 * i + 1], d1[2 * i + 1]);
+      }
     }
     ptx::mbar_wait(&c.a_empty[a.i], a.ph ^ 1);  // the MMAs that read A buffer a.i have completed
     ptx::tc_fence_after();

@@ -118,3 +118,44 @@ def test_quant_forward_rejects_bad_layers(pz):
     import ctypes
     d = pz.QuantLayerDesc(8, 4, 4096 + 64, 14336, 4096, 4096, 4096, 4096, 4096)  # d_model % 128
     assert pz.load_library().puzzle_moe_quant_workspace_size(ctypes.byref(d), 64, 2) == 0
+
+
+def test_quant_forward_scale_range_paths(pz):
+    """The decoder's two forms (gemv_tc.cu decode_pass_q): the byte-table decode with the exact
+    +-2^-63 sign / mask product for group scales in [2^-126, 2^61], the integer form for any
+    other finite scale. Groups of every projection are re-scaled by 2^-127 (codes kept: the
+    dequantised values are bf16 subnormals) or 2^70 with their codes zeroed (flags kept), on
+    rows spread over every tile quarter, so that both forms alternate inside one stage range;
+    the reference dequantises the modified layer with the oracle."""
+    cfg = CFGS[0]
+    (c13, s13, c2, s2, slot), _ = quant_layer(cfg)
+    c13, s13, c2, s2 = c13.copy(), s13.copy(), c2.copy(), s2.copy()
+    rng = np.random.default_rng(31)
+    for codes, scales in ((c13.reshape(-1, c13.shape[-1]), s13.reshape(-1, s13.shape[-1])),
+                          (c2.reshape(-1, c2.shape[-1]), s2.reshape(-1, s2.shape[-1]))):
+        rows = rng.choice(scales.shape[0], scales.shape[0] // 5, replace=False)
+        for r in rows:
+            g = int(rng.integers(scales.shape[1]))
+            if r % 2:
+                scales[r, g] = np.float32(scales[r, g] * np.float32(2.0 ** -127))
+            else:
+                scales[r, g] = np.float32(2.0 ** 70)
+                codes[r, 128 * g:128 * (g + 1)] &= 0xF0  # flags kept, code 0
+    P, d, f = cfg.n_pairs, cfg.d_model, cfg.d_ff
+    w13r = np.empty((2 * P, 2, f, d), np.uint16)
+    w2r = np.empty((2 * P, d, f), np.uint16)
+    for p in range(P):
+        for pos in (0, 1):
+            for j in (0, 1):
+                w13r[2 * p + pos, j] = oracle.quant_unpack(c13[p, j], s13[p, j], pos)
+            w2r[2 * p + pos] = oracle.quant_unpack(c2[p], s2[p], pos)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    layer = pz.QuantMoELayer(t(c13), t(s13), t(c2), t(s2), t(slot))
+    T = 64
+    hb = synth.hidden_bits(cfg, T)
+    lg = synth.router_logits(cfg, T)
+    out = layer.forward(t(hb.view(np.int16)).view(torch.bfloat16), t(lg), cfg.top_k, cfg.renormalize)
+    torch.cuda.synchronize()
+    ref = oracle.moe_forward(w13r, w2r, (2 * slot).astype(np.int32), hb, lg, cfg.top_k, cfg.renormalize,
+                             pair_dense=np.ones(2 * P, np.uint8))
+    assert_close(out.float().cpu().numpy(), ref, "quant scale-range paths")
