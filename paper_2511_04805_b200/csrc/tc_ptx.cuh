@@ -174,6 +174,28 @@ __device__ __forceinline__ void mma_bf16_ts_elect(uint32_t tmem_d, uint32_t tmem
       "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One 64-wide K stage of the TS form (4 x K = 16) from ONE elected lane in one asm block: A
+// columns tmem_a + 8 kk, B descriptor start field + 2 kk (32 bytes further in the 128-byte
+// swizzled rows), the first MMA accumulating iff `accumulate`. Measured in
+// scripts/micro/umma_ts_rate.cu (form ts4: ~180 instead of ~280 ns of issue per stage) and in
+// the decode / TS kernels (profiles/r02/mma_stage_ab.txt: within +-3 %, Qwen1.5 decode +5 %):
+// not used by the kernels.
+__device__ __forceinline__ void mma_bf16_ts_stage4_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t desc_b, uint32_t idesc,
+                                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 d1, d2, d3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "add.u64 d1, %2, 2;\n\tadd.u64 d2, %2, 4;\n\tadd.u64 d3, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, t;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

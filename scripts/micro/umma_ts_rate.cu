@@ -42,7 +42,9 @@ __global__ void k_rate(int stages, int N, int ts, int iss, int commits, unsigned
     for (int s = 0; s < stages; ++s) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (ts)
+        if (ts == 2) {
+          if (k == 0) ptx::mma_bf16_ts_stage4_elect(d, tm + 32u * (s & 3), ptx::smem_desc_sw128(sb), idesc, s != 0);
+        } else if (ts)
           ptx::mma_bf16_ts_elect(d, tm + 32u * (s & 3) + 8u * k, ptx::smem_desc_sw128(sb + 32 * k), idesc, (s | k) != 0);
         else {
           if ((threadIdx.x & 31) == 0)
@@ -71,7 +73,7 @@ int main() {
   cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int stages = 512;
   printf("form N_per_issuer issuers commits/stage  ns_per_stage  TFLOP/s(148 SMs)  frac_of_1658\n");
-  for (int ts = 1; ts >= 0; --ts)
+  for (int ts = 2; ts >= 0; --ts)
     for (int N : {64, 96, 128, 144, 176, 192, 256})
       for (int iss : {1, 2})
         for (int commits : {0, 2}) {
@@ -91,7 +93,7 @@ int main() {
           const double per_stage = (double)mx / stages;
           const double flops = 2.0 * 128 * N * 64 * iss;  // per stage per SM
           const double tf = flops / per_stage * 1e-3 * sms;
-          printf("%s %4d %d %d %8.1f %8.1f %.3f\n", ts ? "ts" : "ss", N, iss, commits, per_stage, tf, tf / 1658.6);
+          printf("%s %4d %d %d %8.1f %8.1f %.3f\n", ts == 2 ? "ts4" : ts ? "ts" : "ss", N, iss, commits, per_stage, tf, tf / 1658.6);
         }
   return 0;
 }
