@@ -120,6 +120,25 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PZ_TRD(ev, idx)
 #endif
 
+// mbarrier waits: a spinning waiter re-issues try_wait (and the loop around it) on the SM's
+// issue slots; with a suspend-time hint the hardware parks the thread until the phase
+// completes (or the hint expires). Producers / MMA issuers (PZ_TC_SLEEP_ROLES) and decoders
+// (PZ_TC_SLEEP_DEC) separately selectable; measured, no gain (profiles/r02/wait_sleep_ab.txt): off.
+#ifndef PZ_TC_SLEEP_ROLES
+#define PZ_TC_SLEEP_ROLES 0
+#endif
+#ifndef PZ_TC_SLEEP_DEC
+#define PZ_TC_SLEEP_DEC 0
+#endif
+__device__ __forceinline__ void wait_role(uint64_t* bar, uint32_t parity) {
+  if (PZ_TC_SLEEP_ROLES) ptx::mbar_wait_sleep(bar, parity, 20000);
+  else ptx::mbar_wait(bar, parity);
+}
+__device__ __forceinline__ void wait_dec(uint64_t* bar, uint32_t parity) {
+  if (PZ_TC_SLEEP_DEC) ptx::mbar_wait_sleep(bar, parity, 20000);
+  else ptx::mbar_wait(bar, parity);
+}
+
 template <int WST, int XST, int AST>
 struct alignas(16) Ctl {
   int4 whdr[WST];  // stage headers (see Pass); item -1 = no more work
@@ -312,7 +331,7 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST, AST>& c, uint32_t smem
   (void)tcount;
   (void)kW13;
   for (int kb = 0; kb < n_stages; ++kb) {
-    if (kb) ptx::mbar_wait(&c.wfull[w.i], w.ph);
+    if (kb) wait_dec(&c.wfull[w.i], w.ph);
     PZ_TRD(2, tcount);
     const uint32_t st = smem_w + (uint32_t)w.i * kWBytes;
     uint4 v[KC];
@@ -341,7 +360,7 @@ __device__ __forceinline__ void decode_pass(Ctl<WST, XST, AST>& c, uint32_t smem
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&c.wempty[w.i]);  // packed words consumed: the slot may refill
     w.next<WST>();
-    ptx::mbar_wait(&c.a_empty[a.i], a.ph ^ 1);  // the MMAs that read A buffer a.i have completed
+    wait_dec(&c.a_empty[a.i], a.ph ^ 1);  // the MMAs that read A buffer a.i have completed
     PZ_TRD(3, tcount);
     ptx::tc_fence_after();
     const uint32_t t0 = lane_tmem + 64u * a.i + 4u * KC * kh;
@@ -417,7 +436,7 @@ __device__ __forceinline__ void decode_pass_q(Ctl<WST, XST, AST>& c, uint32_t sm
   (void)tcount;
   float sc_next = __ldg(row_scales + (kb0 >> 1));  // a group = 2 stages of 64
   for (int kb = 0; kb < n_stages; ++kb) {
-    if (kb) ptx::mbar_wait(&c.wfull[w.i], w.ph);
+    if (kb) wait_dec(&c.wfull[w.i], w.ph);
     const uint32_t st = smem_w + (uint32_t)w.i * (kRows * kBK);  // quantised W slots: 8 KB
     const uint4 v0 = lds128(st + w_off[0]), v1 = lds128(st + w_off[1]);
     const float sc = sc_next;
@@ -449,7 +468,7 @@ __device__ __forceinline__ void decode_pass_q(Ctl<WST, XST, AST>& c, uint32_t sm
         qdecode2<MODE>(words[i] >> 16, L, d0[2 * i + 1], d1[2 * i + 1]);
       }
     }
-    ptx::mbar_wait(&c.a_empty[a.i], a.ph ^ 1);  // the MMAs that read A buffer a.i have completed
+    wait_dec(&c.a_empty[a.i], a.ph ^ 1);  // the MMAs that read A buffer a.i have completed
     ptx::tc_fence_after();
     const uint32_t t0 = lane_tmem + 64u * a.i + 16u * kh;
     if (MODE & 1) ptx::tmem_st_32x32b_x16(t0, d0);
@@ -597,7 +616,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         for (int kb = kb0; kb < kb1; ++kb) {
           const int kc = kb * kBK;
           const int4 hv = make_int4(item, base, kb, (kb0 << 16) | kb1);
-          ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
+          wait_role(&c.wempty[w.i], w.ph ^ 1);
           PZ_TR(0, tw);
 #ifdef PZ_TRACE
           if (tw == 0) g_cta[kW13][blockIdx.x][1] = gtimer();
@@ -613,7 +632,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           }
           w.next<kWStages>();
           ++tw;
-          ptx::mbar_wait(&c.sqempty[sq.i], sq.ph ^ 1);
+          wait_role(&c.sqempty[sq.i], sq.ph ^ 1);
           c.sqh[sq.i] = hv;
           c.sq[sq.i] = make_int4(kc, r0, r1, 0);
           ptx::mbar_arrive(&c.sqfull[sq.i]);
@@ -625,10 +644,10 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     g_cta[kW13][blockIdx.x][2] = gtimer();
 #endif
     // "no more work": complete one more phase of the W ring and the queue without data
-    ptx::mbar_wait(&c.wempty[w.i], w.ph ^ 1);
+    wait_role(&c.wempty[w.i], w.ph ^ 1);
     c.whdr[w.i] = make_int4(-1, 0, 0, 0);
     ptx::mbar_arrive(&c.wfull[w.i]);
-    ptx::mbar_wait(&c.sqempty[sq.i], sq.ph ^ 1);
+    wait_role(&c.sqempty[sq.i], sq.ph ^ 1);
     c.sqh[sq.i] = make_int4(-1, 0, 0, 0);
     ptx::mbar_arrive(&c.sqfull[sq.i]);
     return;
@@ -666,12 +685,12 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     };
     for (;;) {
       if (!signalled && ptx::mbar_test(&c.pdone, 0)) signal();
-      ptx::mbar_wait(&c.sqfull[sq.i], sq.ph);
+      wait_role(&c.sqfull[sq.i], sq.ph);
       const int4 h = c.sqh[sq.i];
       const int4 q = c.sq[sq.i];
       ptx::mbar_arrive(&c.sqempty[sq.i]);
       sq.next<kSq>();
-      ptx::mbar_wait(&c.xempty[x.i], x.ph ^ 1);
+      wait_role(&c.xempty[x.i], x.ph ^ 1);
       c.xhdr[x.i] = h;
       if (h.x < 0) {
         ptx::mbar_arrive(&c.xfull[x.i]);  // "no more work"
@@ -704,19 +723,19 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
     int tcount = 0;
     (void)tcount;
     for (;;) {
-      ptx::mbar_wait(&c.xfull[x.i], x.ph);
+      wait_role(&c.xfull[x.i], x.ph);
       const int4 h = lds_int4(xhdr_s + 16u * x.i);
       if (h.x < 0) break;
       const Pass s = make_pass(c, h, n_active, NX);
       const int np = mypos ? s.n1 : s.n0;
       const uint32_t idp = ptx::idesc_bf16_f32(128, (uint32_t)((np + 15) & ~15));
       const uint32_t acc_col = tmem + C::kAccCol + (uint32_t)NX * mypos;
-      ptx::mbar_wait(&c.acc_empty, accph ^ 1);  // the previous pass's epilogue drained TMEM
+      wait_role(&c.acc_empty, accph ^ 1);  // the previous pass's epilogue drained TMEM
       ptx::tc_fence_after();
       for (int kb = s.kb0; kb < s.kb1; ++kb) {
-        if (kb != s.kb0) ptx::mbar_wait(&c.xfull[x.i], x.ph);
+        if (kb != s.kb0) wait_role(&c.xfull[x.i], x.ph);
         if (mypos == 0) PZ_TR(6, tcount);
-        ptx::mbar_wait(&c.a_full[a.i], a.ph);
+        wait_role(&c.a_full[a.i], a.ph);
         if (mypos == 0) PZ_TR(5, tcount);
         ptx::tc_fence_after();
         const uint32_t xs = smem_x + (uint32_t)x.i * kXBytes + (uint32_t)(kXPos * mypos);
@@ -769,7 +788,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
 #ifdef PZ_TRACE
       if (dtid == 0 && !(s.kb0 == 0 && s.kb1 == nk) && g == sk.owner(s.item * nk)) g_red[kW13][blockIdx.x][0] = gtimer();
 #endif
-      ptx::mbar_wait(&c.acc_full, accph);
+      wait_dec(&c.acc_full, accph);
       accph ^= 1;
       ptx::tc_fence_after();
       const bool whole = s.kb0 == 0 && s.kb1 == nk;  // the item is not split: final outputs
@@ -986,7 +1005,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
       have_pend = false;
     };
     for (;;) {
-      ptx::mbar_wait(&c.wfull[w.i], w.ph);
+      wait_dec(&c.wfull[w.i], w.ph);
       const int4 h = lds_int4(whdr_s + 16u * w.i);
       if (h.x < 0) break;
       const Pass s = make_pass(c, h, n_active, NX);
