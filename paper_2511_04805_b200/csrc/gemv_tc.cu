@@ -503,10 +503,12 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
   constexpr int kWStages = C::kWStages, kXStages = C::kXStages, kXBytes = C::kXBytes, kXPos = C::kXPos;
   constexpr int kSlot = 2 * NX * kRows;  // floats per partial slot
   constexpr uint32_t kRowB = kRows * 4;   // one slot row (a (position, token) of 128 outputs): 512 bytes
-  // the reducer stages the partial slots in the idle W / X rings when two full slots fit
-  // (NX = 32); otherwise (NX = 64: 64 KB slots, 96 KB of rings) it sums them from L2 directly
+  // the reducer stages the partial slots in the idle W / X rings when two slots of the item's
+  // active (position, token) rows fit (always at NX = 32); otherwise (wide configurations with
+  // many rows) it sums them from L2 directly
   constexpr uint32_t kRing = kWStages * kWStageBytes + kXStages * kXBytes;
   constexpr bool kStagedRed = kRing >= 2u * (2 * NX) * kRowB;
+  auto staged_red = [&](int n_rows) { return kStagedRed || 2u * (uint32_t)n_rows * kRowB <= kRing; };
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t smem_w = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;  // == smem, shared window
@@ -810,7 +812,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * acc_scale);
-        if (!whole && reducer && kStagedRed) {
+        if (!whole && reducer && staged_red(s.n0 + s.n1)) {
           // the reducer's own piece (the sum's first term): straight into staged slot 0 of the
           // W ring -- idle now: every stage was decoded before the MMAs completed
           const uint32_t a0 = smem_w + (uint32_t)((pos ? s.n0 : 0) + c0) * kRowB + (uint32_t)prow * 4u;
@@ -888,7 +890,7 @@ __global__ void __maxnreg__(80) k_gemv_tc(  // 2 CTAs x 12 warps: 6 warps per SM
           const int cols = kW13 ? kRows / 2 : min(kRows, d - r0);  // outputs of this tile, multiple of 4
           const int q4 = cols / 4;
           const int n_rows = s.n0 + s.n1;                           // active (position, token) rows
-          if constexpr (!kStagedRed) {
+          if (!staged_red(n_rows)) {
             // every piece (own included) is in its global slot: sum them in CTA order from L2
             for (int u = dtid; u < n_rows * q4; u += kDecWarps * 32) {
               const int r = u / q4, cq = 4 * (u % q4);
