@@ -183,7 +183,7 @@ typedef struct {
 } puzzle_moe_layer;
 
 /* Kernel path for puzzle_moe_forward_ex. AUTO: GEMV while T <= 64 or the experts average
- * fewer than 72 tokens (T*top_k < 72*n_experts; 100 when d_ff >= 8192), else TS (else TC,
+ * fewer than 96 tokens (T*top_k < 96*n_experts; 120 when d_ff >= 8192), else TS (else TC,
  * else GEMV). */
 typedef enum {
   PUZZLE_PATH_AUTO = 0,

@@ -178,8 +178,8 @@ struct Plan {
 // Decode shapes (<= 64 tokens) stream each touched pair once through the decode-shape kernels
 // (gemv_tc.cu); larger token counts are tensor-bound and go to the tcgen05 grouped GEMM.
 constexpr int64_t kGemvMaxTokens = 64;
-constexpr int64_t kGemvMaxTokensPerExpert = 72;
-constexpr int64_t kGemvMaxTokensPerExpertCoarse = 100;  // d_ff >= 8192 (Mixtral-like experts)
+constexpr int64_t kGemvMaxTokensPerExpert = 96;
+constexpr int64_t kGemvMaxTokensPerExpertCoarse = 120;  // d_ff >= 8192 (Mixtral-like experts)
 
 struct Layout {
   size_t topk_idx, topk_gate, bucket_off, assign_token, assign_of, active, n_active, cnt13, cnt2, h, y, part,
@@ -194,9 +194,9 @@ Plan make_plan(const puzzle_moe_layer* L, int64_t T, int k, int path) {
   p.max_active = (int)std::min<int64_t>(L->n_pairs, p.n_assign);
   // The decode-shape kernels stream each touched pair once per pass of 32 / 64 / 128 tokens per
   // position (NX chosen from the average tokens per expert, gemv_tc.cu): they win while an
-  // expert averages < 72 tokens (fine-grained layers: NX 128 ahead at 51-68, level with TS at
-  // 72, TS from 96), or < 100 with coarse experts (Mixtral: NX 128 ahead up to 96 tokens per
-  // expert, TS from 128) -- profiles/r02/nx128_crossover.log.
+  // expert averages < 96 tokens (fine-grained layers: ahead at 72-85, level at 96-102), or
+  // < 120 with coarse experts (Mixtral: ahead up to 96, level at 112, TS from 128) --
+  // profiles/r02/retune_crossover.txt (with the staged wide reducer; nx128_crossover.log before).
   // Heavier batches: the decode-into-TMEM prefill kernel (gemm_ts.cu; ahead of or level with the
   // shared-memory-operand kernel on every config), else gemm_tc.cu.
   if (path == PUZZLE_PATH_AUTO)
