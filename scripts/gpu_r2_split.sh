@@ -1,0 +1,10 @@
+#!/bin/bash
+# NX 128: second W / X producer warps (split TMA issue): parity first (bounded), then A/B vs nosplit.
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out/r2
+timeout 600 python -m pytest tests/test_gpu_nx64.py -x -q -m gpu > gpurun_out/r2/split_tests.log 2>&1; rc=$?; echo "rc=$rc" >> gpurun_out/r2/split_tests.log
+if [ $rc -ne 0 ]; then exit 0; fi
+timeout 900 python -m pytest tests/test_gpu_moe.py tests/test_gpu_ep.py tests/test_gpu_edge.py -x -q -m gpu >> gpurun_out/r2/split_tests.log 2>&1; echo "rc2=$?" >> gpurun_out/r2/split_tests.log
+for rep in 1 2; do for v in nosplit cur; do
+  if [ $v = cur ]; then L=""; else L="PUZZLE_LIB=build/variants/$v/libpuzzlemoe.so"; fi
+  env $L timeout 600 python scripts/decode_ab.py mixtral:256 mixtral:384 qwen15:1024 deepseek:768 qwen15:1280 > gpurun_out/r2/split_${v}_$rep.log 2>&1
+done; done
